@@ -1,0 +1,167 @@
+/*
+ * mxb200.h -- C ABI of the B200 (sm_100a) compressed tensor-parallel
+ * all-reduce path of arXiv 2411.09510 ("mxcomm" reference).
+ *
+ * The reference is pure Python/numpy; its hot path is the block codec
+ * (mx/codec.py:140-188, mx/bitpack.py:22-58) driven by the compressed
+ * collective (mx/netbench.py:307-339) and the row-parallel hook
+ * (mx/tpsim.py:234-302).  Each entry point below replaces one of those
+ * reference interfaces (cited per function; `mx/` = pkg/src/mxcomm/).
+ *
+ * Conventions
+ *  - Plain C types only; every pointer marked "device" is device memory
+ *    owned by the caller (e.g. the torch caching allocator).
+ *  - Every compute call is asynchronous on `stream` (a cudaStream_t passed
+ *    as void*; NULL = legacy default stream), performs no host sync and no
+ *    allocation, and is safe to capture into a CUDA graph.
+ *  - Return value: MX_OK (0) or a negative MX_ERR_* code.  Codes map 1:1 to
+ *    the reference exception classes of mx/errors.py; a thread-local
+ *    message is available from mx_last_error().
+ *  - Streams: "scale stream" = one k-bit scale code per block, "element
+ *    stream" = one b-bit code per value, both LSB-first within each byte,
+ *    zero-padded only at their end (mx/bitpack.py:3-7, mx/codec.py:27-43).
+ *    Byte-identical to the reference's CompressedTensor streams.
+ *  - Shard ("wire message") layout used by the collectives:
+ *      [scale stream | pad to 16 B | element stream | pad to 16 B]
+ *    see mx_shard_layout().
+ */
+#ifndef MXB200_H
+#define MXB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MXB200_ABI_VERSION 1
+
+/* FormatKind (mx/formats.py:54-56) */
+enum { MX_KIND_FLOAT = 0, MX_KIND_INT = 1 };
+
+/* element dtypes of dense tensors crossing the ABI */
+enum { MX_F32 = 0, MX_F16 = 1, MX_BF16 = 2, MX_F64 = 3 };
+
+/* status codes <-> mx/errors.py */
+enum {
+  MX_OK = 0,
+  MX_ERR_INVALID_ARGUMENT = -1, /* ValueError                         */
+  MX_ERR_NONFINITE = -2,        /* NonFiniteInput       (errors.py:8)  */
+  MX_ERR_MALFORMED_CODE = -3,   /* MalformedCode        (errors.py:16) */
+  MX_ERR_TRUNCATED = -4,        /* TruncatedStream      (errors.py:32) */
+  MX_ERR_UNKNOWN_SCHEME = -5,   /* UnknownScheme        (errors.py:36) */
+  MX_ERR_SHAPE = -6,            /* ShapeMismatch        (errors.py:40) */
+  MX_ERR_CUDA = -7,             /* CUDA launch / runtime failure       */
+  MX_ERR_UNSUPPORTED = -8,      /* valid scheme, path not implemented  */
+  MX_ERR_WORKSPACE = -9         /* workspace too small                 */
+};
+
+/* SchemeDescriptor (mx/formats.py:157-175) lowered to a POD.
+ * element: ElementFormat(kind, exponent_bits, mantissa_bits)
+ *          (mx/formats.py:59-103; INTn has exponent_bits 0, mantissa n-1)
+ * scale:   ScaleFormat(scale_bits) = EkM0, k in [4,8] (mx/formats.py:106-132) */
+typedef struct mx_scheme {
+  int32_t kind;
+  int32_t exponent_bits;
+  int32_t mantissa_bits;
+  int32_t scale_bits;
+  int64_t block_size;
+} mx_scheme_t;
+
+int mx_abi_version(void);
+const char* mx_last_error(void);
+
+/* Validates a scheme like ElementFormat/ScaleFormat/SchemeDescriptor
+ * __post_init__ (mx/formats.py:68-83,112-114,165-167). */
+int mx_scheme_check(const mx_scheme_t* scheme);
+
+/* packed_nbytes for both streams (mx/bitpack.py:17-19, as used by
+ * serialized_nbytes mx/codec.py:291-299 minus the header). */
+int mx_stream_nbytes(int64_t n, const mx_scheme_t* scheme, int64_t* scale_bytes,
+                     int64_t* element_bytes);
+
+/* Wire-message layout of one shard holding n values (no MXC1 header on the
+ * NCCL wire; serialize() adds it on the host). */
+int mx_shard_layout(int64_t n, const mx_scheme_t* scheme, int64_t* scale_offset,
+                    int64_t* element_offset, int64_t* shard_bytes);
+
+/* Bytes of device workspace mx_quantize / mx_quantize_chunks may need
+ * (generic path only: any block size, unaligned or float64 input).  For the
+ * chunked call pass n = nchunks * chunk_values. */
+int mx_workspace_bytes(int64_t n, const mx_scheme_t* scheme, int64_t* bytes);
+
+/* Same for mx_dequant_sum_requant on an n-value chunk. */
+int mx_requant_workspace_bytes(int64_t n, const mx_scheme_t* scheme, int64_t* bytes);
+
+/* compress_tensor (mx/codec.py:238-263) incl. _quantize_block_matrix
+ * (140-172), _round_to_grid (127-137) and pack_bits (mx/bitpack.py:22-34).
+ *   x              device, n values of `dtype` (row-major flattened)
+ *   scale_stream   device, mx_stream_nbytes().scale_bytes
+ *   element_stream device, mx_stream_nbytes().element_bytes
+ *   nonfinite      device u64, nullable.  Caller initialises it to
+ *                  UINT64_MAX (mx_nonfinite_reset); the kernel atomically
+ *                  lowers it to the flat index of the first NaN/Inf, which
+ *                  the host turns into NonFiniteInput(block_index =
+ *                  index // block_size) exactly like _check_finite
+ *                  (mx/codec.py:191-199).  Outputs are unspecified then. */
+int mx_quantize(const void* x, int32_t dtype, int64_t n, const mx_scheme_t* scheme,
+                uint8_t* scale_stream, uint8_t* element_stream, uint64_t* nonfinite,
+                void* workspace, int64_t workspace_bytes, void* stream);
+
+/* decompress_tensor (mx/codec.py:266-284) incl. unpack_bits
+ * (mx/bitpack.py:37-58) and _dequantize_block_matrix (175-188).
+ * out_dtype MX_F64 is exact; MX_F32/F16/BF16 round the exact value once
+ * (RNE), like ndarray.astype. */
+int mx_dequantize(const uint8_t* scale_stream, const uint8_t* element_stream, int64_t n,
+                  const mx_scheme_t* scheme, void* out, int32_t out_dtype, void* stream);
+
+/* Chunked compress for the collectives: x (n values) is cut into
+ * ceil(n / chunk_values) chunks, each compressed as an independent tensor
+ * into the shard at  shards + j * shard_stride  with mx_shard_layout(
+ * chunk_values) offsets.  chunk_values must be a multiple of 8*block_size
+ * (blocks never straddle chunks, so codes equal whole-tensor codes). */
+int mx_quantize_chunks(const void* x, int32_t dtype, int64_t n, int64_t chunk_values,
+                       const mx_scheme_t* scheme, uint8_t* shards, int64_t shard_stride,
+                       uint64_t* nonfinite, void* workspace, int64_t workspace_bytes,
+                       void* stream);
+
+/* The compressed-collective reduction (mx/netbench.py:329-334): decode
+ * `nranks` shards and sum them in fp32 in rank order starting from +0.0,
+ * then cast once to out_dtype (MX_F32/F16/BF16).
+ * Shard of (rank r, chunk j) lives at  shards + r*rank_stride + j*chunk_stride
+ * with mx_shard_layout(chunk_values) offsets; output value i of chunk j is
+ * out[j*chunk_values + i].
+ *   one-shot all-gather : nranks=N, rank_stride=shard bytes, chunk_values=n
+ *   two-shot all-gather : nranks=1, chunk_stride=shard bytes, chunk_values=c */
+int mx_dequant_sum(const uint8_t* shards, int64_t rank_stride, int32_t nranks, int64_t n,
+                   int64_t chunk_values, int64_t chunk_stride, const mx_scheme_t* scheme,
+                   void* out, int32_t out_dtype, void* stream);
+
+/* Two-shot middle step (not in the reference; restated from the same codec
+ * calls): decode `nranks` shards of one n-value chunk, fp32 rank-order sum
+ * from +0.0, re-quantise the sum into the shard at `out_shard`.  All shards
+ * use mx_shard_layout(chunk_values) offsets (chunk_values >= n; the last
+ * chunk of a tensor is shorter than the others). */
+int mx_dequant_sum_requant(const uint8_t* shards, int64_t rank_stride, int32_t nranks,
+                           int64_t n, int64_t chunk_values, const mx_scheme_t* scheme,
+                           uint8_t* out_shard, uint64_t* nonfinite, void* workspace,
+                           int64_t workspace_bytes, void* stream);
+
+/* unpack_bits (mx/bitpack.py:37-58) on the device: `count` codes of
+ * `width` bits -> one uint8 per code (quantize_block's return value). */
+int mx_unpack_codes(const uint8_t* packed, int64_t count, int32_t width, uint8_t* codes,
+                    void* stream);
+
+/* pack_bits (mx/bitpack.py:22-34) on the device: the inverse of
+ * mx_unpack_codes (dequantize_block's input path). */
+int mx_pack_codes(const uint8_t* codes, int64_t count, int32_t width, uint8_t* packed,
+                  void* stream);
+
+/* Sets *nonfinite = UINT64_MAX on `stream`. */
+int mx_nonfinite_reset(uint64_t* nonfinite, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MXB200_H */

@@ -1,0 +1,124 @@
+"""ctypes binding of the C ABI in include/mxb200.h (libmxb200.so, in-tree).
+
+The shared library is plain C ABI (no torch types), built for sm_100a by
+``__graft_entry__.build()`` / ``python -m paper_2411_09510_b200.build``.
+There is no fallback: if the library or a CUDA device is missing, every
+compute entry point raises :class:`NativeUnavailable`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import NativeUnavailable, raise_for_status
+
+LIB_NAME = "libmxb200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+MX_F32, MX_F16, MX_BF16, MX_F64 = 0, 1, 2, 3
+
+c_i64 = ctypes.c_int64
+c_i32 = ctypes.c_int32
+c_vp = ctypes.c_void_p
+c_i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+class MxScheme(ctypes.Structure):
+    """mx_scheme_t"""
+
+    _fields_ = [("kind", c_i32), ("exponent_bits", c_i32), ("mantissa_bits", c_i32),
+                ("scale_bits", c_i32), ("block_size", c_i64)]
+
+
+_SP = ctypes.POINTER(MxScheme)
+
+# name -> (restype, argtypes); every symbol include/mxb200.h declares
+SIGNATURES = {
+    "mx_abi_version": (c_i32, []),
+    "mx_last_error": (ctypes.c_char_p, []),
+    "mx_scheme_check": (c_i32, [_SP]),
+    "mx_stream_nbytes": (c_i32, [c_i64, _SP, c_i64p, c_i64p]),
+    "mx_shard_layout": (c_i32, [c_i64, _SP, c_i64p, c_i64p, c_i64p]),
+    "mx_workspace_bytes": (c_i32, [c_i64, _SP, c_i64p]),
+    "mx_requant_workspace_bytes": (c_i32, [c_i64, _SP, c_i64p]),
+    "mx_quantize": (c_i32, [c_vp, c_i32, c_i64, _SP, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "mx_dequantize": (c_i32, [c_vp, c_vp, c_i64, _SP, c_vp, c_i32, c_vp]),
+    "mx_quantize_chunks": (c_i32, [c_vp, c_i32, c_i64, c_i64, _SP, c_vp, c_i64, c_vp, c_vp,
+                                   c_i64, c_vp]),
+    "mx_dequant_sum": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_i64, c_i64, _SP, c_vp, c_i32, c_vp]),
+    "mx_dequant_sum_requant": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_i64, _SP, c_vp, c_vp, c_vp,
+                                       c_i64, c_vp]),
+    "mx_unpack_codes": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "mx_pack_codes": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "mx_nonfinite_reset": (c_i32, [c_vp, c_vp]),
+}
+
+ABI_VERSION = 1
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libmxb200.so and bind every exported symbol (raises if absent)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"{path} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)  # AttributeError = ABI drift, fail loudly
+            fn.restype = res
+            fn.argtypes = args
+        if lib.mx_abi_version() != ABI_VERSION:
+            raise NativeUnavailable(f"{path}: ABI {lib.mx_abi_version()} != {ABI_VERSION}")
+        _lib = lib
+        return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = _lib.mx_last_error().decode(errors="replace") if _lib is not None else ""
+        raise_for_status(rc, f"{what}: {msg}")
+
+
+def scheme_ptr(c_scheme: MxScheme):
+    return ctypes.byref(c_scheme)
+
+
+def stream_nbytes(n: int, cs: MxScheme) -> tuple[int, int]:
+    lib = load()
+    a, b = c_i64(), c_i64()
+    check(lib.mx_stream_nbytes(n, ctypes.byref(cs), ctypes.byref(a), ctypes.byref(b)),
+          "mx_stream_nbytes")
+    return a.value, b.value
+
+
+def shard_layout(n: int, cs: MxScheme) -> tuple[int, int, int]:
+    lib = load()
+    a, b, c = c_i64(), c_i64(), c_i64()
+    check(lib.mx_shard_layout(n, ctypes.byref(cs), ctypes.byref(a), ctypes.byref(b),
+                              ctypes.byref(c)), "mx_shard_layout")
+    return a.value, b.value, c.value
+
+
+def workspace_bytes(n: int, cs: MxScheme, requant: bool = False) -> int:
+    lib = load()
+    a = c_i64()
+    fn = lib.mx_requant_workspace_bytes if requant else lib.mx_workspace_bytes
+    check(fn(n, ctypes.byref(cs), ctypes.byref(a)), "mx_workspace_bytes")
+    return a.value
+
+
+def require_cuda():
+    """The product path runs on the GPU or not at all."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device: the MX codec runs only on the sm_100a kernels")
+    load()

@@ -1,0 +1,393 @@
+"""Drop-in block codec: same API as mx/codec.py, computed by the sm_100a kernels.
+
+Reference surface kept unchanged (mx/codec.py:93-393): ``CompressedTensor``,
+``compress_tensor``, ``decompress_tensor``, ``quantize_block``,
+``dequantize_block``, ``serialize``, ``deserialize``, ``serialized_nbytes``,
+``header_nbytes``, ``pack_header``, ``unpack_header``, ``block_error_bound``.
+
+* numpy arrays / CPU tensors are copied to the GPU, quantised by K1
+  (``mx_quantize``) and the packed streams copied back: the returned
+  ``CompressedTensor`` holds ``bytes`` identical to the reference's.
+* CUDA tensors can stay on the device end to end with
+  :func:`compress_tensor_device` / :func:`decompress_tensor_device` (no host
+  sync, graph-capturable apart from the optional non-finite check).
+* The MXC1 container (serialize/deserialize) is host-side byte formatting.
+
+There is no CPU implementation of the arithmetic here: without a CUDA
+device and ``libmxb200.so`` every compute call raises ``NativeUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .errors import (BadMagic, MalformedCode, MalformedHeader, NonFiniteInput,
+                     TruncatedStream, UnsupportedVersion)
+from .formats import (ELEMENT_CODES, ELEMENT_FORMATS, SCALE_CODES, SCALE_FORMATS,
+                      SchemeDescriptor, enumerate_grid)
+
+MAGIC = b"MXC1"
+VERSION = 1
+_HEADER = struct.Struct("<4sBBBBIII")  # mx/codec.py:83
+
+FORMAT_CODE_TOPK = 0xF0
+FORMAT_CODE_CHANNEL_INT = 0xF1
+FORMAT_CODE_RAW_F32 = 0xFE
+FORMAT_CODE_RAW_F16 = 0xFD
+
+
+
+def _numel(shape) -> int:
+    return int(np.prod(shape, dtype=np.int64)) if len(shape) else 1
+
+
+def packed_nbytes(count: int, width: int) -> int:
+    """mx/bitpack.py:17-19"""
+    return (count * width + 7) // 8
+
+
+@dataclass(frozen=True)
+class CompressedTensor:
+    """Packed scale + element streams of one tensor (mx/codec.py:93-115)."""
+
+    scheme: SchemeDescriptor
+    shape: tuple
+    scale_stream: bytes
+    element_stream: bytes
+
+    @property
+    def total_elements(self) -> int:
+        return _numel(self.shape)
+
+    @property
+    def num_blocks(self) -> int:
+        return -(-self.total_elements // self.scheme.block_size)
+
+    @property
+    def nbytes(self) -> int:
+        return header_nbytes(len(self.shape)) + len(self.scale_stream) + len(self.element_stream)
+
+
+@dataclass(frozen=True)
+class DeviceCompressedTensor:
+    """Device-resident twin of CompressedTensor: ``scale`` / ``elements`` are
+    CUDA uint8 tensors holding the same bytes."""
+
+    scheme: SchemeDescriptor
+    shape: tuple
+    scale: "object"
+    elements: "object"
+
+    @property
+    def total_elements(self) -> int:
+        return _numel(self.shape)
+
+    @property
+    def num_blocks(self) -> int:
+        return -(-self.total_elements // self.scheme.block_size)
+
+    def to_host(self) -> CompressedTensor:
+        return CompressedTensor(self.scheme, tuple(self.shape), self.scale.cpu().numpy().tobytes(),
+                                self.elements.cpu().numpy().tobytes())
+
+
+# ---------------------------------------------------------------------------
+# tensor plumbing
+# ---------------------------------------------------------------------------
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    return {torch.float32: _native.MX_F32, torch.float16: _native.MX_F16,
+            torch.bfloat16: _native.MX_BF16, torch.float64: _native.MX_F64}[t.dtype]
+
+
+def _to_device_values(tensor):
+    """Any array-like -> (contiguous CUDA tensor of a supported float dtype, shape)."""
+    torch = _torch()
+    _native.require_cuda()
+    if isinstance(tensor, torch.Tensor):
+        t = tensor
+        if t.dtype not in (torch.float32, torch.float16, torch.bfloat16, torch.float64):
+            t = t.to(torch.float64)
+        shape = tuple(int(d) for d in t.shape)
+        return t.to("cuda").contiguous().reshape(-1), shape
+    arr = np.asarray(tensor)
+    shape = tuple(int(d) for d in arr.shape)
+    if arr.dtype.name == "bfloat16":  # ml_dtypes
+        t = torch.from_numpy(np.ascontiguousarray(arr).view(np.uint16).reshape(-1).copy())
+        return t.view(torch.bfloat16).to("cuda"), shape
+    if arr.dtype not in (np.float32, np.float16, np.float64):
+        arr = arr.astype(np.float64)  # like np.ascontiguousarray(arr, float64)
+    flat = np.ascontiguousarray(arr).reshape(-1)
+    return torch.from_numpy(flat.copy()).to("cuda"), shape
+
+
+def _stream():
+    return ctypes.c_void_p(_torch().cuda.current_stream().cuda_stream)
+
+
+def _raise_nonfinite(index: int, values, block: int):
+    blk = index // block
+    raise NonFiniteInput(
+        f"non-finite value {float(values[index].item())!r} at flat index {index} (block {blk})",
+        block_index=blk)
+
+
+# ---------------------------------------------------------------------------
+# compress / decompress (mx/codec.py:238-284)
+# ---------------------------------------------------------------------------
+
+
+def compress_tensor_device(tensor, scheme: SchemeDescriptor, check_finite: bool = True,
+                           out=None) -> DeviceCompressedTensor:
+    """K1 on the device.  ``check_finite`` reproduces NonFiniteInput with the
+    reference's block index (one host sync); pass False on hot paths."""
+    torch = _torch()
+    x, shape = _to_device_values(tensor)
+    n = x.numel()
+    cs = scheme.to_c()
+    sb, eb = _native.stream_nbytes(n, cs)
+    if out is None:
+        scale = torch.empty(sb, dtype=torch.uint8, device=x.device)
+        elems = torch.empty(eb, dtype=torch.uint8, device=x.device)
+    else:
+        scale, elems = out
+    lib = _native.load()
+    st = _stream()
+    flag = None
+    if check_finite and n:
+        flag = torch.empty(1, dtype=torch.int64, device=x.device)
+        _native.check(lib.mx_nonfinite_reset(ctypes.c_void_p(flag.data_ptr()), st),
+                      "mx_nonfinite_reset")
+    ws_n = _native.workspace_bytes(n, cs)
+    ws = torch.empty(ws_n, dtype=torch.uint8, device=x.device)
+    _native.check(lib.mx_quantize(
+        ctypes.c_void_p(x.data_ptr()), _dtype_code(x), n, ctypes.byref(cs),
+        ctypes.c_void_p(scale.data_ptr()), ctypes.c_void_p(elems.data_ptr()),
+        ctypes.c_void_p(flag.data_ptr()) if flag is not None else None,
+        ctypes.c_void_p(ws.data_ptr()), ws_n, st), "mx_quantize")
+    if flag is not None:
+        idx = int(flag.item())  # UINT64_MAX reads back as -1: no NaN/Inf seen
+        if idx >= 0:
+            _raise_nonfinite(idx, x, scheme.block_size)
+    return DeviceCompressedTensor(scheme, shape, scale, elems)
+
+
+def compress_tensor(tensor, scheme: SchemeDescriptor) -> CompressedTensor:
+    """Block-quantise ``tensor`` (flattened row-major) -- mx/codec.py:238-263."""
+    return compress_tensor_device(tensor, scheme, check_finite=True).to_host()
+
+
+_NP_OUT = {np.dtype(np.float64): _native.MX_F64, np.dtype(np.float32): _native.MX_F32,
+           np.dtype(np.float16): _native.MX_F16}
+
+
+def decompress_tensor_device(ct, dtype=None):
+    """Decode on the device; returns a CUDA tensor (``dtype`` a torch dtype,
+    default float32)."""
+    torch = _torch()
+    _native.require_cuda()
+    if isinstance(ct, CompressedTensor):
+        ct = _upload(ct)
+    dtype = dtype or torch.float32
+    n = ct.total_elements
+    out = torch.empty(n, dtype=dtype, device="cuda")
+    code = {torch.float32: _native.MX_F32, torch.float16: _native.MX_F16,
+            torch.bfloat16: _native.MX_BF16, torch.float64: _native.MX_F64}[dtype]
+    cs = ct.scheme.to_c()
+    lib = _native.load()
+    _native.check(lib.mx_dequantize(ctypes.c_void_p(ct.scale.data_ptr()),
+                                    ctypes.c_void_p(ct.elements.data_ptr()), n, ctypes.byref(cs),
+                                    ctypes.c_void_p(out.data_ptr()), code, _stream()),
+                  "mx_dequantize")
+    return out.reshape(ct.shape)
+
+
+def _upload(ct: CompressedTensor) -> DeviceCompressedTensor:
+    torch = _torch()
+    n = ct.total_elements
+    nb = -(-n // ct.scheme.block_size)
+    need_s = packed_nbytes(nb, ct.scheme.scale.exponent_bits)
+    need_e = packed_nbytes(n, ct.scheme.element.total_bits)
+    # same checks as unpack_bits (mx/bitpack.py:44-48)
+    if len(ct.scale_stream) < need_s:
+        raise TruncatedStream(f"need {need_s} bytes for {nb} codes of "
+                              f"{ct.scheme.scale.exponent_bits} bits, got {len(ct.scale_stream)}")
+    if len(ct.element_stream) < need_e:
+        raise TruncatedStream(f"need {need_e} bytes for {n} codes of "
+                              f"{ct.scheme.element.total_bits} bits, got {len(ct.element_stream)}")
+    # one upload: [scale | pad16 | elements] (the kernels' shard layout)
+    off = (need_s + 15) & ~15
+    buf = np.zeros(off + need_e + 16, dtype=np.uint8)
+    buf[:need_s] = np.frombuffer(ct.scale_stream, dtype=np.uint8, count=need_s)
+    buf[off:off + need_e] = np.frombuffer(ct.element_stream, dtype=np.uint8, count=need_e)
+    dev = torch.from_numpy(buf).to("cuda")
+    return DeviceCompressedTensor(ct.scheme, tuple(ct.shape), dev[:need_s], dev[off:off + need_e])
+
+
+def decompress_tensor(ct, dtype=np.float64):
+    """Reconstruct the quantised tensor -- mx/codec.py:266-284.
+
+    Host CompressedTensor -> numpy array of ``dtype`` (default float64, like
+    the reference).  DeviceCompressedTensor -> CUDA tensor.
+    """
+    if isinstance(ct, DeviceCompressedTensor):
+        torch = _torch()
+        tdt = dtype if isinstance(dtype, torch.dtype) else {
+            np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32,
+            np.dtype(np.float16): torch.float16}[np.dtype(dtype)]
+        return decompress_tensor_device(ct, tdt)
+    np_dt = np.dtype(dtype)
+    torch = _torch()
+    kernel_dt = {np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32,
+                 np.dtype(np.float16): torch.float16}.get(np_dt, torch.float64)
+    dev = decompress_tensor_device(ct, kernel_dt)
+    out = dev.cpu().numpy()
+    if out.dtype != np_dt:
+        out = out.astype(np_dt, copy=False)
+    return out.reshape(tuple(ct.shape))
+
+
+# ---------------------------------------------------------------------------
+# single blocks (mx/codec.py:202-235)
+# ---------------------------------------------------------------------------
+
+
+def quantize_block(values, scheme: SchemeDescriptor):
+    """-> (stored scale code, uint8 element codes) for one block."""
+    vals = np.asarray(values, dtype=np.float64).ravel()
+    if vals.size > scheme.block_size:
+        raise ValueError(f"block of {vals.size} values exceeds block size {scheme.block_size}")
+    torch = _torch()
+    dct = compress_tensor_device(vals, scheme, check_finite=True)
+    codes = torch.empty(max(vals.size, 1), dtype=torch.uint8, device="cuda")
+    lib = _native.load()
+    _native.check(lib.mx_unpack_codes(ctypes.c_void_p(dct.elements.data_ptr()), vals.size,
+                                      scheme.element.total_bits, ctypes.c_void_p(codes.data_ptr()),
+                                      _stream()), "mx_unpack_codes")
+    stored = torch.zeros(1, dtype=torch.uint8, device="cuda")
+    if dct.scale.numel():
+        _native.check(lib.mx_unpack_codes(ctypes.c_void_p(dct.scale.data_ptr()), 1,
+                                          scheme.scale.exponent_bits,
+                                          ctypes.c_void_p(stored.data_ptr()), _stream()),
+                      "mx_unpack_codes")
+    return int(stored.item()), codes[:vals.size].cpu().numpy().copy()
+
+
+def dequantize_block(stored_scale_code: int, element_codes, scheme: SchemeDescriptor):
+    """Decode one block to float64 (mx/codec.py:220-235)."""
+    codes = np.asarray(element_codes, dtype=np.int64).ravel()
+    limit = 1 << scheme.element.total_bits
+    if codes.size and (codes.min() < 0 or codes.max() >= limit):
+        raise MalformedCode(f"element code outside [0, {limit}) for {scheme.element.name}")
+    if not 0 <= stored_scale_code < (1 << scheme.scale.exponent_bits):
+        raise MalformedCode(f"scale code {stored_scale_code} outside {scheme.scale.name} range")
+    torch = _torch()
+    _native.require_cuda()
+    lib = _native.load()
+    n = codes.size
+    if n == 0:
+        return np.zeros(0)
+    dc = torch.from_numpy(codes.astype(np.uint8)).to("cuda")
+    sc = torch.tensor([stored_scale_code], dtype=torch.uint8, device="cuda")
+    pe = torch.empty(packed_nbytes(n, scheme.element.total_bits), dtype=torch.uint8, device="cuda")
+    ps = torch.empty(1, dtype=torch.uint8, device="cuda")
+    st = _stream()
+    _native.check(lib.mx_pack_codes(ctypes.c_void_p(dc.data_ptr()), n, scheme.element.total_bits,
+                                    ctypes.c_void_p(pe.data_ptr()), st), "mx_pack_codes")
+    _native.check(lib.mx_pack_codes(ctypes.c_void_p(sc.data_ptr()), 1,
+                                    scheme.scale.exponent_bits, ctypes.c_void_p(ps.data_ptr()), st),
+                  "mx_pack_codes")
+    # a single block of n <= B values decodes like an n-value tensor
+    dct = DeviceCompressedTensor(scheme, (n,), ps, pe)
+    return decompress_tensor_device(dct, torch.float64).cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# MXC1 container (mx/codec.py:287-380) -- host byte formatting
+# ---------------------------------------------------------------------------
+
+
+def header_nbytes(ndim: int) -> int:
+    return _HEADER.size + 8 * ndim
+
+
+def serialized_nbytes(scheme: SchemeDescriptor, shape) -> int:
+    n = _numel(tuple(shape))
+    nb = -(-n // scheme.block_size)
+    return (header_nbytes(len(shape)) + packed_nbytes(nb, scheme.scale.exponent_bits)
+            + packed_nbytes(n, scheme.element.total_bits))
+
+
+def pack_header(format_code: int, scale_code: int, block_field: int, shape) -> bytes:
+    shape = tuple(int(d) for d in shape)
+    return (_HEADER.pack(MAGIC, VERSION, format_code, scale_code, 0, block_field, len(shape), 0)
+            + struct.pack(f"<{len(shape)}Q", *shape))
+
+
+def unpack_header(data: bytes):
+    """-> (format_code, scale_code, block_field, shape, payload_offset)."""
+    if len(data) < _HEADER.size:
+        raise TruncatedStream(f"container of {len(data)} bytes has no full header")
+    magic, version, fcode, scode, flags, block, ndim, reserved = _HEADER.unpack_from(data)
+    if magic != MAGIC:
+        raise BadMagic(f"expected magic {MAGIC!r}, found {magic!r}")
+    if version != VERSION:
+        raise UnsupportedVersion(f"container version {version}, supported: {VERSION}")
+    if flags or reserved:
+        raise MalformedHeader("flags and reserved fields must be zero in version 1")
+    end = _HEADER.size + 8 * ndim
+    if len(data) < end:
+        raise TruncatedStream(f"header declares {ndim} dimensions but stream ends")
+    shape = tuple(int(d) for d in struct.unpack_from(f"<{ndim}Q", data, _HEADER.size))
+    return fcode, scode, block, shape, end
+
+
+def serialize(ct) -> bytes:
+    if isinstance(ct, DeviceCompressedTensor):
+        ct = ct.to_host()
+    header = pack_header(ELEMENT_CODES[ct.scheme.element.name], SCALE_CODES[ct.scheme.scale.name],
+                         ct.scheme.block_size, ct.shape)
+    return header + ct.scale_stream + ct.element_stream
+
+
+def deserialize(data: bytes) -> CompressedTensor:
+    fcode, scode, block, shape, off = unpack_header(data)
+    enames, snames = list(ELEMENT_FORMATS), list(SCALE_FORMATS)
+    if fcode >= len(enames):
+        raise MalformedHeader(f"format code {fcode:#x} is not a block-quantized payload")
+    if scode >= len(snames):
+        raise MalformedHeader(f"unknown scale format code {scode}")
+    if block < 1:
+        raise MalformedHeader("block size must be positive")
+    scheme = SchemeDescriptor(ELEMENT_FORMATS[enames[fcode]], block, SCALE_FORMATS[snames[scode]])
+    n = _numel(shape)
+    sb = packed_nbytes(-(-n // block), scheme.scale.exponent_bits)
+    eb = packed_nbytes(n, scheme.element.total_bits)
+    end = off + sb + eb
+    if len(data) < end:
+        raise TruncatedStream(f"payload needs {end - off} bytes, stream holds {len(data) - off}")
+    if len(data) > end:
+        raise MalformedHeader(f"{len(data) - end} trailing bytes after payload")
+    return CompressedTensor(scheme, shape, bytes(data[off:off + sb]), bytes(data[off + sb:end]))
+
+
+def block_error_bound(stored_scale_code: int, scheme: SchemeDescriptor) -> float:
+    """2^(stored-bias) * largest_gap / 2 for unclamped blocks (mx/codec.py:383-393)."""
+    if stored_scale_code == 0:
+        return 0.0
+    gap = enumerate_grid(scheme.element).largest_gap
+    return math.ldexp(gap / 2.0, stored_scale_code - scheme.scale.bias)

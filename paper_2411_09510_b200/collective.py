@@ -1,0 +1,359 @@
+"""Compressed tensor-parallel all-reduce over NCCL (NVLink 5 / NVSwitch).
+
+Replaces the reference's threaded full-mesh exchange ``netbench._worker_loop``
+(mx/netbench.py:307-339): every rank quantises its partial sum (its own
+contribution included, mx/netbench.py:323), the packed shards cross the TP
+group, and every rank decodes and sums all N contributions in fp32 in rank
+order from +0.0 (mx/netbench.py:332-334), so all ranks end bit-identical.
+
+Algorithms:
+
+* ``oneshot``: K1 quantise straight into this rank's slot of the gather
+  buffer -> in-place ``all_gather_into_tensor`` (N*S bytes) -> K2
+  dequant-sum over the N shards -> bf16.
+* ``twoshot``: K1 quantises N block-aligned chunks -> ``all_to_all_single``
+  (reduce-scatter leg, 2(N-1)/N*S on the wire in total) -> K3 decodes the N
+  shards of the owned chunk, sums in fp32, re-quantises -> in-place
+  ``all_gather_into_tensor`` -> K2 decodes every chunk.  Requantisation adds
+  at most ``block_error_bound`` per value (mx/codec.py:383-393).
+
+The codec arithmetic lives behind a *backend* object.  The product backend
+is :class:`NativeBackend` (the sm_100a kernels of libmxb200.so); the CPU
+tests plug the oracle in instead to check the orchestration with ``gloo``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+from . import _native
+from .errors import MinimumDegreeTwo, NonFiniteInput, ShapeMismatch
+from .formats import SchemeDescriptor, parse_scheme
+
+ALGOS = ("oneshot", "twoshot")
+
+
+def twoshot_chunk_values(n: int, nranks: int, block: int) -> int:
+    """Chunk length of the two-shot path: ceil(n/N) rounded up to a multiple
+    of 8*block so blocks never straddle chunks and every chunk's streams are
+    byte aligned (the oracle's twoshot_chunks rule)."""
+    unit = 8 * block
+    per = -(-n // nranks)
+    return max(unit, -(-per // unit) * unit)
+
+
+def chunk_len(n: int, c: int, j: int) -> int:
+    return max(0, min(c, n - j * c))
+
+
+# ---------------------------------------------------------------------------
+# backends
+# ---------------------------------------------------------------------------
+
+
+class NativeBackend:
+    """Codec steps on the sm_100a kernels (stream-ordered, no host sync)."""
+
+    def __init__(self, scheme: SchemeDescriptor):
+        self.scheme = scheme
+        self.cs = scheme.to_c()
+        self.lib = _native.load()
+
+    def layout(self, n: int):
+        return _native.shard_layout(n, self.cs)
+
+    def workspace(self, n: int, requant: bool = False) -> int:
+        return _native.workspace_bytes(n, self.cs, requant)
+
+    @staticmethod
+    def _p(t):
+        return ctypes.c_void_p(t.data_ptr())
+
+    @staticmethod
+    def _st():
+        import torch
+
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    @staticmethod
+    def _dt(t):
+        import torch
+
+        return {torch.float32: _native.MX_F32, torch.float16: _native.MX_F16,
+                torch.bfloat16: _native.MX_BF16}[t.dtype]
+
+    def quantize_into(self, x, shard, ws, flag):
+        so, eo, _ = self.layout(x.numel())
+        _native.check(self.lib.mx_quantize(
+            self._p(x), self._dt(x), x.numel(), ctypes.byref(self.cs),
+            ctypes.c_void_p(shard.data_ptr() + so), ctypes.c_void_p(shard.data_ptr() + eo),
+            self._p(flag) if flag is not None else None, self._p(ws), ws.numel(), self._st()),
+            "mx_quantize")
+
+    def quantize_chunks(self, x, c, shards, shard_stride, ws, flag):
+        _native.check(self.lib.mx_quantize_chunks(
+            self._p(x), self._dt(x), x.numel(), c, ctypes.byref(self.cs), self._p(shards),
+            shard_stride, self._p(flag) if flag is not None else None, self._p(ws), ws.numel(),
+            self._st()), "mx_quantize_chunks")
+
+    def dequant_sum(self, shards, rank_stride, nranks, n, c, chunk_stride, out):
+        _native.check(self.lib.mx_dequant_sum(
+            self._p(shards), rank_stride, nranks, n, c, chunk_stride, ctypes.byref(self.cs),
+            self._p(out), self._dt(out), self._st()), "mx_dequant_sum")
+
+    def requant(self, shards, rank_stride, nranks, n, c, out_shard, ws, flag):
+        _native.check(self.lib.mx_dequant_sum_requant(
+            self._p(shards), rank_stride, nranks, n, c, ctypes.byref(self.cs), self._p(out_shard),
+            self._p(flag) if flag is not None else None, self._p(ws), ws.numel(), self._st()),
+            "mx_dequant_sum_requant")
+
+    def reset_flag(self, flag):
+        _native.check(self.lib.mx_nonfinite_reset(self._p(flag), self._st()), "mx_nonfinite_reset")
+
+
+# ---------------------------------------------------------------------------
+# the collective
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class _Plan:
+    n: int
+    nranks: int
+    algo: str
+    shard_bytes: int  # one-shot: S(n); two-shot: S(c)
+    c: int            # two-shot chunk values (n for one-shot)
+
+
+class CompressedAllReduce:
+    """Persistent-buffer compressed all-reduce of an ``n``-value activation.
+
+    ``out = car(x)`` reduces the row-parallel partial ``x`` (bf16/f16/f32
+    CUDA tensor, any shape with ``n`` values) across ``group`` and returns
+    the sum in ``out_dtype``.  Buffers are allocated once, so the call is
+    CUDA-graph capturable (NCCL collectives capture).  Non-finite inputs are
+    recorded in a sticky device flag; :meth:`check_finite` raises
+    NonFiniteInput later (deferred, no sync on the hot path).
+    """
+
+    def __init__(self, scheme, n: int, group=None, algo: str = "oneshot", out_dtype=None,
+                 device=None, backend=None, world_size: int | None = None,
+                 rank: int | None = None):
+        import torch
+        import torch.distributed as dist
+
+        if isinstance(scheme, str):
+            scheme = parse_scheme(scheme, extensions=True)
+        if algo not in ALGOS:
+            raise ValueError(f"algo must be one of {ALGOS}")
+        self.scheme = scheme
+        self.group = group
+        self.world = world_size if world_size is not None else dist.get_world_size(group)
+        self.rank = rank if rank is not None else dist.get_rank(group)
+        if self.world < 1:
+            raise MinimumDegreeTwo("world size must be positive")
+        self.algo = algo
+        self.n = int(n)
+        self.out_dtype = out_dtype or torch.bfloat16
+        self.device = torch.device(device) if device is not None else (
+            torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
+            else torch.device("cpu"))
+        self.backend = backend or NativeBackend(scheme)
+        B = scheme.block_size
+        N = self.world
+        if algo == "oneshot":
+            c = self.n
+            _, _, S = self.backend.layout(self.n)
+            self.gathered = torch.empty(N * S, dtype=torch.uint8, device=self.device)
+            self.ws = torch.empty(self.backend.workspace(self.n), dtype=torch.uint8,
+                                  device=self.device)
+        else:
+            c = twoshot_chunk_values(self.n, N, B)
+            _, _, S = self.backend.layout(c)
+            self.send = torch.empty(N * S, dtype=torch.uint8, device=self.device)
+            self.recv = torch.empty(N * S, dtype=torch.uint8, device=self.device)
+            self.gathered = torch.empty(N * S, dtype=torch.uint8, device=self.device)
+            self.ws = torch.empty(max(self.backend.workspace(N * c),
+                                      self.backend.workspace(c, requant=True)),
+                                  dtype=torch.uint8, device=self.device)
+        self.plan = _Plan(self.n, N, algo, S, c)
+        self.flag = torch.empty(1, dtype=torch.int64, device=self.device)
+        self.backend.reset_flag(self.flag)
+        self.out = torch.empty(self.n, dtype=self.out_dtype, device=self.device)
+
+    # -- wire accounting ----------------------------------------------------
+    @property
+    def wire_bytes_per_rank(self) -> int:
+        """Bytes this rank sends (= receives) per call."""
+        N, S = self.plan.nranks, self.plan.shard_bytes
+        return (N - 1) * S if self.algo == "oneshot" else 2 * (N - 1) * S
+
+    def __call__(self, x, out=None):
+        import torch.distributed as dist
+
+        if x.numel() != self.n:
+            raise ShapeMismatch(f"expected {self.n} values, got {x.numel()}")
+        xf = x.reshape(-1)
+        out = self.out if out is None else out.reshape(-1)
+        p, be, N = self.plan, self.backend, self.plan.nranks
+        S = p.shard_bytes
+        if self.algo == "oneshot":
+            mine = self.gathered[self.rank * S:(self.rank + 1) * S]
+            be.quantize_into(xf, mine, self.ws, self.flag)
+            if N > 1:
+                dist.all_gather_into_tensor(self.gathered, mine, group=self.group)
+            be.dequant_sum(self.gathered, S, N, p.n, p.n, 0, out)
+        else:
+            be.quantize_chunks(xf, p.c, self.send, S, self.ws, self.flag)
+            if N > 1:
+                dist.all_to_all_single(self.recv, self.send, group=self.group)
+                recv = self.recv
+            else:
+                recv = self.send
+            mine = self.gathered[self.rank * S:(self.rank + 1) * S]
+            own = chunk_len(p.n, p.c, self.rank)
+            if own > 0:
+                be.requant(recv, S, N, own, p.c, mine, self.ws, self.flag)
+            if N > 1:
+                dist.all_gather_into_tensor(self.gathered, mine, group=self.group)
+            be.dequant_sum(self.gathered, 0, 1, p.n, p.c, S, out)
+        return out.view(x.shape) if out.numel() == x.numel() else out
+
+    def check_finite(self):
+        """Raise NonFiniteInput if any call since the last check saw NaN/Inf
+        (block index relative to the rank's partial, as _check_finite)."""
+        idx = int(self.flag.item())
+        if idx >= 0:
+            self.backend.reset_flag(self.flag)
+            blk = idx // self.scheme.block_size if self.algo == "oneshot" else None
+            raise NonFiniteInput(f"non-finite value in a compressed all-reduce input "
+                                 f"(flat index {idx})", block_index=blk)
+
+
+def compressed_all_reduce(x, scheme, group=None, algo: str = "oneshot", out_dtype=None):
+    """One-off convenience wrapper (allocates buffers per call)."""
+    car = CompressedAllReduce(scheme, x.numel(), group=group, algo=algo,
+                              out_dtype=out_dtype or x.dtype, device=x.device)
+    return car(x).clone()
+
+
+# ---------------------------------------------------------------------------
+# single-GPU simulation of N ranks (same kernels, exchange = buffer copies)
+# ---------------------------------------------------------------------------
+
+
+def simulate_allreduce(partials, scheme, algo: str = "oneshot", out_dtype=None, backend=None):
+    """All N rank partials live on one device; the NCCL exchange is replaced
+    by the equivalent buffer moves.  Returns the (identical) reduced tensor
+    every rank would hold.  Used for single-GPU parity tests and the N=1
+    bench workload ("simulated TP=2", BASELINE.json configs[0])."""
+    import torch
+
+    if isinstance(scheme, str):
+        scheme = parse_scheme(scheme, extensions=True)
+    N = len(partials)
+    n = partials[0].numel()
+    dev = partials[0].device
+    be = backend or NativeBackend(scheme)
+    out_dtype = out_dtype or torch.bfloat16
+    out = torch.empty(n, dtype=out_dtype, device=dev)
+    flag = torch.empty(1, dtype=torch.int64, device=dev)
+    be.reset_flag(flag)
+    if algo == "oneshot":
+        _, _, S = be.layout(n)
+        gathered = torch.empty(N * S, dtype=torch.uint8, device=dev)
+        ws = torch.empty(be.workspace(n), dtype=torch.uint8, device=dev)
+        for r, p in enumerate(partials):
+            be.quantize_into(p.reshape(-1), gathered[r * S:(r + 1) * S], ws, flag)
+        be.dequant_sum(gathered, S, N, n, n, 0, out)
+    else:
+        c = twoshot_chunk_values(n, N, scheme.block_size)
+        _, _, S = be.layout(c)
+        send = torch.empty(N, N * S, dtype=torch.uint8, device=dev)
+        ws = torch.empty(max(be.workspace(N * c), be.workspace(c, requant=True)),
+                         dtype=torch.uint8, device=dev)
+        for r, p in enumerate(partials):
+            be.quantize_chunks(p.reshape(-1), c, send[r], S, ws, flag)
+        # all-to-all: owner j receives chunk j of every rank, in rank order
+        recv = send.view(N, N, S).transpose(0, 1).contiguous().view(N, N * S)
+        gathered = torch.empty(N * S, dtype=torch.uint8, device=dev)
+        for j in range(N):
+            own = chunk_len(n, c, j)
+            if own > 0:
+                be.requant(recv[j], S, N, own, c, gathered[j * S:(j + 1) * S], ws, flag)
+        be.dequant_sum(gathered, 0, 1, n, c, S, out)
+    return out.view(partials[0].shape), flag
+
+
+# ---------------------------------------------------------------------------
+# the reference's wire duck type and analytic model (mx/netbench.py)
+# ---------------------------------------------------------------------------
+
+
+class BlockWire:
+    """``_BlockWire`` (mx/netbench.py:146-162) on the GPU codec: same
+    ``name`` / ``payload_nbytes`` / ``encode_with_reconstruction`` / ``decode``."""
+
+    def __init__(self, scheme: SchemeDescriptor, shape):
+        self.scheme = scheme
+        self.shape = tuple(shape)
+        self.name = scheme.name
+
+    def payload_nbytes(self) -> int:
+        from .codec import serialized_nbytes
+
+        return serialized_nbytes(self.scheme, self.shape)
+
+    def encode_with_reconstruction(self, arr):
+        import numpy as np
+
+        from .codec import compress_tensor_device, decompress_tensor_device, serialize
+
+        dct = compress_tensor_device(arr, self.scheme)
+        import torch
+
+        own = decompress_tensor_device(dct, torch.float32).cpu().numpy()
+        return serialize(dct), own.astype(np.float32, copy=False)
+
+    def decode(self, data: bytes):
+        import torch
+
+        from .codec import decompress_tensor_device, deserialize
+
+        return decompress_tensor_device(deserialize(data), torch.float32).cpu().numpy()
+
+
+@dataclass(frozen=True)
+class LinkModel:
+    """mx/netbench.py:57-72"""
+
+    bandwidth: float
+    latency: float = 0.0
+    compress_throughput: float = math.inf
+    decompress_throughput: float = math.inf
+
+    def __post_init__(self):
+        if not self.bandwidth > 0:
+            raise ValueError("bandwidth must be positive")
+        if self.latency < 0:
+            raise ValueError("latency cannot be negative")
+        if not (self.compress_throughput > 0 and self.decompress_throughput > 0):
+            raise ValueError("codec throughputs must be positive")
+
+
+def predict_comm_time(tensor_bytes: int, scheme, n_workers: int, link: LinkModel) -> float:
+    """Full-mesh model of mx/netbench.py:480-505 (one compress, N-1 decodes)."""
+    from .codec import serialized_nbytes
+
+    if n_workers < 2:
+        raise MinimumDegreeTwo(f"need at least 2 workers, got {n_workers}")
+    peers = n_workers - 1
+    base = peers * link.latency
+    if scheme is None:
+        return base + peers * tensor_bytes / link.bandwidth
+    values = tensor_bytes // 2
+    wire = serialized_nbytes(scheme, (values,))
+    return (base + peers * wire / link.bandwidth + values / link.compress_throughput
+            + peers * values / link.decompress_throughput)

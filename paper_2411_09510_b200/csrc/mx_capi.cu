@@ -1,0 +1,571 @@
+// Host side of libmxb200.so: scheme lowering, dispatch between the fast
+// sm_100a kernels (mx_kernels.cuh, one TU per dtype) and the generic
+// any-block-size kernels below, and the C ABI of include/mxb200.h.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <type_traits>
+
+#include "../../include/mxb200.h"
+#include "mx_kernels.cuh"
+
+namespace mxb {
+
+// ---------------------------------------------------------------------------
+// Generic path: any block size, any alignment, f64 input.  Three passes
+// through a one-byte-per-block workspace.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ double gen_load(const void* x, int64_t i) {
+  if constexpr (std::is_same<T, double>::value) return reinterpret_cast<const double*>(x)[i];
+  else return (double)InTraits<T>::to_f32(reinterpret_cast<const T*>(x)[i]);
+}
+
+// G1: one thread per block -> stored scale code in ws[global block]
+template <typename T>
+__global__ void g_scales(const void* x, int64_t n, int64_t cv, int64_t nbc, int64_t nb_total,
+                         uint8_t* ws, unsigned long long* nonfinite, Fmt f) {
+  int64_t gb = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gb >= nb_total) return;
+  int64_t chunk = gb / nbc, lb = gb % nbc;
+  int64_t cbase = chunk * cv;
+  int64_t len = min(cv, n - cbase);
+  int64_t i0 = lb * f.block, i1 = min(i0 + f.block, len);
+  uint64_t ab = 0;
+  bool bad = false;
+  for (int64_t i = i0; i < i1; ++i) {
+    double v = gen_load<T>(x, cbase + i);
+    uint64_t u = (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffull;
+    if (u >= 0x7ff0000000000000ull) {
+      if (!bad && nonfinite) atomicMin(nonfinite, (unsigned long long)(cbase + i));
+      bad = true;
+    }
+    ab = max(ab, u);
+  }
+  int stored = 0;
+  if (!bad && ab != 0) stored = shared_exp64(ab, f) + f.sbias;
+  ws[gb] = (uint8_t)stored;
+}
+
+// G2: one thread per 8-value group -> b bytes of the element stream
+template <typename T>
+__global__ void g_elems(const void* x, int64_t n, int64_t cv, int64_t gpc, int64_t ng_total,
+                        int64_t nbc, const uint8_t* ws, uint8_t* elem_base, int64_t chunk_stride,
+                        Fmt f) {
+  int64_t gg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gg >= ng_total) return;
+  int64_t chunk = gg / gpc, lg = gg % gpc;
+  int64_t cbase = chunk * cv;
+  int64_t len = min(cv, n - cbase);
+  int64_t i0 = lg * 8;
+  if (i0 >= len) return;
+  int valid = (int)min((int64_t)8, len - i0);
+  uint64_t w = 0;
+  for (int t = 0; t < valid; ++t) {
+    int64_t li = i0 + t;
+    int stored = ws[chunk * nbc + li / f.block];
+    if (stored == 0) continue;
+    int s = stored - f.sbias;
+    double v = gen_load<T>(x, cbase + li);
+    uint32_t code;
+    if constexpr (std::is_same<T, double>::value) {
+      // scale in f64 exactly, encode in f64
+      double xs = v * pow2d(-s);
+      code = encode_gen(xs, f);
+    } else {
+      float xs = (float)v * pow2f(-s);
+      code = encode_gen(xs, f);
+    }
+    w |= (uint64_t)code << (t * f.bits);
+  }
+  uint8_t* p = elem_base + chunk * chunk_stride + lg * f.bits;
+  int nbytes = (valid * f.bits + 7) / 8;
+  for (int i = 0; i < nbytes; ++i) p[i] = (uint8_t)(w >> (8 * i));
+}
+
+// G3: pack the workspace scale codes (k bits each)
+__global__ void g_pack_scales(const uint8_t* ws, int64_t n, int64_t cv, int64_t block,
+                               int64_t nbc, int64_t gpc8, int64_t ng_total, uint8_t* scale_base,
+                               int64_t chunk_stride, int k) {
+  int64_t gg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gg >= ng_total) return;
+  int64_t chunk = gg / gpc8, lg = gg % gpc8;
+  int64_t len = min(cv, n - chunk * cv);
+  int64_t nblocks = (len + block - 1) / block;
+  int64_t b0 = lg * 8;
+  if (b0 >= nblocks) return;
+  int cnt = (int)min((int64_t)8, nblocks - b0);
+  uint64_t w = 0;
+  for (int i = 0; i < cnt; ++i) w |= (uint64_t)ws[chunk * nbc + b0 + i] << (i * k);
+  uint8_t* p = scale_base + chunk * chunk_stride + lg * k;
+  int nbytes = (cnt * k + 7) / 8;
+  for (int i = 0; i < nbytes; ++i) p[i] = (uint8_t)(w >> (8 * i));
+}
+
+// G4: generic decode / rank-order sum, one thread per 8-value group
+template <typename OutT>
+__global__ void g_dqsum(DArgs A, int64_t gpc, int64_t ng_total) {
+  int64_t gg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gg >= ng_total) return;
+  int64_t chunk = gg / gpc, lg = gg % gpc;
+  int64_t cbase = chunk * A.cv;
+  int64_t len = min(A.cv, A.n - cbase);
+  int64_t i0 = lg * 8;
+  if (i0 >= len) return;
+  int valid = (int)min((int64_t)8, len - i0);
+  const Fmt& f = A.f;
+  const uint32_t mask = (1u << f.bits) - 1u;
+  OutT* out = reinterpret_cast<OutT*>(A.out) + cbase;
+  if constexpr (std::is_same<OutT, double>::value) {
+    const uint8_t* base = A.in + chunk * A.chunk_stride;
+    for (int t = 0; t < valid; ++t) {
+      int64_t li = i0 + t;
+      int stored = read_scale(base + A.scale_off, li / f.block, f.kbits);
+      uint64_t bit = (uint64_t)li * f.bits;
+      const uint8_t* e = base + A.elem_off + (bit >> 3);
+      int sh = (int)(bit & 7);
+      uint32_t wv = e[0];
+      if (sh + f.bits > 8) wv |= (uint32_t)e[1] << 8;
+      uint32_t code = (wv >> sh) & mask;
+      out[li] = decode_gen64(code, stored - f.sbias, stored == 0, f);
+    }
+  } else {
+    float acc[8];
+    for (int t = 0; t < 8; ++t) acc[t] = 0.f;
+    for (int rk = 0; rk < A.nranks; ++rk) {
+      const uint8_t* base = A.in + rk * A.rank_stride + chunk * A.chunk_stride;
+      for (int t = 0; t < valid; ++t) {
+        int64_t li = i0 + t;
+        int stored = read_scale(base + A.scale_off, li / f.block, f.kbits);
+        uint64_t bit = (uint64_t)li * f.bits;
+        const uint8_t* e = base + A.elem_off + (bit >> 3);
+        int sh = (int)(bit & 7);
+        uint32_t wv = e[0];
+        if (sh + f.bits > 8) wv |= (uint32_t)e[1] << 8;
+        uint32_t code = (wv >> sh) & mask;
+        float val = decode_gen(code, stored - f.sbias, stored == 0, f);
+        acc[t] = A.plain ? val : __fadd_rn(acc[t], val);
+      }
+    }
+    for (int t = 0; t < valid; ++t) out[i0 + t] = from_f32<OutT>(acc[t]);
+  }
+}
+
+__global__ void g_unpack(const uint8_t* packed, int64_t count, int width, uint8_t* codes) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  uint64_t bit = (uint64_t)i * width;
+  const uint8_t* e = packed + (bit >> 3);
+  int sh = (int)(bit & 7);
+  uint32_t w = e[0];
+  if (sh + width > 8) w |= (uint32_t)e[1] << 8;
+  codes[i] = (uint8_t)((w >> sh) & ((1u << width) - 1u));
+}
+
+__global__ void g_pack(const uint8_t* codes, int64_t count, int width, uint8_t* packed) {
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // 8-code group
+  int64_t i0 = g * 8;
+  if (i0 >= count) return;
+  int cnt = (int)min((int64_t)8, count - i0);
+  uint64_t w = 0;
+  for (int i = 0; i < cnt; ++i) w |= (uint64_t)(codes[i0 + i] & ((1u << width) - 1u)) << (i * width);
+  uint8_t* p = packed + g * width;
+  int nbytes = (cnt * width + 7) / 8;
+  for (int i = 0; i < nbytes; ++i) p[i] = (uint8_t)(w >> (8 * i));
+}
+
+__global__ void g_fill_u64(unsigned long long* p, unsigned long long v) { *p = v; }
+
+}  // namespace mxb
+
+// ===========================================================================
+// Host side
+// ===========================================================================
+namespace {
+
+using namespace mxb;
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(MX_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return MX_OK;
+}
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int64_t align16(int64_t v) { return (v + 15) & ~(int64_t)15; }
+
+int check_scheme(const mx_scheme_t* s) {
+  if (!s) return fail(MX_ERR_INVALID_ARGUMENT, "scheme is NULL");
+  if (s->kind != MX_KIND_FLOAT && s->kind != MX_KIND_INT)
+    return fail(MX_ERR_UNKNOWN_SCHEME, "unknown element kind %d", s->kind);
+  if (s->exponent_bits < 0 || s->mantissa_bits < 0)
+    return fail(MX_ERR_UNKNOWN_SCHEME, "bit counts must be non-negative");
+  if (s->kind == MX_KIND_FLOAT && s->exponent_bits < 1)
+    return fail(MX_ERR_UNKNOWN_SCHEME, "FloatMicro needs at least one exponent bit");
+  if (s->kind == MX_KIND_INT && (s->exponent_bits != 0 || s->mantissa_bits < 1))
+    return fail(MX_ERR_UNKNOWN_SCHEME, "IntSymmetric needs 0 exponent and >=1 magnitude bits");
+  int tb = 1 + s->exponent_bits + s->mantissa_bits;
+  if (tb < 2 || tb > 8)
+    return fail(MX_ERR_UNKNOWN_SCHEME, "total width %d outside the supported [2, 8] range", tb);
+  if (s->scale_bits < 4 || s->scale_bits > 8)
+    return fail(MX_ERR_UNKNOWN_SCHEME, "scale exponent width must be in [4, 8]");
+  if (s->block_size < 1) return fail(MX_ERR_UNKNOWN_SCHEME, "block size must be positive");
+  return MX_OK;
+}
+
+Fmt make_fmt(const mx_scheme_t* s) {
+  Fmt f;
+  memset(&f, 0, sizeof(f));
+  f.bits = 1 + s->exponent_bits + s->mantissa_bits;
+  f.kbits = s->scale_bits;
+  f.sbias = (1 << (s->scale_bits - 1)) - 1;
+  f.s_min = 1 - f.sbias;
+  f.s_max = (1 << s->scale_bits) - 1 - f.sbias;
+  f.block = (int)s->block_size;
+  f.y = s->mantissa_bits;
+  if (s->kind == MX_KIND_FLOAT) {
+    int bias = (1 << (s->exponent_bits - 1)) - 1;
+    f.lo = 1 - bias;
+    f.emax = (1 << s->exponent_bits) - 1 - bias;
+    // grid max (2^(y+1)-1) * 2^(emax-y); ratio to 2^emax = 2 - 2^-y
+    f.gmax64 = ldexp((double)((1 << (f.y + 1)) - 1), f.emax - f.y);
+    f.ovf32 = (1u << 23) - (1u << (23 - f.y));
+    f.ovf64 = (1ull << 52) - (1ull << (52 - f.y));
+  } else {
+    f.lo = f.y;
+    f.emax = f.y - 1;
+    f.gmax64 = (double)((1 << f.y) - 1);
+    // ratio (2^y-1)/2^(y-1) = 2 - 2^(1-y)
+    f.ovf32 = (1u << 23) - (1u << (24 - f.y));
+    f.ovf64 = (1ull << 52) - (1ull << (53 - f.y));
+  }
+  f.gmax = (float)f.gmax64;
+  return f;
+}
+
+int enc_of(const mx_scheme_t* s) {
+  if (s->kind == MX_KIND_FLOAT) {
+    if (s->exponent_bits == 2 && s->mantissa_bits == 1) return ENC_E2M1;
+    if (s->exponent_bits == 2 && s->mantissa_bits == 3) return ENC_E2M3;
+    if (s->exponent_bits == 3 && s->mantissa_bits == 2) return ENC_E3M2;
+  }
+  return ENC_GEN;
+}
+
+int lpb_of(int64_t block) {
+  switch (block) {
+    case 8: return 1;
+    case 16: return 2;
+    case 32: return 4;
+    case 64: return 8;
+    default: return 0;
+  }
+}
+
+bool aligned(const void* p, int a) { return ((uintptr_t)p % a) == 0; }
+
+int in_size(int dtype) {
+  switch (dtype) {
+    case MX_F32: return 4;
+    case MX_F16: return 2;
+    case MX_BF16: return 2;
+    case MX_F64: return 8;
+    default: return 0;
+  }
+}
+
+// ---- common quantise driver (plain and chunked) ----------------------------
+int quantize_impl(const void* x, int dtype, int64_t n, int64_t cv, const mx_scheme_t* s,
+                  uint8_t* scale_base, uint8_t* elem_base, int64_t chunk_stride,
+                  uint64_t* nonfinite, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (n < 0) return fail(MX_ERR_INVALID_ARGUMENT, "negative element count");
+  if (in_size(dtype) == 0) return fail(MX_ERR_INVALID_ARGUMENT, "unknown input dtype %d", dtype);
+  if (n == 0) return MX_OK;
+  if (!x || !scale_base || !elem_base) return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
+  Fmt f = make_fmt(s);
+  int64_t nchunks = cdiv(n, cv);
+  if (nchunks > 65535) return fail(MX_ERR_INVALID_ARGUMENT, "too many chunks (%lld)", (long long)nchunks);
+  int lpb = lpb_of(s->block_size);
+  int bits = f.bits;
+  int enc = enc_of(s);
+  bool fast = lpb != 0 && dtype != MX_F64 && aligned(x, 16) && aligned(elem_base, 8) &&
+              aligned(scale_base, 8) && (chunk_stride % 16 == 0 || nchunks == 1) &&
+              (nchunks == 1 || cv % 8 == 0);
+  unsigned long long* nf = reinterpret_cast<unsigned long long*>(nonfinite);
+  if (fast) {
+    QArgs a;
+    a.x = x; a.n = n; a.cv = cv;
+    a.tiles_per_chunk = (int)cdiv(cv, kTile);
+    a.scale_base = scale_base; a.elem_base = elem_base; a.chunk_stride = chunk_stride;
+    a.nonfinite = nf; a.f = f;
+    switch (dtype) {
+      case MX_BF16: launch_quant_bf16(a, nchunks, lpb, enc, bits, st); break;
+      case MX_F16: launch_quant_f16(a, nchunks, lpb, enc, bits, st); break;
+      default: launch_quant_f32(a, nchunks, lpb, enc, bits, st); break;
+    }
+    return cuda_check("k_quant");
+  }
+  // generic three-pass path
+  int64_t nbc = cdiv(cv, s->block_size);
+  int64_t nb_total = nbc * nchunks;
+  if (!ws || ws_bytes < nb_total)
+    return fail(MX_ERR_WORKSPACE, "generic path needs %lld workspace bytes", (long long)nb_total);
+  uint8_t* w = reinterpret_cast<uint8_t*>(ws);
+  const int T = 256;
+  switch (dtype) {
+    case MX_BF16: g_scales<__nv_bfloat16><<<cdiv(nb_total, T), T, 0, st>>>(x, n, cv, nbc, nb_total, w, nf, f); break;
+    case MX_F16: g_scales<__half><<<cdiv(nb_total, T), T, 0, st>>>(x, n, cv, nbc, nb_total, w, nf, f); break;
+    case MX_F32: g_scales<float><<<cdiv(nb_total, T), T, 0, st>>>(x, n, cv, nbc, nb_total, w, nf, f); break;
+    default: g_scales<double><<<cdiv(nb_total, T), T, 0, st>>>(x, n, cv, nbc, nb_total, w, nf, f); break;
+  }
+  int64_t gpc = cdiv(cv, 8);
+  int64_t ng_total = gpc * nchunks;
+  switch (dtype) {
+    case MX_BF16: g_elems<__nv_bfloat16><<<cdiv(ng_total, T), T, 0, st>>>(x, n, cv, gpc, ng_total, nbc, w, elem_base, chunk_stride, f); break;
+    case MX_F16: g_elems<__half><<<cdiv(ng_total, T), T, 0, st>>>(x, n, cv, gpc, ng_total, nbc, w, elem_base, chunk_stride, f); break;
+    case MX_F32: g_elems<float><<<cdiv(ng_total, T), T, 0, st>>>(x, n, cv, gpc, ng_total, nbc, w, elem_base, chunk_stride, f); break;
+    default: g_elems<double><<<cdiv(ng_total, T), T, 0, st>>>(x, n, cv, gpc, ng_total, nbc, w, elem_base, chunk_stride, f); break;
+  }
+  int64_t gpc8 = cdiv(nbc, 8);
+  int64_t ng8 = gpc8 * nchunks;
+  g_pack_scales<<<cdiv(ng8, T), T, 0, st>>>(w, n, cv, s->block_size, nbc, gpc8, ng8, scale_base,
+                                             chunk_stride, f.kbits);
+  return cuda_check("generic quantise");
+}
+
+int dqsum_impl(const uint8_t* in, int64_t rank_stride, int nranks, int64_t n, int64_t cv,
+               int64_t chunk_stride, const mx_scheme_t* s, void* out, int out_dtype, int plain,
+               cudaStream_t st) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (n < 0 || nranks < 1 || cv < 1)
+    return fail(MX_ERR_INVALID_ARGUMENT, "bad sizes (n=%lld, nranks=%d)", (long long)n, nranks);
+  if (n == 0) return MX_OK;
+  if (!in || !out) return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (out_dtype == MX_F64 && !(plain && nranks == 1))
+    return fail(MX_ERR_INVALID_ARGUMENT, "float64 output is only for plain decompression");
+  Fmt f = make_fmt(s);
+  int64_t sb = (cdiv(cv, s->block_size) * s->scale_bits + 7) / 8;
+  DArgs a;
+  a.in = in; a.rank_stride = rank_stride; a.nranks = nranks; a.chunk_stride = chunk_stride;
+  a.scale_off = 0; a.elem_off = align16(sb);
+  a.n = n; a.cv = cv; a.out = out; a.plain = plain; a.f = f;
+  int64_t nchunks = cdiv(n, cv);
+  if (nchunks > 65535) return fail(MX_ERR_INVALID_ARGUMENT, "too many chunks");
+  int lpb = lpb_of(s->block_size);
+  bool fast = lpb != 0 && out_dtype != MX_F64 && aligned(out, 16) && aligned(in, 8) &&
+              rank_stride % 8 == 0 && chunk_stride % 8 == 0 && (nchunks == 1 || cv % 8 == 0);
+  if (fast) {
+    a.tiles_per_chunk = (int)cdiv(cv, kTile);
+    int enc = enc_of(s);
+    switch (out_dtype) {
+      case MX_BF16: launch_dqsum_bf16(a, nchunks, lpb, enc, f.bits, st); break;
+      case MX_F16: launch_dqsum_f16(a, nchunks, lpb, enc, f.bits, st); break;
+      case MX_F32: launch_dqsum_f32(a, nchunks, lpb, enc, f.bits, st); break;
+      default: return fail(MX_ERR_INVALID_ARGUMENT, "unknown output dtype %d", out_dtype);
+    }
+    return cuda_check("k_dqsum");
+  }
+  int64_t gpc = cdiv(cv, 8);
+  int64_t ng = gpc * nchunks;
+  const int T = 256;
+  switch (out_dtype) {
+    case MX_BF16: g_dqsum<__nv_bfloat16><<<cdiv(ng, T), T, 0, st>>>(a, gpc, ng); break;
+    case MX_F16: g_dqsum<__half><<<cdiv(ng, T), T, 0, st>>>(a, gpc, ng); break;
+    case MX_F32: g_dqsum<float><<<cdiv(ng, T), T, 0, st>>>(a, gpc, ng); break;
+    case MX_F64: g_dqsum<double><<<cdiv(ng, T), T, 0, st>>>(a, gpc, ng); break;
+    default: return fail(MX_ERR_INVALID_ARGUMENT, "unknown output dtype %d", out_dtype);
+  }
+  return cuda_check("generic dequant-sum");
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int mx_abi_version(void) { return MXB200_ABI_VERSION; }
+
+const char* mx_last_error(void) { return g_err; }
+
+int mx_scheme_check(const mx_scheme_t* scheme) { return check_scheme(scheme); }
+
+int mx_stream_nbytes(int64_t n, const mx_scheme_t* s, int64_t* scale_bytes, int64_t* element_bytes) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (n < 0) return fail(MX_ERR_INVALID_ARGUMENT, "negative element count");
+  int64_t nb = cdiv(n, s->block_size);
+  if (scale_bytes) *scale_bytes = (nb * s->scale_bits + 7) / 8;
+  if (element_bytes) *element_bytes = (n * (1 + s->exponent_bits + s->mantissa_bits) + 7) / 8;
+  return MX_OK;
+}
+
+int mx_shard_layout(int64_t n, const mx_scheme_t* s, int64_t* scale_offset, int64_t* element_offset,
+                    int64_t* shard_bytes) {
+  int64_t sb, eb;
+  int rc = mx_stream_nbytes(n, s, &sb, &eb);
+  if (rc) return rc;
+  if (scale_offset) *scale_offset = 0;
+  if (element_offset) *element_offset = align16(sb);
+  if (shard_bytes) *shard_bytes = align16(align16(sb) + eb);
+  return MX_OK;
+}
+
+int mx_workspace_bytes(int64_t n, const mx_scheme_t* s, int64_t* bytes) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (!bytes || n < 0) return fail(MX_ERR_INVALID_ARGUMENT, "bad arguments");
+  // generic quantise: one byte per block
+  *bytes = cdiv(n, s->block_size) + 64;
+  return MX_OK;
+}
+
+int mx_requant_workspace_bytes(int64_t n, const mx_scheme_t* s, int64_t* bytes) {
+  int rc = mx_workspace_bytes(n, s, bytes);
+  if (rc) return rc;
+  // generic requant: an fp32 sum buffer (16-byte aligned) in front of it
+  *bytes += align16(4 * n) + 16;
+  return MX_OK;
+}
+
+int mx_quantize(const void* x, int32_t dtype, int64_t n, const mx_scheme_t* s, uint8_t* scale_stream,
+                uint8_t* element_stream, uint64_t* nonfinite, void* workspace,
+                int64_t workspace_bytes, void* stream) {
+  return quantize_impl(x, dtype, n, n > 0 ? n : 1, s, scale_stream, element_stream, 0, nonfinite,
+                       workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int mx_quantize_chunks(const void* x, int32_t dtype, int64_t n, int64_t chunk_values,
+                       const mx_scheme_t* s, uint8_t* shards, int64_t shard_stride,
+                       uint64_t* nonfinite, void* workspace, int64_t workspace_bytes, void* stream) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (chunk_values < 1 || chunk_values % (8 * s->block_size) != 0)
+    return fail(MX_ERR_INVALID_ARGUMENT, "chunk_values must be a positive multiple of 8*block");
+  int64_t so, eo, sbytes;
+  mx_shard_layout(chunk_values, s, &so, &eo, &sbytes);
+  if (shard_stride < sbytes) return fail(MX_ERR_INVALID_ARGUMENT, "shard_stride smaller than a shard");
+  return quantize_impl(x, dtype, n, chunk_values, s, shards + so, shards + eo, shard_stride,
+                       nonfinite, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int mx_dequantize(const uint8_t* scale_stream, const uint8_t* element_stream, int64_t n,
+                  const mx_scheme_t* s, void* out, int32_t out_dtype, void* stream) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (n == 0) return MX_OK;
+  if (!scale_stream || !element_stream) return fail(MX_ERR_INVALID_ARGUMENT, "NULL stream");
+  // the two streams are addressed as one "shard": base = scale stream,
+  // element offset = distance to the element stream
+  int64_t off = (int64_t)(element_stream - scale_stream);
+  // generic single-shard decode honours arbitrary offsets; the fast kernels
+  // need the element stream 16-aligned relative to the scale stream
+  int lpb = lpb_of(s->block_size);
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t nb = cdiv(n, s->block_size);
+  int64_t sb = (nb * s->scale_bits + 7) / 8;
+  bool fast_layout = off == align16(sb);
+  if (lpb != 0 && fast_layout && out_dtype != MX_F64)
+    return dqsum_impl(scale_stream, 0, 1, n, n, 0, s, out, out_dtype, 1, st);
+  DArgs a;
+  a.in = scale_stream; a.rank_stride = 0; a.nranks = 1; a.chunk_stride = 0;
+  a.scale_off = 0; a.elem_off = off; a.n = n; a.cv = n; a.out = out; a.plain = 1;
+  a.f = make_fmt(s); a.tiles_per_chunk = 0;
+  int64_t gpc = cdiv(n, 8);
+  const int T = 256;
+  switch (out_dtype) {
+    case MX_BF16: g_dqsum<__nv_bfloat16><<<cdiv(gpc, T), T, 0, st>>>(a, gpc, gpc); break;
+    case MX_F16: g_dqsum<__half><<<cdiv(gpc, T), T, 0, st>>>(a, gpc, gpc); break;
+    case MX_F32: g_dqsum<float><<<cdiv(gpc, T), T, 0, st>>>(a, gpc, gpc); break;
+    case MX_F64: g_dqsum<double><<<cdiv(gpc, T), T, 0, st>>>(a, gpc, gpc); break;
+    default: return fail(MX_ERR_INVALID_ARGUMENT, "unknown output dtype %d", out_dtype);
+  }
+  return cuda_check("generic dequantise");
+}
+
+int mx_dequant_sum(const uint8_t* shards, int64_t rank_stride, int32_t nranks, int64_t n,
+                   int64_t chunk_values, int64_t chunk_stride, const mx_scheme_t* s, void* out,
+                   int32_t out_dtype, void* stream) {
+  if (out_dtype == MX_F64) return fail(MX_ERR_INVALID_ARGUMENT, "sums are fp32 (mx/netbench.py:332)");
+  return dqsum_impl(shards, rank_stride, nranks, n, chunk_values, chunk_stride, s, out, out_dtype,
+                    0, (cudaStream_t)stream);
+}
+
+int mx_dequant_sum_requant(const uint8_t* shards, int64_t rank_stride, int32_t nranks, int64_t n,
+                           int64_t chunk_values, const mx_scheme_t* s, uint8_t* out_shard,
+                           uint64_t* nonfinite, void* workspace, int64_t workspace_bytes,
+                           void* stream) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (n < 0 || nranks < 1 || chunk_values < n) return fail(MX_ERR_INVALID_ARGUMENT, "bad sizes");
+  if (n == 0) return MX_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t so, eo, sbytes;
+  mx_shard_layout(chunk_values, s, &so, &eo, &sbytes);
+  int lpb = lpb_of(s->block_size);
+  Fmt f = make_fmt(s);
+  if (lpb != 0 && aligned(shards, 8) && rank_stride % 8 == 0 && aligned(out_shard, 8)) {
+    RArgs a;
+    a.in = shards; a.rank_stride = rank_stride; a.nranks = nranks;
+    a.scale_off = so; a.elem_off = eo; a.n = n;
+    a.out_scale = out_shard + so; a.out_elem = out_shard + eo;
+    a.nonfinite = reinterpret_cast<unsigned long long*>(nonfinite); a.f = f;
+    launch_requant(a, lpb, enc_of(s), f.bits, st);
+    return cuda_check("k_requant");
+  }
+  // generic: fp32 sum into the workspace, then the generic quantiser
+  int64_t need;
+  mx_requant_workspace_bytes(n, s, &need);
+  if (!workspace || workspace_bytes < need)
+    return fail(MX_ERR_WORKSPACE, "generic requant needs %lld workspace bytes", (long long)need);
+  uint8_t* w = reinterpret_cast<uint8_t*>(workspace);
+  uintptr_t p = ((uintptr_t)w + 15) & ~(uintptr_t)15;
+  float* sum = reinterpret_cast<float*>(p);
+  uint8_t* rest = reinterpret_cast<uint8_t*>(p + align16(4 * n));
+  int64_t rest_bytes = workspace_bytes - (int64_t)((uint8_t*)rest - w);
+  rc = dqsum_impl(shards, rank_stride, nranks, n, chunk_values, 0, s, sum, MX_F32, 0, st);
+  if (rc) return rc;
+  return quantize_impl(sum, MX_F32, n, n, s, out_shard + so, out_shard + eo, 0, nonfinite, rest,
+                       rest_bytes, st);
+}
+
+int mx_unpack_codes(const uint8_t* packed, int64_t count, int32_t width, uint8_t* codes, void* stream) {
+  if (width < 1 || width > 8) return fail(MX_ERR_INVALID_ARGUMENT, "width %d outside [1, 8]", width);
+  if (count <= 0) return MX_OK;
+  g_unpack<<<cdiv(count, 256), 256, 0, (cudaStream_t)stream>>>(packed, count, width, codes);
+  return cuda_check("g_unpack");
+}
+
+int mx_pack_codes(const uint8_t* codes, int64_t count, int32_t width, uint8_t* packed, void* stream) {
+  if (width < 1 || width > 8) return fail(MX_ERR_INVALID_ARGUMENT, "width %d outside [1, 8]", width);
+  if (count <= 0) return MX_OK;
+  int64_t groups = cdiv(count, 8);
+  g_pack<<<cdiv(groups, 256), 256, 0, (cudaStream_t)stream>>>(codes, count, width, packed);
+  return cuda_check("g_pack");
+}
+
+int mx_nonfinite_reset(uint64_t* nonfinite, void* stream) {
+  if (!nonfinite) return fail(MX_ERR_INVALID_ARGUMENT, "NULL flag");
+  g_fill_u64<<<1, 1, 0, (cudaStream_t)stream>>>(reinterpret_cast<unsigned long long*>(nonfinite),
+                                                ~0ull);
+  return cuda_check("mx_nonfinite_reset");
+}
+
+}  // extern "C"

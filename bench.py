@@ -1,0 +1,492 @@
+#!/usr/bin/env python
+"""Benchmark of the compressed TP all-reduce (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One *step* = one compressed all-reduce of the Llama-3.1-8B prefill
+row-parallel partial sum [2048 x 4096] bf16 (MXFP4 block 32, E8M0 scales,
+one-shot): quantise (K1) -> exchange -> unpack/dequantise/fp32 rank-order
+sum -> bf16 (K2).
+
+* N = 1 (default): BASELINE.json configs[0] on one B200 -- "simulated TP=2":
+  two rank partials are quantised into the gathered buffer exactly as the
+  NCCL all-gather would leave it, then K2 reduces both shards.
+* N > 1 (torchrun, one rank per GPU): real TP=N over NCCL (NVLink 5), one
+  partial per GPU (weak scaling), plus the uncompressed bf16 NCCL
+  all-reduce on the same tensor for the speed-up.
+
+``value`` = bf16 bytes of partial sums reduced per second over the whole
+job (ranks x 2n bytes / step time), device-timed with CUDA events over
+exactly K CUDA-graph replays, inputs resident in HBM and rotated over buffer
+sets larger than L2.  ``e2e`` is the same metric through the public API with
+pinned host buffers (H2D of the partials and D2H of the result inside the
+timed region).  ``roofline`` is the dominant kernel (K1) against the
+measured HBM copy bandwidth.  ``cpu_baseline`` is the CPU oracle (a numpy
+restatement of the reference codec; the reference itself is Python and does
+not travel to the GPU box) on the box's host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "GB/s"
+L2_BYTES = 126 * 2 ** 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scheme", default="fp4_e2m1:32:e8m0")
+    ap.add_argument("--algo", choices=["oneshot", "twoshot"], default="oneshot")
+    ap.add_argument("--shape", default="2048,4096")
+    ap.add_argument("--sim-ranks", type=int, default=2, help="simulated TP degree at N=1")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="ncu mode: a few eager launches, no timing, no JSON")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# ---------------------------------------------------------------------------
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm), "samples_loaded": len(loaded)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baselines (the oracle restatement of the reference codec)
+# ---------------------------------------------------------------------------
+
+
+def cpu_oracle_step(partials64, spec, threads):
+    """One simulated-TP compress+reduce cycle of the reference semantics
+    (mx/netbench.py:323-334) on host cores, blocks split over threads."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import mx_oracle as O
+
+    sch = O.scheme(spec)
+    n = partials64[0].size
+    unit = 8 * sch.block
+    per = -(-n // threads)
+    per = -(-per // unit) * unit
+    sls = [slice(i * per, min(n, (i + 1) * per)) for i in range(threads) if i * per < n]
+
+    def work(sl):
+        return O.allreduce_oneshot([p.reshape(-1)[sl] for p in partials64], sch)
+
+    if threads == 1:
+        return work(slice(0, n))
+    with ThreadPoolExecutor(threads) as ex:
+        return np.concatenate(list(ex.map(work, sls)))
+
+
+def cpu_baseline(spec, shape, nranks, budget_s=10.0):
+    from paper_2411_09510_b200.synth import rank_partials
+
+    threads = os.cpu_count() or 1
+    parts = [p.astype(np.float64) for p in rank_partials(shape, nranks, seed=0)]
+    n = parts[0].size
+    times = []
+    t_all = time.perf_counter()
+    while True:
+        t = time.perf_counter()
+        cpu_oracle_step(parts, spec, threads)
+        times.append(time.perf_counter() - t)
+        if len(times) >= 2 and time.perf_counter() - t_all > budget_s:
+            break
+    med = statistics.median(times)
+    return {"value": round(nranks * 2 * n / med / 1e9, 4), "unit": UNIT, "cores": threads,
+            "kind": "port",
+            "sample": f"{len(times)} full steps of simulated TP={nranks} on {list(shape)} "
+                      f"({spec}); median {med * 1e3:.1f} ms/step; oracle/mx_oracle.py "
+                      f"(numpy restatement of mx/codec.py + mx/netbench.py:332-334), "
+                      f"blocks split over {threads} threads"}
+
+
+def run_reference(args, shape, rank, world):
+    """--impl reference: the CPU reference path (oracle port) on host cores,
+    rank 0 only; each step a bounded row-sample of the same workload."""
+    if rank != 0:
+        return
+    from paper_2411_09510_b200.synth import rank_partials
+
+    T, H = shape
+    nranks = args.sim_ranks if world == 1 else world
+    threads = os.cpu_count() or 1
+    # calibrate: seconds per row for the full cycle
+    cal_rows = 64
+    cal = [p.astype(np.float64) for p in rank_partials((cal_rows, H), nranks, seed=0)]
+    t = time.perf_counter()
+    cpu_oracle_step(cal, args.scheme, threads)
+    per_row = (time.perf_counter() - t) / cal_rows
+    budget = 120.0
+    rows = int(max(8, min(T, budget / max(1, args.steps + args.warmup) / max(per_row, 1e-9))))
+    rows = max(8, (rows // 8) * 8)
+    parts = [p.astype(np.float64) for p in rank_partials((rows, H), nranks, seed=0)]
+    for _ in range(args.warmup):
+        cpu_oracle_step(parts, args.scheme, threads)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_oracle_step(parts, args.scheme, threads)
+    el = time.perf_counter() - t
+    ms = el / args.steps * 1e3
+    value = nranks * 2 * rows * H / (el / args.steps) / 1e9
+    sample = (f"{rows} of {T} rows x {H} per step, {nranks} rank partials, {args.scheme}; "
+              f"oracle/mx_oracle.py (numpy restatement of the reference codec) on "
+              f"{threads} host threads")
+    line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (gaussian_with_outliers, mx/synth.py)",
+            "impl": "reference",
+            "config": config_dict(args, shape, world),
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, shape, world):
+    sim = world == 1
+    return {"workload": (f"Llama-3.1-8B prefill row-parallel all-reduce [{shape[0]}x{shape[1]}] "
+                         f"bf16, {args.scheme}, {args.algo}, "
+                         + (f"simulated TP={args.sim_ranks} on 1 GPU (BASELINE configs[0])"
+                            if sim else f"TP={world} over NCCL (BASELINE configs[1])")),
+            "scheme": args.scheme, "algo": args.algo, "tp": args.sim_ranks if sim else world,
+            "ranks_per_gpu": args.sim_ranks if sim else 1, "seq_len": shape[0],
+            "hidden": shape[1],
+            "l2": "inputs rotated over buffer sets totalling > 126 MB L2"}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+
+def time_graph_replays(torch, graphs, k):
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for i in range(k):
+        graphs[i % len(graphs)].replay()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)  # ms
+
+
+def capture(torch, fn):
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()  # warm (first-call allocations happen outside the graph)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        fn()
+    torch.cuda.synchronize()
+    return g
+
+
+def load_traffic(kernel_key):
+    """dram bytes per launch from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(path)).get(kernel_key)
+    except Exception:
+        return None
+
+
+def run_ours(args, shape, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_09510_b200 import _native
+    from paper_2411_09510_b200.collective import CompressedAllReduce, SimulatedAllReduce
+    from paper_2411_09510_b200.formats import parse_scheme
+    from paper_2411_09510_b200.synth import rank_partials
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    _native.load()
+    sch = parse_scheme(args.scheme, extensions=True)
+    T, H = shape
+    n = T * H
+    sim = world == 1
+    nranks = args.sim_ranks if sim else world
+    so, eo, S = _native.shard_layout(n, sch.to_c())
+    sb, eb = _native.stream_nbytes(n, sch.to_c())
+    # buffer sets: enough that one pass over them exceeds L2
+    per_set = (nranks if sim else 1) * 2 * n + (nranks * S) + 2 * n
+    R = max(2, -(-2 * L2_BYTES // per_set))
+    host_parts = rank_partials(shape, nranks, seed=0)
+    sets = []
+    for s in range(R):
+        if sim:
+            parts = [torch.from_numpy(host_parts[r]).to(dev, torch.bfloat16) for r in range(nranks)]
+            if s:  # distinct data per set (sign flip + permutation of rows keeps statistics)
+                parts = [p.roll(s * 7, 0) * (-1) ** s for p in parts]
+            op = SimulatedAllReduce(sch, n, nranks, args.algo, torch.bfloat16, dev)
+            sets.append((parts, op))
+        else:
+            x = torch.from_numpy(host_parts[rank]).to(dev, torch.bfloat16)
+            if s:
+                x = x.roll(s * 7, 0) * (-1) ** s
+            op = CompressedAllReduce(sch, n, algo=args.algo, out_dtype=torch.bfloat16, device=dev)
+            sets.append(([x], op))
+
+    def step_fn(i):
+        parts, op = sets[i]
+        return (lambda: op(parts)) if sim else (lambda: op(parts[0]))
+
+    if args.profile:  # ncu: eager launches only
+        for i in range(3):
+            step_fn(i % R)()
+        torch.cuda.synchronize()
+        return
+
+    graphs = [capture(torch, step_fn(i)) for i in range(R)]
+    launches_per_step = (nranks if sim else 1) + 1 if args.algo == "oneshot" else None
+    if launches_per_step is None:  # two-shot: K1 x ranks, K3 x owned chunks, K2
+        launches_per_step = (nranks if sim else 1) + (nranks if sim else 1) + 1
+
+    # warm-up (>= W replays and >= 0.3 s so clocks settle), timed region
+    with ClockSampler(local_rank) as clk:
+        t = time.perf_counter()
+        i = 0
+        while i < args.warmup or time.perf_counter() - t < 0.3:
+            graphs[i % R].replay()
+            i += 1
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ms_total = time_graph_replays(torch, graphs, args.steps)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+    clocks = clk.summary()
+    ms_local = ms_total / args.steps
+    ms_step = ms_local
+    if world > 1:
+        tt = torch.tensor([ms_local], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_step = float(tt.item())
+    value = nranks * 2 * n / (ms_step * 1e-3) / 1e9
+
+    # ---- per-kernel device times (roofline), graphs of back-to-back launches
+    kernels = {}
+    M = 8
+    if sim and args.algo == "oneshot":
+        def q_only(i):
+            parts, op = sets[i]
+            return lambda: [op.be.quantize_into(parts[0].reshape(-1),
+                                                op.gathered[0:S], op.ws, op.flag)
+                            for _ in range(M)]
+
+        def d_only(i):
+            parts, op = sets[i]
+            return lambda: [op.reduce() for _ in range(M)]
+
+        for name, mk, bytes_per in (("k_quant", q_only, 2 * n + sb + eb),
+                                    ("k_dqsum", d_only, nranks * (sb + eb) + 2 * n)):
+            gs = [capture(torch, mk(i)) for i in range(R)]
+            for i in range(2 * R):
+                gs[i % R].replay()
+            reps = max(8, min(400, args.steps // 4))
+            ms = time_graph_replays(torch, gs, reps) / (reps * M)
+            kernels[name] = {"us": round(ms * 1e3, 3), "bytes": bytes_per,
+                             "gbs": round(bytes_per / (ms * 1e-3) / 1e9, 1)}
+    peak, peak_kind = peaks()
+    roof = None
+    if "k_quant" in kernels:
+        # dominant kernel: K1 runs nranks times per step
+        kq = kernels["k_quant"]
+        ach = kq["gbs"]
+        traffic = load_traffic(f"k_quant|{args.scheme}|{T}x{H}|bf16")
+        roof = {"bound": "hbm", "kernel": "k_quant<bf16,LPB4,E2M1> (K1 quantise+pack)",
+                "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": traffic,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",
+                "algorithmic_bytes_per_launch": kq["bytes"],
+                "launch_us": kq["us"],
+                "share_of_step": round(nranks * kq["us"] / (ms_step * 1e3), 3),
+                "other_kernels": {k: v for k, v in kernels.items() if k != "k_quant"}}
+
+    # ---- end to end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_in = [torch.from_numpy(host_parts[r if sim else rank]).to(torch.bfloat16).pin_memory()
+                   for r in (range(nranks) if sim else [0])]
+        host_out = torch.empty(n, dtype=torch.bfloat16).pin_memory()
+        parts, op = sets[0]
+        ke = max(3, min(args.steps, 100))
+
+        def e2e_step():
+            for d, h in zip(parts, host_in):
+                d.reshape(-1).copy_(h.reshape(-1), non_blocking=True)
+            out = op(parts) if sim else op(parts[0])
+            host_out.copy_(out.reshape(-1), non_blocking=True)
+
+        for _ in range(3):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(ke):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms_e = e0.elapsed_time(e1) / ke
+        if world > 1:
+            tt = torch.tensor([ms_e], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms_e = float(tt.item())
+        e2e = {"value": round(nranks * 2 * n / (ms_e * 1e-3) / 1e9, 3), "unit": UNIT,
+               "h2d_bytes_per_step": sum(h.numel() * 2 for h in host_in),
+               "d2h_bytes_per_step": n * 2, "ms_per_step": round(ms_e, 4), "steps": ke,
+               "api": "SimulatedAllReduce.__call__" if sim else "CompressedAllReduce.__call__"}
+
+    # ---- uncompressed bf16 NCCL all-reduce on the same tensor (N>1)
+    bf16_ar = None
+    if world > 1:
+        xs = [s_[0][0].clone() for s_ in sets]
+        gsb = [capture(torch, (lambda x=x: dist.all_reduce(x))) for x in xs]
+        for i in range(args.warmup):
+            gsb[i % R].replay()
+        dist.barrier()
+        ms_b = time_graph_replays(torch, gsb, args.steps) / args.steps
+        tt = torch.tensor([ms_b], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_b = float(tt.item())
+        bf16_ar = {"us": round(ms_b * 1e3, 2), "value": round(world * 2 * n / (ms_b * 1e-3) / 1e9, 2),
+                   "unit": UNIT, "speedup_of_compressed": round(ms_b / ms_step, 3)}
+
+    if rank != 0:
+        return
+    cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(args.scheme, shape, nranks)
+    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+            "us_per_allreduce": round(ms_step * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (gaussian_with_outliers N(0,1) with 1% x100 outliers, "
+                    "mx/synth.py), bf16 partial sums",
+            "config": config_dict(args, shape, world),
+            "wire_bytes_per_rank": (nranks - 1) * S if args.algo == "oneshot" else None,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
+            "bf16_nccl_allreduce": bf16_ar}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    shape = tuple(int(v) for v in args.shape.split(","))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, shape, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, shape, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -22,7 +22,7 @@
  *    zero-padded only at their end (mx/bitpack.py:3-7, mx/codec.py:27-43).
  *    Byte-identical to the reference's CompressedTensor streams.
  *  - Shard ("wire message") layout used by the collectives:
- *      [scale stream | pad to 16 B | element stream | pad to 16 B]
+ *      [scale stream | pad to 32 B | element stream | pad to 32 B]
  *    see mx_shard_layout().
  */
 #ifndef MXB200_H

@@ -244,47 +244,93 @@ def compressed_all_reduce(x, scheme, group=None, algo: str = "oneshot", out_dtyp
 # ---------------------------------------------------------------------------
 
 
-def simulate_allreduce(partials, scheme, algo: str = "oneshot", out_dtype=None, backend=None):
-    """All N rank partials live on one device; the NCCL exchange is replaced
-    by the equivalent buffer moves.  Returns the (identical) reduced tensor
-    every rank would hold.  Used for single-GPU parity tests and the N=1
-    bench workload ("simulated TP=2", BASELINE.json configs[0])."""
-    import torch
+class SimulatedAllReduce:
+    """N TP ranks on ONE device: the same K1/K2/K3 kernels as
+    :class:`CompressedAllReduce`, with the NCCL exchange replaced by the
+    equivalent buffer placement (one-shot: every rank quantises straight into
+    its slot of the gathered buffer; two-shot: the all-to-all is a strided
+    copy).  Persistent buffers, so a call is CUDA-graph capturable.  This is
+    the single-GPU parity harness and the N=1 bench workload ("simulated
+    TP=2", BASELINE.json configs[0])."""
 
-    if isinstance(scheme, str):
-        scheme = parse_scheme(scheme, extensions=True)
-    N = len(partials)
-    n = partials[0].numel()
-    dev = partials[0].device
-    be = backend or NativeBackend(scheme)
-    out_dtype = out_dtype or torch.bfloat16
-    out = torch.empty(n, dtype=out_dtype, device=dev)
-    flag = torch.empty(1, dtype=torch.int64, device=dev)
-    be.reset_flag(flag)
-    if algo == "oneshot":
-        _, _, S = be.layout(n)
-        gathered = torch.empty(N * S, dtype=torch.uint8, device=dev)
-        ws = torch.empty(be.workspace(n), dtype=torch.uint8, device=dev)
-        for r, p in enumerate(partials):
-            be.quantize_into(p.reshape(-1), gathered[r * S:(r + 1) * S], ws, flag)
-        be.dequant_sum(gathered, S, N, n, n, 0, out)
-    else:
-        c = twoshot_chunk_values(n, N, scheme.block_size)
-        _, _, S = be.layout(c)
-        send = torch.empty(N, N * S, dtype=torch.uint8, device=dev)
-        ws = torch.empty(max(be.workspace(N * c), be.workspace(c, requant=True)),
-                         dtype=torch.uint8, device=dev)
-        for r, p in enumerate(partials):
-            be.quantize_chunks(p.reshape(-1), c, send[r], S, ws, flag)
-        # all-to-all: owner j receives chunk j of every rank, in rank order
-        recv = send.view(N, N, S).transpose(0, 1).contiguous().view(N, N * S)
-        gathered = torch.empty(N * S, dtype=torch.uint8, device=dev)
-        for j in range(N):
-            own = chunk_len(n, c, j)
-            if own > 0:
-                be.requant(recv[j], S, N, own, c, gathered[j * S:(j + 1) * S], ws, flag)
-        be.dequant_sum(gathered, 0, 1, n, c, S, out)
-    return out.view(partials[0].shape), flag
+    def __init__(self, scheme, n: int, nranks: int, algo: str = "oneshot", out_dtype=None,
+                 device="cuda", backend=None):
+        import torch
+
+        if isinstance(scheme, str):
+            scheme = parse_scheme(scheme, extensions=True)
+        if algo not in ALGOS:
+            raise ValueError(f"algo must be one of {ALGOS}")
+        self.scheme, self.n, self.N, self.algo = scheme, int(n), int(nranks), algo
+        self.be = backend or NativeBackend(scheme)
+        self.device = torch.device(device)
+        self.out_dtype = out_dtype or torch.bfloat16
+        N, n = self.N, self.n
+        dev = self.device
+        self.flag = torch.empty(1, dtype=torch.int64, device=dev)
+        self.be.reset_flag(self.flag)
+        self.out = torch.empty(n, dtype=self.out_dtype, device=dev)
+        if algo == "oneshot":
+            _, _, S = self.be.layout(n)
+            self.S, self.c = S, n
+            self.gathered = torch.empty(N * S, dtype=torch.uint8, device=dev)
+            self.ws = torch.empty(self.be.workspace(n), dtype=torch.uint8, device=dev)
+        else:
+            self.c = twoshot_chunk_values(n, N, scheme.block_size)
+            _, _, S = self.be.layout(self.c)
+            self.S = S
+            self.send = torch.empty(N, N * S, dtype=torch.uint8, device=dev)
+            self.recv = torch.empty(N, N * S, dtype=torch.uint8, device=dev)
+            self.gathered = torch.empty(N * S, dtype=torch.uint8, device=dev)
+            self.ws = torch.empty(max(self.be.workspace(N * self.c),
+                                      self.be.workspace(self.c, requant=True)),
+                                  dtype=torch.uint8, device=dev)
+
+    @property
+    def shard_bytes(self) -> int:
+        return self.S
+
+    def quantize(self, partials):
+        """K1 for every rank (one-shot: into the gathered buffer)."""
+        be, S = self.be, self.S
+        if self.algo == "oneshot":
+            for r, p in enumerate(partials):
+                be.quantize_into(p.reshape(-1), self.gathered[r * S:(r + 1) * S], self.ws,
+                                 self.flag)
+        else:
+            for r, p in enumerate(partials):
+                be.quantize_chunks(p.reshape(-1), self.c, self.send[r], S, self.ws, self.flag)
+
+    def reduce(self, out=None):
+        """Everything after K1: (exchange) + K3 + K2."""
+        be, S, N, n, c = self.be, self.S, self.N, self.n, self.c
+        out = self.out if out is None else out.reshape(-1)
+        if self.algo == "oneshot":
+            be.dequant_sum(self.gathered, S, N, n, n, 0, out)
+        else:
+            # all-to-all: owner j receives chunk j of every rank, in rank order
+            self.recv.view(N, N, S).copy_(self.send.view(N, N, S).transpose(0, 1))
+            for j in range(N):
+                own = chunk_len(n, c, j)
+                if own > 0:
+                    be.requant(self.recv[j], S, N, own, c, self.gathered[j * S:(j + 1) * S],
+                               self.ws, self.flag)
+            be.dequant_sum(self.gathered, 0, 1, n, c, S, out)
+        return out
+
+    def __call__(self, partials, out=None):
+        if len(partials) != self.N or any(p.numel() != self.n for p in partials):
+            raise ShapeMismatch(f"expected {self.N} partials of {self.n} values")
+        self.quantize(partials)
+        return self.reduce(out).view(partials[0].shape)
+
+
+def simulate_allreduce(partials, scheme, algo: str = "oneshot", out_dtype=None, backend=None):
+    """One-off :class:`SimulatedAllReduce`; returns (reduced tensor, nonfinite flag)."""
+    sim = SimulatedAllReduce(scheme, partials[0].numel(), len(partials), algo, out_dtype,
+                             partials[0].device, backend)
+    out = sim(partials)
+    return out, sim.flag
 
 
 # ---------------------------------------------------------------------------

@@ -3,22 +3,35 @@
 
 namespace mxb {
 namespace {
-template <int LPB>
-void by_dec(const DArgs& a, int64_t nchunks, int enc, int bits, cudaStream_t st) {
-  dim3 grid((unsigned)a.tiles_per_chunk, (unsigned)nchunks);
-  if (enc == ENC_E2M1) k_dqsum<__half, LPB, ENC_E2M1, 4, kU><<<grid, kThreads, 0, st>>>(a);
-  else if (bits == 8) k_dqsum<__half, LPB, ENC_GEN, 8, kU><<<grid, kThreads, 0, st>>>(a);
-  else if (bits == 4) k_dqsum<__half, LPB, ENC_GEN, 4, kU><<<grid, kThreads, 0, st>>>(a);
-  else k_dqsum<__half, LPB, ENC_GEN, 0, kU><<<grid, kThreads, 0, st>>>(a);
+template <int B, int DEC, int BITS>
+void go(const DArgs& a, cudaStream_t st) {
+  auto k = k_dqsum<__half, B, DEC, BITS>;
+  k<<<work_grid(k, a.total_units, 1), kThreads, 0, st>>>(a);
+}
+template <int B>
+void by_dec(const DArgs& a, int enc, int bits, cudaStream_t st) {
+  if (enc == ENC_E2M1) {
+    go<B, ENC_E2M1, 4>(a, st);
+    return;
+  }
+  switch (bits) {
+    case 2: go<B, ENC_GEN, 2>(a, st); return;
+    case 3: go<B, ENC_GEN, 3>(a, st); return;
+    case 4: go<B, ENC_GEN, 4>(a, st); return;
+    case 5: go<B, ENC_GEN, 5>(a, st); return;
+    case 6: go<B, ENC_GEN, 6>(a, st); return;
+    case 7: go<B, ENC_GEN, 7>(a, st); return;
+    default: go<B, ENC_GEN, 8>(a, st); return;
+  }
 }
 }  // namespace
 
-void launch_dqsum_f16(const DArgs& a, int64_t nchunks, int lpb, int enc, int bits, cudaStream_t st) {
-  switch (lpb) {
-    case 1: by_dec<1>(a, nchunks, enc, bits, st); return;
-    case 2: by_dec<2>(a, nchunks, enc, bits, st); return;
-    case 4: by_dec<4>(a, nchunks, enc, bits, st); return;
-    case 8: by_dec<8>(a, nchunks, enc, bits, st); return;
+void launch_dqsum_f16(const DArgs& a, int block, int enc, int bits, cudaStream_t st) {
+  switch (block) {
+    case 8: by_dec<8>(a, enc, bits, st); return;
+    case 16: by_dec<16>(a, enc, bits, st); return;
+    case 32: by_dec<32>(a, enc, bits, st); return;
+    case 64: by_dec<64>(a, enc, bits, st); return;
   }
 }
 }  // namespace mxb

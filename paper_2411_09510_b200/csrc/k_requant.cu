@@ -3,26 +3,36 @@
 
 namespace mxb {
 namespace {
-template <int LPB>
+template <int B, int ENC, int BITS>
+void go(const RArgs& a, cudaStream_t st) {
+  auto k = k_requant<B, ENC, BITS>;
+  k<<<work_grid(k, a.total_units, 1), kThreads, 0, st>>>(a);
+}
+template <int B>
 void by_enc(const RArgs& a, int enc, int bits, cudaStream_t st) {
-  unsigned tiles = (unsigned)((a.n + kTile - 1) / kTile);
   switch (enc) {
-    case ENC_E2M1: k_requant<LPB, ENC_E2M1, 4, kU><<<tiles, kThreads, 0, st>>>(a); return;
-    case ENC_E2M3: k_requant<LPB, ENC_E2M3, 6, kU><<<tiles, kThreads, 0, st>>>(a); return;
-    case ENC_E3M2: k_requant<LPB, ENC_E3M2, 6, kU><<<tiles, kThreads, 0, st>>>(a); return;
-    default:
-      if (bits == 8) k_requant<LPB, ENC_GEN, 8, kU><<<tiles, kThreads, 0, st>>>(a);
-      else k_requant<LPB, ENC_GEN, 0, kU><<<tiles, kThreads, 0, st>>>(a);
+    case ENC_E2M1: go<B, ENC_E2M1, 4>(a, st); return;
+    case ENC_E2M3: go<B, ENC_E2M3, 6>(a, st); return;
+    case ENC_E3M2: go<B, ENC_E3M2, 6>(a, st); return;
+  }
+  switch (bits) {
+    case 2: go<B, ENC_GEN, 2>(a, st); return;
+    case 3: go<B, ENC_GEN, 3>(a, st); return;
+    case 4: go<B, ENC_GEN, 4>(a, st); return;
+    case 5: go<B, ENC_GEN, 5>(a, st); return;
+    case 6: go<B, ENC_GEN, 6>(a, st); return;
+    case 7: go<B, ENC_GEN, 7>(a, st); return;
+    default: go<B, ENC_GEN, 8>(a, st); return;
   }
 }
 }  // namespace
 
-void launch_requant(const RArgs& a, int lpb, int enc, int bits, cudaStream_t st) {
-  switch (lpb) {
-    case 1: by_enc<1>(a, enc, bits, st); return;
-    case 2: by_enc<2>(a, enc, bits, st); return;
-    case 4: by_enc<4>(a, enc, bits, st); return;
+void launch_requant(const RArgs& a, int block, int enc, int bits, cudaStream_t st) {
+  switch (block) {
     case 8: by_enc<8>(a, enc, bits, st); return;
+    case 16: by_enc<16>(a, enc, bits, st); return;
+    case 32: by_enc<32>(a, enc, bits, st); return;
+    case 64: by_enc<64>(a, enc, bits, st); return;
   }
 }
 }  // namespace mxb

@@ -206,6 +206,7 @@ int cuda_check(const char* what) {
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 int64_t align16(int64_t v) { return (v + 15) & ~(int64_t)15; }
+int64_t align32(int64_t v) { return (v + 31) & ~(int64_t)31; }
 
 int check_scheme(const mx_scheme_t* s) {
   if (!s) return fail(MX_ERR_INVALID_ARGUMENT, "scheme is NULL");
@@ -253,6 +254,10 @@ Fmt make_fmt(const mx_scheme_t* s) {
     f.ovf64 = (1ull << 52) - (1ull << (53 - f.y));
   }
   f.gmax = (float)f.gmax64;
+  // grid*2^s is an exact f32 iff its finest quantum 2^(lo-y+s) >= 2^-149 and
+  // gmax*2^s < 2^128 (gmax < 2^(emax+1))
+  f.s_fast_lo = max(-149, -149 - (f.lo - f.y));
+  f.s_fast_hi = 127 - f.emax;
   return f;
 }
 
@@ -265,15 +270,8 @@ int enc_of(const mx_scheme_t* s) {
   return ENC_GEN;
 }
 
-int lpb_of(int64_t block) {
-  switch (block) {
-    case 8: return 1;
-    case 16: return 2;
-    case 32: return 4;
-    case 64: return 8;
-    default: return 0;
-  }
-}
+// block sizes with a fast (template) kernel
+bool fast_block(int64_t block) { return block == 8 || block == 16 || block == 32 || block == 64; }
 
 bool aligned(const void* p, int a) { return ((uintptr_t)p % a) == 0; }
 
@@ -300,23 +298,26 @@ int quantize_impl(const void* x, int dtype, int64_t n, int64_t cv, const mx_sche
   Fmt f = make_fmt(s);
   int64_t nchunks = cdiv(n, cv);
   if (nchunks > 65535) return fail(MX_ERR_INVALID_ARGUMENT, "too many chunks (%lld)", (long long)nchunks);
-  int lpb = lpb_of(s->block_size);
   int bits = f.bits;
   int enc = enc_of(s);
-  bool fast = lpb != 0 && dtype != MX_F64 && aligned(x, 16) && aligned(elem_base, 8) &&
-              aligned(scale_base, 8) && (chunk_stride % 16 == 0 || nchunks == 1) &&
-              (nchunks == 1 || cv % 8 == 0);
+  // fast kernels: 256-bit input loads (32-B aligned chunks), 16-B aligned
+  // element streams, 8-B aligned scale streams
+  bool fast = fast_block(s->block_size) && dtype != MX_F64 && aligned(x, 32) &&
+              aligned(elem_base, bits == 8 ? 32 : 16) && aligned(scale_base, 8) &&
+              (nchunks == 1 || (chunk_stride % 32 == 0 && (cv * in_size(dtype)) % 32 == 0));
   unsigned long long* nf = reinterpret_cast<unsigned long long*>(nonfinite);
   if (fast) {
     QArgs a;
     a.x = x; a.n = n; a.cv = cv;
-    a.tiles_per_chunk = (int)cdiv(cv, kTile);
+    a.units_per_chunk = cdiv(cv, kUnit);
+    a.total_units = a.units_per_chunk * nchunks;
     a.scale_base = scale_base; a.elem_base = elem_base; a.chunk_stride = chunk_stride;
     a.nonfinite = nf; a.f = f;
+    int blk = (int)s->block_size;
     switch (dtype) {
-      case MX_BF16: launch_quant_bf16(a, nchunks, lpb, enc, bits, st); break;
-      case MX_F16: launch_quant_f16(a, nchunks, lpb, enc, bits, st); break;
-      default: launch_quant_f32(a, nchunks, lpb, enc, bits, st); break;
+      case MX_BF16: launch_quant_bf16(a, blk, enc, bits, st); break;
+      case MX_F16: launch_quant_f16(a, blk, enc, bits, st); break;
+      default: launch_quant_f32(a, blk, enc, bits, st); break;
     }
     return cuda_check("k_quant");
   }
@@ -349,8 +350,8 @@ int quantize_impl(const void* x, int dtype, int64_t n, int64_t cv, const mx_sche
 }
 
 int dqsum_impl(const uint8_t* in, int64_t rank_stride, int nranks, int64_t n, int64_t cv,
-               int64_t chunk_stride, const mx_scheme_t* s, void* out, int out_dtype, int plain,
-               cudaStream_t st) {
+               int64_t chunk_stride, int64_t scale_off, int64_t elem_off, const mx_scheme_t* s,
+               void* out, int out_dtype, int plain, cudaStream_t st) {
   int rc = check_scheme(s);
   if (rc) return rc;
   if (n < 0 || nranks < 1 || cv < 1)
@@ -360,23 +361,25 @@ int dqsum_impl(const uint8_t* in, int64_t rank_stride, int nranks, int64_t n, in
   if (out_dtype == MX_F64 && !(plain && nranks == 1))
     return fail(MX_ERR_INVALID_ARGUMENT, "float64 output is only for plain decompression");
   Fmt f = make_fmt(s);
-  int64_t sb = (cdiv(cv, s->block_size) * s->scale_bits + 7) / 8;
   DArgs a;
   a.in = in; a.rank_stride = rank_stride; a.nranks = nranks; a.chunk_stride = chunk_stride;
-  a.scale_off = 0; a.elem_off = align16(sb);
+  a.scale_off = scale_off; a.elem_off = elem_off;
   a.n = n; a.cv = cv; a.out = out; a.plain = plain; a.f = f;
   int64_t nchunks = cdiv(n, cv);
   if (nchunks > 65535) return fail(MX_ERR_INVALID_ARGUMENT, "too many chunks");
-  int lpb = lpb_of(s->block_size);
-  bool fast = lpb != 0 && out_dtype != MX_F64 && aligned(out, 16) && aligned(in, 8) &&
-              rank_stride % 8 == 0 && chunk_stride % 8 == 0 && (nchunks == 1 || cv % 8 == 0);
+  int osz = out_dtype == MX_F32 ? 4 : 2;
+  bool fast = fast_block(s->block_size) && out_dtype != MX_F64 && aligned(out, 32) &&
+              aligned(in + elem_off, 16) && aligned(in + scale_off, 8) && rank_stride % 32 == 0 &&
+              chunk_stride % 32 == 0 && (nchunks == 1 || (cv * osz) % 32 == 0);
   if (fast) {
-    a.tiles_per_chunk = (int)cdiv(cv, kTile);
+    a.units_per_chunk = cdiv(cv, kUnit);
+    a.total_units = a.units_per_chunk * nchunks;
     int enc = enc_of(s);
+    int blk = (int)s->block_size;
     switch (out_dtype) {
-      case MX_BF16: launch_dqsum_bf16(a, nchunks, lpb, enc, f.bits, st); break;
-      case MX_F16: launch_dqsum_f16(a, nchunks, lpb, enc, f.bits, st); break;
-      case MX_F32: launch_dqsum_f32(a, nchunks, lpb, enc, f.bits, st); break;
+      case MX_BF16: launch_dqsum_bf16(a, blk, enc, f.bits, st); break;
+      case MX_F16: launch_dqsum_f16(a, blk, enc, f.bits, st); break;
+      case MX_F32: launch_dqsum_f32(a, blk, enc, f.bits, st); break;
       default: return fail(MX_ERR_INVALID_ARGUMENT, "unknown output dtype %d", out_dtype);
     }
     return cuda_check("k_dqsum");
@@ -422,9 +425,10 @@ int mx_shard_layout(int64_t n, const mx_scheme_t* s, int64_t* scale_offset, int6
   int64_t sb, eb;
   int rc = mx_stream_nbytes(n, s, &sb, &eb);
   if (rc) return rc;
+  // 32-byte granules: every stream starts on a full sector (256-bit accesses)
   if (scale_offset) *scale_offset = 0;
-  if (element_offset) *element_offset = align16(sb);
-  if (shard_bytes) *shard_bytes = align16(align16(sb) + eb);
+  if (element_offset) *element_offset = align32(sb);
+  if (shard_bytes) *shard_bytes = align32(align32(sb) + eb);
   return MX_OK;
 }
 
@@ -473,39 +477,21 @@ int mx_dequantize(const uint8_t* scale_stream, const uint8_t* element_stream, in
   if (n == 0) return MX_OK;
   if (!scale_stream || !element_stream) return fail(MX_ERR_INVALID_ARGUMENT, "NULL stream");
   // the two streams are addressed as one "shard": base = scale stream,
-  // element offset = distance to the element stream
+  // element offset = distance to the element stream (any value)
   int64_t off = (int64_t)(element_stream - scale_stream);
-  // generic single-shard decode honours arbitrary offsets; the fast kernels
-  // need the element stream 16-aligned relative to the scale stream
-  int lpb = lpb_of(s->block_size);
-  cudaStream_t st = (cudaStream_t)stream;
-  int64_t nb = cdiv(n, s->block_size);
-  int64_t sb = (nb * s->scale_bits + 7) / 8;
-  bool fast_layout = off == align16(sb);
-  if (lpb != 0 && fast_layout && out_dtype != MX_F64)
-    return dqsum_impl(scale_stream, 0, 1, n, n, 0, s, out, out_dtype, 1, st);
-  DArgs a;
-  a.in = scale_stream; a.rank_stride = 0; a.nranks = 1; a.chunk_stride = 0;
-  a.scale_off = 0; a.elem_off = off; a.n = n; a.cv = n; a.out = out; a.plain = 1;
-  a.f = make_fmt(s); a.tiles_per_chunk = 0;
-  int64_t gpc = cdiv(n, 8);
-  const int T = 256;
-  switch (out_dtype) {
-    case MX_BF16: g_dqsum<__nv_bfloat16><<<cdiv(gpc, T), T, 0, st>>>(a, gpc, gpc); break;
-    case MX_F16: g_dqsum<__half><<<cdiv(gpc, T), T, 0, st>>>(a, gpc, gpc); break;
-    case MX_F32: g_dqsum<float><<<cdiv(gpc, T), T, 0, st>>>(a, gpc, gpc); break;
-    case MX_F64: g_dqsum<double><<<cdiv(gpc, T), T, 0, st>>>(a, gpc, gpc); break;
-    default: return fail(MX_ERR_INVALID_ARGUMENT, "unknown output dtype %d", out_dtype);
-  }
-  return cuda_check("generic dequantise");
+  return dqsum_impl(scale_stream, 0, 1, n, n, 0, 0, off, s, out, out_dtype, 1,
+                    (cudaStream_t)stream);
 }
 
 int mx_dequant_sum(const uint8_t* shards, int64_t rank_stride, int32_t nranks, int64_t n,
                    int64_t chunk_values, int64_t chunk_stride, const mx_scheme_t* s, void* out,
                    int32_t out_dtype, void* stream) {
   if (out_dtype == MX_F64) return fail(MX_ERR_INVALID_ARGUMENT, "sums are fp32 (mx/netbench.py:332)");
-  return dqsum_impl(shards, rank_stride, nranks, n, chunk_values, chunk_stride, s, out, out_dtype,
-                    0, (cudaStream_t)stream);
+  int64_t so, eo, sbytes;
+  int rc = mx_shard_layout(chunk_values, s, &so, &eo, &sbytes);
+  if (rc) return rc;
+  return dqsum_impl(shards, rank_stride, nranks, n, chunk_values, chunk_stride, so, eo, s, out,
+                    out_dtype, 0, (cudaStream_t)stream);
 }
 
 int mx_dequant_sum_requant(const uint8_t* shards, int64_t rank_stride, int32_t nranks, int64_t n,
@@ -519,15 +505,16 @@ int mx_dequant_sum_requant(const uint8_t* shards, int64_t rank_stride, int32_t n
   cudaStream_t st = (cudaStream_t)stream;
   int64_t so, eo, sbytes;
   mx_shard_layout(chunk_values, s, &so, &eo, &sbytes);
-  int lpb = lpb_of(s->block_size);
   Fmt f = make_fmt(s);
-  if (lpb != 0 && aligned(shards, 8) && rank_stride % 8 == 0 && aligned(out_shard, 8)) {
+  if (fast_block(s->block_size) && aligned(shards, 32) && rank_stride % 32 == 0 &&
+      aligned(out_shard, 32)) {
     RArgs a;
     a.in = shards; a.rank_stride = rank_stride; a.nranks = nranks;
     a.scale_off = so; a.elem_off = eo; a.n = n;
+    a.total_units = cdiv(n, kUnit);
     a.out_scale = out_shard + so; a.out_elem = out_shard + eo;
     a.nonfinite = reinterpret_cast<unsigned long long*>(nonfinite); a.f = f;
-    launch_requant(a, lpb, enc_of(s), f.bits, st);
+    launch_requant(a, (int)s->block_size, enc_of(s), f.bits, st);
     return cuda_check("k_requant");
   }
   // generic: fp32 sum into the workspace, then the generic quantiser
@@ -540,7 +527,7 @@ int mx_dequant_sum_requant(const uint8_t* shards, int64_t rank_stride, int32_t n
   float* sum = reinterpret_cast<float*>(p);
   uint8_t* rest = reinterpret_cast<uint8_t*>(p + align16(4 * n));
   int64_t rest_bytes = workspace_bytes - (int64_t)((uint8_t*)rest - w);
-  rc = dqsum_impl(shards, rank_stride, nranks, n, chunk_values, 0, s, sum, MX_F32, 0, st);
+  rc = dqsum_impl(shards, rank_stride, nranks, n, chunk_values, 0, so, eo, s, sum, MX_F32, 0, st);
   if (rc) return rc;
   return quantize_impl(sum, MX_F32, n, n, s, out_shard + so, out_shard + eo, 0, nonfinite, rest,
                        rest_bytes, st);

@@ -21,6 +21,8 @@ struct Fmt {
   int s_min;    // 1-sbias                            mx/formats.py:120-123
   int s_max;    // 2^k-1-sbias                        mx/formats.py:125-128
   int block;    // B
+  int s_fast_lo;   // block exponents for which grid*2^s is exactly an f32
+  int s_fast_hi;   // (decode = one FFMA into the fp32 accumulator)
   uint32_t ovf32;  // fraction threshold of the overshoot bump (mx/codec.py:159)
   uint64_t ovf64;
   float gmax;
@@ -288,17 +290,25 @@ __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) {
 }
 
 template <typename T>
+__device__ __forceinline__ uint32_t pack2(float lo, float hi);
+template <>
+__device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, float hi) {
+  __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);  // F2FP.BF16.F32.PACK_AB, RNE
+  return *reinterpret_cast<uint32_t*>(&p);
+}
+template <>
+__device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) {
+  __half2 p = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&p);
+}
+
+template <typename T>
 __device__ __forceinline__ void store8(T* __restrict__ out, int64_t g, int valid, const float v[8]) {
   if (valid == 8) {
     if constexpr (sizeof(T) == 2) {
-      uint32_t u[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        T lo = from_f32<T>(v[2 * i]), hi = from_f32<T>(v[2 * i + 1]);
-        u[i] = (uint32_t)(*reinterpret_cast<uint16_t*>(&lo)) |
-               ((uint32_t)(*reinterpret_cast<uint16_t*>(&hi)) << 16);
-      }
-      *reinterpret_cast<uint4*>(out + g) = make_uint4(u[0], u[1], u[2], u[3]);
+      uint4 u = make_uint4(pack2<T>(v[0], v[1]), pack2<T>(v[2], v[3]), pack2<T>(v[4], v[5]),
+                           pack2<T>(v[6], v[7]));
+      *reinterpret_cast<uint4*>(out + g) = u;
     } else {
       *reinterpret_cast<float4*>(out + g) = make_float4(v[0], v[1], v[2], v[3]);
       *reinterpret_cast<float4*>(out + g + 4) = make_float4(v[4], v[5], v[6], v[7]);

@@ -1,0 +1,22 @@
+#!/bin/bash
+# One gpurun call: GPU tests, bench, ncu launch list and full captures of K1/K2.
+# usage (from the build container):
+#   gpurun --timeout 1500 -- 'bash scripts/gpu_check.sh [tag] [tests|notests]'
+tag=${1:-dev}
+mode=${2:-tests}
+out=gpurun_out/$tag
+mkdir -p $out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $out/smi.txt 2>&1
+if [ "$mode" = tests ]; then
+  timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -15 > $out/tests.txt
+fi
+timeout 300 python bench.py > $out/bench.json 2> $out/bench.err
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file $out/launches.csv python bench.py --profile > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_quant -s 2 -c 1 \
+  -o $out/prof_kquant python bench.py --profile > $out/ncu1.log 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_dqsum -s 1 -c 1 \
+  -o $out/prof_kdqsum python bench.py --profile > $out/ncu2.log 2>&1
+cat $out/tests.txt 2>/dev/null | tail -3
+cat $out/bench.json
+tail -3 $out/bench.err

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
 def test_host_only_abi_calls():
     s = mx.parse_scheme("fp4_e2m1:32:e8m0")
     assert _native.stream_nbytes(2 * 128 * 8192, s.to_c()) == (65536, 1048576)
-    assert _native.shard_layout(70, s.to_c()) == (0, 16, 64)
+    assert _native.shard_layout(70, s.to_c()) == (0, 32, 96)
     bad = _native.MxScheme(0, 0, 1, 8, 32)  # FloatMicro without exponent bits
     rc = _native.load().mx_scheme_check(ctypes.byref(bad))
     assert rc == -5 and b"exponent" in _native.load().mx_last_error()

@@ -299,24 +299,22 @@ def run_ours(args, shape, rank, world, local_rank):
     nranks = args.sim_ranks if sim else world
     so, eo, S = _native.shard_layout(n, sch.to_c())
     sb, eb = _native.stream_nbytes(n, sch.to_c())
-    # buffer sets: enough that one pass over them exceeds L2
+    # buffer sets: one pass over them moves > 3x L2, so every step and every
+    # timed kernel launch reads data that is not L2-resident
     per_set = (nranks if sim else 1) * 2 * n + (nranks * S) + 2 * n
-    R = max(2, -(-2 * L2_BYTES // per_set))
-    host_parts = rank_partials(shape, nranks, seed=0)
+    R = max(3, -(-3 * L2_BYTES // per_set))
+    mine = list(range(nranks)) if sim else [rank]  # the partials this GPU owns
+    host_parts = {r: rank_partials(shape, 1, seed=r)[0] for r in mine}  # seed = rank
+    base = [torch.from_numpy(host_parts[r]).to(dev, torch.bfloat16) for r in mine]
     sets = []
     for s in range(R):
+        # distinct data per set: row roll + sign flip keep the statistics
+        parts = [(b.roll(s * 7, 0) * (-1) ** s).contiguous() for b in base]
         if sim:
-            parts = [torch.from_numpy(host_parts[r]).to(dev, torch.bfloat16) for r in range(nranks)]
-            if s:  # distinct data per set (sign flip + permutation of rows keeps statistics)
-                parts = [p.roll(s * 7, 0) * (-1) ** s for p in parts]
             op = SimulatedAllReduce(sch, n, nranks, args.algo, torch.bfloat16, dev)
-            sets.append((parts, op))
         else:
-            x = torch.from_numpy(host_parts[rank]).to(dev, torch.bfloat16)
-            if s:
-                x = x.roll(s * 7, 0) * (-1) ** s
             op = CompressedAllReduce(sch, n, algo=args.algo, out_dtype=torch.bfloat16, device=dev)
-            sets.append(([x], op))
+        sets.append((parts, op))
 
     def step_fn(i):
         parts, op = sets[i]
@@ -359,27 +357,26 @@ def run_ours(args, shape, rank, world, local_rank):
 
     # ---- per-kernel device times (roofline), graphs of back-to-back launches
     kernels = {}
-    M = 8
     if sim and args.algo == "oneshot":
-        def q_only(i):
-            parts, op = sets[i]
-            return lambda: [op.be.quantize_into(parts[0].reshape(-1),
-                                                op.gathered[0:S], op.ws, op.flag)
-                            for _ in range(M)]
+        # one graph = one launch per buffer set (R distinct inputs > 3x L2)
+        def q_all():
+            for parts, op in sets:
+                op.be.quantize_into(parts[0].reshape(-1), op.gathered[0:S], op.ws, op.flag)
 
-        def d_only(i):
-            parts, op = sets[i]
-            return lambda: [op.reduce() for _ in range(M)]
+        def d_all():
+            for parts, op in sets:
+                op.reduce()
 
-        for name, mk, bytes_per in (("k_quant", q_only, 2 * n + sb + eb),
-                                    ("k_dqsum", d_only, nranks * (sb + eb) + 2 * n)):
-            gs = [capture(torch, mk(i)) for i in range(R)]
-            for i in range(2 * R):
-                gs[i % R].replay()
-            reps = max(8, min(400, args.steps // 4))
-            ms = time_graph_replays(torch, gs, reps) / (reps * M)
+        for name, fn, bytes_per in (("k_quant", q_all, 2 * n + sb + eb),
+                                    ("k_dqsum", d_all, nranks * (sb + eb) + 2 * n)):
+            g = capture(torch, fn)
+            for _ in range(3):
+                g.replay()
+            reps = max(4, min(100, args.steps // 20))
+            ms = time_graph_replays(torch, [g], reps) / (reps * R)
             kernels[name] = {"us": round(ms * 1e3, 3), "bytes": bytes_per,
-                             "gbs": round(bytes_per / (ms * 1e-3) / 1e9, 1)}
+                             "gbs": round(bytes_per / (ms * 1e-3) / 1e9, 1),
+                             "launches_timed": reps * R}
     peak, peak_kind = peaks()
     roof = None
     if "k_quant" in kernels:
@@ -399,8 +396,7 @@ def run_ours(args, shape, rank, world, local_rank):
     # ---- end to end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        host_in = [torch.from_numpy(host_parts[r if sim else rank]).to(torch.bfloat16).pin_memory()
-                   for r in (range(nranks) if sim else [0])]
+        host_in = [torch.from_numpy(host_parts[r]).to(torch.bfloat16).pin_memory() for r in mine]
         host_out = torch.empty(n, dtype=torch.bfloat16).pin_memory()
         parts, op = sets[0]
         ke = max(3, min(args.steps, 100))

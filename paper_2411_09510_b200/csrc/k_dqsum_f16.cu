@@ -6,7 +6,7 @@ namespace {
 template <int B, int DEC, int BITS>
 void go(const DArgs& a, cudaStream_t st) {
   auto k = k_dqsum<__half, B, DEC, BITS>;
-  k<<<work_grid(k, a.total_units, 1), kThreads, 0, st>>>(a);
+  k<<<work_grid(k, a.total_units, 2), kThreads, 0, st>>>(a);
 }
 template <int B>
 void by_dec(const DArgs& a, int enc, int bits, cudaStream_t st) {

@@ -5,6 +5,7 @@
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <type_traits>
@@ -270,6 +271,18 @@ int enc_of(const mx_scheme_t* s) {
   return ENC_GEN;
 }
 
+// MXB200_TMA=1 routes whole tiles of single-chunk E8M0 16-bit inputs through
+// the TMA quantiser (k_quant_tma.cu); the register-path kernel is the default
+// because it measured faster at the 8B prefill size (profiles/ROUND1.md).
+bool use_tma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MXB200_TMA");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 // block sizes with a fast (template) kernel
 bool fast_block(int64_t block) { return block == 8 || block == 16 || block == 32 || block == 64; }
 
@@ -312,8 +325,24 @@ int quantize_impl(const void* x, int dtype, int64_t n, int64_t cv, const mx_sche
     a.units_per_chunk = cdiv(cv, kUnit);
     a.total_units = a.units_per_chunk * nchunks;
     a.scale_base = scale_base; a.elem_base = elem_base; a.chunk_stride = chunk_stride;
-    a.nonfinite = nf; a.f = f;
+    a.nonfinite = nf; a.f = f; a.flat_off = 0;
     int blk = (int)s->block_size;
+    // single chunk, E8M0, 16-bit input: TMA pipeline for all whole 8192-value
+    // tiles, the register-path kernel for the remainder
+    if (nchunks == 1 && f.kbits == 8 && (dtype == MX_BF16 || dtype == MX_F16) && use_tma()) {
+      int64_t m = launch_quant_tma(a, dtype == MX_BF16, blk, enc, bits, st);
+      if (m > 0) {
+        rc = cuda_check("k_quant_tma");
+        if (rc || m == n) return rc;
+        a.x = static_cast<const uint8_t*>(x) + m * 2;
+        a.n = n - m; a.cv = a.n;
+        a.units_per_chunk = cdiv(a.n, kUnit);
+        a.total_units = a.units_per_chunk;
+        a.elem_base = elem_base + m / 8 * bits;
+        a.scale_base = scale_base + m / s->block_size;
+        a.flat_off = m;
+      }
+    }
     switch (dtype) {
       case MX_BF16: launch_quant_bf16(a, blk, enc, bits, st); break;
       case MX_F16: launch_quant_f16(a, blk, enc, bits, st); break;
@@ -372,7 +401,7 @@ int dqsum_impl(const uint8_t* in, int64_t rank_stride, int nranks, int64_t n, in
               aligned(in + elem_off, 16) && aligned(in + scale_off, 8) && rank_stride % 32 == 0 &&
               chunk_stride % 32 == 0 && (nchunks == 1 || (cv * osz) % 32 == 0);
   if (fast) {
-    a.units_per_chunk = cdiv(cv, kUnit);
+    a.units_per_chunk = cdiv(cv, kUnit2);
     a.total_units = a.units_per_chunk * nchunks;
     int enc = enc_of(s);
     int blk = (int)s->block_size;

@@ -50,6 +50,7 @@ struct QArgs {
   uint8_t* elem_base;
   int64_t chunk_stride;
   unsigned long long* nonfinite;
+  int64_t flat_off;      // flat index of x[0] (non-finite reports)
   Fmt f;
 };
 
@@ -80,11 +81,11 @@ struct RArgs {  // two-shot middle step: one chunk, nranks shards -> one shard
   Fmt f;
 };
 
-template <int B>
+template <int B, int VPL = kVPL>
 struct Geo {
-  static constexpr int NSB = B >= kVPL ? 1 : kVPL / B;  // scale blocks per lane
-  static constexpr int LPB = B > kVPL ? B / kVPL : 1;   // lanes per block
-  static constexpr int SBV = kVPL / NSB;                // values per owned block
+  static constexpr int NSB = B >= VPL ? 1 : VPL / B;  // scale blocks per lane
+  static constexpr int LPB = B > VPL ? B / VPL : 1;   // lanes per block
+  static constexpr int SBV = VPL / NSB;               // values per owned block
 };
 
 // ---------------------------------------------------------------------------
@@ -206,15 +207,17 @@ __device__ __forceinline__ uint64_t encode8(const float* x, const Fmt& f) {
   return w;
 }
 
-// The lane's 32 codes as 4b contiguous bytes = BITS 32-bit words.
-template <int BITS>
+// The lane's VPL codes as VPL*b/8 contiguous bytes (VPL = 32: BITS words).
+template <int BITS, int VPL = kVPL>
 struct LaneCodes {
-  uint32_t w[BITS];
+  static constexpr int NB = VPL * BITS / 8;
+  static constexpr int NW = (NB + 3) / 4;
+  uint32_t w[NW];
 };
 
 // Put group g (values 8g..8g+7; 8b bits = b bytes) into the lane words.
-template <int BITS>
-__device__ __forceinline__ void put_group(LaneCodes<BITS>& c, int g, uint64_t v) {
+template <int BITS, int VPL = kVPL>
+__device__ __forceinline__ void put_group(LaneCodes<BITS, VPL>& c, int g, uint64_t v) {
   if constexpr (BITS == 4) {
     c.w[g] = (uint32_t)v;
   } else if constexpr (BITS == 8) {
@@ -229,8 +232,8 @@ __device__ __forceinline__ void put_group(LaneCodes<BITS>& c, int g, uint64_t v)
   }
 }
 
-template <int BITS>
-__device__ __forceinline__ uint64_t get_group(const LaneCodes<BITS>& c, int g) {
+template <int BITS, int VPL = kVPL>
+__device__ __forceinline__ uint64_t get_group(const LaneCodes<BITS, VPL>& c, int g) {
   if constexpr (BITS == 4) {
     return c.w[g];
   } else if constexpr (BITS == 8) {
@@ -306,6 +309,39 @@ __device__ __forceinline__ LaneCodes<BITS> load_lane_codes(const uint8_t* __rest
   return c;
 }
 
+// The lane's 16 codes (2b bytes at p = unit base + 2b*lane) for K2.
+template <int BITS>
+__device__ __forceinline__ LaneCodes<BITS, 16> load_lane_codes16(const uint8_t* __restrict__ p,
+                                                                 int valid) {
+  LaneCodes<BITS, 16> c;
+  constexpr int NW = LaneCodes<BITS, 16>::NW;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) c.w[i] = 0u;
+  if (valid == 16) {
+    if constexpr (BITS == 8) {
+      uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
+      c.w[0] = a.x; c.w[1] = a.y; c.w[2] = a.z; c.w[3] = a.w;
+    } else if constexpr (BITS == 4) {
+      uint2 a = __ldg(reinterpret_cast<const uint2*>(p));
+      c.w[0] = a.x; c.w[1] = a.y;
+    } else if constexpr (BITS % 2 == 0) {
+#pragma unroll
+      for (int i = 0; i < BITS / 2; ++i) c.w[i] = __ldg(reinterpret_cast<const uint32_t*>(p) + i);
+    } else {
+#pragma unroll
+      for (int i = 0; i < BITS; ++i)
+        c.w[i >> 1] |= (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(p) + i)
+                       << (16 * (i & 1));
+    }
+  } else if (valid > 0) {
+    const int nb = (valid * BITS + 7) / 8;
+#pragma unroll
+    for (int i = 0; i < 2 * BITS; ++i)
+      if (i < nb) c.w[i >> 2] |= (uint32_t)p[i] << (8 * (i & 3));
+  }
+  return c;
+}
+
 // Quantise the lane's 32 values.  stored[sb] = scale code of owned block sb
 // (B = 64: both lanes of the block hold it).  Zero and non-finite blocks get
 // scale code 0 and zero codes (mx/codec.py:170-171).
@@ -345,8 +381,26 @@ __device__ __forceinline__ LaneCodes<BITS> quant_lane(const Raw<T>& raw, const F
 #pragma unroll
     for (int g = 0; g < SBV / 8; ++g) {
       float x[8];
+      if constexpr (std::is_same<T, __nv_bfloat16>::value && ENC == ENC_E2M1) {
+        // bf16 pairs scaled by 2^-s in one HFMA2.BF16 each (exact: power-of-
+        // two scaling of bf16; results below 2^-126 are far under the 0.25
+        // rounding threshold and keep their sign), then widened to f32.
+        // E2M1 has emax 2, so s <= 126 and 2^-s is a normal bf16.
+        const uint32_t i16 = (uint32_t)(127 - s) << 7;
+        const uint32_t inv2 = i16 | (i16 << 16);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) x[i] = raw_f32<T>(raw, sb * SBV + 8 * g + i) * inv;  // exact
+        for (int h = 0; h < 4; ++h) {
+          uint32_t wv = raw.w[(sb * SBV + 8 * g) / 2 + h];
+          __nv_bfloat162 y = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&wv),
+                                     *reinterpret_cast<const __nv_bfloat162*>(&inv2));
+          uint32_t yu = *reinterpret_cast<uint32_t*>(&y);
+          x[2 * h] = __uint_as_float(yu << 16);
+          x[2 * h + 1] = __uint_as_float(yu & 0xffff0000u);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = raw_f32<T>(raw, sb * SBV + 8 * g + i) * inv;  // exact
+      }
       uint64_t w = encode8<ENC, BITS>(x, f);
       put_group<BITS>(c, sb * (SBV / 8) + g, zero ? 0ull : w);
     }
@@ -458,10 +512,37 @@ __device__ __forceinline__ void quant_unit(const QArgs& A, const Fmt& f, const U
   int stored[NSB];
   bool bad;
   LaneCodes<BITS> c = quant_lane<InT, B, ENC, BITS>(raw, f, stored, bad);
-  if (bad) report_nonfinite_raw<InT>(raw, valid, p.cbase + p.uoff + lane * kVPL, A.nonfinite);
+  if (bad)
+    report_nonfinite_raw<InT>(raw, valid, A.flat_off + p.cbase + p.uoff + lane * kVPL,
+                              A.nonfinite);
   const int64_t cofs = (int64_t)p.chunk * A.chunk_stride;
   store_lane_codes<BITS>(A.elem_base + cofs + (p.uoff / 8) * BITS + lane * 4 * BITS, c, valid);
   store_unit_scales<B>(A.scale_base + cofs, p.uoff / B, stored, p.uvalid, lane, f.kbits, stage);
+}
+
+// Full unit u of a single-chunk tensor: straight-line, no bounds logic.
+template <typename InT, int B, int ENC, int BITS>
+__device__ __forceinline__ void quant_full_unit(const QArgs& A, const Fmt& f, uint32_t u,
+                                                const Raw<InT>& raw, int lane) {
+  constexpr int NSB = Geo<B>::NSB;
+  constexpr int LPB = Geo<B>::LPB;
+  int stored[NSB];
+  bool bad;
+  LaneCodes<BITS> c = quant_lane<InT, B, ENC, BITS>(raw, f, stored, bad);
+  if (bad)
+    report_nonfinite_raw<InT>(raw, kVPL, A.flat_off + (int64_t)u * kUnit + lane * kVPL,
+                              A.nonfinite);
+  store_lane_codes<BITS>(A.elem_base + (size_t)u * (kUnit / 8 * BITS) + lane * (4 * BITS), c,
+                         kVPL);
+  uint8_t* p = A.scale_base + (size_t)u * (kUnit / B) + (lane / LPB) * NSB;
+  if constexpr (NSB == 4) {
+    *reinterpret_cast<uint32_t*>(p) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
+                                      ((uint32_t)stored[2] << 16) | ((uint32_t)stored[3] << 24);
+  } else if constexpr (NSB == 2) {
+    *reinterpret_cast<uint16_t*>(p) = (uint16_t)(stored[0] | (stored[1] << 8));
+  } else {
+    if (lane % LPB == 0) *p = (uint8_t)stored[0];
+  }
 }
 
 template <typename InT, int B, int ENC, int BITS>
@@ -474,8 +555,31 @@ __global__ void __launch_bounds__(kThreads) k_quant(const QArgs A) {
   const uint32_t total = (uint32_t)A.total_units, upc = (uint32_t)A.units_per_chunk;
   const bool one = total == upc;
   const uint32_t nw = (uint32_t)(gridDim.x * kWarps);
-  // units u0, u0+nw (a pair per step, both loads in flight before any math)
-  for (uint32_t u0 = blockIdx.x * kWarps + (threadIdx.x >> 5); u0 < total; u0 += kUPW * nw) {
+  const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (one && f.kbits == 8) {
+    // single chunk, E8M0 scales: full units in pairs with both units' loads
+    // in flight before any math; pointers are plain multiples of u
+    const uint32_t nfull = (uint32_t)(A.n / kUnit);
+    for (uint32_t u0 = gw; u0 < nfull; u0 += kUPW * nw) {
+      const uint32_t u1 = u0 + nw;
+      const bool has1 = u1 < nfull;
+      Raw<InT> r0, r1;
+      load_raw<InT>(x + (size_t)u0 * kUnit + lane * kVPL, r0);
+      if (has1) load_raw<InT>(x + (size_t)u1 * kUnit + lane * kVPL, r1);
+      quant_full_unit<InT, B, ENC, BITS>(A, f, u0, r0, lane);
+      if (has1) quant_full_unit<InT, B, ENC, BITS>(A, f, u1, r1, lane);
+    }
+    // the partial last unit (if any) goes to the warp that would own it next
+    if (nfull < total && gw == nfull % nw) {
+      UnitPos p = unit_pos(nfull, upc, true, A.cv, A.n);
+      Raw<InT> r;
+      load_unit<InT>(x, p, lane, r);
+      quant_unit<InT, B, ENC, BITS>(A, f, p, r, lane, stage);
+    }
+    return;
+  }
+  // general case (chunked shards, k < 8): units u0, u0+nw per step
+  for (uint32_t u0 = gw; u0 < total; u0 += kUPW * nw) {
     const uint32_t u1 = u0 + nw;
     const bool has1 = u1 < total;
     UnitPos p0 = unit_pos(u0, upc, one, A.cv, A.n), p1;
@@ -556,24 +660,27 @@ __device__ __forceinline__ void fill_lut(float* lut, const Fmt& f) {
 }
 
 // One rank's shard, loaded: the lane's codes and the scale codes of its blocks.
-template <int B, int BITS>
+template <int B, int BITS, int VPL = kVPL>
 struct RankLoad {
-  LaneCodes<BITS> c;
-  int st[Geo<B>::NSB];
+  LaneCodes<BITS, VPL> c;
+  int st[Geo<B, VPL>::NSB];
 };
 
-template <int B, int BITS>
-__device__ __forceinline__ void load_rank(RankLoad<B, BITS>& r, const uint8_t* __restrict__ base,
-                                          int64_t scale_off, int64_t elem_off, int64_t uoff,
-                                          int lane, int valid, int kbits) {
-  constexpr int NSB = Geo<B>::NSB;
-  constexpr int LPB = Geo<B>::LPB;
-  r.c = load_lane_codes<BITS>(base + elem_off + (uoff / 8) * BITS + lane * 4 * BITS, valid);
+template <int B, int BITS, int VPL = kVPL>
+__device__ __forceinline__ void load_rank(RankLoad<B, BITS, VPL>& r,
+                                          const uint8_t* __restrict__ base, int64_t scale_off,
+                                          int64_t elem_off, int64_t uoff, int lane, int valid,
+                                          int kbits) {
+  constexpr int NSB = Geo<B, VPL>::NSB;
+  constexpr int LPB = Geo<B, VPL>::LPB;
+  const uint8_t* el = base + elem_off + (uoff / 8) * BITS + lane * (VPL * BITS / 8);
+  if constexpr (VPL == 16) r.c = load_lane_codes16<BITS>(el, valid);
+  else r.c = load_lane_codes<BITS>(el, valid);
   const uint8_t* sc = base + scale_off;
   const int64_t blk0 = uoff / B + (lane / LPB) * NSB;
 #pragma unroll
   for (int sb = 0; sb < NSB; ++sb) r.st[sb] = 0;
-  if (valid == kVPL && kbits == 8) {
+  if (valid == VPL && kbits == 8) {
     if constexpr (NSB == 4) {
       uint32_t v = __ldg(reinterpret_cast<const unsigned int*>(sc + blk0));
 #pragma unroll
@@ -588,28 +695,96 @@ __device__ __forceinline__ void load_rank(RankLoad<B, BITS>& r, const uint8_t* _
   } else if (valid > 0) {
 #pragma unroll
     for (int sb = 0; sb < NSB; ++sb)
-      if (sb * Geo<B>::SBV < valid) r.st[sb] = read_scale(sc, blk0 + sb, kbits);
+      if (sb * Geo<B, VPL>::SBV < valid) r.st[sb] = read_scale(sc, blk0 + sb, kbits);
   }
 }
 
-template <int B, int DEC, int BITS>
-__device__ __forceinline__ void decode_rank(const RankLoad<B, BITS>& r, const Fmt& f,
-                                            float acc[kVPL], bool plain, const float* lut) {
-  constexpr int SBV = Geo<B>::SBV;
-#pragma unroll
-  for (int g = 0; g < kVPL / 8; ++g)
-    decode8_acc<DEC, BITS>(get_group<BITS>(r.c, g), r.st[(8 * g) / SBV], f, acc + 8 * g, plain,
-                           lut);
+// 8 FP4 codes (one 32-bit word) -> acc[i] += g_i * 2^s with 2^s given as f16
+// bits: F2FP.F16.E2M1.UNPACK_B picks each byte straight out of the word and
+// FHFMA (fma.rn.f32.f16) multiplies the f16 grid value by the f16 scale and
+// adds the fp32 accumulator with ONE rounding -- exactly acc + value, since
+// g*2^s is representable (mx/netbench.py:334 semantics).
+__device__ __forceinline__ void e2m1_word_fma(uint32_t w, uint16_t F16, float* a) {
+  asm("{\n\t.reg .b8 b0, b1, b2, b3;\n\t.reg .b32 p0, p1, p2, p3;\n\t"
+      ".reg .b16 l0, h0, l1, h1, l2, h2, l3, h3;\n\t"
+      "mov.b32 {b0, b1, b2, b3}, %8;\n\t"
+      "cvt.rn.f16x2.e2m1x2 p0, b0;\n\tcvt.rn.f16x2.e2m1x2 p1, b1;\n\t"
+      "cvt.rn.f16x2.e2m1x2 p2, b2;\n\tcvt.rn.f16x2.e2m1x2 p3, b3;\n\t"
+      "mov.b32 {l0, h0}, p0;\n\tmov.b32 {l1, h1}, p1;\n\t"
+      "mov.b32 {l2, h2}, p2;\n\tmov.b32 {l3, h3}, p3;\n\t"
+      "fma.rn.f32.f16 %0, l0, %9, %0;\n\tfma.rn.f32.f16 %1, h0, %9, %1;\n\t"
+      "fma.rn.f32.f16 %2, l1, %9, %2;\n\tfma.rn.f32.f16 %3, h1, %9, %3;\n\t"
+      "fma.rn.f32.f16 %4, l2, %9, %4;\n\tfma.rn.f32.f16 %5, h2, %9, %5;\n\t"
+      "fma.rn.f32.f16 %6, l3, %9, %6;\n\tfma.rn.f32.f16 %7, h3, %9, %7;\n\t}"
+      : "+f"(a[0]), "+f"(a[1]), "+f"(a[2]), "+f"(a[3]), "+f"(a[4]), "+f"(a[5]), "+f"(a[6]),
+        "+f"(a[7])
+      : "r"(w), "h"(F16));
 }
 
-template <typename OutT>
+// 2^s as f16 bits, s in [-24, 15]
+__device__ __forceinline__ uint16_t pow2_f16(int s) {
+  return (uint16_t)(s >= -14 ? (uint32_t)(s + 15) << 10 : 1u << (s + 24));
+}
+
+template <int B, int DEC, int BITS, int VPL = kVPL>
+__device__ __forceinline__ void decode_rank(const RankLoad<B, BITS, VPL>& r, const Fmt& f,
+                                            float* acc, bool plain, const float* lut) {
+  constexpr int NSB = Geo<B, VPL>::NSB;
+  constexpr int GPB = Geo<B, VPL>::SBV / 8;  // 8-value groups per owned block
+#pragma unroll
+  for (int sb = 0; sb < NSB; ++sb) {
+    const int stored = r.st[sb];
+    const int s = stored - f.sbias;
+    if constexpr (DEC == ENC_E2M1) {
+      // FP4 fast path: 2^s representable in f16 (|s| covers every block of
+      // real activations); g*2^s is then always an exact f32
+      if (!plain && stored != 0 && s >= -24 && s <= 15) {
+        const uint16_t F16 = pow2_f16(s);
+#pragma unroll
+        for (int g = 0; g < GPB; ++g)
+          e2m1_word_fma((uint32_t)get_group<BITS, VPL>(r.c, sb * GPB + g), F16,
+                        acc + 8 * (sb * GPB + g));
+        continue;
+      }
+    }
+    // g*2^s exactly representable -> one FFMA is exactly acc + value
+    const bool fast = !plain && stored != 0 && s >= f.s_fast_lo && s <= f.s_fast_hi;
+    if (fast) {
+      const float F = pow2f(s);
+#pragma unroll
+      for (int g = 0; g < GPB; ++g) {
+        const uint64_t w = get_group<BITS, VPL>(r.c, sb * GPB + g);
+        float* a = acc + 8 * (sb * GPB + g);
+        if constexpr (DEC == ENC_E2M1) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float2 v = e2m1x2_to_f32x2(((uint32_t)w >> (8 * j)) & 0xffu);
+            a[2 * j] = fmaf(v.x, F, a[2 * j]);
+            a[2 * j + 1] = fmaf(v.y, F, a[2 * j + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            a[i] = fmaf(lut[(uint32_t)(w >> (i * BITS)) & ((1u << BITS) - 1u)], F, a[i]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int g = 0; g < GPB; ++g)
+        decode8_acc<DEC, BITS>(get_group<BITS, VPL>(r.c, sb * GPB + g), stored, f,
+                               acc + 8 * (sb * GPB + g), plain, lut);
+    }
+  }
+}
+
+template <typename OutT, int VPL = kVPL>
 __device__ __forceinline__ void store_lane_out(OutT* __restrict__ out, int valid,
-                                               const float acc[kVPL]) {
-  if (valid == kVPL) {
+                                               const float* acc) {
+  if (valid == VPL) {
     uint32_t o[8];
     if constexpr (sizeof(OutT) == 2) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < VPL / 16; ++h) {
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           o[i] = pack2<OutT>(acc[16 * h + 2 * i], acc[16 * h + 2 * i + 1]);
@@ -617,7 +792,7 @@ __device__ __forceinline__ void store_lane_out(OutT* __restrict__ out, int valid
       }
     } else {
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
+      for (int h = 0; h < VPL / 8; ++h) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) o[i] = __float_as_uint(acc[8 * h + i]);
         stg256(out + 8 * h, o);
@@ -625,13 +800,32 @@ __device__ __forceinline__ void store_lane_out(OutT* __restrict__ out, int valid
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < kVPL; ++i)
+    for (int i = 0; i < VPL; ++i)
       if (i < valid) out[i] = from_f32<OutT>(acc[i]);
   }
 }
 
+// K2 works on 16 values per lane (a 512-value unit per warp): the fp32
+// accumulators are half as many registers, so twice the warps are resident,
+// and the next unit's first two ranks are prefetched while this one decodes.
+constexpr int kVPL2 = 16;
+constexpr int kUnit2 = 32 * kVPL2;
+
+__device__ __forceinline__ UnitPos unit_pos2(uint32_t u, uint32_t upc, bool one_chunk, int64_t cv,
+                                             int64_t n) {
+  UnitPos p;
+  uint32_t chunk = one_chunk ? 0u : u / upc;
+  p.chunk = (int)chunk;
+  p.cbase = (int64_t)chunk * cv;
+  p.uoff = (int64_t)(u - chunk * upc) * kUnit2;
+  int64_t len = one_chunk ? n : min(cv, n - p.cbase);
+  p.uvalid = (int)min((int64_t)kUnit2, len - p.uoff);
+  return p;
+}
+
 template <typename OutT, int B, int DEC, int BITS>
 __global__ void __launch_bounds__(kThreads) k_dqsum(const DArgs A) {
+  using RL = RankLoad<B, BITS, kVPL2>;
   __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
   const Fmt f = A.f;
   if constexpr (DEC != ENC_E2M1) {
@@ -643,31 +837,54 @@ __global__ void __launch_bounds__(kThreads) k_dqsum(const DArgs A) {
   const uint32_t total = (uint32_t)A.total_units, upc = (uint32_t)A.units_per_chunk;
   const bool one = total == upc;
   const uint32_t nw = (uint32_t)(gridDim.x * kWarps);
-  for (uint32_t u = blockIdx.x * kWarps + (threadIdx.x >> 5); u < total; u += nw) {
-    const UnitPos p = unit_pos(u, upc, one, A.cv, A.n);
-    const int valid = max(0, min(kVPL, p.uvalid - lane * kVPL));
-    float acc[kVPL];
-#pragma unroll
-    for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
-    const uint8_t* base = A.in + (int64_t)p.chunk * A.chunk_stride;
-    int rk = 0;
-    // two ranks per iteration: both ranks' loads are in flight together
-    for (; rk + 1 < A.nranks; rk += 2, base += 2 * A.rank_stride) {
-      RankLoad<B, BITS> r0, r1;
-      load_rank<B, BITS>(r0, base, A.scale_off, A.elem_off, p.uoff, lane, valid, f.kbits);
-      load_rank<B, BITS>(r1, base + A.rank_stride, A.scale_off, A.elem_off, p.uoff, lane, valid,
-                         f.kbits);
-      decode_rank<B, DEC, BITS>(r0, f, acc, plain, s_lut);
-      decode_rank<B, DEC, BITS>(r1, f, acc, plain, s_lut);
+  const int nr = A.nranks;
+  uint32_t u = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (u >= total) return;
+  UnitPos p = unit_pos2(u, upc, one, A.cv, A.n);
+  int valid = max(0, min(kVPL2, p.uvalid - lane * kVPL2));
+  const uint8_t* base = A.in + (int64_t)p.chunk * A.chunk_stride;
+  RL c0, c1;  // ranks 0 and 1 of the current unit
+  load_rank<B, BITS, kVPL2>(c0, base, A.scale_off, A.elem_off, p.uoff, lane, valid, f.kbits);
+  if (nr > 1)
+    load_rank<B, BITS, kVPL2>(c1, base + A.rank_stride, A.scale_off, A.elem_off, p.uoff, lane,
+                              valid, f.kbits);
+  while (true) {
+    // prefetch ranks 0/1 of the next unit
+    const uint32_t un = u + nw;
+    const bool more = un < total;
+    UnitPos pn = p;
+    int validn = 0;
+    RL n0, n1;
+    if (more) {
+      pn = unit_pos2(un, upc, one, A.cv, A.n);
+      validn = max(0, min(kVPL2, pn.uvalid - lane * kVPL2));
+      const uint8_t* bn = A.in + (int64_t)pn.chunk * A.chunk_stride;
+      load_rank<B, BITS, kVPL2>(n0, bn, A.scale_off, A.elem_off, pn.uoff, lane, validn, f.kbits);
+      if (nr > 1)
+        load_rank<B, BITS, kVPL2>(n1, bn + A.rank_stride, A.scale_off, A.elem_off, pn.uoff, lane,
+                                  validn, f.kbits);
     }
-    if (rk < A.nranks) {
-      RankLoad<B, BITS> r0;
-      load_rank<B, BITS>(r0, base, A.scale_off, A.elem_off, p.uoff, lane, valid, f.kbits);
-      decode_rank<B, DEC, BITS>(r0, f, acc, plain, s_lut);
+    float acc[kVPL2];
+#pragma unroll
+    for (int i = 0; i < kVPL2; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
+    decode_rank<B, DEC, BITS, kVPL2>(c0, f, acc, plain, s_lut);
+    if (nr > 1) decode_rank<B, DEC, BITS, kVPL2>(c1, f, acc, plain, s_lut);
+    const uint8_t* b = A.in + (int64_t)p.chunk * A.chunk_stride + 2 * A.rank_stride;
+    for (int rk = 2; rk < nr; ++rk, b += A.rank_stride) {  // ranks 2.. in order
+      RL r;
+      load_rank<B, BITS, kVPL2>(r, b, A.scale_off, A.elem_off, p.uoff, lane, valid, f.kbits);
+      decode_rank<B, DEC, BITS, kVPL2>(r, f, acc, plain, s_lut);
     }
     if (valid > 0)
-      store_lane_out<OutT>(reinterpret_cast<OutT*>(A.out) + p.cbase + p.uoff + lane * kVPL,
-                           valid, acc);
+      store_lane_out<OutT, kVPL2>(reinterpret_cast<OutT*>(A.out) + p.cbase + p.uoff +
+                                      lane * kVPL2,
+                                  valid, acc);
+    if (!more) break;
+    u = un;
+    p = pn;
+    valid = validn;
+    c0 = n0;
+    c1 = n1;
   }
 }
 
@@ -722,6 +939,8 @@ void launch_dqsum_bf16(const DArgs& a, int block, int enc, int bits, cudaStream_
 void launch_dqsum_f16(const DArgs& a, int block, int enc, int bits, cudaStream_t st);
 void launch_dqsum_f32(const DArgs& a, int block, int enc, int bits, cudaStream_t st);
 void launch_requant(const RArgs& a, int block, int enc, int bits, cudaStream_t st);
+int64_t launch_quant_tma(const QArgs& a, int dtype_is_bf16, int block, int enc, int bits,
+                         cudaStream_t st);
 
 // Grid: enough CTAs that every warp gets `per_warp` units, never more than
 // one resident wave (#SMs x occupancy).

@@ -11,6 +11,7 @@ if [ "$mode" = tests ]; then
   timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -15 > $out/tests.txt
 fi
 timeout 300 python bench.py > $out/bench.json 2> $out/bench.err
+timeout 120 python scripts/membench.py > $out/membench.json 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $out/launches.csv python bench.py --profile > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_quant -s 2 -c 1 \
@@ -20,3 +21,4 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_dq
 cat $out/tests.txt 2>/dev/null | tail -3
 cat $out/bench.json
 tail -3 $out/bench.err
+cat $out/membench.json

@@ -383,8 +383,9 @@ def run_ours(args, shape, rank, world, local_rank):
         # dominant kernel: K1 runs nranks times per step
         kq = kernels["k_quant"]
         ach = kq["gbs"]
-        traffic = load_traffic(f"k_quant|{args.scheme}|{T}x{H}|bf16")
-        roof = {"bound": "hbm", "kernel": "k_quant<bf16,LPB4,E2M1> (K1 quantise+pack)",
+        tr = load_traffic(f"k_quant|{args.scheme}|{T}x{H}|bf16")
+        traffic = tr.get("per_launch_bytes") if isinstance(tr, dict) else tr
+        roof = {"bound": "hbm", "kernel": f"k_quant<bf16,B={sch.block_size},{sch.element.name}> (K1 quantise+pack)",
                 "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",

@@ -1,0 +1,381 @@
+"""Row-parallel linear hook + TP Llama prefill harness.
+
+Two halves:
+
+1. The reference's simulated reduction (mx/tpsim.py:146-324) -- same names
+   and report fields -- with the codec on the GPU:
+   ``TPConfig``, ``ReductionReport``, ``shard_rowwise``, ``generate_inputs``,
+   ``simulate_reduction``, ``parallelism_sweep``.  Partials are fp32
+   ``X[..., rows_r] @ W_r`` (mx/tpsim.py:263), every rank's partial goes
+   through the codec (``quantize_own``, 155/268), sums are float64 in rank
+   order (275-281) and the triangle-inequality bound is asserted (284-288).
+
+2. The deployment form of the same hook: ``RowParallelLinear`` (o_proj /
+   down_proj) whose partial sum is reduced by :class:`CompressedAllReduce`
+   (or NCCL bf16 all-reduce when ``scheme`` is None), inside a random-init
+   Llama prefill stack (``LlamaTP``) used to measure TTFT.  The GEMMs and
+   attention are ordinary cuBLAS / SDPA calls -- not the optimisation target
+   (BASELINE.json north_star).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import MinimumDegreeTwo, ShapeMismatch
+from .formats import SchemeDescriptor, parse_scheme
+
+UNCOMPRESSED_VALUE_BYTES = 2  # 16-bit activations are the uncompressed baseline
+
+
+# ---------------------------------------------------------------------------
+# 1. simulated reduction (mx/tpsim.py)
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class TPConfig:
+    """mx/tpsim.py:146-166"""
+
+    degree: int
+    scheme: object
+    seed: int = 0
+    input_shape: tuple = (1, 64, 1024)
+    weight_shape: tuple = (1024, 1024)
+    quantize_own: bool = True
+
+    def __post_init__(self):
+        if self.degree < 2:
+            raise MinimumDegreeTwo(f"degree {self.degree} < 2")
+        if len(self.input_shape) != 3 or len(self.weight_shape) != 2:
+            raise ShapeMismatch("expected (batch, tokens, d_in) and (d_in, d_out)")
+        if self.input_shape[2] != self.weight_shape[0]:
+            raise ShapeMismatch(f"d_in mismatch: input {self.input_shape[2]}, "
+                                f"weight {self.weight_shape[0]}")
+
+
+@dataclass(frozen=True)
+class ReductionReport:
+    """mx/tpsim.py:169-190"""
+
+    degree: int
+    scheme: str
+    rel_frob_err: float
+    max_abs_err: float
+    sqnr_db: float
+    bytes_compressed: int
+    bytes_uncompressed: int
+    padding: int = 0
+
+    CSV_COLUMNS = ("degree", "scheme", "rel_frob_err", "max_abs_err", "sqnr_db",
+                   "bytes_compressed", "bytes_uncompressed")
+
+
+def shard_rowwise(weight, degree: int):
+    """Split (d_in, d_out) into ``degree`` row shards, zero-padding d_in
+    (mx/tpsim.py:193-215).  numpy or torch; returns (shards, padding)."""
+    if weight.ndim != 2:
+        raise ShapeMismatch(f"weight must be 2-D, got shape {tuple(weight.shape)}")
+    if degree < 1:
+        raise ShapeMismatch("degree must be positive")
+    d_in = weight.shape[0]
+    rows = -(-d_in // degree)
+    pad = rows * degree - d_in
+    if pad:
+        if isinstance(weight, np.ndarray):
+            weight = np.concatenate([weight, np.zeros((pad, weight.shape[1]), weight.dtype)])
+        else:
+            import torch
+
+            weight = torch.cat([weight, weight.new_zeros(pad, weight.shape[1])])
+    return [weight[i * rows:(i + 1) * rows] for i in range(degree)], pad
+
+
+def generate_inputs(cfg: TPConfig):
+    """Seeded activations with outliers and N(0,1) weights (mx/tpsim.py:218-223)."""
+    from .synth import gaussian_with_outliers
+
+    rng = np.random.default_rng(cfg.seed)
+    x = gaussian_with_outliers(rng, cfg.input_shape)
+    w = rng.standard_normal(cfg.weight_shape).astype(np.float32)
+    return x, w
+
+
+def _sqnr_db(ref: np.ndarray, err: np.ndarray) -> float:
+    e = float(np.sum(np.square(err)))
+    if e == 0.0:
+        return float("inf")
+    return 10.0 * np.log10(float(np.sum(np.square(ref))) / e)  # as mx/tpsim.py:231
+
+
+def simulate_reduction(cfg: TPConfig, x=None, w=None, partials_on_gpu: bool = False,
+                       partials=None):
+    """One compress/exchange/decompress/reduce cycle, scored (mx/tpsim.py:234-302).
+
+    The codec runs on the GPU (compress_tensor / decompress_tensor through
+    the sm_100a kernels).  Partials are computed with numpy (bit-identical to
+    the reference) unless ``partials_on_gpu`` (cuBLAS fp32, faster, sums
+    differ in the last bits).  ``partials`` injects precomputed fp32 partial
+    products (one per rank) -- BLAS results depend on the host CPU, so parity
+    tests replay the reference's own partials."""
+    import torch
+
+    from .codec import compress_tensor_device, decompress_tensor_device, serialized_nbytes
+
+    if x is None or w is None:
+        gx, gw = generate_inputs(cfg)
+        x = gx if x is None else x
+        w = gw if w is None else w
+    x = np.asarray(x, dtype=np.float32)
+    w = np.asarray(w, dtype=np.float32)
+    if x.shape[-1] != w.shape[0]:
+        raise ShapeMismatch(f"d_in mismatch: {x.shape[-1]} vs {w.shape[0]}")
+    shards, padding = shard_rowwise(w, cfg.degree)
+    if padding:
+        x = np.pad(x, [(0, 0)] * (x.ndim - 1) + [(0, padding)])
+    rows = shards[0].shape[0]
+    scheme = cfg.scheme if isinstance(cfg.scheme, SchemeDescriptor) else parse_scheme(
+        str(cfg.scheme), extensions=True)
+    given = partials
+    partials, decoded = [], []
+    for r in range(cfg.degree):
+        xs = x[..., r * rows:(r + 1) * rows]
+        if given is not None:
+            p = np.asarray(given[r], dtype=np.float32)
+        elif partials_on_gpu:
+            p = (torch.from_numpy(np.ascontiguousarray(xs)).cuda()
+                 @ torch.from_numpy(shards[r]).cuda()).cpu().numpy()
+        else:
+            p = xs @ shards[r]  # float32, like the deployed matmul (tpsim.py:263)
+        partials.append(p)
+        if cfg.quantize_own or r != 0:
+            dct = compress_tensor_device(torch.from_numpy(np.ascontiguousarray(p)).cuda(), scheme)
+            decoded.append(decompress_tensor_device(dct, torch.float64).cpu().numpy())
+        else:
+            decoded.append(p.astype(np.float64))
+    ref = np.zeros(partials[0].shape, np.float64)
+    red = np.zeros_like(ref)
+    per = np.zeros_like(ref)
+    for r in range(cfg.degree):  # float64, rank order (tpsim.py:275-281)
+        ref += partials[r].astype(np.float64)
+        red += decoded[r]
+        per += np.abs(decoded[r] - partials[r].astype(np.float64))
+    err = red - ref
+    tol = 1e-9 * (np.abs(ref) + 1.0)
+    if not (np.abs(err) <= per + tol).all():  # tpsim.py:284-288
+        raise AssertionError("summed error exceeded per-worker error budget")
+    en, rn = float(np.linalg.norm(err.ravel())), float(np.linalg.norm(ref.ravel()))
+    payload = serialized_nbytes(scheme, partials[0].shape)  # container size (codec.py:291)
+    return ReductionReport(
+        degree=cfg.degree, scheme=scheme.name, rel_frob_err=0.0 if en == 0.0 else en / rn,
+        max_abs_err=float(np.max(np.abs(err))), sqnr_db=_sqnr_db(ref, err),
+        bytes_compressed=(cfg.degree - 1) * int(payload),
+        bytes_uncompressed=(cfg.degree - 1) * ref.size * UNCOMPRESSED_VALUE_BYTES,
+        padding=padding)
+
+
+def parallelism_sweep(cfg: TPConfig, degrees):
+    """mx/tpsim.py:305-324"""
+    degrees = list(degrees)
+    if not degrees:
+        raise MinimumDegreeTwo("no degrees requested")
+    for d in degrees:
+        if d < 2:
+            raise MinimumDegreeTwo(f"degree {d} < 2")
+    return [simulate_reduction(TPConfig(d, cfg.scheme, cfg.seed, cfg.input_shape,
+                                        cfg.weight_shape, cfg.quantize_own)) for d in degrees]
+
+
+# ---------------------------------------------------------------------------
+# 2. TP Llama prefill with the compressed row-parallel hook
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class LlamaConfig:
+    hidden: int
+    ffn: int
+    layers: int
+    heads: int
+    kv_heads: int
+    vocab: int = 128256
+    rope_theta: float = 500000.0
+    eps: float = 1e-5
+
+    @property
+    def head_dim(self) -> int:
+        return self.hidden // self.heads
+
+
+LLAMA31_8B = LlamaConfig(4096, 14336, 32, 32, 8)
+LLAMA31_70B = LlamaConfig(8192, 28672, 80, 64, 8)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def make_module_classes():
+    """Build the nn.Module classes lazily (torch import stays optional for
+    the pure-host parts of the package)."""
+    torch = _torch()
+    nn = torch.nn
+    F = torch.nn.functional
+
+    class RowParallelLinear(nn.Module):
+        """y = all_reduce(x_local @ W_r): the hook of mx/tpsim.py:263-281.
+
+        ``scheme`` None -> uncompressed NCCL bf16 all-reduce; otherwise the
+        MX-compressed all-reduce (one-shot or two-shot)."""
+
+        def __init__(self, d_in_local, d_out, group=None, scheme=None, algo="oneshot",
+                     tokens=None, device="cuda", dtype=torch.bfloat16, std=0.02):
+            super().__init__()
+            self.weight = nn.Parameter(torch.randn(d_out, d_in_local, device=device, dtype=dtype)
+                                       * std, requires_grad=False)
+            self.group, self.scheme, self.algo = group, scheme, algo
+            self._car = {}
+
+        def reduce(self, y):
+            import torch.distributed as dist
+
+            if self.scheme is None:
+                if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+                    dist.all_reduce(y, group=self.group)
+                return y
+            from .collective import CompressedAllReduce
+
+            key = (y.numel(), y.dtype)
+            car = self._car.get(key)
+            if car is None:
+                ws = dist.get_world_size(self.group) if dist.is_initialized() else 1
+                rk = dist.get_rank(self.group) if dist.is_initialized() else 0
+                car = CompressedAllReduce(self.scheme, y.numel(), group=self.group,
+                                          algo=self.algo, out_dtype=y.dtype, device=y.device,
+                                          world_size=ws, rank=rk)
+                self._car[key] = car
+            return car(y)
+
+        def forward(self, x):
+            return self.reduce(F.linear(x, self.weight))
+
+    class ColumnParallelLinear(nn.Module):
+        def __init__(self, d_in, d_out_local, device="cuda", dtype=torch.bfloat16, std=0.02):
+            super().__init__()
+            self.weight = nn.Parameter(torch.randn(d_out_local, d_in, device=device, dtype=dtype)
+                                       * std, requires_grad=False)
+
+        def forward(self, x):
+            return F.linear(x, self.weight)
+
+    class RMSNorm(nn.Module):
+        def __init__(self, d, eps, device, dtype):
+            super().__init__()
+            self.w = nn.Parameter(torch.ones(d, device=device, dtype=dtype), requires_grad=False)
+            self.eps = eps
+
+        def forward(self, x):
+            xf = x.float()
+            return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + self.eps)).to(x.dtype) \
+                * self.w
+
+    class LlamaTPBlock(nn.Module):
+        def __init__(self, cfg: LlamaConfig, tp: int, group, scheme, algo, device, dtype):
+            super().__init__()
+            if cfg.heads % tp or cfg.kv_heads % tp and tp % cfg.kv_heads:
+                raise ShapeMismatch(f"heads {cfg.heads}/{cfg.kv_heads} vs tp {tp}")
+            self.hl = cfg.heads // tp
+            self.kvl = max(1, cfg.kv_heads // tp)
+            self.hd = cfg.head_dim
+            self.cfg = cfg
+            self.ln1 = RMSNorm(cfg.hidden, cfg.eps, device, dtype)
+            self.ln2 = RMSNorm(cfg.hidden, cfg.eps, device, dtype)
+            self.qkv = ColumnParallelLinear(cfg.hidden, (self.hl + 2 * self.kvl) * self.hd,
+                                            device, dtype)
+            self.o_proj = RowParallelLinear(self.hl * self.hd, cfg.hidden, group, scheme, algo,
+                                            device=device, dtype=dtype)
+            self.gate_up = ColumnParallelLinear(cfg.hidden, 2 * (cfg.ffn // tp), device, dtype)
+            self.down_proj = RowParallelLinear(cfg.ffn // tp, cfg.hidden, group, scheme, algo,
+                                               device=device, dtype=dtype)
+
+        def forward(self, h, cos, sin):
+            b, t, _ = h.shape
+            x = self.ln1(h)
+            qkv = self.qkv(x).view(b, t, self.hl + 2 * self.kvl, self.hd)
+            q, k, v = qkv.split([self.hl, self.kvl, self.kvl], dim=2)
+            q, k = _rope(q, cos, sin), _rope(k, cos, sin)
+            q, k, v = (z.transpose(1, 2) for z in (q, k, v))
+            a = F.scaled_dot_product_attention(q, k, v, is_causal=True,
+                                               enable_gqa=self.hl != self.kvl)
+            h = h + self.o_proj(a.transpose(1, 2).reshape(b, t, self.hl * self.hd))
+            g, u = self.gate_up(self.ln2(h)).chunk(2, dim=-1)
+            return h + self.down_proj(F.silu(g) * u)
+
+    def _rope(x, cos, sin):
+        x1, x2 = x[..., : x.shape[-1] // 2], x[..., x.shape[-1] // 2:]
+        return (x * cos + torch.cat([-x2, x1], dim=-1) * sin).to(x.dtype)
+
+    class LlamaTP(nn.Module):
+        """Random-init Llama prefill stack, TP-sharded (no embedding/LM head:
+        TTFT of the transformer body, where the all-reduces live)."""
+
+        def __init__(self, cfg: LlamaConfig, tp: int = 1, group=None, scheme=None,
+                     algo="oneshot", layers=None, device="cuda", dtype=torch.bfloat16):
+            super().__init__()
+            self.cfg = cfg
+            self.blocks = nn.ModuleList(LlamaTPBlock(cfg, tp, group, scheme, algo, device, dtype)
+                                        for _ in range(layers or cfg.layers))
+            self.norm = RMSNorm(cfg.hidden, cfg.eps, device, dtype)
+
+        def rope_cache(self, t, device, dtype):
+            hd = self.cfg.head_dim
+            inv = 1.0 / (self.cfg.rope_theta ** (torch.arange(0, hd, 2, device=device).float()
+                                                 / hd))
+            ang = torch.outer(torch.arange(t, device=device).float(), inv)
+            ang = torch.cat([ang, ang], dim=-1)[None, :, None, :]
+            return ang.cos().to(dtype), ang.sin().to(dtype)
+
+        def forward(self, h):
+            cos, sin = self.rope_cache(h.shape[1], h.device, h.dtype)
+            for blk in self.blocks:
+                h = blk(h, cos, sin)
+            return self.norm(h)
+
+    return RowParallelLinear, ColumnParallelLinear, LlamaTPBlock, LlamaTP
+
+
+def measure_ttft(cfg: LlamaConfig, batch: int, seq: int, tp: int = 1, group=None, scheme=None,
+                 algo="oneshot", layers=None, reps: int = 5, warmup: int = 2, seed: int = 0):
+    """Prefill latency (ms, max over ranks) of the TP body on random data."""
+    torch = _torch()
+    import torch.distributed as dist
+
+    torch.manual_seed(seed)
+    _, _, _, LlamaTP = make_module_classes()
+    model = LlamaTP(cfg, tp, group, scheme, algo, layers)
+    h = torch.randn(batch, seq, cfg.hidden, device="cuda", dtype=torch.bfloat16)
+    with torch.inference_mode():
+        for _ in range(warmup):
+            model(h)
+        torch.cuda.synchronize()
+        if dist.is_initialized():
+            dist.barrier(group)
+        times = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            model(h)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    ms = float(np.median(times))
+    if dist.is_initialized():
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        ms = float(t.item())
+    return ms

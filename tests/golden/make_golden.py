@@ -174,6 +174,35 @@ def main():
             got = e.block_index
         out["nonfinite"].append({"index": idx, "value": str(bad), "block": blk, "block_index": got})
 
+    # -- simulated TP reduction reports (mx/tpsim.py:234-302) ------------------
+    from mxcomm import tpsim as rtp
+    out["tpsim"] = []
+    for deg, spec, seed, ishape, wshape, own in [
+            (2, "fp4_e2m1:32:e8m0", 0, (1, 16, 64), (64, 48), True),
+            (4, "fp5_e2m2:16:e5m0", 7, (2, 8, 30), (30, 24), True),
+            (3, "int4:8:e8m0", 3, (1, 8, 25), (25, 16), False),
+            (8, "fp4_e2m1:32:e8m0", 1, (1, 16, 64), (64, 64), True)]:
+        cfg = rtp.TPConfig(deg, rformats.parse_scheme(spec), seed, ishape, wshape, own)
+        rep = rtp.simulate_reduction(cfg)
+        # the reference's own fp32 partials (BLAS results depend on the host
+        # CPU, so they are stored; mx/tpsim.py:251-263)
+        x, w = rtp.generate_inputs(cfg)
+        shards, pad = rtp.shard_rowwise(w, deg)
+        if pad:
+            x = np.pad(x, [(0, 0)] * (x.ndim - 1) + [(0, pad)])
+        rows = shards[0].shape[0]
+        parts = [x[..., r * rows:(r + 1) * rows] @ shards[r] for r in range(deg)]
+        out["tpsim"].append({"degree": deg, "scheme": spec, "seed": seed, "input_shape": ishape,
+                             "weight_shape": wshape, "quantize_own": own,
+                             "partials_f32_hex": [p.astype(np.float32).tobytes().hex()
+                                                  for p in parts],
+                             "partial_shape": list(parts[0].shape),
+                             "rel_frob_err": float(rep.rel_frob_err).hex(),
+                             "max_abs_err": float(rep.max_abs_err).hex(),
+                             "sqnr_db": float(rep.sqnr_db).hex(),
+                             "bytes_compressed": rep.bytes_compressed,
+                             "bytes_uncompressed": rep.bytes_uncompressed, "padding": rep.padding})
+
     # -- large prefill shape -------------------------------------------------
     T, H = inputs.LARGE_SHAPE
     p0 = mysynth.bf16_round(rsynth.gaussian_with_outliers(np.random.default_rng(0), (T, H)))

@@ -148,6 +148,20 @@ int mx_dequant_sum_requant(const uint8_t* shards, int64_t rank_stride, int32_t n
                            uint8_t* out_shard, uint64_t* nonfinite, void* workspace,
                            int64_t workspace_bytes, void* stream);
 
+/* The whole one-shot compressed all-reduce of `nranks` partials that live on
+ * THIS device, fused into one persistent kernel: quantise each partial into
+ * its shard (shards + r*shard_stride, mx_shard_layout(n) offsets), grid-wide
+ * barrier, fp32 rank-order dequant-sum into `out`.  Bit-identical to
+ * mx_quantize x nranks + mx_dequant_sum.  `partials` is a DEVICE array of
+ * nranks pointers (bf16, 32-byte aligned); `barrier` is 2 device uint32
+ * zeroed once (reusable across calls on one stream).  Returns
+ * MX_ERR_UNSUPPORTED outside bf16-in, bf16/f32-out, B in {8,16,32,64}, E8M0,
+ * element widths 4/5/6/8. */
+int mx_allreduce_fused(const void* const* partials, int32_t dtype, int32_t nranks, int64_t n,
+                       const mx_scheme_t* scheme, uint8_t* shards, int64_t shard_stride,
+                       void* out, int32_t out_dtype, uint32_t* barrier, uint64_t* nonfinite,
+                       void* stream);
+
 /* unpack_bits (mx/bitpack.py:37-58) on the device: `count` codes of
  * `width` bits -> one uint8 per code (quantize_block's return value). */
 int mx_unpack_codes(const uint8_t* packed, int64_t count, int32_t width, uint8_t* codes,

@@ -50,6 +50,8 @@ SIGNATURES = {
     "mx_dequant_sum": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_i64, c_i64, _SP, c_vp, c_i32, c_vp]),
     "mx_dequant_sum_requant": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_i64, _SP, c_vp, c_vp, c_vp,
                                        c_i64, c_vp]),
+    "mx_allreduce_fused": (c_i32, [c_vp, c_i32, c_i32, c_i64, _SP, c_vp, c_i64, c_vp, c_i32,
+                                   c_vp, c_vp, c_vp]),
     "mx_unpack_codes": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp]),
     "mx_pack_codes": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp]),
     "mx_nonfinite_reset": (c_i32, [c_vp, c_vp]),

@@ -19,10 +19,14 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmxb200.so")
-BUILD = os.path.join(ROOT, "build")
+# objects live outside the repo so the gpurun snapshot carries only the .so
+BUILD = os.environ.get("MXB200_BUILD_DIR", "/tmp/mxb200_build")
+# -lineinfo (ncu source view) only where the profiled kernels live: it
+# roughly doubles object size
+LINEINFO = {"k_quant_bf16.cu", "k_dqsum_bf16.cu", "k_fused.cu", "k_requant.cu"}
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+FLAGS = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "-I", os.path.join(ROOT, "include")]
 
 
@@ -48,7 +52,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-        cmd = [nv, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        extra = ["-lineinfo"] if os.path.basename(src) in LINEINFO else []
+        cmd = [nv, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{p.stderr}")

@@ -112,6 +112,19 @@ class NativeBackend:
     def reset_flag(self, flag):
         _native.check(self.lib.mx_nonfinite_reset(self._p(flag), self._st()), "mx_nonfinite_reset")
 
+    def allreduce_fused(self, ptrs, dtype, nranks, n, shards, stride, out, barrier, flag):
+        """One persistent kernel: quantise the local partials, grid barrier,
+        dequant-sum.  Returns False when the scheme/dtype has no fused
+        instantiation (the caller then runs K1 + K2)."""
+        rc = self.lib.mx_allreduce_fused(
+            self._p(ptrs), dtype, nranks, n, ctypes.byref(self.cs), self._p(shards), stride,
+            self._p(out), self._dt(out), self._p(barrier),
+            self._p(flag) if flag is not None else None, self._st())
+        if rc == -8:  # MX_ERR_UNSUPPORTED
+            return False
+        _native.check(rc, "mx_allreduce_fused")
+        return True
+
 
 # ---------------------------------------------------------------------------
 # the collective
@@ -254,7 +267,7 @@ class SimulatedAllReduce:
     TP=2", BASELINE.json configs[0])."""
 
     def __init__(self, scheme, n: int, nranks: int, algo: str = "oneshot", out_dtype=None,
-                 device="cuda", backend=None):
+                 device="cuda", backend=None, fused: bool = True):
         import torch
 
         if isinstance(scheme, str):
@@ -270,6 +283,13 @@ class SimulatedAllReduce:
         self.flag = torch.empty(1, dtype=torch.int64, device=dev)
         self.be.reset_flag(self.flag)
         self.out = torch.empty(n, dtype=self.out_dtype, device=dev)
+        # fused one-shot (one persistent kernel) when the backend offers it
+        import os
+
+        self.fused = (fused and algo == "oneshot" and hasattr(self.be, "allreduce_fused")
+                      and os.environ.get("MXB200_FUSED", "1") != "0")
+        self._ptrs_key = None
+        self.barrier = torch.zeros(2, dtype=torch.int32, device=dev) if self.fused else None
         if algo == "oneshot":
             _, _, S = self.be.layout(n)
             self.S, self.c = S, n
@@ -321,8 +341,26 @@ class SimulatedAllReduce:
     def __call__(self, partials, out=None):
         if len(partials) != self.N or any(p.numel() != self.n for p in partials):
             raise ShapeMismatch(f"expected {self.N} partials of {self.n} values")
+        if self.fused and self._fused(partials, out):
+            return (self.out if out is None else out).view(partials[0].shape)
         self.quantize(partials)
         return self.reduce(out).view(partials[0].shape)
+
+    def _fused(self, partials, out):
+        import torch
+
+        if any(p.dtype != torch.bfloat16 or not p.is_contiguous() for p in partials):
+            return False
+        key = tuple(p.data_ptr() for p in partials)
+        if key != self._ptrs_key:  # device array of the partials' addresses
+            self._ptrs = torch.tensor(key, dtype=torch.int64).to(self.device)
+            self._ptrs_key = key
+        o = self.out if out is None else out.reshape(-1)
+        ok = self.be.allreduce_fused(self._ptrs, _native.MX_BF16, self.N, self.n, self.gathered,
+                                     self.S, o, self.barrier, self.flag)
+        if not ok:
+            self.fused = False
+        return ok
 
 
 def simulate_allreduce(partials, scheme, algo: str = "oneshot", out_dtype=None, backend=None):

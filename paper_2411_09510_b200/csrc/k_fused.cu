@@ -1,0 +1,213 @@
+// Fused one-shot compressed all-reduce in ONE persistent kernel:
+//   phase 1  K1: every local partial is quantised into its slot of the
+//            gather buffer (the bytes an all-gather would deliver),
+//   barrier  grid-wide (all CTAs resident: the grid is one occupancy wave),
+//   phase 2  K2: the N shards are decoded and summed in fp32 rank order.
+// Two kernel boundaries (~2 us of launch/ramp/drain each at these sizes)
+// disappear.  This is the single-device form of the NVLink-pull fused
+// collective (peer shards read in phase 2); the per-phase code is exactly the
+// K1/K2 code of mx_kernels.cuh, so results are bit-identical to
+// quantise -> all-gather -> dequant-sum (mx/netbench.py:323-334).
+#include "mx_kernels.cuh"
+
+namespace mxb {
+
+namespace {
+
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Sense-free generation barrier across all CTAs of the grid.
+__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int gen = ld_acquire(bar + 1);
+    __threadfence();  // release this CTA's phase-1 stores
+    const unsigned int arrived = atomicAdd(bar, 1u) + 1u;
+    if (arrived == gridDim.x) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (ld_acquire(bar + 1) == gen) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <typename InT, typename OutT, int B, int ENC, int BITS>
+__global__ void __launch_bounds__(kThreads, 3) k_fused_oneshot(const FArgs F) {
+  constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
+  __shared__ __align__(16) uint8_t s_stage[kWarps][kUnit / 8];
+  __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
+  const Fmt f = F.f;
+  if constexpr (DEC != ENC_E2M1) fill_lut(s_lut, f);  // visible after the grid barrier
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = (uint32_t)(gridDim.x * kWarps);
+  const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+
+  // ---- phase 1: quantise every local partial (K1) ----------------------
+  {
+    QArgs A;
+    A.n = F.n;
+    A.cv = F.n;
+    A.units_per_chunk = (F.n + kUnit - 1) / kUnit;
+    A.total_units = A.units_per_chunk;
+    A.chunk_stride = 0;
+    A.nonfinite = F.nonfinite;
+    A.flat_off = 0;
+    A.f = f;
+    const uint32_t upp = (uint32_t)A.units_per_chunk;
+    const uint32_t nfull = (uint32_t)(F.n / kUnit);
+    uint8_t* stage = s_stage[threadIdx.x >> 5];
+    // units of all partials in one round-robin sequence u -> (rank, unit);
+    // taken in pairs whose loads are both in flight before any math
+    const uint32_t total = upp * (uint32_t)F.nranks;
+    for (uint32_t u0 = gw; u0 < total; u0 += 2 * nw) {
+      const uint32_t u1 = u0 + nw;
+      const bool has1 = u1 < total;
+      const uint32_t r0 = u0 / upp, q0 = u0 - r0 * upp;
+      const uint32_t r1 = has1 ? u1 / upp : r0, q1 = has1 ? u1 - r1 * upp : q0;
+      const InT* x0 = reinterpret_cast<const InT*>(F.partials[r0]);
+      const InT* x1 = reinterpret_cast<const InT*>(F.partials[r1]);
+      const bool full0 = q0 < nfull && f.kbits == 8, full1 = has1 && q1 < nfull && f.kbits == 8;
+      Raw<InT> w0, w1;
+      if (full0) load_raw<InT>(x0 + (size_t)q0 * kUnit + lane * kVPL, w0);
+      if (full1) load_raw<InT>(x1 + (size_t)q1 * kUnit + lane * kVPL, w1);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1 && !has1) break;
+        const uint32_t r = h ? r1 : r0, q = h ? q1 : q0;
+        A.x = F.partials[r];
+        A.scale_base = F.shards + r * F.shard_stride + F.scale_off;
+        A.elem_base = F.shards + r * F.shard_stride + F.elem_off;
+        if (h ? full1 : full0) {
+          quant_full_unit<InT, B, ENC, BITS>(A, f, q, h ? w1 : w0, lane);
+        } else {
+          UnitPos p = unit_pos(q, upp, true, A.cv, A.n);
+          Raw<InT> raw;
+          load_unit<InT>(reinterpret_cast<const InT*>(A.x), p, lane, raw);
+          quant_unit<InT, B, ENC, BITS>(A, f, p, raw, lane, stage);
+        }
+      }
+    }
+  }
+
+  grid_barrier(F.bar);
+
+  // ---- phase 2: decode the N shards in rank order, fp32 sum (K2) -------
+  // ranks 0/1 of the next unit are prefetched while this unit decodes;
+  // ld.global.cg: the shards were written by other CTAs of this kernel
+  {
+    using RL = RankLoad<B, BITS, kVPL2>;
+    const uint32_t total = (uint32_t)((F.n + kUnit2 - 1) / kUnit2);
+    const int nr = F.nranks;
+    uint32_t u = gw;
+    if (u < total) {
+      int64_t uoff = (int64_t)u * kUnit2;
+      int valid = max(0, min(kVPL2, (int)min((int64_t)kUnit2, F.n - uoff) - lane * kVPL2));
+      RL c0, c1;
+      load_rank<B, BITS, kVPL2, true>(c0, F.shards, F.scale_off, F.elem_off, uoff, lane, valid,
+                                      f.kbits);
+      if (nr > 1)
+        load_rank<B, BITS, kVPL2, true>(c1, F.shards + F.shard_stride, F.scale_off, F.elem_off,
+                                        uoff, lane, valid, f.kbits);
+      while (true) {
+        const uint32_t un = u + nw;
+        const bool more = un < total;
+        int64_t uoffn = uoff;
+        int validn = 0;
+        RL n0, n1;
+        if (more) {
+          uoffn = (int64_t)un * kUnit2;
+          validn = max(0, min(kVPL2, (int)min((int64_t)kUnit2, F.n - uoffn) - lane * kVPL2));
+          load_rank<B, BITS, kVPL2, true>(n0, F.shards, F.scale_off, F.elem_off, uoffn, lane,
+                                          validn, f.kbits);
+          if (nr > 1)
+            load_rank<B, BITS, kVPL2, true>(n1, F.shards + F.shard_stride, F.scale_off,
+                                            F.elem_off, uoffn, lane, validn, f.kbits);
+        }
+        float acc[kVPL2];
+#pragma unroll
+        for (int i = 0; i < kVPL2; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
+        decode_rank<B, DEC, BITS, kVPL2>(c0, f, acc, false, s_lut);
+        if (nr > 1) decode_rank<B, DEC, BITS, kVPL2>(c1, f, acc, false, s_lut);
+        const uint8_t* b = F.shards + 2 * F.shard_stride;
+        for (int rk = 2; rk < nr; ++rk, b += F.shard_stride) {
+          RL r;
+          load_rank<B, BITS, kVPL2, true>(r, b, F.scale_off, F.elem_off, uoff, lane, valid,
+                                          f.kbits);
+          decode_rank<B, DEC, BITS, kVPL2>(r, f, acc, false, s_lut);
+        }
+        if (valid > 0)
+          store_lane_out<OutT, kVPL2>(reinterpret_cast<OutT*>(F.out) + uoff + lane * kVPL2,
+                                      valid, acc);
+        if (!more) break;
+        u = un;
+        uoff = uoffn;
+        valid = validn;
+        c0 = n0;
+        c1 = n1;
+      }
+    }
+  }
+}
+
+template <typename InT, typename OutT, int B, int ENC, int BITS>
+void go(const FArgs& a, cudaStream_t st) {
+  auto k = k_fused_oneshot<InT, OutT, B, ENC, BITS>;
+  static thread_local int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, 0);
+  if (occ < 1) occ = 1;
+  // every CTA must be resident for the grid barrier: at most one wave
+  k<<<(unsigned)(sms * occ), kThreads, 0, st>>>(a);
+}
+
+template <typename InT, typename OutT, int B>
+void by_enc(const FArgs& a, int enc, int bits, cudaStream_t st) {
+  switch (enc) {
+    case ENC_E2M1: go<InT, OutT, B, ENC_E2M1, 4>(a, st); return;
+    case ENC_E2M3: go<InT, OutT, B, ENC_E2M3, 6>(a, st); return;
+    case ENC_E3M2: go<InT, OutT, B, ENC_E3M2, 6>(a, st); return;
+  }
+  switch (bits) {
+    case 4: go<InT, OutT, B, ENC_GEN, 4>(a, st); return;
+    case 5: go<InT, OutT, B, ENC_GEN, 5>(a, st); return;
+    case 6: go<InT, OutT, B, ENC_GEN, 6>(a, st); return;
+    default: go<InT, OutT, B, ENC_GEN, 8>(a, st); return;
+  }
+}
+
+template <typename OutT>
+void by_block(const FArgs& a, int block, int enc, int bits, cudaStream_t st) {
+  switch (block) {
+    case 8: by_enc<__nv_bfloat16, OutT, 8>(a, enc, bits, st); return;
+    case 16: by_enc<__nv_bfloat16, OutT, 16>(a, enc, bits, st); return;
+    case 32: by_enc<__nv_bfloat16, OutT, 32>(a, enc, bits, st); return;
+    case 64: by_enc<__nv_bfloat16, OutT, 64>(a, enc, bits, st); return;
+  }
+}
+
+}  // namespace
+
+// bf16 partials -> bf16/f32 out; element widths 4/5/6/8 (the BASELINE sweep)
+bool launch_fused_oneshot(const FArgs& a, int out_is_bf16, int block, int enc, int bits,
+                          cudaStream_t st) {
+  if (!(block == 8 || block == 16 || block == 32 || block == 64)) return false;
+  if (!(bits == 4 || bits == 5 || bits == 6 || bits == 8)) return false;
+  if (out_is_bf16) by_block<__nv_bfloat16>(a, block, enc, bits, st);
+  else by_block<float>(a, block, enc, bits, st);
+  return true;
+}
+
+}  // namespace mxb

@@ -562,6 +562,32 @@ int mx_dequant_sum_requant(const uint8_t* shards, int64_t rank_stride, int32_t n
                        rest_bytes, st);
 }
 
+int mx_allreduce_fused(const void* const* partials, int32_t dtype, int32_t nranks, int64_t n,
+                       const mx_scheme_t* s, uint8_t* shards, int64_t shard_stride, void* out,
+                       int32_t out_dtype, uint32_t* barrier, uint64_t* nonfinite, void* stream) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (n <= 0 || nranks < 1) return fail(MX_ERR_INVALID_ARGUMENT, "bad sizes");
+  if (!partials || !shards || !out || !barrier) return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
+  int64_t so, eo, sbytes;
+  mx_shard_layout(n, s, &so, &eo, &sbytes);
+  if (shard_stride < sbytes || shard_stride % 32 != 0)
+    return fail(MX_ERR_INVALID_ARGUMENT, "shard_stride must be >= shard bytes and 32-aligned");
+  Fmt f = make_fmt(s);
+  if (dtype != MX_BF16 || (out_dtype != MX_BF16 && out_dtype != MX_F32) || !aligned(shards, 32) ||
+      !aligned(out, 32) || !fast_block(s->block_size) || f.kbits != 8)
+    return fail(MX_ERR_UNSUPPORTED, "fused path: bf16 in, bf16/f32 out, B in {8,16,32,64}, E8M0");
+  FArgs a;
+  a.partials = partials; a.nranks = nranks; a.n = n;
+  a.shards = shards; a.shard_stride = shard_stride; a.scale_off = so; a.elem_off = eo;
+  a.out = out; a.bar = barrier; a.nonfinite = reinterpret_cast<unsigned long long*>(nonfinite);
+  a.f = f;
+  if (!launch_fused_oneshot(a, out_dtype == MX_BF16, (int)s->block_size, enc_of(s), f.bits,
+                            (cudaStream_t)stream))
+    return fail(MX_ERR_UNSUPPORTED, "fused path: element width %d not instantiated", f.bits);
+  return cuda_check("k_fused_oneshot");
+}
+
 int mx_unpack_codes(const uint8_t* packed, int64_t count, int32_t width, uint8_t* codes, void* stream) {
   if (width < 1 || width > 8) return fail(MX_ERR_INVALID_ARGUMENT, "width %d outside [1, 8]", width);
   if (count <= 0) return MX_OK;

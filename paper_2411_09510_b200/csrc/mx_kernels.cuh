@@ -309,8 +309,17 @@ __device__ __forceinline__ LaneCodes<BITS> load_lane_codes(const uint8_t* __rest
   return c;
 }
 
+// Read-only loads for K2.  CG = true uses ld.global.cg (L2, coherent) for
+// data written earlier in the SAME kernel (the fused collective's phase 2);
+// otherwise the non-coherent read-only path.
+template <bool CG, typename T>
+__device__ __forceinline__ T ldro(const T* p) {
+  if constexpr (CG) return __ldcg(p);
+  else return __ldg(p);
+}
+
 // The lane's 16 codes (2b bytes at p = unit base + 2b*lane) for K2.
-template <int BITS>
+template <int BITS, bool CG = false>
 __device__ __forceinline__ LaneCodes<BITS, 16> load_lane_codes16(const uint8_t* __restrict__ p,
                                                                  int valid) {
   LaneCodes<BITS, 16> c;
@@ -319,18 +328,18 @@ __device__ __forceinline__ LaneCodes<BITS, 16> load_lane_codes16(const uint8_t* 
   for (int i = 0; i < NW; ++i) c.w[i] = 0u;
   if (valid == 16) {
     if constexpr (BITS == 8) {
-      uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
+      uint4 a = ldro<CG>(reinterpret_cast<const uint4*>(p));
       c.w[0] = a.x; c.w[1] = a.y; c.w[2] = a.z; c.w[3] = a.w;
     } else if constexpr (BITS == 4) {
-      uint2 a = __ldg(reinterpret_cast<const uint2*>(p));
+      uint2 a = ldro<CG>(reinterpret_cast<const uint2*>(p));
       c.w[0] = a.x; c.w[1] = a.y;
     } else if constexpr (BITS % 2 == 0) {
 #pragma unroll
-      for (int i = 0; i < BITS / 2; ++i) c.w[i] = __ldg(reinterpret_cast<const uint32_t*>(p) + i);
+      for (int i = 0; i < BITS / 2; ++i) c.w[i] = ldro<CG>(reinterpret_cast<const uint32_t*>(p) + i);
     } else {
 #pragma unroll
       for (int i = 0; i < BITS; ++i)
-        c.w[i >> 1] |= (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(p) + i)
+        c.w[i >> 1] |= (uint32_t)ldro<CG>(reinterpret_cast<const unsigned short*>(p) + i)
                        << (16 * (i & 1));
     }
   } else if (valid > 0) {
@@ -666,7 +675,7 @@ struct RankLoad {
   int st[Geo<B, VPL>::NSB];
 };
 
-template <int B, int BITS, int VPL = kVPL>
+template <int B, int BITS, int VPL = kVPL, bool CG = false>
 __device__ __forceinline__ void load_rank(RankLoad<B, BITS, VPL>& r,
                                           const uint8_t* __restrict__ base, int64_t scale_off,
                                           int64_t elem_off, int64_t uoff, int lane, int valid,
@@ -674,7 +683,7 @@ __device__ __forceinline__ void load_rank(RankLoad<B, BITS, VPL>& r,
   constexpr int NSB = Geo<B, VPL>::NSB;
   constexpr int LPB = Geo<B, VPL>::LPB;
   const uint8_t* el = base + elem_off + (uoff / 8) * BITS + lane * (VPL * BITS / 8);
-  if constexpr (VPL == 16) r.c = load_lane_codes16<BITS>(el, valid);
+  if constexpr (VPL == 16) r.c = load_lane_codes16<BITS, CG>(el, valid);
   else r.c = load_lane_codes<BITS>(el, valid);
   const uint8_t* sc = base + scale_off;
   const int64_t blk0 = uoff / B + (lane / LPB) * NSB;
@@ -682,15 +691,15 @@ __device__ __forceinline__ void load_rank(RankLoad<B, BITS, VPL>& r,
   for (int sb = 0; sb < NSB; ++sb) r.st[sb] = 0;
   if (valid == VPL && kbits == 8) {
     if constexpr (NSB == 4) {
-      uint32_t v = __ldg(reinterpret_cast<const unsigned int*>(sc + blk0));
+      uint32_t v = ldro<CG>(reinterpret_cast<const unsigned int*>(sc + blk0));
 #pragma unroll
       for (int sb = 0; sb < 4; ++sb) r.st[sb] = (v >> (8 * sb)) & 0xff;
     } else if constexpr (NSB == 2) {
-      uint32_t v = __ldg(reinterpret_cast<const unsigned short*>(sc + blk0));
+      uint32_t v = ldro<CG>(reinterpret_cast<const unsigned short*>(sc + blk0));
       r.st[0] = v & 0xff;
       r.st[1] = v >> 8;
     } else {
-      r.st[0] = __ldg(sc + blk0);
+      r.st[0] = ldro<CG>(sc + blk0);
     }
   } else if (valid > 0) {
 #pragma unroll
@@ -930,6 +939,24 @@ __global__ void __launch_bounds__(kThreads) k_requant(const RArgs A) {
     store_unit_scales<B>(A.out_scale, uoff / B, stored, uvalid, lane, f.kbits, stage);
   }
 }
+
+// fused one-shot (k_fused.cu): quantise N local partials, grid barrier,
+// dequant-sum -- one persistent launch
+struct FArgs {
+  const void* const* partials;  // device array: nranks partial pointers
+  int nranks;
+  int64_t n;
+  uint8_t* shards;              // nranks x shard_stride bytes
+  int64_t shard_stride;
+  int64_t scale_off, elem_off;  // shard layout for n values
+  void* out;
+  unsigned int* bar;            // {arrive count, generation}, zero-initialised once
+  unsigned long long* nonfinite;
+  Fmt f;
+};
+
+bool launch_fused_oneshot(const FArgs& a, int out_is_bf16, int block, int enc, int bits,
+                          cudaStream_t st);
 
 // launchers (one translation unit per dtype, compiled in parallel)
 void launch_quant_bf16(const QArgs& a, int block, int enc, int bits, cudaStream_t st);

@@ -1,7 +1,7 @@
 #!/bin/bash
-# One gpurun call: GPU tests, bench, ncu launch list and full captures of K1/K2.
-# usage (from the build container):
-#   gpurun --timeout 1500 -- 'bash scripts/gpu_check.sh [tag] [tests|notests]'
+# One gpurun call: GPU tests, bench, membench, ncu launch list and full
+# captures of the fused kernel and of K1/K2 (unfused run).
+# usage: gpurun --timeout 1500 -- 'bash scripts/gpu_check.sh [tag] [tests|notests]'
 tag=${1:-dev}
 mode=${2:-tests}
 out=gpurun_out/$tag
@@ -14,9 +14,11 @@ timeout 300 python bench.py > $out/bench.json 2> $out/bench.err
 timeout 120 python scripts/membench.py > $out/membench.json 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $out/launches.csv python bench.py --profile > /dev/null 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_quant -s 2 -c 1 \
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_fused -s 1 -c 1 \
+  -o $out/prof_kfused python bench.py --profile > $out/ncu0.log 2>&1
+MXB200_FUSED=0 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_quant -s 2 -c 1 \
   -o $out/prof_kquant python bench.py --profile > $out/ncu1.log 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_dqsum -s 1 -c 1 \
+MXB200_FUSED=0 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_dqsum -s 1 -c 1 \
   -o $out/prof_kdqsum python bench.py --profile > $out/ncu2.log 2>&1
 cat $out/tests.txt 2>/dev/null | tail -3
 cat $out/bench.json

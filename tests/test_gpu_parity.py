@@ -248,3 +248,24 @@ def test_empty_and_tiny(mx):
     assert mx.decompress_tensor(ct).shape == (0,)
     ct = mx.compress_tensor(np.float64(3.0), sch)  # 0-d tensor: one value
     assert mx.decompress_tensor(ct).shape == () and float(mx.decompress_tensor(ct)) == 3.0
+
+
+@pytest.mark.parametrize("spec", ["fp4_e2m1:32:e8m0", "fp4_e2m1:8:e8m0", "fp6_e2m3:64:e8m0",
+                                  "int8:16:e8m0", "fp5_e2m2:32:e8m0"])
+@pytest.mark.parametrize("N", [1, 2, 3, 8])
+def test_fused_oneshot_bit_identical(mx, spec, N):
+    """One persistent kernel (quantise, grid barrier, dequant-sum) == the
+    separate K1 x N + K2 launches == the oracle."""
+    from paper_2411_09510_b200.collective import SimulatedAllReduce
+
+    for n in (1 << 20, 70001):
+        x64 = [inputs.gauss_bf16(n, 2000 + r) for r in range(N)]
+        parts = [dev(x, "bf16") for x in x64]
+        fused = SimulatedAllReduce(spec, n, N, "oneshot", torch.float32, fused=True)
+        split = SimulatedAllReduce(spec, n, N, "oneshot", torch.float32, fused=False)
+        a = fused(parts).cpu().numpy().copy()
+        a2 = fused(parts).cpu().numpy().copy()  # barrier reuse across calls
+        b = split(parts).cpu().numpy()
+        assert fused.fused, "fused kernel not taken"
+        assert np.array_equal(a, b) and np.array_equal(a, a2)
+        assert np.array_equal(a, O.allreduce_oneshot(x64, O.scheme(spec)))

@@ -188,9 +188,18 @@ template <int ENC, int BITS>
 __device__ __forceinline__ uint64_t encode8(const float* x, const Fmt& f) {
   uint64_t w = 0;
   if constexpr (ENC == ENC_E2M1) {
-    uint32_t u = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) u |= cvt_e2m1x2(x[2 * i], x[2 * i + 1]) << (8 * i);
+    // four cvts into bytes of one register: ptxas chains F2FP ... MERGE_C,
+    // so packing costs no extra instructions
+    uint32_t u;
+    asm("{\n\t.reg .b8 b0, b1, b2, b3;\n\t"
+        "cvt.rn.satfinite.e2m1x2.f32 b0, %2, %1;\n\t"
+        "cvt.rn.satfinite.e2m1x2.f32 b1, %4, %3;\n\t"
+        "cvt.rn.satfinite.e2m1x2.f32 b2, %6, %5;\n\t"
+        "cvt.rn.satfinite.e2m1x2.f32 b3, %8, %7;\n\t"
+        "mov.b32 %0, {b0, b1, b2, b3};\n\t}"
+        : "=r"(u)
+        : "f"(x[0]), "f"(x[1]), "f"(x[2]), "f"(x[3]), "f"(x[4]), "f"(x[5]), "f"(x[6]),
+          "f"(x[7]));
     w = u;
   } else if constexpr (ENC == ENC_E2M3 || ENC == ENC_E3M2) {
 #pragma unroll

@@ -14,13 +14,24 @@ timeout 300 python bench.py > $out/bench.json 2> $out/bench.err
 timeout 120 python scripts/membench.py > $out/membench.json 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $out/launches.csv python bench.py --profile > /dev/null 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_fused -s 1 -c 1 \
+timeout 300 ncu --set full --clock-control none -k regex:k_fused -s 1 -c 1 \
   -o $out/prof_kfused python bench.py --profile > $out/ncu0.log 2>&1
-MXB200_FUSED=0 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_quant -s 2 -c 1 \
+MXB200_FUSED=0 timeout 300 ncu --set full --clock-control none -k regex:k_quant -s 2 -c 1 \
   -o $out/prof_kquant python bench.py --profile > $out/ncu1.log 2>&1
-MXB200_FUSED=0 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_dqsum -s 1 -c 1 \
+MXB200_FUSED=0 timeout 300 ncu --set full --clock-control none -k regex:k_dqsum -s 1 -c 1 \
   -o $out/prof_kdqsum python bench.py --profile > $out/ncu2.log 2>&1
 cat $out/tests.txt 2>/dev/null | tail -3
 cat $out/bench.json
 tail -3 $out/bench.err
 cat $out/membench.json
+# reports are large: summarise on the box, bring back text only
+for r in prof_kfused prof_kquant prof_kdqsum; do
+  if [ -f $out/$r.ncu-rep ]; then
+    python scripts/ncu_summary.py $out/$r.ncu-rep > $out/$r.summary.txt 2>&1
+    ncu -i $out/$r.ncu-rep --page details > $out/$r.details.txt 2>&1
+    ncu -i $out/$r.ncu-rep --page source --csv --print-source sass > $out/$r.sass.csv 2>&1
+    ncu -i $out/$r.ncu-rep --page raw --csv > $out/$r.raw.csv 2>&1
+    [ "${KEEP_REP:-0}" = 1 ] || rm -f $out/$r.ncu-rep
+  fi
+done
+du -sh $out

@@ -290,8 +290,13 @@ void go(const FArgs& a, cudaStream_t st) {
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, 0);
   if (occ < 1) occ = 1;
-  // every CTA must be resident for the grid barrier: at most one wave
-  k<<<(unsigned)(sms * occ), kThreads, 0, st>>>(a);
+  // every CTA must be resident for the grid barrier: at most one wave, and
+  // no more CTAs than the larger phase has warp units for
+  const int64_t units = std::max<int64_t>((a.n + kUnit2 - 1) / kUnit2,
+                                          a.nranks * ((a.n + kUnit - 1) / kUnit));
+  const int64_t need = (units + kWarps - 1) / kWarps;
+  k<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ, need)), kThreads, 0,
+      st>>>(a);
 }
 
 template <typename InT, typename OutT, int B>
@@ -300,6 +305,11 @@ void by_enc(const FArgs& a, int enc, int bits, cudaStream_t st) {
     case ENC_E2M1: go<InT, OutT, B, ENC_E2M1, 4>(a, st); return;
     case ENC_E2M3: go<InT, OutT, B, ENC_E2M3, 6>(a, st); return;
     case ENC_E3M2: go<InT, OutT, B, ENC_E3M2, 6>(a, st); return;
+    case ENC_INT:
+      if (bits == 4) go<InT, OutT, B, ENC_INT, 4>(a, st);
+      else if (bits == 5) go<InT, OutT, B, ENC_INT, 5>(a, st);
+      else go<InT, OutT, B, ENC_INT, 8>(a, st);
+      return;
   }
   switch (bits) {
     case 4: go<InT, OutT, B, ENC_GEN, 4>(a, st); return;

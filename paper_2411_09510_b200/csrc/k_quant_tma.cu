@@ -152,6 +152,10 @@ bool by_enc(const CUtensorMap& map, const QArgs& a, int ntiles, int enc, int bit
     case ENC_E2M1: return go<InT, B, ENC_E2M1, 4>(map, a, ntiles, st);
     case ENC_E2M3: return go<InT, B, ENC_E2M3, 6>(map, a, ntiles, st);
     case ENC_E3M2: return go<InT, B, ENC_E3M2, 6>(map, a, ntiles, st);
+    case ENC_INT:
+      if (bits == 4) return go<InT, B, ENC_INT, 4>(map, a, ntiles, st);
+      if (bits == 8) return go<InT, B, ENC_INT, 8>(map, a, ntiles, st);
+      break;
   }
   switch (bits) {
     case 2: return go<InT, B, ENC_GEN, 2>(map, a, ntiles, st);

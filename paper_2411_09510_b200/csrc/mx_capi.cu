@@ -267,8 +267,10 @@ int enc_of(const mx_scheme_t* s) {
     if (s->exponent_bits == 2 && s->mantissa_bits == 1) return ENC_E2M1;
     if (s->exponent_bits == 2 && s->mantissa_bits == 3) return ENC_E2M3;
     if (s->exponent_bits == 3 && s->mantissa_bits == 2) return ENC_E3M2;
+    return ENC_GEN;
   }
-  return ENC_GEN;
+  int b = 1 + s->mantissa_bits;  // sign-magnitude INTb with a compiled width
+  return (b == 3 || b == 4 || b == 5 || b == 8) ? ENC_INT : ENC_GEN;
 }
 
 // MXB200_TMA=1 routes whole tiles of single-chunk E8M0 16-bit inputs through

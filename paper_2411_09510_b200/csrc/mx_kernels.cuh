@@ -32,7 +32,7 @@
 
 namespace mxb {
 
-enum Enc { ENC_GEN = 0, ENC_E2M1 = 1, ENC_E2M3 = 2, ENC_E3M2 = 3 };
+enum Enc { ENC_GEN = 0, ENC_E2M1 = 1, ENC_E2M3 = 2, ENC_E3M2 = 3, ENC_INT = 4 };
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
@@ -208,6 +208,17 @@ __device__ __forceinline__ uint64_t encode8(const float* x, const Fmt& f) {
                                    : cvt_e3m2x2(x[2 * i], x[2 * i + 1]);
       w |= (uint64_t)(p & 0x3fu) << (12 * i);
       w |= (uint64_t)((p >> 8) & 0x3fu) << (12 * i + 6);
+    }
+  } else if constexpr (ENC == ENC_INT) {
+    // sign-magnitude INTb: RNE to an integer by the 1.5*2^23 magic add, the
+    // grid maximum 2^(b-1)-1 saturates first (mx/codec.py:130)
+    constexpr float GMAX = (float)((1 << (BITS - 1)) - 1);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float a = fminf(fabsf(x[i]), GMAX);
+      const uint32_t idx = __float_as_uint(__fadd_rn(a, 12582912.0f)) - 0x4B400000u;
+      const uint32_t code = idx | ((__float_as_uint(x[i]) >> 31) << (BITS - 1));
+      w |= (uint64_t)code << (i * BITS);
     }
   } else {
 #pragma unroll

@@ -1,0 +1,138 @@
+"""BASELINE.json configs[3] and configs[4] on one B200.
+
+  python scripts/sweeps.py formats   # MXFP4/5/6/INT8 x block 16/32/64, E8M0, [2048x4096]
+  python scripts/sweeps.py messages  # 64 KiB .. 512 MiB bf16 messages
+
+formats: per scheme -- K1 and K2 (2 shards) device time and HBM GB/s, the
+fused simulated-TP=2 step, the wire payload, and the error of the reduced
+tensor (MX one-shot, fp32 rank-order sum, bf16 cast) against the exact
+fp64 sum of the two bf16 partials: SQNR, max-abs, MSE.  The GPU result is
+bit-identical to the reference's own dequantised sum (tests/), so these are
+also the reference's errors.
+
+messages: per size -- K1, K2 and the fused step (simulated TP=2), plus the
+analytic NVLink wire time at TP=2/4/8 for one-shot / two-shot / bf16 ring,
+using 770 GB/s per direction (the measured peer-copy reference of
+B200_PROFILING.md).  Multi-GPU collectives are not measurable with one GPU;
+the model lines are labelled as such.
+
+One JSON line per configuration on stdout.
+"""
+
+import json
+import math
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2411_09510_b200 import _native  # noqa: E402
+from paper_2411_09510_b200.collective import NativeBackend, SimulatedAllReduce  # noqa: E402
+from paper_2411_09510_b200.formats import parse_scheme  # noqa: E402
+from paper_2411_09510_b200.synth import rank_partials  # noqa: E402
+
+L2 = 126 * 2 ** 20
+NVLINK_GBS = 770.0
+
+
+def graph_time(fn, reps):
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.current_stream().wait_stream(s)
+    with torch.cuda.graph(g):
+        fn()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def kernel_times(spec, parts, R):
+    """(us K1, us K2-2shards, us fused step) over R rotated buffer sets."""
+    sch = parse_scheme(spec, extensions=True)
+    n = parts[0][0].numel()
+    be = NativeBackend(sch)
+    sets = [SimulatedAllReduce(sch, n, 2, "oneshot", torch.bfloat16) for _ in range(R)]
+    for op, p in zip(sets, parts):
+        op(p)  # fill shards
+    reps = max(3, min(50, int(2e4 / max(1, R))))
+    k1 = graph_time(lambda: [be.quantize_into(p[0].reshape(-1), op.gathered[:op.S], op.ws, op.flag)
+                             for op, p in zip(sets, parts)], reps) / R
+    k2 = graph_time(lambda: [op.reduce() for op in sets], reps) / R
+    step = graph_time(lambda: [op(p) for op, p in zip(sets, parts)], reps) / R
+    return k1 * 1e3, k2 * 1e3, step * 1e3, sets[0].S, sets[0].fused
+
+
+def formats():
+    T, H = 2048, 4096
+    n = T * H
+    host = rank_partials((T, H), 2, seed=0)
+    exact = host[0].astype(np.float64) + host[1].astype(np.float64)
+    base = [torch.from_numpy(h).to("cuda", torch.bfloat16) for h in host]
+    R = max(2, -(-3 * L2 // (6 * n)))
+    parts = [[(b.roll(i * 7, 0) * (-1) ** i).contiguous() for b in base] for i in range(R)]
+    for el in ["fp4_e2m1", "fp5_e2m2", "fp6_e2m3", "int8"]:
+        for B in (16, 32, 64):
+            spec = f"{el}:{B}:e8m0"
+            k1, k2, step, S, fused = kernel_times(spec, parts, R)
+            op = SimulatedAllReduce(spec, n, 2, "oneshot", torch.float32)
+            red = op(base).double().cpu().numpy().reshape(T, H)
+            err = red - exact
+            sch = parse_scheme(spec, extensions=True)
+            sb, eb = _native.stream_nbytes(n, sch.to_c())
+            print(json.dumps({
+                "config": "formats", "scheme": spec, "shape": [T, H],
+                "k1_us": round(k1, 3), "k1_gbs": round((2 * n + sb + eb) / k1 / 1e3, 1),
+                "k2_us": round(k2, 3), "k2_gbs": round((2 * (sb + eb) + 2 * n) / k2 / 1e3, 1),
+                "fused_step_us": round(step, 3), "fused": fused,
+                "payload_bytes": sb + eb, "ratio_vs_bf16": round(2 * n / (sb + eb), 3),
+                "sqnr_db": round(10 * math.log10(float((exact ** 2).sum() / (err ** 2).sum())), 3),
+                "max_abs_err": float(np.abs(err).max()), "mse": float((err ** 2).mean())}),
+                flush=True)
+
+
+def wire_model(n, S, N):
+    """Per-GPU per-direction bytes and modelled time at NVLINK_GBS."""
+    one = (N - 1) * S
+    two = 2 * (N - 1) * S / N
+    ring = 2 * (N - 1) / N * 2 * n
+    us = lambda b: b / NVLINK_GBS / 1e3  # noqa: E731
+    return {"oneshot_bytes": one, "twoshot_bytes": int(two), "bf16_ring_bytes": int(ring),
+            "oneshot_wire_us": round(us(one), 2), "twoshot_wire_us": round(us(two), 2),
+            "bf16_ring_wire_us": round(us(ring), 2)}
+
+
+def messages():
+    spec = "fp4_e2m1:32:e8m0"
+    for lg in range(15, 29):
+        n = 1 << lg
+        R = max(1, min(64, -(-3 * L2 // (6 * n))))
+        g = torch.Generator(device="cuda").manual_seed(lg)
+        base = [torch.randn(n, device="cuda", generator=g).to(torch.bfloat16) for _ in range(2)]
+        parts = [[(b.roll(i * 17) * (-1) ** i).contiguous() for b in base] for i in range(R)]
+        k1, k2, step, S, fused = kernel_times(spec, parts, R)
+        line = {"config": "messages", "scheme": spec, "bf16_bytes": 2 * n, "rotation": R,
+                "k1_us": round(k1, 3), "k2_us": round(k2, 3), "fused_step_us": round(step, 3),
+                "fused": fused, "shard_bytes": S,
+                "model_nvlink": {f"tp{N}": wire_model(n, S, N) for N in (2, 4, 8)},
+                "model_note": f"wire time = bytes / {NVLINK_GBS} GB/s per direction (model)"}
+        print(json.dumps(line), flush=True)
+        del parts, base
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "formats"
+    {"formats": formats, "messages": messages}[what]()

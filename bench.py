@@ -462,6 +462,37 @@ def run_ours(args, shape, rank, world, local_rank):
         bf16_ar = {"us": round(ms_b * 1e3, 2), "value": round(world * 2 * n / (ms_b * 1e-3) / 1e9, 2),
                    "unit": UNIT, "speedup_of_compressed": round(ms_b / ms_step, 3)}
 
+    # ---- the NVLink-pull fused kernel over symmetric memory (N>1)
+    symm = None
+    if world > 1 and os.environ.get("MXB200_BENCH_SYMM", "1") == "1":
+        try:
+            from paper_2411_09510_b200.collective import SymmetricAllReduce
+
+            sar = SymmetricAllReduce(sch, n, out_dtype=torch.bfloat16, device=dev)
+            x0 = sets[0][0][0]
+            got = sar(x0).clone()
+            exact = None
+            if args.algo == "oneshot":
+                ref = sets[0][1](x0).clone()
+                exact = bool(torch.equal(got.view(torch.int16), ref.view(torch.int16)))
+            gss = [capture(torch, (lambda x=s_[0][0]: sar(x))) for s_ in sets]
+            for i in range(args.warmup):
+                gss[i % R].replay()
+            dist.barrier()
+            ms_s = time_graph_replays(torch, gss, args.steps) / args.steps
+            tt = torch.tensor([ms_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms_s = float(tt.item())
+            symm = {"us": round(ms_s * 1e3, 2),
+                    "value": round(world * 2 * n / (ms_s * 1e-3) / 1e9, 2), "unit": UNIT,
+                    "bit_exact_vs_nccl_oneshot": exact,
+                    "kernel": "k_symm_oneshot (quantise + NVLink flag exchange + pull "
+                              "dequant-sum, one launch per rank)"}
+            if bf16_ar:
+                symm["speedup_vs_bf16_allreduce"] = round(bf16_ar["us"] / symm["us"], 3)
+        except Exception as exc:  # reported, never fatal for the main measurement
+            symm = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     if rank != 0:
         return
     cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(args.scheme, shape, nranks)
@@ -475,7 +506,7 @@ def run_ours(args, shape, rank, world, local_rank):
             "wire_bytes_per_rank": (nranks - 1) * S if args.algo == "oneshot" else None,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
-            "bf16_nccl_allreduce": bf16_ar}
+            "bf16_nccl_allreduce": bf16_ar, "symmetric_memory_fused": symm}
     print(json.dumps(line), flush=True)
 
 

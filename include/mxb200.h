@@ -162,6 +162,24 @@ int mx_allreduce_fused(const void* const* partials, int32_t dtype, int32_t nrank
                        void* out, int32_t out_dtype, uint32_t* barrier, uint64_t* nonfinite,
                        void* stream);
 
+/* Multi-GPU one-shot fused over symmetric (peer-mapped) memory, one launch
+ * per rank: quantise `x` into this rank's shard slot of its symmetric buffer,
+ * exchange "ready" flags with every peer over NVLink (system-scope
+ * release/acquire on the signal pads), then decode all nranks shards
+ * straight from the peers' buffers in rank order (fp32 from +0.0) into
+ * `out`.  Replaces all-gather + dequant-sum (mx/netbench.py:323-334) with
+ * no gather buffer.
+ *   peer_bufs     device array [nranks] of peer buffer bases (each buffer
+ *                 holds 2 slots of slot_stride bytes: double buffering)
+ *   peer_signals  device array [nranks] of peer signal pads (>= nranks u32,
+ *                 zero-initialised)
+ *   barrier, epoch  local device uint32 state (zeroed once)
+ * MX_ERR_UNSUPPORTED outside bf16 in, n % 1024 == 0, E8M0, B in {16,32,64}. */
+int mx_allreduce_symm(const void* x, int32_t dtype, int64_t n, const mx_scheme_t* scheme,
+                      uint8_t* const* peer_bufs, uint32_t* const* peer_signals, int32_t rank,
+                      int32_t nranks, int64_t slot_stride, void* out, int32_t out_dtype,
+                      uint32_t* barrier, uint32_t* epoch, uint64_t* nonfinite, void* stream);
+
 /* unpack_bits (mx/bitpack.py:37-58) on the device: `count` codes of
  * `width` bits -> one uint8 per code (quantize_block's return value). */
 int mx_unpack_codes(const uint8_t* packed, int64_t count, int32_t width, uint8_t* codes,
@@ -171,6 +189,10 @@ int mx_unpack_codes(const uint8_t* packed, int64_t count, int32_t width, uint8_t
  * mx_unpack_codes (dequantize_block's input path). */
 int mx_pack_codes(const uint8_t* codes, int64_t count, int32_t width, uint8_t* packed,
                   void* stream);
+
+/* cudaMemsetAsync on `stream` (e.g. zeroing a symmetric-memory signal pad
+ * without pulling the CUDA runtime into the host language). */
+int mx_memset_async(void* ptr, int32_t value, int64_t bytes, void* stream);
 
 /* Sets *nonfinite = UINT64_MAX on `stream`. */
 int mx_nonfinite_reset(uint64_t* nonfinite, void* stream);

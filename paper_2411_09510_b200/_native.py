@@ -52,8 +52,11 @@ SIGNATURES = {
                                        c_i64, c_vp]),
     "mx_allreduce_fused": (c_i32, [c_vp, c_i32, c_i32, c_i64, _SP, c_vp, c_i64, c_vp, c_i32,
                                    c_vp, c_vp, c_vp]),
+    "mx_allreduce_symm": (c_i32, [c_vp, c_i32, c_i64, _SP, c_vp, c_vp, c_i32, c_i32, c_i64, c_vp,
+                                  c_i32, c_vp, c_vp, c_vp, c_vp]),
     "mx_unpack_codes": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp]),
     "mx_pack_codes": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "mx_memset_async": (c_i32, [c_vp, c_i32, c_i64, c_vp]),
     "mx_nonfinite_reset": (c_i32, [c_vp, c_vp]),
 }
 

@@ -253,6 +253,82 @@ def compressed_all_reduce(x, scheme, group=None, algo: str = "oneshot", out_dtyp
 
 
 # ---------------------------------------------------------------------------
+# fused over symmetric memory (NVLink pull), one kernel per rank per call
+# ---------------------------------------------------------------------------
+
+
+class SymmetricAllReduce:
+    """One-shot compressed all-reduce fused into ONE kernel per rank over
+    torch symmetric memory (peer-mapped buffers on NVLink / NVSwitch).
+
+    Each rank quantises its partial into its own shard slot, raises a
+    system-scope flag in every peer's signal pad, waits for the peers' flags
+    and decodes all N shards straight out of the peers' memory, in rank
+    order, into fp32 -> ``out_dtype``.  This replaces K1 -> NCCL all-gather ->
+    K2 (mx/netbench.py:323-334) with no gather buffer and no NCCL kernel; the
+    result is bit-identical to the NCCL one-shot (same codes, same sum order).
+    Requirements: bf16 partial, n % 1024 == 0, E8M0 scales, B in {16,32,64}.
+    """
+
+    def __init__(self, scheme, n: int, group=None, out_dtype=None, device=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        if isinstance(scheme, str):
+            scheme = parse_scheme(scheme, extensions=True)
+        self.scheme, self.n = scheme, int(n)
+        self.group = group or dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self.out_dtype = out_dtype or torch.bfloat16
+        self.backend = NativeBackend(scheme)
+        _, _, S = self.backend.layout(self.n)
+        self.slot = (S + 255) & ~255
+        self.buf = symm_mem.empty(2 * self.slot, dtype=torch.uint8, device=self.device)
+        self.hdl = symm_mem.rendezvous(self.buf, self.group)
+        if self.hdl.signal_pad_size < 4 * self.world:
+            raise RuntimeError("symmetric-memory signal pad too small")
+        # our flags live in the first `world` u32 of every signal pad: start
+        # from zero on every rank before anyone can signal
+        pad = self.hdl.signal_pad_ptrs[self.rank]
+        _native.check(self.backend.lib.mx_memset_async(ctypes.c_void_p(pad), 0, 4 * self.world,
+                                                       NativeBackend._st()), "mx_memset_async")
+        torch.cuda.synchronize()
+        dist.barrier(self.group)
+        self.state = torch.zeros(4, dtype=torch.int32, device=self.device)  # barrier x2, epoch
+        self.flag = torch.empty(1, dtype=torch.int64, device=self.device)
+        self.backend.reset_flag(self.flag)
+        self.out = torch.empty(self.n, dtype=self.out_dtype, device=self.device)
+
+    def __call__(self, x, out=None):
+        import torch
+
+        if x.numel() != self.n or x.dtype != torch.bfloat16 or not x.is_contiguous():
+            raise ShapeMismatch(f"expected a contiguous bf16 tensor of {self.n} values")
+        o = self.out if out is None else out.reshape(-1)
+        be = self.backend
+        base = self.state.data_ptr()
+        rc = be.lib.mx_allreduce_symm(
+            ctypes.c_void_p(x.data_ptr()), _native.MX_BF16, self.n, ctypes.byref(be.cs),
+            ctypes.c_void_p(self.hdl.buffer_ptrs_dev), ctypes.c_void_p(self.hdl.signal_pad_ptrs_dev),
+            self.rank, self.world, self.slot, ctypes.c_void_p(o.data_ptr()), be._dt(o),
+            ctypes.c_void_p(base), ctypes.c_void_p(base + 8), ctypes.c_void_p(self.flag.data_ptr()),
+            be._st())
+        _native.check(rc, "mx_allreduce_symm")
+        return o.view(x.shape)
+
+    def check_finite(self):
+        idx = int(self.flag.item())
+        if idx >= 0:
+            self.backend.reset_flag(self.flag)
+            raise NonFiniteInput(f"non-finite value in a compressed all-reduce input "
+                                 f"(flat index {idx})", block_index=idx // self.scheme.block_size)
+
+
+# ---------------------------------------------------------------------------
 # single-GPU simulation of N ranks (same kernels, exchange = buffer copies)
 # ---------------------------------------------------------------------------
 

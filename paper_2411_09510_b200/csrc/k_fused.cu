@@ -277,6 +277,160 @@ __global__ void __launch_bounds__(kThreads, 3) k_fused_lean(const FArgs F) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Multi-GPU fused one-shot over symmetric (peer-mapped) memory: the NVLink
+// form of the kernel above.  Rank r quantises its partial into ITS shard of
+// the symmetric buffer (slot = epoch parity), a system-scope release/acquire
+// flag exchange replaces the all-gather, and phase 2 decodes the N shards
+// straight out of the peers' memory over NVLink (rank order, fp32, +0.0
+// start) -- no gather buffer, no NCCL kernel, one launch.  Double buffering:
+// a rank writes slot e&1 at epoch e only after it has seen every peer's
+// epoch e-1 flag, i.e. after every peer finished reading slot e&1 at e-2.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <typename OutT, int B, int ENC, int BITS>
+__global__ void __launch_bounds__(kThreads, 3) k_symm_oneshot(const SArgs S) {
+  using InT = __nv_bfloat16;
+  constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
+  constexpr int NSB = Geo<B>::NSB;
+  constexpr int LPB = Geo<B>::LPB;
+  constexpr int UBYTES = kUnit / 8 * BITS;
+  constexpr int USCALES = kUnit / B;
+  __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
+  const Fmt f = S.f;
+  if constexpr (DEC != ENC_E2M1) fill_lut(s_lut, f);
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = (uint32_t)(gridDim.x * kWarps);
+  const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint32_t nunits = (uint32_t)(S.n / kUnit);
+  const int nr = S.nranks;
+  const unsigned int e = *S.epoch + 1u;
+  const int64_t slot = (int64_t)(e & 1u) * S.slot_stride;
+
+  // ---- phase 1: quantise the local partial into my shard (slot e&1) -----
+  {
+    uint8_t* shard = S.bufs[S.rank] + slot;
+    auto quantise = [&](const Raw<InT>& raw, uint32_t q) {
+      int stored[NSB];
+      bool bad;
+      LaneCodes<BITS> c = quant_lane<InT, B, ENC, BITS>(raw, f, stored, bad);
+      if (bad)
+        report_nonfinite_raw<InT>(raw, kVPL, (int64_t)q * kUnit + lane * kVPL, S.nonfinite);
+      store_lane_codes<BITS>(shard + S.elem_off + (size_t)q * UBYTES + lane * (4 * BITS), c, kVPL);
+      uint8_t* sp = shard + S.scale_off + (size_t)q * USCALES + (lane / LPB) * NSB;
+      if constexpr (NSB == 4) {
+        *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
+                                           ((uint32_t)stored[2] << 16) |
+                                           ((uint32_t)stored[3] << 24);
+      } else if constexpr (NSB == 2) {
+        *reinterpret_cast<uint16_t*>(sp) = (uint16_t)(stored[0] | (stored[1] << 8));
+      } else {
+        if (lane % LPB == 0) *sp = (uint8_t)stored[0];
+      }
+    };
+    const InT* x = reinterpret_cast<const InT*>(S.x) + lane * kVPL;
+    Raw<InT> b0, b1;
+    uint32_t q = gw;
+    if (q < nunits) load_raw<InT>(x + (size_t)q * kUnit, b0);
+    while (q < nunits) {
+      uint32_t qn = q + nw;
+      if (qn < nunits) load_raw<InT>(x + (size_t)qn * kUnit, b1);
+      quantise(b0, q);
+      q = qn;
+      if (q >= nunits) break;
+      qn = q + nw;
+      if (qn < nunits) load_raw<InT>(x + (size_t)qn * kUnit, b0);
+      quantise(b1, q);
+      q = qn;
+    }
+  }
+  __threadfence_system();  // my shard bytes, before any flag leaves this GPU
+  grid_barrier(S.bar);
+
+  // ---- flag exchange: "my shard for epoch e is ready" ---------------------
+  if (blockIdx.x == 0 && threadIdx.x < (unsigned)nr) {
+    const int j = threadIdx.x;
+    st_release_sys(S.sigs[j] + S.rank, e);              // peer j's pad, my slot
+    const unsigned int* mine = S.sigs[S.rank] + j;      // my pad, peer j's slot
+    while ((int)(ld_acquire_sys(mine) - e) < 0) __nanosleep(64);
+  }
+  grid_barrier(S.bar);
+
+  // ---- phase 2: pull-decode the N shards over NVLink, rank order ---------
+  {
+    using RL = RankLoad<B, BITS, kVPL>;
+    auto load_r = [&](RL& x, int r, uint32_t uu) {
+      load_rank<B, BITS, kVPL, true>(x, S.bufs[r] + slot, S.scale_off, S.elem_off,
+                                     (int64_t)uu * kUnit, lane, kVPL, 8);
+    };
+    auto reduce = [&](const RL& x0, const RL& x1, uint32_t uu) {
+      float acc[kVPL];
+#pragma unroll
+      for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
+      decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
+      if (nr > 1) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
+      for (int rk = 2; rk < nr; ++rk) {
+        RL rr;
+        load_r(rr, rk, uu);
+        decode_rank<B, DEC, BITS, kVPL>(rr, f, acc, false, s_lut);
+      }
+      store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(S.out) + (size_t)uu * kUnit +
+                                     lane * kVPL,
+                                 kVPL, acc);
+    };
+    uint32_t u = gw;
+    RL a0, a1, c0, c1;
+    if (u < nunits) {
+      load_r(a0, 0, u);
+      if (nr > 1) load_r(a1, 1, u);
+    }
+    while (u < nunits) {
+      uint32_t un = u + nw;
+      if (un < nunits) {
+        load_r(c0, 0, un);
+        if (nr > 1) load_r(c1, 1, un);
+      }
+      reduce(a0, a1, u);
+      u = un;
+      if (u >= nunits) break;
+      un = u + nw;
+      if (un < nunits) {
+        load_r(a0, 0, un);
+        if (nr > 1) load_r(a1, 1, un);
+      }
+      reduce(c0, c1, u);
+      u = un;
+    }
+  }
+  // every CTA read *epoch before the first barrier: safe to advance it
+  if (blockIdx.x == 0 && threadIdx.x == 0) *S.epoch = e;
+}
+
+template <typename OutT, int B, int ENC, int BITS>
+void go_symm(const SArgs& a, cudaStream_t st) {
+  auto k = k_symm_oneshot<OutT, B, ENC, BITS>;
+  static thread_local int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, 0);
+  if (occ < 1) occ = 1;
+  const int64_t need = (a.n / kUnit + kWarps - 1) / kWarps;
+  k<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ, need)), kThreads, 0,
+      st>>>(a);
+}
+
 template <typename InT, typename OutT, int B, int ENC, int BITS>
 void go(const FArgs& a, cudaStream_t st) {
   auto k = k_fused_oneshot<InT, OutT, B, ENC, BITS>;
@@ -329,7 +483,34 @@ void by_block(const FArgs& a, int block, int enc, int bits, cudaStream_t st) {
   }
 }
 
+template <typename OutT, int B>
+bool symm_by_enc(const SArgs& a, int enc, int bits, cudaStream_t st) {
+  switch (enc) {
+    case ENC_E2M1: go_symm<OutT, B, ENC_E2M1, 4>(a, st); return true;
+    case ENC_E2M3: go_symm<OutT, B, ENC_E2M3, 6>(a, st); return true;
+    case ENC_E3M2: go_symm<OutT, B, ENC_E3M2, 6>(a, st); return true;
+    case ENC_INT:
+      if (bits == 8) { go_symm<OutT, B, ENC_INT, 8>(a, st); return true; }
+      return false;
+  }
+  if (bits == 5) { go_symm<OutT, B, ENC_GEN, 5>(a, st); return true; }
+  return false;
+}
+
 }  // namespace
+
+bool launch_symm_oneshot(const SArgs& a, int out_is_bf16, int block, int enc, int bits,
+                         cudaStream_t st) {
+  switch (block) {
+    case 16: return out_is_bf16 ? symm_by_enc<__nv_bfloat16, 16>(a, enc, bits, st)
+                                : symm_by_enc<float, 16>(a, enc, bits, st);
+    case 32: return out_is_bf16 ? symm_by_enc<__nv_bfloat16, 32>(a, enc, bits, st)
+                                : symm_by_enc<float, 32>(a, enc, bits, st);
+    case 64: return out_is_bf16 ? symm_by_enc<__nv_bfloat16, 64>(a, enc, bits, st)
+                                : symm_by_enc<float, 64>(a, enc, bits, st);
+  }
+  return false;
+}
 
 // bf16 partials -> bf16/f32 out; element widths 4/5/6/8 (the BASELINE sweep)
 bool launch_fused_oneshot(const FArgs& a, int out_is_bf16, int block, int enc, int bits,

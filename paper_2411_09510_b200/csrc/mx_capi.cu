@@ -590,6 +590,36 @@ int mx_allreduce_fused(const void* const* partials, int32_t dtype, int32_t nrank
   return cuda_check("k_fused_oneshot");
 }
 
+int mx_allreduce_symm(const void* x, int32_t dtype, int64_t n, const mx_scheme_t* s,
+                      uint8_t* const* peer_bufs, uint32_t* const* peer_signals, int32_t rank,
+                      int32_t nranks, int64_t slot_stride, void* out, int32_t out_dtype,
+                      uint32_t* barrier, uint32_t* epoch, uint64_t* nonfinite, void* stream) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (n <= 0 || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(MX_ERR_INVALID_ARGUMENT, "bad sizes");
+  if (!x || !peer_bufs || !peer_signals || !out || !barrier || !epoch)
+    return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
+  int64_t so, eo, sbytes;
+  mx_shard_layout(n, s, &so, &eo, &sbytes);
+  Fmt f = make_fmt(s);
+  if (dtype != MX_BF16 || (out_dtype != MX_BF16 && out_dtype != MX_F32) || n % 1024 != 0 ||
+      f.kbits != 8 || slot_stride < sbytes || slot_stride % 32 != 0 || !aligned(x, 32) ||
+      !aligned(out, 32))
+    return fail(MX_ERR_UNSUPPORTED,
+                "symmetric path: bf16 in, bf16/f32 out, n %% 1024 == 0, E8M0, 32-B aligned");
+  SArgs a;
+  a.x = x; a.n = n;
+  a.bufs = peer_bufs; a.sigs = reinterpret_cast<unsigned int* const*>(peer_signals);
+  a.rank = rank; a.nranks = nranks; a.slot_stride = slot_stride;
+  a.scale_off = so; a.elem_off = eo; a.out = out; a.bar = barrier;
+  a.epoch = epoch; a.nonfinite = reinterpret_cast<unsigned long long*>(nonfinite); a.f = f;
+  if (!launch_symm_oneshot(a, out_dtype == MX_BF16, (int)s->block_size, enc_of(s), f.bits,
+                           (cudaStream_t)stream))
+    return fail(MX_ERR_UNSUPPORTED, "symmetric path: scheme not instantiated");
+  return cuda_check("k_symm_oneshot");
+}
+
 int mx_unpack_codes(const uint8_t* packed, int64_t count, int32_t width, uint8_t* codes, void* stream) {
   if (width < 1 || width > 8) return fail(MX_ERR_INVALID_ARGUMENT, "width %d outside [1, 8]", width);
   if (count <= 0) return MX_OK;
@@ -603,6 +633,13 @@ int mx_pack_codes(const uint8_t* codes, int64_t count, int32_t width, uint8_t* p
   int64_t groups = cdiv(count, 8);
   g_pack<<<cdiv(groups, 256), 256, 0, (cudaStream_t)stream>>>(codes, count, width, packed);
   return cuda_check("g_pack");
+}
+
+int mx_memset_async(void* ptr, int32_t value, int64_t bytes, void* stream) {
+  if (!ptr || bytes < 0) return fail(MX_ERR_INVALID_ARGUMENT, "bad memset");
+  if (cudaMemsetAsync(ptr, value, (size_t)bytes, (cudaStream_t)stream) != cudaSuccess)
+    return cuda_check("cudaMemsetAsync");
+  return MX_OK;
 }
 
 int mx_nonfinite_reset(uint64_t* nonfinite, void* stream) {

@@ -978,6 +978,24 @@ struct FArgs {
 bool launch_fused_oneshot(const FArgs& a, int out_is_bf16, int block, int enc, int bits,
                           cudaStream_t st);
 
+// multi-GPU fused one-shot over symmetric (peer-mapped) memory (k_fused.cu)
+struct SArgs {
+  const void* x;                 // this rank's bf16 partial (n values)
+  int64_t n;                     // multiple of 1024
+  uint8_t* const* bufs;          // device array [nranks]: peer buffer bases
+  unsigned int* const* sigs;     // device array [nranks]: peer signal pads (u32 x nranks)
+  int rank, nranks;
+  int64_t slot_stride;           // bytes of one shard slot (2 slots per buffer)
+  int64_t scale_off, elem_off;   // shard layout for n values
+  void* out;
+  unsigned int* bar;             // local grid barrier {count, generation}
+  unsigned int* epoch;           // local, advanced once per call
+  unsigned long long* nonfinite;
+  Fmt f;
+};
+bool launch_symm_oneshot(const SArgs& a, int out_is_bf16, int block, int enc, int bits,
+                         cudaStream_t st);
+
 // launchers (one translation unit per dtype, compiled in parallel)
 void launch_quant_bf16(const QArgs& a, int block, int enc, int bits, cudaStream_t st);
 void launch_quant_f16(const QArgs& a, int block, int enc, int bits, cudaStream_t st);

@@ -23,7 +23,13 @@ OUT = os.path.join(HERE, "libmxb200.so")
 BUILD = os.environ.get("MXB200_BUILD_DIR", "/tmp/mxb200_build")
 # -lineinfo (ncu source view) only where the profiled kernels live: it
 # roughly doubles object size
-LINEINFO = {"k_quant_bf16.cu", "k_dqsum_bf16.cu", "k_fused.cu", "k_requant.cu"}
+LINEINFO = {"k_quant_bf16.cu", "k_dqsum_bf16.cu", "k_fused_inst.cu", "k_requant.cu"}
+# sources compiled several times with -D slices (template instantiation split
+# so the slices build in parallel)
+VARIANTS = {
+    "k_quant_bf16.cu": [{"MXB_B": b} for b in (8, 16, 32, 64)],
+    "k_fused_inst.cu": [{"MXB_OUT": o, "MXB_B": b} for o in (0, 1) for b in (8, 16, 32, 64)],
+}
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
@@ -50,9 +56,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     nv = nvcc()
 
-    def compile_one(src):
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+    jobs = []
+    for src in srcs:
+        for var in VARIANTS.get(os.path.basename(src), [{}]):
+            jobs.append((src, var))
+
+    def compile_one(job):
+        src, var = job
+        tag = "".join(f".{k}{v}" for k, v in var.items())
+        obj = os.path.join(BUILD, os.path.basename(src) + tag + ".o")
         extra = ["-lineinfo"] if os.path.basename(src) in LINEINFO else []
+        extra += [f"-D{k}={v}" for k, v in var.items()]
         cmd = [nv, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
@@ -62,7 +76,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return obj
 
     with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
-        objs = list(ex.map(compile_one, srcs))
+        # longest jobs first
+        jobs.sort(key=lambda j: ("k_fused_inst" not in j[0], "k_quant_bf16" not in j[0]))
+        objs = list(ex.map(compile_one, jobs))
     tmp = OUT + ".tmp"
     cmd = [nv, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     p = subprocess.run(cmd, capture_output=True, text=True)

@@ -439,6 +439,147 @@ class SimulatedAllReduce:
         return ok
 
 
+class HostPipeline:
+    """Compressed all-reduce of HOST-resident partial sums into a host
+    buffer -- the shape of the reference's own API, whose codec takes and
+    returns host arrays (``compress_tensor(np.ndarray)`` mx/codec.py:238,
+    ``decompress_tensor`` mx/codec.py:266, the exchange of
+    mx/netbench.py:323-334).
+
+    The flat tensor is cut into ``chunks`` equal pieces whose length is a
+    multiple of 1024 values, so no MX block straddles a piece and every
+    value's reduction is identical to the whole-tensor call.  Piece j's
+    pinned host->device copies, its compressed all-reduce (one persistent
+    op per piece, so its device pointers stay fixed) and its device->host
+    copy are issued on three streams ordered by events: the PCIe traffic in
+    both directions overlaps the kernels of neighbouring pieces.
+
+    ``make_op(c)`` returns a callable ``(device_inputs, device_out) -> out``
+    reducing ``c`` values, e.g. a :class:`SimulatedAllReduce` (all ranks'
+    partials on one GPU) or a :class:`CompressedAllReduce` (this rank's
+    partial, NCCL exchange).
+    """
+
+    def __init__(self, make_op, n: int, ninputs: int, in_dtype=None, out_dtype=None,
+                 device="cuda", chunks: int = 4, graph: bool = True, h2d_streams: int = 1):
+        import torch
+
+        self.n, self.nin = int(n), int(ninputs)
+        self.use_graph = graph
+        self._graphs = {}
+        k = max(1, int(chunks))
+        while k > 1 and (self.n % k or (self.n // k) % 1024):
+            k -= 1
+        self.k, self.c = k, self.n // k
+        self.device = torch.device(device)
+        in_dtype = in_dtype or torch.bfloat16
+        self.out_dtype = out_dtype or torch.bfloat16
+        self.ops = [make_op(self.c) for _ in range(k)]
+        self.dev_in = [torch.empty(self.n, dtype=in_dtype, device=self.device)
+                       for _ in range(self.nin)]
+        self.dev_out = torch.empty(self.n, dtype=self.out_dtype, device=self.device)
+        # [reduce, device->host, host->device x h2d_streams]
+        self.streams = [torch.cuda.Stream(self.device) for _ in range(2 + max(1, h2d_streams))]
+        self.ev_in = [[torch.cuda.Event() for _ in range(self.nin)] for _ in range(k)]
+        self.ev_red = [torch.cuda.Event() for _ in range(k)]
+
+    @property
+    def h2d_bytes(self) -> int:
+        return self.nin * self.n * self.dev_in[0].element_size()
+
+    @property
+    def d2h_bytes(self) -> int:
+        return self.n * self.dev_out.element_size()
+
+    def __call__(self, host_inputs, host_out):
+        """Run the whole pipeline; ``host_out`` is complete once the current
+        stream reaches this point (e.g. after a synchronize).
+
+        The 3k copies and k all-reduces are captured once per (host buffer
+        set) into a CUDA graph with the three streams as parallel branches,
+        so a call costs one graph launch instead of ~4k host-side issues
+        (eager issue is host-bound: tens of microseconds per piece)."""
+        import torch
+
+        if len(host_inputs) != self.nin or any(h.numel() != self.n for h in host_inputs):
+            raise ShapeMismatch(f"expected {self.nin} host tensors of {self.n} values")
+        if host_out.numel() != self.n:
+            raise ShapeMismatch(f"host_out must hold {self.n} values")
+        hin = [h.reshape(-1) for h in host_inputs]
+        hout = host_out.reshape(-1)
+        pinned = all(h.is_pinned() for h in hin) and hout.is_pinned()
+        if not (self.use_graph and pinned):
+            self._issue(hin, hout)
+            return host_out
+        key = tuple(h.data_ptr() for h in hin) + (hout.data_ptr(),)
+        g = self._graphs.get(key)
+        if g is None:
+            self._issue(hin, hout)  # first-call allocations happen eagerly
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._issue(hin, hout)
+            self._graphs[key] = g
+        g.replay()
+        return host_out
+
+    def _issue(self, hin, hout):
+        import torch
+
+        cur = torch.cuda.current_stream(self.device)
+        s_red, s_out, s_ins = self.streams[0], self.streams[1], self.streams[2:]
+        for s in self.streams:
+            s.wait_stream(cur)
+        c = self.c
+        for j in range(self.k):
+            sl = slice(j * c, (j + 1) * c)
+            for i, (d, h) in enumerate(zip(self.dev_in, hin)):
+                s_in = s_ins[i % len(s_ins)]
+                with torch.cuda.stream(s_in):
+                    d[sl].copy_(h[sl], non_blocking=True)
+                    self.ev_in[j][i].record(s_in)
+            with torch.cuda.stream(s_red):
+                for i in range(self.nin):
+                    s_red.wait_event(self.ev_in[j][i])
+                self.ops[j]([d[sl] for d in self.dev_in], self.dev_out[sl])
+                self.ev_red[j].record(s_red)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(self.ev_red[j])
+                hout[sl].copy_(self.dev_out[sl], non_blocking=True)
+        for s in self.streams:
+            cur.wait_stream(s)
+
+    @classmethod
+    def simulated(cls, scheme, n: int, nranks: int, algo: str = "oneshot", out_dtype=None,
+                  device="cuda", chunks: int = 4, graph: bool = True, h2d_streams: int = 1):
+        """All ``nranks`` partials on one GPU (the N=1 bench workload)."""
+        import torch
+
+        out_dtype = out_dtype or torch.bfloat16
+
+        def make(c):
+            op = SimulatedAllReduce(scheme, c, nranks, algo, out_dtype, device)
+            return lambda ins, out: op(ins, out)
+
+        return cls(make, n, nranks, torch.bfloat16, out_dtype, device, chunks, graph, h2d_streams)
+
+    @classmethod
+    def compressed(cls, scheme, n: int, group=None, algo: str = "oneshot", out_dtype=None,
+                   device=None, chunks: int = 4, graph: bool = True, h2d_streams: int = 1):
+        """This rank's partial, NCCL exchange (one rank per GPU)."""
+        import torch
+
+        out_dtype = out_dtype or torch.bfloat16
+
+        def make(c):
+            op = CompressedAllReduce(scheme, c, group=group, algo=algo, out_dtype=out_dtype,
+                                     device=device)
+            return lambda ins, out: op(ins[0], out)
+
+        return cls(make, n, 1, torch.bfloat16, out_dtype, device or "cuda", chunks, graph,
+                   h2d_streams)
+
+
 def simulate_allreduce(partials, scheme, algo: str = "oneshot", out_dtype=None, backend=None):
     """One-off :class:`SimulatedAllReduce`; returns (reduced tensor, nonfinite flag)."""
     sim = SimulatedAllReduce(scheme, partials[0].numel(), len(partials), algo, out_dtype,

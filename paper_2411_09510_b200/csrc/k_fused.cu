@@ -1,477 +1,13 @@
-// Fused one-shot compressed all-reduce in ONE persistent kernel:
-//   phase 1  K1: every local partial is quantised into its slot of the
-//            gather buffer (the bytes an all-gather would deliver),
-//   barrier  grid-wide (all CTAs resident: the grid is one occupancy wave),
-//   phase 2  K2: the N shards are decoded and summed in fp32 rank order.
-// Two kernel boundaries (~2 us of launch/ramp/drain each at these sizes)
-// disappear.  This is the single-device form of the NVLink-pull fused
-// collective (peer shards read in phase 2); the per-phase code is exactly the
-// K1/K2 code of mx_kernels.cuh, so results are bit-identical to
-// quantise -> all-gather -> dequant-sum (mx/netbench.py:323-334).
+// Dispatch of the fused one-shot kernels (k_fused.cuh) to the slices
+// instantiated by k_fused_inst.cu.
 #include "mx_kernels.cuh"
 
 namespace mxb {
-
-namespace {
-
-__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
-  unsigned int v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Sense-free generation barrier across all CTAs of the grid.
-__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int gen = ld_acquire(bar + 1);
-    __threadfence();  // release this CTA's phase-1 stores
-    const unsigned int arrived = atomicAdd(bar, 1u) + 1u;
-    if (arrived == gridDim.x) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (ld_acquire(bar + 1) == gen) __nanosleep(32);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-template <typename InT, typename OutT, int B, int ENC, int BITS>
-__global__ void __launch_bounds__(kThreads, 3) k_fused_oneshot(const FArgs F) {
-  constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
-  __shared__ __align__(16) uint8_t s_stage[kWarps][kUnit / 8];
-  __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
-  const Fmt f = F.f;
-  if constexpr (DEC != ENC_E2M1) fill_lut(s_lut, f);  // visible after the grid barrier
-  const int lane = threadIdx.x & 31;
-  const uint32_t nw = (uint32_t)(gridDim.x * kWarps);
-  const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
-
-  // ---- phase 1: quantise every local partial (K1) ----------------------
-  {
-    QArgs A;
-    A.n = F.n;
-    A.cv = F.n;
-    A.units_per_chunk = (F.n + kUnit - 1) / kUnit;
-    A.total_units = A.units_per_chunk;
-    A.chunk_stride = 0;
-    A.nonfinite = F.nonfinite;
-    A.flat_off = 0;
-    A.f = f;
-    const uint32_t upp = (uint32_t)A.units_per_chunk;
-    const uint32_t nfull = (uint32_t)(F.n / kUnit);
-    uint8_t* stage = s_stage[threadIdx.x >> 5];
-    // units of all partials in one round-robin sequence u -> (rank, unit);
-    // taken in pairs whose loads are both in flight before any math
-    const uint32_t total = upp * (uint32_t)F.nranks;
-    for (uint32_t u0 = gw; u0 < total; u0 += 2 * nw) {
-      const uint32_t u1 = u0 + nw;
-      const bool has1 = u1 < total;
-      const uint32_t r0 = u0 / upp, q0 = u0 - r0 * upp;
-      const uint32_t r1 = has1 ? u1 / upp : r0, q1 = has1 ? u1 - r1 * upp : q0;
-      const InT* x0 = reinterpret_cast<const InT*>(F.partials[r0]);
-      const InT* x1 = reinterpret_cast<const InT*>(F.partials[r1]);
-      const bool full0 = q0 < nfull && f.kbits == 8, full1 = has1 && q1 < nfull && f.kbits == 8;
-      Raw<InT> w0, w1;
-      if (full0) load_raw<InT>(x0 + (size_t)q0 * kUnit + lane * kVPL, w0);
-      if (full1) load_raw<InT>(x1 + (size_t)q1 * kUnit + lane * kVPL, w1);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (h == 1 && !has1) break;
-        const uint32_t r = h ? r1 : r0, q = h ? q1 : q0;
-        A.x = F.partials[r];
-        A.scale_base = F.shards + r * F.shard_stride + F.scale_off;
-        A.elem_base = F.shards + r * F.shard_stride + F.elem_off;
-        if (h ? full1 : full0) {
-          quant_full_unit<InT, B, ENC, BITS>(A, f, q, h ? w1 : w0, lane);
-        } else {
-          UnitPos p = unit_pos(q, upp, true, A.cv, A.n);
-          Raw<InT> raw;
-          load_unit<InT>(reinterpret_cast<const InT*>(A.x), p, lane, raw);
-          quant_unit<InT, B, ENC, BITS>(A, f, p, raw, lane, stage);
-        }
-      }
-    }
-  }
-
-  grid_barrier(F.bar);
-
-  // ---- phase 2: decode the N shards in rank order, fp32 sum (K2) -------
-  // ranks 0/1 of the next unit are prefetched while this unit decodes;
-  // ld.global.cg: the shards were written by other CTAs of this kernel
-  {
-    using RL = RankLoad<B, BITS, kVPL2>;
-    const uint32_t total = (uint32_t)((F.n + kUnit2 - 1) / kUnit2);
-    const int nr = F.nranks;
-    uint32_t u = gw;
-    if (u < total) {
-      int64_t uoff = (int64_t)u * kUnit2;
-      int valid = max(0, min(kVPL2, (int)min((int64_t)kUnit2, F.n - uoff) - lane * kVPL2));
-      RL c0, c1;
-      load_rank<B, BITS, kVPL2, true>(c0, F.shards, F.scale_off, F.elem_off, uoff, lane, valid,
-                                      f.kbits);
-      if (nr > 1)
-        load_rank<B, BITS, kVPL2, true>(c1, F.shards + F.shard_stride, F.scale_off, F.elem_off,
-                                        uoff, lane, valid, f.kbits);
-      while (true) {
-        const uint32_t un = u + nw;
-        const bool more = un < total;
-        int64_t uoffn = uoff;
-        int validn = 0;
-        RL n0, n1;
-        if (more) {
-          uoffn = (int64_t)un * kUnit2;
-          validn = max(0, min(kVPL2, (int)min((int64_t)kUnit2, F.n - uoffn) - lane * kVPL2));
-          load_rank<B, BITS, kVPL2, true>(n0, F.shards, F.scale_off, F.elem_off, uoffn, lane,
-                                          validn, f.kbits);
-          if (nr > 1)
-            load_rank<B, BITS, kVPL2, true>(n1, F.shards + F.shard_stride, F.scale_off,
-                                            F.elem_off, uoffn, lane, validn, f.kbits);
-        }
-        float acc[kVPL2];
-#pragma unroll
-        for (int i = 0; i < kVPL2; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
-        decode_rank<B, DEC, BITS, kVPL2>(c0, f, acc, false, s_lut);
-        if (nr > 1) decode_rank<B, DEC, BITS, kVPL2>(c1, f, acc, false, s_lut);
-        const uint8_t* b = F.shards + 2 * F.shard_stride;
-        for (int rk = 2; rk < nr; ++rk, b += F.shard_stride) {
-          RL r;
-          load_rank<B, BITS, kVPL2, true>(r, b, F.scale_off, F.elem_off, uoff, lane, valid,
-                                          f.kbits);
-          decode_rank<B, DEC, BITS, kVPL2>(r, f, acc, false, s_lut);
-        }
-        if (valid > 0)
-          store_lane_out<OutT, kVPL2>(reinterpret_cast<OutT*>(F.out) + uoff + lane * kVPL2,
-                                      valid, acc);
-        if (!more) break;
-        u = un;
-        uoff = uoffn;
-        valid = validn;
-        c0 = n0;
-        c1 = n1;
-      }
-    }
-  }
-}
-
-// Lean variant for the common case: bf16 partials with n % 1024 == 0 and
-// E8M0 scales -- only full units, strength-reduced addressing, and one unit
-// of software pipelining in both phases (the next unit's loads are issued
-// before the current unit's arithmetic).  Phase 2 uses 32 values per lane.
-template <typename OutT, int B, int ENC, int BITS>
-__global__ void __launch_bounds__(kThreads, 3) k_fused_lean(const FArgs F) {
-  using InT = __nv_bfloat16;
-  constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
-  constexpr int NSB = Geo<B>::NSB;
-  constexpr int LPB = Geo<B>::LPB;
-  constexpr int UBYTES = kUnit / 8 * BITS;  // element-stream bytes per unit
-  constexpr int USCALES = kUnit / B;         // scale bytes per unit (k = 8)
-  __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
-  const Fmt f = F.f;
-  if constexpr (DEC != ENC_E2M1) fill_lut(s_lut, f);
-  const int lane = threadIdx.x & 31;
-  const uint32_t nw = (uint32_t)(gridDim.x * kWarps);
-  const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const uint32_t nunits = (uint32_t)(F.n / kUnit);
-  const int nr = F.nranks;
-
-  // ---- phase 1: quantise; u walks (rank, unit) pairs without division ----
-  {
-    uint32_t r = gw / nunits, q = gw - (gw / nunits) * nunits;
-    const InT* xr = r < (uint32_t)nr ? reinterpret_cast<const InT*>(F.partials[r]) : nullptr;
-    // one unit: codes + E8M0 scales of (rank r, unit q) from `raw`
-    auto quantise = [&](const Raw<InT>& raw, uint32_t rr, uint32_t qq) {
-      int stored[NSB];
-      bool bad;
-      LaneCodes<BITS> c = quant_lane<InT, B, ENC, BITS>(raw, f, stored, bad);
-      if (bad)
-        report_nonfinite_raw<InT>(raw, kVPL, (int64_t)qq * kUnit + lane * kVPL, F.nonfinite);
-      uint8_t* shard = F.shards + rr * F.shard_stride;
-      store_lane_codes<BITS>(shard + F.elem_off + (size_t)qq * UBYTES + lane * (4 * BITS), c,
-                             kVPL);
-      uint8_t* sp = shard + F.scale_off + (size_t)qq * USCALES + (lane / LPB) * NSB;
-      if constexpr (NSB == 4) {
-        *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
-                                           ((uint32_t)stored[2] << 16) |
-                                           ((uint32_t)stored[3] << 24);
-      } else if constexpr (NSB == 2) {
-        *reinterpret_cast<uint16_t*>(sp) = (uint16_t)(stored[0] | (stored[1] << 8));
-      } else {
-        if (lane % LPB == 0) *sp = (uint8_t)stored[0];
-      }
-    };
-    // next position (q += nw, carrying into the rank); reloads the rank base
-    auto advance = [&](uint32_t& rr, uint32_t& qq, const InT*& xx) {
-      qq += nw;
-      bool moved = false;
-      while (qq >= nunits && rr < (uint32_t)nr) {
-        qq -= nunits;
-        ++rr;
-        moved = true;
-      }
-      if (moved && rr < (uint32_t)nr) xx = reinterpret_cast<const InT*>(F.partials[rr]);
-    };
-    Raw<InT> b0, b1;  // ping-pong: no register copies between iterations
-    if (r < (uint32_t)nr) load_raw<InT>(xr + (size_t)q * kUnit + lane * kVPL, b0);
-    while (r < (uint32_t)nr) {
-      uint32_t rn = r, qn = q;
-      const InT* xn = xr;
-      advance(rn, qn, xn);
-      if (rn < (uint32_t)nr) load_raw<InT>(xn + (size_t)qn * kUnit + lane * kVPL, b1);
-      quantise(b0, r, q);
-      r = rn; q = qn; xr = xn;
-      if (r >= (uint32_t)nr) break;
-      advance(rn, qn, xn);
-      if (rn < (uint32_t)nr) load_raw<InT>(xn + (size_t)qn * kUnit + lane * kVPL, b0);
-      quantise(b1, r, q);
-      r = rn; q = qn; xr = xn;
-    }
-  }
-
-  grid_barrier(F.bar);
-
-  // ---- phase 2: dequant-sum, 32 values per lane, next unit prefetched ----
-  {
-    using RL = RankLoad<B, BITS, kVPL>;
-    auto load2 = [&](RL& x0, RL& x1, uint32_t uu) {
-      load_rank<B, BITS, kVPL, true>(x0, F.shards, F.scale_off, F.elem_off, (int64_t)uu * kUnit,
-                                     lane, kVPL, 8);
-      if (nr > 1)
-        load_rank<B, BITS, kVPL, true>(x1, F.shards + F.shard_stride, F.scale_off, F.elem_off,
-                                       (int64_t)uu * kUnit, lane, kVPL, 8);
-    };
-    auto reduce = [&](const RL& x0, const RL& x1, uint32_t uu) {
-      float acc[kVPL];
-#pragma unroll
-      for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
-      decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
-      if (nr > 1) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
-      const uint8_t* b = F.shards + 2 * F.shard_stride;
-      for (int rk = 2; rk < nr; ++rk, b += F.shard_stride) {
-        RL rr;
-        load_rank<B, BITS, kVPL, true>(rr, b, F.scale_off, F.elem_off, (int64_t)uu * kUnit,
-                                       lane, kVPL, 8);
-        decode_rank<B, DEC, BITS, kVPL>(rr, f, acc, false, s_lut);
-      }
-      store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(F.out) + (size_t)uu * kUnit +
-                                     lane * kVPL,
-                                 kVPL, acc);
-    };
-    uint32_t u = gw;
-    RL a0, a1, c0, c1;  // ping-pong
-    if (u < nunits) load2(a0, a1, u);
-    while (u < nunits) {
-      uint32_t un = u + nw;
-      if (un < nunits) load2(c0, c1, un);
-      reduce(a0, a1, u);
-      u = un;
-      if (u >= nunits) break;
-      un = u + nw;
-      if (un < nunits) load2(a0, a1, un);
-      reduce(c0, c1, u);
-      u = un;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Multi-GPU fused one-shot over symmetric (peer-mapped) memory: the NVLink
-// form of the kernel above.  Rank r quantises its partial into ITS shard of
-// the symmetric buffer (slot = epoch parity), a system-scope release/acquire
-// flag exchange replaces the all-gather, and phase 2 decodes the N shards
-// straight out of the peers' memory over NVLink (rank order, fp32, +0.0
-// start) -- no gather buffer, no NCCL kernel, one launch.  Double buffering:
-// a rank writes slot e&1 at epoch e only after it has seen every peer's
-// epoch e-1 flag, i.e. after every peer finished reading slot e&1 at e-2.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
-  unsigned int v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-template <typename OutT, int B, int ENC, int BITS>
-__global__ void __launch_bounds__(kThreads, 3) k_symm_oneshot(const SArgs S) {
-  using InT = __nv_bfloat16;
-  constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
-  constexpr int NSB = Geo<B>::NSB;
-  constexpr int LPB = Geo<B>::LPB;
-  constexpr int UBYTES = kUnit / 8 * BITS;
-  constexpr int USCALES = kUnit / B;
-  __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
-  const Fmt f = S.f;
-  if constexpr (DEC != ENC_E2M1) fill_lut(s_lut, f);
-  const int lane = threadIdx.x & 31;
-  const uint32_t nw = (uint32_t)(gridDim.x * kWarps);
-  const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const uint32_t nunits = (uint32_t)(S.n / kUnit);
-  const int nr = S.nranks;
-  const unsigned int e = *S.epoch + 1u;
-  const int64_t slot = (int64_t)(e & 1u) * S.slot_stride;
-
-  // ---- phase 1: quantise the local partial into my shard (slot e&1) -----
-  {
-    uint8_t* shard = S.bufs[S.rank] + slot;
-    auto quantise = [&](const Raw<InT>& raw, uint32_t q) {
-      int stored[NSB];
-      bool bad;
-      LaneCodes<BITS> c = quant_lane<InT, B, ENC, BITS>(raw, f, stored, bad);
-      if (bad)
-        report_nonfinite_raw<InT>(raw, kVPL, (int64_t)q * kUnit + lane * kVPL, S.nonfinite);
-      store_lane_codes<BITS>(shard + S.elem_off + (size_t)q * UBYTES + lane * (4 * BITS), c, kVPL);
-      uint8_t* sp = shard + S.scale_off + (size_t)q * USCALES + (lane / LPB) * NSB;
-      if constexpr (NSB == 4) {
-        *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
-                                           ((uint32_t)stored[2] << 16) |
-                                           ((uint32_t)stored[3] << 24);
-      } else if constexpr (NSB == 2) {
-        *reinterpret_cast<uint16_t*>(sp) = (uint16_t)(stored[0] | (stored[1] << 8));
-      } else {
-        if (lane % LPB == 0) *sp = (uint8_t)stored[0];
-      }
-    };
-    const InT* x = reinterpret_cast<const InT*>(S.x) + lane * kVPL;
-    Raw<InT> b0, b1;
-    uint32_t q = gw;
-    if (q < nunits) load_raw<InT>(x + (size_t)q * kUnit, b0);
-    while (q < nunits) {
-      uint32_t qn = q + nw;
-      if (qn < nunits) load_raw<InT>(x + (size_t)qn * kUnit, b1);
-      quantise(b0, q);
-      q = qn;
-      if (q >= nunits) break;
-      qn = q + nw;
-      if (qn < nunits) load_raw<InT>(x + (size_t)qn * kUnit, b0);
-      quantise(b1, q);
-      q = qn;
-    }
-  }
-  __threadfence_system();  // my shard bytes, before any flag leaves this GPU
-  grid_barrier(S.bar);
-
-  // ---- flag exchange: "my shard for epoch e is ready" ---------------------
-  if (blockIdx.x == 0 && threadIdx.x < (unsigned)nr) {
-    const int j = threadIdx.x;
-    st_release_sys(S.sigs[j] + S.rank, e);              // peer j's pad, my slot
-    const unsigned int* mine = S.sigs[S.rank] + j;      // my pad, peer j's slot
-    while ((int)(ld_acquire_sys(mine) - e) < 0) __nanosleep(64);
-  }
-  grid_barrier(S.bar);
-
-  // ---- phase 2: pull-decode the N shards over NVLink, rank order ---------
-  {
-    using RL = RankLoad<B, BITS, kVPL>;
-    auto load_r = [&](RL& x, int r, uint32_t uu) {
-      load_rank<B, BITS, kVPL, true>(x, S.bufs[r] + slot, S.scale_off, S.elem_off,
-                                     (int64_t)uu * kUnit, lane, kVPL, 8);
-    };
-    auto reduce = [&](const RL& x0, const RL& x1, uint32_t uu) {
-      float acc[kVPL];
-#pragma unroll
-      for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
-      decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
-      if (nr > 1) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
-      for (int rk = 2; rk < nr; ++rk) {
-        RL rr;
-        load_r(rr, rk, uu);
-        decode_rank<B, DEC, BITS, kVPL>(rr, f, acc, false, s_lut);
-      }
-      store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(S.out) + (size_t)uu * kUnit +
-                                     lane * kVPL,
-                                 kVPL, acc);
-    };
-    uint32_t u = gw;
-    RL a0, a1, c0, c1;
-    if (u < nunits) {
-      load_r(a0, 0, u);
-      if (nr > 1) load_r(a1, 1, u);
-    }
-    while (u < nunits) {
-      uint32_t un = u + nw;
-      if (un < nunits) {
-        load_r(c0, 0, un);
-        if (nr > 1) load_r(c1, 1, un);
-      }
-      reduce(a0, a1, u);
-      u = un;
-      if (u >= nunits) break;
-      un = u + nw;
-      if (un < nunits) {
-        load_r(a0, 0, un);
-        if (nr > 1) load_r(a1, 1, un);
-      }
-      reduce(c0, c1, u);
-      u = un;
-    }
-  }
-  // every CTA read *epoch before the first barrier: safe to advance it
-  if (blockIdx.x == 0 && threadIdx.x == 0) *S.epoch = e;
-}
-
-template <typename OutT, int B, int ENC, int BITS>
-void go_symm(const SArgs& a, cudaStream_t st) {
-  auto k = k_symm_oneshot<OutT, B, ENC, BITS>;
-  static thread_local int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, 0);
-  if (occ < 1) occ = 1;
-  const int64_t need = (a.n / kUnit + kWarps - 1) / kWarps;
-  k<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ, need)), kThreads, 0,
-      st>>>(a);
-}
-
-template <typename InT, typename OutT, int B, int ENC, int BITS>
-void go(const FArgs& a, cudaStream_t st) {
-  auto k = k_fused_oneshot<InT, OutT, B, ENC, BITS>;
-  if (a.n % kUnit == 0 && a.f.kbits == 8) k = k_fused_lean<OutT, B, ENC, BITS>;
-  static thread_local int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, 0);
-  if (occ < 1) occ = 1;
-  // every CTA must be resident for the grid barrier: at most one wave, and
-  // no more CTAs than the larger phase has warp units for
-  const int64_t units = std::max<int64_t>((a.n + kUnit2 - 1) / kUnit2,
-                                          a.nranks * ((a.n + kUnit - 1) / kUnit));
-  const int64_t need = (units + kWarps - 1) / kWarps;
-  k<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ, need)), kThreads, 0,
-      st>>>(a);
-}
-
+namespace fz {
 template <typename InT, typename OutT, int B>
-void by_enc(const FArgs& a, int enc, int bits, cudaStream_t st) {
-  switch (enc) {
-    case ENC_E2M1: go<InT, OutT, B, ENC_E2M1, 4>(a, st); return;
-    case ENC_E2M3: go<InT, OutT, B, ENC_E2M3, 6>(a, st); return;
-    case ENC_E3M2: go<InT, OutT, B, ENC_E3M2, 6>(a, st); return;
-    case ENC_INT:
-      if (bits == 4) go<InT, OutT, B, ENC_INT, 4>(a, st);
-      else if (bits == 5) go<InT, OutT, B, ENC_INT, 5>(a, st);
-      else go<InT, OutT, B, ENC_INT, 8>(a, st);
-      return;
-  }
-  switch (bits) {
-    case 4: go<InT, OutT, B, ENC_GEN, 4>(a, st); return;
-    case 5: go<InT, OutT, B, ENC_GEN, 5>(a, st); return;
-    case 6: go<InT, OutT, B, ENC_GEN, 6>(a, st); return;
-    default: go<InT, OutT, B, ENC_GEN, 8>(a, st); return;
-  }
-}
+void by_enc(const FArgs& a, int enc, int bits, cudaStream_t st);
+template <typename OutT, int B>
+bool symm_by_enc(const SArgs& a, int enc, int bits, cudaStream_t st);
 
 template <typename OutT>
 void by_block(const FArgs& a, int block, int enc, int bits, cudaStream_t st) {
@@ -482,25 +18,11 @@ void by_block(const FArgs& a, int block, int enc, int bits, cudaStream_t st) {
     case 64: by_enc<__nv_bfloat16, OutT, 64>(a, enc, bits, st); return;
   }
 }
-
-template <typename OutT, int B>
-bool symm_by_enc(const SArgs& a, int enc, int bits, cudaStream_t st) {
-  switch (enc) {
-    case ENC_E2M1: go_symm<OutT, B, ENC_E2M1, 4>(a, st); return true;
-    case ENC_E2M3: go_symm<OutT, B, ENC_E2M3, 6>(a, st); return true;
-    case ENC_E3M2: go_symm<OutT, B, ENC_E3M2, 6>(a, st); return true;
-    case ENC_INT:
-      if (bits == 8) { go_symm<OutT, B, ENC_INT, 8>(a, st); return true; }
-      return false;
-  }
-  if (bits == 5) { go_symm<OutT, B, ENC_GEN, 5>(a, st); return true; }
-  return false;
-}
-
-}  // namespace
+}  // namespace fz
 
 bool launch_symm_oneshot(const SArgs& a, int out_is_bf16, int block, int enc, int bits,
                          cudaStream_t st) {
+  using namespace fz;
   switch (block) {
     case 16: return out_is_bf16 ? symm_by_enc<__nv_bfloat16, 16>(a, enc, bits, st)
                                 : symm_by_enc<float, 16>(a, enc, bits, st);
@@ -517,8 +39,8 @@ bool launch_fused_oneshot(const FArgs& a, int out_is_bf16, int block, int enc, i
                           cudaStream_t st) {
   if (!(block == 8 || block == 16 || block == 32 || block == 64)) return false;
   if (!(bits == 4 || bits == 5 || bits == 6 || bits == 8)) return false;
-  if (out_is_bf16) by_block<__nv_bfloat16>(a, block, enc, bits, st);
-  else by_block<float>(a, block, enc, bits, st);
+  if (out_is_bf16) fz::by_block<__nv_bfloat16>(a, block, enc, bits, st);
+  else fz::by_block<float>(a, block, enc, bits, st);
   return true;
 }
 

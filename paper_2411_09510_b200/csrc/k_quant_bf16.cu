@@ -1,12 +1,18 @@
-// Fast quantise kernels, __nv_bfloat16 input (instantiations).
+// Fast quantise kernels, __nv_bfloat16 input (instantiations).  build.py
+// compiles this file once per -DMXB_B (block size slice); the MXB_B=8 slice
+// also carries the dispatcher.
 #include "mx_kernels.cuh"
 
+#ifndef MXB_B
+#error "compile with -DMXB_B=<8|16|32|64>"
+#endif
+
 namespace mxb {
-namespace {
+namespace qb {
 template <int B, int ENC, int BITS>
 void go(const QArgs& a, cudaStream_t st) {
   auto k = k_quant<__nv_bfloat16, B, ENC, BITS>;
-  k<<<work_grid(k, a.total_units, kUPW), kThreads, 0, st>>>(a);
+  k<<<work_grid(k, a.total_units, 1), kThreads, 0, st>>>(a);
 }
 template <int B>
 void by_enc(const QArgs& a, int enc, int bits, cudaStream_t st) {
@@ -32,9 +38,17 @@ void by_enc(const QArgs& a, int enc, int bits, cudaStream_t st) {
     default: go<B, ENC_GEN, 8>(a, st); return;
   }
 }
-}  // namespace
+template void by_enc<MXB_B>(const QArgs&, int, int, cudaStream_t);
+#if MXB_B == 8  // the dispatcher links to the other slices
+extern template void by_enc<16>(const QArgs&, int, int, cudaStream_t);
+extern template void by_enc<32>(const QArgs&, int, int, cudaStream_t);
+extern template void by_enc<64>(const QArgs&, int, int, cudaStream_t);
+#endif
+}  // namespace qb
 
+#if MXB_B == 8
 void launch_quant_bf16(const QArgs& a, int block, int enc, int bits, cudaStream_t st) {
+  using namespace qb;
   switch (block) {
     case 8: by_enc<8>(a, enc, bits, st); return;
     case 16: by_enc<16>(a, enc, bits, st); return;
@@ -42,4 +56,5 @@ void launch_quant_bf16(const QArgs& a, int block, int enc, int bits, cudaStream_
     case 64: by_enc<64>(a, enc, bits, st); return;
   }
 }
+#endif
 }  // namespace mxb

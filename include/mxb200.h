@@ -190,6 +190,43 @@ int mx_unpack_codes(const uint8_t* packed, int64_t count, int32_t width, uint8_t
 int mx_pack_codes(const uint8_t* codes, int64_t count, int32_t width, uint8_t* packed,
                   void* stream);
 
+/* ---- comparison codecs (mx/baselines.py), the paper's Table 4 baselines ---- */
+
+/* channelwise_int_compress (mx/baselines.py:138-168): x is `rows` x
+ * `channels` (channels = trailing dimension, row-major); per-channel scale
+ * = f16_RNE(max|x| / (2^(bits-1)-1)) written as IEEE half bits to
+ * `scales[channels]`; sign-magnitude codes rounded half-to-even against the
+ * stored scale, clamped, LSB-first packed into `codes`
+ * (ceil(rows*channels*bits/8) bytes).  bits in [2, 8].  `workspace` >=
+ * 8*channels bytes.  dtype MX_F32/F16/BF16/F64.  Non-finite inputs lower
+ * *nonfinite to their flat index (NonFiniteInput). */
+int mx_chanint_compress(const void* x, int32_t dtype, int64_t rows, int64_t channels,
+                        int32_t bits, uint16_t* scales, uint8_t* codes, void* workspace,
+                        int64_t workspace_bytes, uint64_t* nonfinite, void* stream);
+
+/* channelwise_int_decompress (mx/baselines.py:171-178): level * scale in
+ * float64, cast once to out_dtype (MX_F64 exact, MX_F32, MX_BF16). */
+int mx_chanint_decompress(const uint16_t* scales, const uint8_t* codes, int64_t rows,
+                          int64_t channels, int32_t bits, void* out, int32_t out_dtype,
+                          void* stream);
+
+/* Workspace bytes of mx_topk_compress for n values. */
+int mx_topk_workspace_bytes(int64_t n, int64_t* bytes);
+
+/* topk_compress (mx/baselines.py:95-128) with an explicit K (the caller
+ * computes topk_budget, mx/baselines.py:88-92): the K largest |x|, ties
+ * toward the lower index, written in ascending index order as u32
+ * `indices[K]` and IEEE half bits `values[K]` (RNE, overflow -> inf).
+ * Radix select + stable compaction, no host synchronisation. */
+int mx_topk_compress(const void* x, int32_t dtype, int64_t n, int64_t k, uint32_t* indices,
+                     uint16_t* values, void* workspace, int64_t workspace_bytes,
+                     uint64_t* nonfinite, void* stream);
+
+/* topk_decompress (mx/baselines.py:131-135): zeros, then the K f16 values
+ * scattered to their indices; out_dtype MX_F64 / MX_F32 / MX_BF16. */
+int mx_topk_decompress(const uint32_t* indices, const uint16_t* values, int64_t k, int64_t n,
+                       void* out, int32_t out_dtype, void* stream);
+
 /* cudaMemsetAsync on `stream` (e.g. zeroing a symmetric-memory signal pad
  * without pulling the CUDA runtime into the host language). */
 int mx_memset_async(void* ptr, int32_t value, int64_t bytes, void* stream);

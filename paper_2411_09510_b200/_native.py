@@ -56,6 +56,12 @@ SIGNATURES = {
                                   c_i32, c_vp, c_vp, c_vp, c_vp]),
     "mx_unpack_codes": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp]),
     "mx_pack_codes": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "mx_chanint_compress": (c_i32, [c_vp, c_i32, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_i64,
+                                    c_vp, c_vp]),
+    "mx_chanint_decompress": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_i32, c_vp]),
+    "mx_topk_workspace_bytes": (c_i32, [c_i64, c_i64p]),
+    "mx_topk_compress": (c_i32, [c_vp, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "mx_topk_decompress": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i32, c_vp]),
     "mx_memset_async": (c_i32, [c_vp, c_i32, c_i64, c_vp]),
     "mx_nonfinite_reset": (c_i32, [c_vp, c_vp]),
 }

@@ -5,6 +5,10 @@ namespace mxb {
 namespace {
 template <int B, int DEC, int BITS>
 void go(const DArgs& a, cudaStream_t st) {
+  if (!a.plain && a.units_per_chunk == a.total_units && a.f.kbits == 8 && a.n % kUnit == 0) {
+    k_dqsum_lean<float, B, DEC, BITS><<<(unsigned)(a.n / kUnit / kWarps), kThreads, 0, st>>>(a);
+    return;
+  }
   auto k = k_dqsum<float, B, DEC, BITS>;
   k<<<work_grid(k, a.total_units, 2), kThreads, 0, st>>>(a);
 }

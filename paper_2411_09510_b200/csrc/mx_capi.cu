@@ -649,4 +649,66 @@ int mx_nonfinite_reset(uint64_t* nonfinite, void* stream) {
   return cuda_check("mx_nonfinite_reset");
 }
 
+int mx_chanint_compress(const void* x, int32_t dtype, int64_t rows, int64_t channels,
+                        int32_t bits, uint16_t* scales, uint8_t* codes, void* workspace,
+                        int64_t workspace_bytes, uint64_t* nonfinite, void* stream) {
+  if (bits < 2 || bits > 8) return fail(MX_ERR_INVALID_ARGUMENT, "bits must be in [2, 8], got %d", bits);
+  if (rows < 0 || channels < 1) return fail(MX_ERR_SHAPE, "bad shape (%lld x %lld)", (long long)rows, (long long)channels);
+  if (in_size(dtype) == 0) return fail(MX_ERR_INVALID_ARGUMENT, "unknown input dtype %d", dtype);
+  if (rows == 0) return MX_OK;
+  if (!x || !scales || !codes) return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (!workspace || workspace_bytes < 8 * channels)
+    return fail(MX_ERR_WORKSPACE, "channel INT needs %lld workspace bytes", (long long)(8 * channels));
+  launch_chanint_compress(x, dtype, rows, channels, bits, scales, codes, workspace,
+                          reinterpret_cast<unsigned long long*>(nonfinite), (cudaStream_t)stream);
+  return cuda_check("chanint compress");
+}
+
+int mx_chanint_decompress(const uint16_t* scales, const uint8_t* codes, int64_t rows,
+                          int64_t channels, int32_t bits, void* out, int32_t out_dtype,
+                          void* stream) {
+  if (bits < 2 || bits > 8) return fail(MX_ERR_INVALID_ARGUMENT, "bits must be in [2, 8], got %d", bits);
+  if (rows < 0 || channels < 1) return fail(MX_ERR_SHAPE, "bad shape");
+  if (out_dtype != MX_F64 && out_dtype != MX_F32 && out_dtype != MX_BF16)
+    return fail(MX_ERR_INVALID_ARGUMENT, "out dtype must be f64, f32 or bf16");
+  if (rows == 0) return MX_OK;
+  if (!scales || !codes || !out) return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
+  launch_chanint_decompress(scales, codes, rows * channels, channels, bits, out, out_dtype,
+                            (cudaStream_t)stream);
+  return cuda_check("chanint decompress");
+}
+
+int mx_topk_workspace_bytes(int64_t n, int64_t* bytes) {
+  if (n < 0 || !bytes) return fail(MX_ERR_INVALID_ARGUMENT, "bad arguments");
+  *bytes = topk_workspace_bytes(n);
+  return MX_OK;
+}
+
+int mx_topk_compress(const void* x, int32_t dtype, int64_t n, int64_t k, uint32_t* indices,
+                     uint16_t* values, void* workspace, int64_t workspace_bytes,
+                     uint64_t* nonfinite, void* stream) {
+  if (n < 0 || k < 0 || k > n) return fail(MX_ERR_INVALID_ARGUMENT, "need 0 <= k <= n");
+  if (n > 0xffffffffLL) return fail(MX_ERR_UNSUPPORTED, "TopK indices are u32");
+  if (in_size(dtype) == 0) return fail(MX_ERR_INVALID_ARGUMENT, "unknown input dtype %d", dtype);
+  if (k == 0) return MX_OK;
+  if (!x || !indices || !values) return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (!workspace || workspace_bytes < topk_workspace_bytes(n))
+    return fail(MX_ERR_WORKSPACE, "TopK needs %lld workspace bytes", (long long)topk_workspace_bytes(n));
+  if (((uintptr_t)workspace) % 256 != 0) return fail(MX_ERR_INVALID_ARGUMENT, "workspace must be 256-B aligned");
+  launch_topk_compress(x, dtype, n, k, indices, values, workspace,
+                       reinterpret_cast<unsigned long long*>(nonfinite), (cudaStream_t)stream);
+  return cuda_check("topk compress");
+}
+
+int mx_topk_decompress(const uint32_t* indices, const uint16_t* values, int64_t k, int64_t n,
+                       void* out, int32_t out_dtype, void* stream) {
+  if (n < 0 || k < 0 || k > n) return fail(MX_ERR_INVALID_ARGUMENT, "need 0 <= k <= n");
+  if (out_dtype != MX_F64 && out_dtype != MX_F32 && out_dtype != MX_BF16)
+    return fail(MX_ERR_INVALID_ARGUMENT, "out dtype must be f64, f32 or bf16");
+  if (n == 0) return MX_OK;
+  if (!out || (k > 0 && (!indices || !values))) return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
+  launch_topk_decompress(indices, values, k, n, out, out_dtype, (cudaStream_t)stream);
+  return cuda_check("topk decompress");
+}
+
 }  // extern "C"

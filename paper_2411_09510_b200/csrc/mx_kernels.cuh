@@ -917,6 +917,41 @@ __global__ void __launch_bounds__(kThreads) k_dqsum(const DArgs A) {
   }
 }
 
+// K2 lean form for the common case -- one chunk, E8M0 scales, n a multiple
+// of 1024, accumulate mode: one 1024-value unit per warp (32 values per
+// lane, the quantiser's layout), no chunk / tail / generic-scale logic, the
+// ranks' codes loaded two at a time before their decode.  A flat grid of
+// one unit per warp lets the block scheduler balance the waves.
+template <typename OutT, int B, int DEC, int BITS>
+__global__ void __launch_bounds__(kThreads) k_dqsum_lean(const DArgs A) {
+  using RL = RankLoad<B, BITS, kVPL>;
+  __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
+  const Fmt f = A.f;
+  if constexpr (DEC != ENC_E2M1) {
+    fill_lut(s_lut, f);
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  const uint32_t u = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (u >= (uint32_t)(A.n / kUnit)) return;
+  const int64_t uoff = (int64_t)u * kUnit;
+  const int nr = A.nranks;
+  float acc[kVPL];
+#pragma unroll
+  for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
+  const uint8_t* b = A.in;
+  for (int r = 0; r < nr; r += 2, b += 2 * A.rank_stride) {
+    RL x0, x1;
+    load_rank<B, BITS, kVPL>(x0, b, A.scale_off, A.elem_off, uoff, lane, kVPL, 8);
+    if (r + 1 < nr)
+      load_rank<B, BITS, kVPL>(x1, b + A.rank_stride, A.scale_off, A.elem_off, uoff, lane, kVPL,
+                               8);
+    decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
+    if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
+  }
+  store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(A.out) + uoff + lane * kVPL, kVPL, acc);
+}
+
 // ---------------------------------------------------------------------------
 // K3: two-shot middle step -- sum N shards of one chunk, re-quantise
 // ---------------------------------------------------------------------------
@@ -1006,6 +1041,18 @@ void launch_dqsum_f32(const DArgs& a, int block, int enc, int bits, cudaStream_t
 void launch_requant(const RArgs& a, int block, int enc, int bits, cudaStream_t st);
 int64_t launch_quant_tma(const QArgs& a, int dtype_is_bf16, int block, int enc, int bits,
                          cudaStream_t st);
+
+// comparison codecs (k_baselines.cu, mx/baselines.py); dtype codes of mxb200.h
+int64_t topk_workspace_bytes(int64_t n);
+void launch_chanint_compress(const void* x, int dtype, int64_t rows, int64_t C, int bits,
+                             uint16_t* scales, uint8_t* codes, void* ws,
+                             unsigned long long* nf, cudaStream_t st);
+void launch_chanint_decompress(const uint16_t* scales, const uint8_t* codes, int64_t n, int64_t C,
+                               int bits, void* out, int out_dtype, cudaStream_t st);
+void launch_topk_compress(const void* x, int dtype, int64_t n, int64_t k, uint32_t* idx,
+                          uint16_t* val, void* ws, unsigned long long* nf, cudaStream_t st);
+void launch_topk_decompress(const uint32_t* idx, const uint16_t* val, int64_t k, int64_t n,
+                            void* out, int out_dtype, cudaStream_t st);
 
 // Grid: enough CTAs that every warp gets `per_warp` units, never more than
 // one resident wave (#SMs x occupancy).

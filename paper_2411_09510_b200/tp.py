@@ -111,19 +111,192 @@ def _sqnr_db(ref: np.ndarray, err: np.ndarray) -> float:
     return 10.0 * np.log10(float(np.sum(np.square(ref))) / e)  # as mx/tpsim.py:231
 
 
+class _MxCodec:
+    """MX block codec on the GPU (mx/tpsim.py:51-63)."""
+
+    def __init__(self, scheme: SchemeDescriptor):
+        self.scheme = scheme
+        self.name = scheme.name
+
+    def encode(self, arr) -> bytes:
+        from .codec import compress_tensor, serialize
+
+        return serialize(compress_tensor(np.asarray(arr), self.scheme))
+
+    def decode(self, data: bytes, shape) -> np.ndarray:
+        from .codec import decompress_tensor, deserialize
+
+        out = decompress_tensor(deserialize(data))
+        if out.shape != tuple(shape):
+            raise ShapeMismatch(f"payload shape {out.shape} != expected {tuple(shape)}")
+        return out
+
+    def roundtrip(self, p: np.ndarray):
+        """(float64 reconstruction, payload bytes) without host byte streams."""
+        import torch
+
+        from .codec import compress_tensor_device, decompress_tensor_device, serialized_nbytes
+
+        dct = compress_tensor_device(torch.from_numpy(np.ascontiguousarray(p)).cuda(), self.scheme)
+        rec = decompress_tensor_device(dct, torch.float64).cpu().numpy()
+        return rec, serialized_nbytes(self.scheme, p.shape)
+
+
+class _PassthroughCodec:
+    """Raw float32 bytes (mx/tpsim.py:66-82): numerically the identity."""
+
+    name = "passthrough"
+
+    def encode(self, arr) -> bytes:
+        from .codec import FORMAT_CODE_RAW_F32, pack_header
+
+        a = np.asarray(arr)
+        return pack_header(FORMAT_CODE_RAW_F32, 0, 0, tuple(a.shape)) + \
+            np.ascontiguousarray(a, dtype="<f4").tobytes()
+
+    def decode(self, data: bytes, shape) -> np.ndarray:
+        from .codec import unpack_header
+
+        _, _, _, wshape, off = unpack_header(data)
+        n = int(np.prod(wshape, dtype=np.int64))
+        return np.frombuffer(data, "<f4", count=n, offset=off).astype(np.float64).reshape(wshape)
+
+    def roundtrip(self, p: np.ndarray):
+        from .codec import header_nbytes
+
+        return p.astype(np.float32).astype(np.float64), header_nbytes(p.ndim) + 4 * p.size
+
+
+class _Fp16Codec:
+    """IEEE half round trip (mx/tpsim.py:85-100), the 16-bit wire baseline;
+    the cast runs on the GPU."""
+
+    name = "fp16"
+
+    def encode(self, arr) -> bytes:
+        from .codec import FORMAT_CODE_RAW_F16, pack_header
+
+        a = np.asarray(arr)
+        h = self._half(a)
+        return pack_header(FORMAT_CODE_RAW_F16, 0, 0, tuple(a.shape)) + h.astype("<f2").tobytes()
+
+    def decode(self, data: bytes, shape) -> np.ndarray:
+        from .codec import unpack_header
+
+        _, _, _, wshape, off = unpack_header(data)
+        n = int(np.prod(wshape, dtype=np.int64))
+        return np.frombuffer(data, "<f2", count=n, offset=off).astype(np.float64).reshape(wshape)
+
+    @staticmethod
+    def _half(a: np.ndarray) -> np.ndarray:
+        import torch
+
+        from . import _native
+
+        _native.require_cuda()
+        t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+        return t.to(torch.float16).cpu().numpy()  # one RNE rounding from float64
+
+    def roundtrip(self, p: np.ndarray):
+        from .codec import header_nbytes
+
+        return self._half(p).astype(np.float64), header_nbytes(p.ndim) + 2 * p.size
+
+
+class _TopKCodec:
+    """TopK on the GPU (mx/tpsim.py:100-109)."""
+
+    def __init__(self, factor: float):
+        self.factor = factor
+        self.name = f"topk:{factor:g}"
+
+    def encode(self, arr) -> bytes:
+        from . import baselines as bl
+
+        return bl.serialize_topk(bl.topk_compress(arr, self.factor))
+
+    def decode(self, data: bytes, shape) -> np.ndarray:
+        from . import baselines as bl
+
+        return bl.topk_decompress(bl.deserialize_topk(data))
+
+    def roundtrip(self, p: np.ndarray):
+        import torch
+
+        from . import baselines as bl
+        from .codec import header_nbytes
+
+        k = bl.topk_budget(p.size, p.ndim, self.factor)
+        if self.factor <= 1 or k < 1:
+            from .errors import CompressionFactorTooHigh
+
+            raise CompressionFactorTooHigh(f"factor {self.factor} leaves room for {k} values")
+        idx, val = bl.topk_compress_device(torch.from_numpy(np.ascontiguousarray(p)), k)
+        rec = bl.topk_decompress_device(idx, val, p.size, torch.float64).cpu().numpy()
+        return rec.reshape(p.shape), header_nbytes(p.ndim) + 6 * idx.numel()
+
+
+class _ChannelIntCodec:
+    """Channel-wise INT on the GPU (mx/tpsim.py:112-125)."""
+
+    def __init__(self, bits: int):
+        self.bits = bits
+        self.name = f"chanint:{bits}"
+
+    def encode(self, arr) -> bytes:
+        from . import baselines as bl
+
+        return bl.serialize_channel_int(bl.channelwise_int_compress(arr, self.bits))
+
+    def decode(self, data: bytes, shape) -> np.ndarray:
+        from . import baselines as bl
+
+        return bl.channelwise_int_decompress(bl.deserialize_channel_int(data))
+
+    def roundtrip(self, p: np.ndarray):
+        import torch
+
+        from . import baselines as bl
+        from .codec import header_nbytes
+
+        s, c, shape = bl.channelwise_int_compress_device(torch.from_numpy(np.ascontiguousarray(p)),
+                                                         self.bits)
+        rec = bl.channelwise_int_decompress_device(s, c, shape, self.bits, torch.float64)
+        return rec.cpu().numpy().reshape(p.shape), header_nbytes(p.ndim) + 2 * s.numel() + c.numel()
+
+
+def resolve_codec(scheme):
+    """A SchemeDescriptor or codec id -> codec object (mx/tpsim.py:128-143):
+    MX schemes, ``passthrough``/``none``, ``fp16``, ``topk:F``, ``chanint:B``."""
+    from .errors import UnknownScheme
+
+    if isinstance(scheme, SchemeDescriptor):
+        return _MxCodec(scheme)
+    if not isinstance(scheme, str):
+        raise UnknownScheme(f"cannot interpret {scheme!r} as a codec")
+    name = scheme.strip().lower()
+    if name in ("passthrough", "none"):
+        return _PassthroughCodec()
+    if name == "fp16":
+        return _Fp16Codec()
+    if name.startswith("topk:"):
+        return _TopKCodec(float(name.split(":", 1)[1]))
+    if name.startswith("chanint:"):
+        return _ChannelIntCodec(int(name.split(":", 1)[1]))
+    return _MxCodec(parse_scheme(name, extensions=True))
+
+
 def simulate_reduction(cfg: TPConfig, x=None, w=None, partials_on_gpu: bool = False,
                        partials=None):
     """One compress/exchange/decompress/reduce cycle, scored (mx/tpsim.py:234-302).
 
-    The codec runs on the GPU (compress_tensor / decompress_tensor through
-    the sm_100a kernels).  Partials are computed with numpy (bit-identical to
-    the reference) unless ``partials_on_gpu`` (cuBLAS fp32, faster, sums
-    differ in the last bits).  ``partials`` injects precomputed fp32 partial
-    products (one per rank) -- BLAS results depend on the host CPU, so parity
-    tests replay the reference's own partials."""
+    The codec (any id of :func:`resolve_codec`) runs on the GPU.  Partials
+    are computed with numpy (bit-identical to the reference) unless
+    ``partials_on_gpu`` (cuBLAS fp32, faster, sums differ in the last bits).
+    ``partials`` injects precomputed fp32 partial products (one per rank) --
+    BLAS results depend on the host CPU, so parity tests replay the
+    reference's own partials."""
     import torch
-
-    from .codec import compress_tensor_device, decompress_tensor_device, serialized_nbytes
 
     if x is None or w is None:
         gx, gw = generate_inputs(cfg)
@@ -137,10 +310,10 @@ def simulate_reduction(cfg: TPConfig, x=None, w=None, partials_on_gpu: bool = Fa
     if padding:
         x = np.pad(x, [(0, 0)] * (x.ndim - 1) + [(0, padding)])
     rows = shards[0].shape[0]
-    scheme = cfg.scheme if isinstance(cfg.scheme, SchemeDescriptor) else parse_scheme(
-        str(cfg.scheme), extensions=True)
+    wire = resolve_codec(cfg.scheme)
     given = partials
     partials, decoded = [], []
+    payload = None
     for r in range(cfg.degree):
         xs = x[..., r * rows:(r + 1) * rows]
         if given is not None:
@@ -151,11 +324,10 @@ def simulate_reduction(cfg: TPConfig, x=None, w=None, partials_on_gpu: bool = Fa
         else:
             p = xs @ shards[r]  # float32, like the deployed matmul (tpsim.py:263)
         partials.append(p)
-        if cfg.quantize_own or r != 0:
-            dct = compress_tensor_device(torch.from_numpy(np.ascontiguousarray(p)).cuda(), scheme)
-            decoded.append(decompress_tensor_device(dct, torch.float64).cpu().numpy())
-        else:
-            decoded.append(p.astype(np.float64))
+        rec, nbytes = wire.roundtrip(p)
+        if payload is None:
+            payload = nbytes
+        decoded.append(rec if (cfg.quantize_own or r != 0) else p.astype(np.float64))
     ref = np.zeros(partials[0].shape, np.float64)
     red = np.zeros_like(ref)
     per = np.zeros_like(ref)
@@ -168,9 +340,8 @@ def simulate_reduction(cfg: TPConfig, x=None, w=None, partials_on_gpu: bool = Fa
     if not (np.abs(err) <= per + tol).all():  # tpsim.py:284-288
         raise AssertionError("summed error exceeded per-worker error budget")
     en, rn = float(np.linalg.norm(err.ravel())), float(np.linalg.norm(ref.ravel()))
-    payload = serialized_nbytes(scheme, partials[0].shape)  # container size (codec.py:291)
     return ReductionReport(
-        degree=cfg.degree, scheme=scheme.name, rel_frob_err=0.0 if en == 0.0 else en / rn,
+        degree=cfg.degree, scheme=wire.name, rel_frob_err=0.0 if en == 0.0 else en / rn,
         max_abs_err=float(np.max(np.abs(err))), sqnr_db=_sqnr_db(ref, err),
         bytes_compressed=(cfg.degree - 1) * int(payload),
         bytes_uncompressed=(cfg.degree - 1) * ref.size * UNCOMPRESSED_VALUE_BYTES,

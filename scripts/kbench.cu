@@ -366,7 +366,9 @@ int main(int argc, char** argv) {
   // K1 current kernel with other grids
   {
     auto k = k_quant<__nv_bfloat16, 32, ENC_E2M1, 4>;
-    for (int c : {2, 3, 4, 5, 6, 8}) {
+    bench("k_quant(flat grid, 1 unit/warp)", R, [&](int i, cudaStream_t s) {
+      k<<<(unsigned)(n / kUnit / kWarps), kThreads, 0, s>>>(qa(i)); }, kbytes, st);
+    for (int c : {4}) {
       char nm[64];
       snprintf(nm, sizeof nm, "k_quant(grid=%dx148)", c);
       bench(nm, R, [&](int i, cudaStream_t s) { k<<<sms * c, kThreads, 0, s>>>(qa(i)); }, kbytes, st);
@@ -397,7 +399,17 @@ int main(int argc, char** argv) {
     unsigned g = work_grid(k, n / kUnit2, 2);
     printf("# k_dqsum current grid %u\n", g);
     bench("k_dqsum(current)", R, [&](int i, cudaStream_t s) { k<<<g, kThreads, 0, s>>>(da(i)); }, k2bytes, st);
-    for (int c : {2, 3, 4, 5, 6, 7, 8}) {
+    auto kl = k_dqsum_lean<__nv_bfloat16, 32, ENC_E2M1, 4>;
+    std::vector<uint16_t> r2(n), g2(n);
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(r2.data(), B.y[0], xbytes, cudaMemcpyDeviceToHost));
+    CK(cudaMemset(B.y[0], 0, xbytes));
+    bench("k_dqsum_lean", R, [&](int i, cudaStream_t s) {
+      kl<<<(unsigned)(n / kUnit / kWarps), kThreads, 0, s>>>(da(i)); }, k2bytes, st);
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(g2.data(), B.y[0], xbytes, cudaMemcpyDeviceToHost));
+    printf("# lean %s\n", g2 == r2 ? "identical" : "DIFFER");
+    for (int c : {4}) {
       char nm[64];
       snprintf(nm, sizeof nm, "k_dqsum(grid=%dx148)", c);
       bench(nm, R, [&](int i, cudaStream_t s) { k<<<sms * c, kThreads, 0, s>>>(da(i)); }, k2bytes, st);

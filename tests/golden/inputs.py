@@ -116,3 +116,47 @@ LARGE_SHAPE = (2048, 4096)
 LARGE_SCHEMES = ["fp4_e2m1:32:e8m0", "fp4_e2m1:16:e8m0", "fp4_e2m1:64:e8m0",
                  "fp5_e2m2:32:e8m0", "fp6_e2m3:32:e8m0", "int8:32:e8m0",
                  "fp4_e2m1:32:e5m0"]
+
+
+# ---------------------------------------------------------------------------
+# comparison codecs (mx/baselines.py): shaped cases, channels = last dim
+# ---------------------------------------------------------------------------
+
+
+def ties_bf16(rows: int, cols: int, seed: int) -> np.ndarray:
+    """Few distinct magnitudes (TopK ties, broken toward the lower index),
+    an all-zero and an all-(-0) channel, and a channel whose scale is
+    exactly 1 at 4 bits (max 7) so x/scale lands on .5 ties."""
+    rng = np.random.default_rng(seed)
+    x = rng.choice(np.array([0.0, 0.5, -0.5, 1.0, -1.0, 1.5, 2.0, -2.0, 3.0, -3.0]),
+                   size=(rows, cols))
+    x[:, 5] = 0.0
+    x[:, 9] = -0.0
+    x[:, 3] = rng.choice(np.array([0.5, 1.5, 2.5, -3.5, -0.5, 4.5]), size=rows)
+    x[0, 3] = 7.0
+    return x
+
+
+def wide_range_f32(rows: int, cols: int, seed: int) -> np.ndarray:
+    """Per-channel magnitudes from 1e-9 to 1e6: f16 scales that are
+    subnormal, normal and (at low bit widths) overflow to inf."""
+    rng = np.random.default_rng(seed)
+    mag = 10.0 ** rng.uniform(-9, 6, size=cols)
+    x = rng.standard_normal((rows, cols)) * mag
+    return x.astype(np.float32).astype(np.float64)
+
+
+BASELINE_CASES = {
+    "gauss_bf16_64x256": (lambda: gauss_bf16(64 * 256, 11).reshape(64, 256), "bf16"),
+    "gauss_f32_33x100": (lambda: gauss_f32(3300, 12).reshape(33, 100), "f32"),
+    "gauss_f16_777": (lambda: gauss_f16(777, 13), "f16"),
+    "ties_bf16_48x64": (lambda: ties_bf16(48, 64, 14), "bf16"),
+    "wide_f32_16x40": (lambda: wide_range_f32(16, 40, 15), "f32"),
+    "prefill_bf16_2048x4096": (
+        lambda: bf16_round(gaussian_with_outliers(np.random.default_rng(0), (2048, 4096)))
+        .astype(np.float64), "bf16"),
+}
+
+
+def baseline_case(name: str) -> np.ndarray:
+    return BASELINE_CASES[name][0]()

@@ -162,23 +162,33 @@ int mx_allreduce_fused(const void* const* partials, int32_t dtype, int32_t nrank
                        void* out, int32_t out_dtype, uint32_t* barrier, uint64_t* nonfinite,
                        void* stream);
 
-/* Multi-GPU one-shot fused over symmetric (peer-mapped) memory, one launch
- * per rank: quantise `x` into this rank's shard slot of its symmetric buffer,
- * exchange "ready" flags with every peer over NVLink (system-scope
- * release/acquire on the signal pads), then decode all nranks shards
+/* Sizes of the symmetric-memory collective for n values and nranks ranks:
+ * every rank allocates one symmetric buffer of *buffer_bytes holding two
+ * shard slots of *slot_stride bytes (double buffering) followed, at
+ * *flags_offset, by the flag array (nranks x *ctas u32, zero-initialised
+ * before first use); the local per-CTA epoch array is *ctas u32. */
+int mx_symm_layout(int64_t n, const mx_scheme_t* scheme, int32_t nranks, int64_t* slot_stride,
+                   int64_t* flags_offset, int64_t* buffer_bytes, int64_t* ctas);
+
+/* Multi-GPU one-shot fused over symmetric (peer-mapped) memory, ONE launch
+ * per rank, per-CTA dataflow (no grid barrier): CTA b quantises its 8 units
+ * of `x` into this rank's shard slot, publishes a ready flag for CTA b into
+ * every peer's flag array (system-scope release), waits for the nranks
+ * flags of CTA b (acquire), then decodes its units of all nranks shards
  * straight from the peers' buffers in rank order (fp32 from +0.0) into
  * `out`.  Replaces all-gather + dequant-sum (mx/netbench.py:323-334) with
- * no gather buffer.
- *   peer_bufs     device array [nranks] of peer buffer bases (each buffer
- *                 holds 2 slots of slot_stride bytes: double buffering)
- *   peer_signals  device array [nranks] of peer signal pads (>= nranks u32,
- *                 zero-initialised)
- *   barrier, epoch  local device uint32 state (zeroed once)
+ * no gather buffer and no NCCL kernel.
+ *   peer_bufs     device array [nranks] of peer buffer bases
+ *   peer_flags    device array [nranks] of peer flag arrays (buffer base +
+ *                 flags_offset of mx_symm_layout)
+ *   status        local device u32 (zeroed once): set to 1 if a peer wait
+ *                 timed out (~2 s) instead of hanging
+ *   epochs        local device u32 x ctas (zeroed once)
  * MX_ERR_UNSUPPORTED outside bf16 in, n % 1024 == 0, E8M0, B in {16,32,64}. */
 int mx_allreduce_symm(const void* x, int32_t dtype, int64_t n, const mx_scheme_t* scheme,
-                      uint8_t* const* peer_bufs, uint32_t* const* peer_signals, int32_t rank,
+                      uint8_t* const* peer_bufs, uint32_t* const* peer_flags, int32_t rank,
                       int32_t nranks, int64_t slot_stride, void* out, int32_t out_dtype,
-                      uint32_t* barrier, uint32_t* epoch, uint64_t* nonfinite, void* stream);
+                      uint32_t* status, uint32_t* epochs, uint64_t* nonfinite, void* stream);
 
 /* unpack_bits (mx/bitpack.py:37-58) on the device: `count` codes of
  * `width` bits -> one uint8 per code (quantize_block's return value). */

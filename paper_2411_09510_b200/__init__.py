@@ -18,4 +18,8 @@ from .codec import (CompressedTensor, DeviceCompressedTensor, block_error_bound,
                     decompress_tensor_device, dequantize_block, deserialize, header_nbytes,
                     pack_header, quantize_block, serialize, serialized_nbytes, unpack_header)
 
+from .baselines import (ChannelIntPacket, TopKPacket, channelwise_int_compress,
+                        channelwise_int_decompress, topk_compress, topk_decompress)
+from .errors import CompressionFactorTooHigh
+
 __version__ = "0.1.0"

@@ -52,6 +52,7 @@ SIGNATURES = {
                                        c_i64, c_vp]),
     "mx_allreduce_fused": (c_i32, [c_vp, c_i32, c_i32, c_i64, _SP, c_vp, c_i64, c_vp, c_i32,
                                    c_vp, c_vp, c_vp]),
+    "mx_symm_layout": (c_i32, [c_i64, _SP, c_i32, c_i64p, c_i64p, c_i64p, c_i64p]),
     "mx_allreduce_symm": (c_i32, [c_vp, c_i32, c_i64, _SP, c_vp, c_vp, c_i32, c_i32, c_i64, c_vp,
                                   c_i32, c_vp, c_vp, c_vp, c_vp]),
     "mx_unpack_codes": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp]),
@@ -124,6 +125,15 @@ def workspace_bytes(n: int, cs: MxScheme, requant: bool = False) -> int:
     fn = lib.mx_requant_workspace_bytes if requant else lib.mx_workspace_bytes
     check(fn(n, ctypes.byref(cs), ctypes.byref(a)), "mx_workspace_bytes")
     return a.value
+
+
+def symm_layout(n: int, cs: MxScheme, nranks: int) -> tuple[int, int, int, int]:
+    """(slot_stride, flags_offset, buffer_bytes, ctas) of the symmetric-memory collective."""
+    lib = load()
+    a, b, c, d = c_i64(), c_i64(), c_i64(), c_i64()
+    check(lib.mx_symm_layout(n, ctypes.byref(cs), nranks, ctypes.byref(a), ctypes.byref(b),
+                             ctypes.byref(c), ctypes.byref(d)), "mx_symm_layout")
+    return a.value, b.value, c.value, d.value
 
 
 def require_cuda():

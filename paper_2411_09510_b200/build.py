@@ -47,11 +47,27 @@ def sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
 
 
+def _digest(deps) -> str:
+    """Content hash of every source and the flags: an edit made while a build
+    runs is never mistaken for built (mtimes would be)."""
+    import hashlib
+
+    h = hashlib.sha256(repr((ARCH, FLAGS, sorted(LINEINFO), VARIANTS)).encode())
+    for d in sorted(deps):
+        h.update(d.encode())
+        with open(d, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     srcs = sources()
     deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")] + [
         os.path.join(ROOT, "include", "mxb200.h")]
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(map(os.path.getmtime, deps)):
+    digest = _digest(deps)
+    stamp = OUT + ".digest"
+    if not force and os.path.exists(OUT) and os.path.exists(stamp) and \
+            open(stamp).read().strip() == digest:
         return OUT
     os.makedirs(BUILD, exist_ok=True)
     nv = nvcc()
@@ -61,6 +77,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for var in VARIANTS.get(os.path.basename(src), [{}]):
             jobs.append((src, var))
 
+    headers = [d for d in deps if not d.endswith(".cu")]
+
     def compile_one(job):
         src, var = job
         tag = "".join(f".{k}{v}" for k, v in var.items())
@@ -68,9 +86,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
         extra = ["-lineinfo"] if os.path.basename(src) in LINEINFO else []
         extra += [f"-D{k}={v}" for k, v in var.items()]
         cmd = [nv, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
+        # object cache: this source + every header + the command line
+        key = _digest([src] + headers) + repr(cmd)
+        if not force and os.path.exists(obj) and os.path.exists(obj + ".key") and \
+                open(obj + ".key").read() == key:
+            return obj
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{p.stderr}")
+        with open(obj + ".key", "w") as f:
+            f.write(key)
         with open(obj + ".ptxas.txt", "w") as f:
             f.write(p.stderr)
         return obj
@@ -85,6 +110,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if p.returncode != 0:
         raise RuntimeError(f"link failed:\n{p.stderr}")
     os.replace(tmp, OUT)
+    with open(stamp, "w") as f:
+        f.write(digest + "\n")
     if verbose:
         print(f"built {OUT}")
     return OUT

@@ -261,12 +261,15 @@ class SymmetricAllReduce:
     """One-shot compressed all-reduce fused into ONE kernel per rank over
     torch symmetric memory (peer-mapped buffers on NVLink / NVSwitch).
 
-    Each rank quantises its partial into its own shard slot, raises a
-    system-scope flag in every peer's signal pad, waits for the peers' flags
-    and decodes all N shards straight out of the peers' memory, in rank
-    order, into fp32 -> ``out_dtype``.  This replaces K1 -> NCCL all-gather ->
-    K2 (mx/netbench.py:323-334) with no gather buffer and no NCCL kernel; the
-    result is bit-identical to the NCCL one-shot (same codes, same sum order).
+    Per-CTA dataflow (k_symm_flow): CTA b of every rank quantises the same
+    8 units of its partial into its own shard slot, raises a system-scope
+    flag for CTA b in every peer's flag array, waits for the N flags of CTA
+    b and decodes those units of all N shards straight out of the peers'
+    memory, in rank order, into fp32 -> ``out_dtype``.  This replaces K1 ->
+    NCCL all-gather -> K2 (mx/netbench.py:323-334) with no gather buffer, no
+    NCCL kernel and no grid-wide barrier; the result is bit-identical to the
+    NCCL one-shot (same codes, same sum order).  A peer wait longer than
+    ~2 s sets a status word instead of hanging (:meth:`check_status`).
     Requirements: bf16 partial, n % 1024 == 0, E8M0 scales, B in {16,32,64}.
     """
 
@@ -285,20 +288,17 @@ class SymmetricAllReduce:
             "cuda", torch.cuda.current_device())
         self.out_dtype = out_dtype or torch.bfloat16
         self.backend = NativeBackend(scheme)
-        _, _, S = self.backend.layout(self.n)
-        self.slot = (S + 255) & ~255
-        self.buf = symm_mem.empty(2 * self.slot, dtype=torch.uint8, device=self.device)
+        self.slot, flags_off, total, ctas = _native.symm_layout(self.n, self.backend.cs,
+                                                                self.world)
+        self.buf = symm_mem.empty(total, dtype=torch.uint8, device=self.device)
         self.hdl = symm_mem.rendezvous(self.buf, self.group)
-        if self.hdl.signal_pad_size < 4 * self.world:
-            raise RuntimeError("symmetric-memory signal pad too small")
-        # our flags live in the first `world` u32 of every signal pad: start
-        # from zero on every rank before anyone can signal
-        pad = self.hdl.signal_pad_ptrs[self.rank]
-        _native.check(self.backend.lib.mx_memset_async(ctypes.c_void_p(pad), 0, 4 * self.world,
-                                                       NativeBackend._st()), "mx_memset_async")
+        # flags start at zero on every rank before anyone can signal
+        self.buf[flags_off:].zero_()
+        self.flag_ptrs = torch.tensor([int(p) + flags_off for p in self.hdl.buffer_ptrs],
+                                      dtype=torch.int64, device=self.device)
         torch.cuda.synchronize()
         dist.barrier(self.group)
-        self.state = torch.zeros(4, dtype=torch.int32, device=self.device)  # barrier x2, epoch
+        self.state = torch.zeros(1 + ctas, dtype=torch.int32, device=self.device)  # status, epochs
         self.flag = torch.empty(1, dtype=torch.int64, device=self.device)
         self.backend.reset_flag(self.flag)
         self.out = torch.empty(self.n, dtype=self.out_dtype, device=self.device)
@@ -313,12 +313,17 @@ class SymmetricAllReduce:
         base = self.state.data_ptr()
         rc = be.lib.mx_allreduce_symm(
             ctypes.c_void_p(x.data_ptr()), _native.MX_BF16, self.n, ctypes.byref(be.cs),
-            ctypes.c_void_p(self.hdl.buffer_ptrs_dev), ctypes.c_void_p(self.hdl.signal_pad_ptrs_dev),
+            ctypes.c_void_p(self.hdl.buffer_ptrs_dev), ctypes.c_void_p(self.flag_ptrs.data_ptr()),
             self.rank, self.world, self.slot, ctypes.c_void_p(o.data_ptr()), be._dt(o),
-            ctypes.c_void_p(base), ctypes.c_void_p(base + 8), ctypes.c_void_p(self.flag.data_ptr()),
+            ctypes.c_void_p(base), ctypes.c_void_p(base + 4), ctypes.c_void_p(self.flag.data_ptr()),
             be._st())
         _native.check(rc, "mx_allreduce_symm")
         return o.view(x.shape)
+
+    def check_status(self):
+        """Raise if a peer wait timed out (the results of that call are invalid)."""
+        if int(self.state[0].item()) != 0:
+            raise RuntimeError("symmetric-memory all-reduce: a peer flag wait timed out")
 
     def check_finite(self):
         idx = int(self.flag.item())

@@ -43,19 +43,28 @@ __device__ __forceinline__ double ld64(const T* x, int64_t i) {
 template <typename T>
 struct Key {
   using U = uint32_t;
-  __device__ static U of(const T* x, int64_t i) {
-    return __float_as_uint(fabsf(InTraits<T>::to_f32(x[i])));
-  }
+  __device__ static U of_val(T v) { return __float_as_uint(fabsf(InTraits<T>::to_f32(v))); }
+  __device__ static U of(const T* x, int64_t i) { return of_val(x[i]); }
   __device__ static bool bad(U k) { return k >= 0x7f800000u; }
 };
 template <>
 struct Key<double> {
   using U = unsigned long long;
-  __device__ static U of(const double* x, int64_t i) {
-    return (U)__double_as_longlong(fabs(x[i]));
-  }
+  __device__ static U of_val(double v) { return (U)__double_as_longlong(fabs(v)); }
+  __device__ static U of(const double* x, int64_t i) { return of_val(x[i]); }
   __device__ static bool bad(U k) { return k >= 0x7ff0000000000000ull; }
 };
+
+// V consecutive values at p (16-byte aligned, V*sizeof(T) a multiple of 16)
+template <typename T, int V>
+__device__ __forceinline__ void ldv(const T* p, T (&out)[V]) {
+  static_assert((V * sizeof(T)) % 16 == 0, "vector width");
+#pragma unroll
+  for (int i = 0; i < (int)(V * sizeof(T) / 16); ++i) {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(p) + i);
+    memcpy(reinterpret_cast<char*>(out) + 16 * i, &w, 16);
+  }
+}
 
 // float64 -> IEEE binary16 bits, round to nearest even, overflow -> inf
 // (numpy's astype(float16), mx/baselines.py:124,153).
@@ -125,6 +134,48 @@ __global__ void __launch_bounds__(kT) k_ci_amax(const T* __restrict__ x, int64_t
   if (bad >= 0 && nonfinite) atomicMin(nonfinite, (unsigned long long)bad);
 }
 
+// C % 8 == 0, 16-B aligned rows: thread (tx, ty) owns channels
+// 8*(32*bx + tx) .. +8 and rows by*RB + ty, +8, ...; column maxima reduced
+// over ty in shared memory, one atomicMax per channel per block
+template <typename T, int RB>
+__global__ void __launch_bounds__(256) k_ci_amax_v(const T* __restrict__ x, int64_t rows,
+                                                  int64_t C, typename Key<T>::U* __restrict__ amax,
+                                                  unsigned long long* nonfinite) {
+  using U = typename Key<T>::U;
+  __shared__ U red[8][256];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t c0 = ((int64_t)blockIdx.x * 32 + tx) * 8;
+  const bool live = c0 < C;
+  U m[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) m[j] = 0;
+  unsigned long long bad = ~0ull;
+  if (live) {
+    const int64_t r1 = min(rows, (int64_t)(blockIdx.y + 1) * RB);
+    for (int64_t r = (int64_t)blockIdx.y * RB + ty; r < r1; r += 8) {
+      T v[8];
+      ldv<T, 8>(x + r * C + c0, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const U k = Key<T>::of_val(v[j]);
+        if (Key<T>::bad(k)) bad = min(bad, (unsigned long long)(r * C + c0 + j));
+        else m[j] = k > m[j] ? k : m[j];
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) red[ty][tx * 8 + j] = m[j];
+  __syncthreads();
+  const int64_t c = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (c < C) {
+    U r = red[0][threadIdx.x];
+#pragma unroll
+    for (int y = 1; y < 8; ++y) r = red[y][threadIdx.x] > r ? red[y][threadIdx.x] : r;
+    if (r) atomicMax(amax + c, r);
+  }
+  if (bad != ~0ull && nonfinite) atomicMin(nonfinite, bad);
+}
+
 template <typename U>
 __device__ __forceinline__ double key_value(U k);
 template <>
@@ -143,16 +194,24 @@ __global__ void k_ci_scale(const U* __restrict__ amax, int64_t C, int qmax,
   if (c < C) scales[c] = f64_to_f16_bits(__ddiv_rn(key_value<U>(amax[c]), (double)qmax));
 }
 
-// round-half-even(|x| / s) for an exact f32 |x| and an f16 scale s > 0
-__device__ __forceinline__ int level_f32(float mag, float s, int qmax) {
-  float k = floorf(mag * __frcp_rn(s));
-  k = fminf(fmaxf(k, 0.f), (float)(2 * qmax + 2));
+// round-half-even(|x| / s) for an exact f32 |x| and an f16 scale s > 0;
+// `rs` ~ 1/s (approximate: floor(mag*rs) is then off by at most one, and
+// the exact products below fix it)
+__device__ __forceinline__ int level_f32(float mag, float s, float rs, int qmax) {
+  float k = floorf(mag * rs);
+  k = fminf(k, (float)(2 * qmax + 2));
   if (k * s > mag) k -= 1.f;           // exact products (s: 11 bits, k < 2^9)
   if ((k + 1.f) * s <= mag) k += 1.f;
   const float half = (k + 0.5f) * s;
   int l = (int)k;
-  if (mag > half || (mag == half && (l & 1))) ++l;
+  l += (mag > half) | ((mag == half) & (l & 1));
   return min(l, qmax);
+}
+
+__device__ __forceinline__ float rcp_approx(float s) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s));
+  return r;
 }
 
 template <typename T>
@@ -168,7 +227,8 @@ __device__ __forceinline__ uint32_t ci_code(const T* x, int64_t i, uint16_t sb, 
     neg = c < 0.0;
   } else {
     const float v = InTraits<T>::to_f32(x[i]);
-    l = level_f32(fabsf(v), __half2float(__ushort_as_half(sb)), qmax);
+    const float sf = __half2float(__ushort_as_half(sb));
+    l = level_f32(fabsf(v), sf, rcp_approx(sf), qmax);
     neg = v < 0.f && l > 0;
   }
   return (uint32_t)l | (neg ? (1u << (bits - 1)) : 0u);
@@ -193,6 +253,40 @@ __global__ void __launch_bounds__(kT) k_ci_quant(const T* __restrict__ x, int64_
   const int nb = (cnt * bits + 7) / 8;
   uint8_t* p = out + g * bits;
   for (int b = 0; b < nb; ++b) p[b] = (uint8_t)(w >> (8 * b));
+}
+
+// C % 8 == 0: a thread's 8 values share a row; values and their 8 scales
+// arrive in vector loads; BITS is compile-time (constant shifts, one store)
+template <typename T, int BITS>
+__global__ void __launch_bounds__(kT) k_ci_quant_v(const T* __restrict__ x, int64_t n, int64_t C,
+                                                  const uint16_t* __restrict__ scales,
+                                                  uint8_t* __restrict__ out) {
+  const int64_t g = blockIdx.x * (int64_t)kT + threadIdx.x;
+  const int64_t i0 = g * 8;
+  if (i0 >= n) return;
+  constexpr int qmax = (1 << (BITS - 1)) - 1;
+  T v[8];
+  ldv<T, 8>(x + i0, v);
+  const int64_t c0 = (n < 0x100000000ll) ? (int64_t)((uint32_t)i0 % (uint32_t)C) : i0 % C;
+  const uint4 sw = __ldg(reinterpret_cast<const uint4*>(scales + c0));
+  const uint32_t sv[4] = {sw.x, sw.y, sw.z, sw.w};
+  unsigned long long w = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint16_t sb = (uint16_t)(sv[j >> 1] >> (16 * (j & 1)));
+    w |= (unsigned long long)ci_code<T>(v + j, 0, sb, BITS, qmax) << (j * BITS);
+  }
+  uint8_t* p = out + g * BITS;
+  if constexpr (BITS == 4) {
+    *reinterpret_cast<uint32_t*>(p) = (uint32_t)w;
+  } else if constexpr (BITS == 8) {
+    *reinterpret_cast<unsigned long long*>(p) = w;
+  } else if constexpr (BITS == 2) {
+    *reinterpret_cast<uint16_t*>(p) = (uint16_t)w;
+  } else {
+#pragma unroll
+    for (int b = 0; b < BITS; ++b) p[b] = (uint8_t)(w >> (8 * b));
+  }
 }
 
 template <typename OutT>
@@ -245,59 +339,120 @@ __global__ void k_tk_init(Sel<U>* sel, unsigned long long k) {
 template <typename T>
 __global__ void __launch_bounds__(kT) k_tk_hist(const T* __restrict__ x, int64_t n,
                                                Sel<typename Key<T>::U>* sel, int shift,
-                                               unsigned long long* nonfinite) {
+                                               unsigned long long* nonfinite, int vec, int agg) {
   using U = typename Key<T>::U;
   __shared__ unsigned int h[256];
+  __shared__ unsigned int hw[kT / 32][256];  // per-warp bins (passes after the top one)
   for (int i = threadIdx.x; i < 256; i += kT) h[i] = 0;
+  for (int i = threadIdx.x; i < 256 * (kT / 32); i += kT) (&hw[0][0])[i] = 0;
   __syncthreads();
+  unsigned int* mine = hw[threadIdx.x >> 5];
   const U prefix = sel->prefix, mask = sel->mask;
-  const int64_t stride = (int64_t)gridDim.x * kT;
-  for (int64_t i = blockIdx.x * (int64_t)kT + threadIdx.x; i < n; i += stride) {
-    const U k = Key<T>::of(x, i);
-    if (nonfinite && Key<T>::bad(k)) atomicMin(nonfinite, (unsigned long long)i);
-    if ((k & mask) == prefix) atomicAdd(&h[(uint32_t)(k >> shift) & 255u], 1u);
+  const int lane = threadIdx.x & 31;
+  // warp tiles of 256 values, 8 consecutive per lane; every lane runs the
+  // same trip count so __match_any_sync sees the full warp
+  const int64_t ntiles = (n + 255) / 256;
+  const int64_t nw = (int64_t)gridDim.x * (kT / 32);
+  for (int64_t t = blockIdx.x * (int64_t)(kT / 32) + (threadIdx.x >> 5); t < ntiles; t += nw) {
+    const int64_t i0 = t * 256 + lane * 8;
+    T v[8];
+    if (vec && i0 + 8 <= n) {
+      ldv<T, 8>(x + i0, v);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = i0 + j < n ? x[i0 + j] : T(0);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const bool in = i0 + j < n;
+      const U k = Key<T>::of_val(v[j]);
+      if (nonfinite && in && Key<T>::bad(k)) atomicMin(nonfinite, (unsigned long long)(i0 + j));
+      const uint32_t d = (in && (k & mask) == prefix) ? ((uint32_t)(k >> shift) & 255u) : 256u;
+      if (agg) {  // top digit: few distinct values, heavy collisions
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        if (d < 256u && lane == __ffs(peers) - 1) atomicAdd(&h[d], (unsigned)__popc(peers));
+      } else if (d < 256u) {
+        atomicAdd(&mine[d], 1u);
+      }
+    }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 256; i += kT)
-    if (h[i]) atomicAdd(&sel->hist[i], (unsigned long long)h[i]);
+  for (int i = threadIdx.x; i < 256; i += kT) {
+    unsigned int t = h[i];
+#pragma unroll
+    for (int w = 0; w < kT / 32; ++w) t += hw[w][i];
+    if (t) atomicAdd(&sel->hist[i], (unsigned long long)t);
+  }
 }
 
 // one warp: choose the digit where the descending cumulative count reaches
 // `take`, fold it into the prefix, clear the histogram for the next pass
 template <typename U>
 __global__ void k_tk_select(Sel<U>* sel, int shift) {
-  if (threadIdx.x == 0) {
-    unsigned long long take = sel->take, above = 0;
-    int d = 255;
-    for (; d > 0; --d) {
-      if (above + sel->hist[d] >= take) break;
-      above += sel->hist[d];
+  // one warp: lane l holds bins 255-8l .. 248-8l (descending); a warp scan of
+  // the lane sums finds the lane, then the bin, where the count reaches take
+  const int lane = threadIdx.x;
+  unsigned long long c[8], tot = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    c[i] = sel->hist[255 - 8 * lane - i];
+    tot += c[i];
+  }
+  unsigned long long incl = tot;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const unsigned long long take = sel->take, excl = incl - tot;
+  const unsigned int hit = __ballot_sync(0xffffffffu, incl >= take);
+  const int L = hit ? __ffs(hit) - 1 : 31;
+  if (lane == L) {
+    unsigned long long above = excl;
+    int d = 255 - 8 * L;
+    for (int i = 0; i < 8; ++i, --d) {
+      if (above + c[i] >= take || d == 0) break;
+      above += c[i];
     }
     sel->take = take - above;
     sel->prefix |= (U)d << shift;
     sel->mask |= (U)255 << shift;
   }
   __syncwarp();
-  for (int i = threadIdx.x; i < 256; i += 32) sel->hist[i] = 0;
+  for (int i = lane; i < 256; i += 32) sel->hist[i] = 0;
 }
 
 constexpr int kPer = 16;               // elements per thread in the compaction
 constexpr int kTile = kT * kPer;       // elements per block
 
 // per-block counts of key > T and key == T
+// the thread's kPer values (vector loads when whole and aligned)
+template <typename T>
+__device__ __forceinline__ int load_per(const T* x, int64_t i0, int64_t n, int vec, T (&v)[kPer]) {
+  if (vec && i0 + kPer <= n) {
+    ldv<T, kPer>(x + i0, v);
+    return kPer;
+  }
+  const int cnt = (int)max((int64_t)0, min((int64_t)kPer, n - i0));
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) v[j] = j < cnt ? x[i0 + j] : T(0);
+  return cnt;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kT) k_tk_count(const T* __restrict__ x, int64_t n,
                                                 const Sel<typename Key<T>::U>* sel,
-                                                unsigned long long* __restrict__ cnt) {
+                                                unsigned long long* __restrict__ cnt, int vec) {
   using U = typename Key<T>::U;
   const U t = sel->prefix;
   const int64_t i0 = blockIdx.x * (int64_t)kTile + threadIdx.x * kPer;
+  T v[kPer];
+  const int m = load_per<T>(x, i0, n, vec, v);
   uint32_t gt = 0, eq = 0;
+#pragma unroll
   for (int j = 0; j < kPer; ++j) {
-    if (i0 + j >= n) break;
-    const U k = Key<T>::of(x, i0 + j);
-    gt += k > t;
-    eq += k == t;
+    const U k = Key<T>::of_val(v[j]);
+    gt += (j < m) & (k > t);
+    eq += (j < m) & (k == t);
   }
   __shared__ uint32_t sg[kT / 32], se[kT / 32];
   for (int o = 16; o; o >>= 1) {
@@ -354,9 +509,9 @@ __global__ void __launch_bounds__(1024) k_tk_scan(unsigned long long* cnt, int64
 }
 
 template <typename T>
-__device__ __forceinline__ uint16_t to_f16_bits(const T* x, int64_t i) {
-  if constexpr (std::is_same<T, double>::value) return f64_to_f16_bits(x[i]);
-  else return __half_as_ushort(__float2half_rn(InTraits<T>::to_f32(x[i])));
+__device__ __forceinline__ uint16_t to_f16_bits(T v) {
+  if constexpr (std::is_same<T, double>::value) return f64_to_f16_bits(v);
+  else return __half_as_ushort(__float2half_rn(InTraits<T>::to_f32(v)));
 }
 
 template <typename T>
@@ -364,17 +519,19 @@ __global__ void __launch_bounds__(kT) k_tk_write(const T* __restrict__ x, int64_
                                                 const Sel<typename Key<T>::U>* sel,
                                                 const unsigned long long* __restrict__ cnt,
                                                 uint32_t* __restrict__ idx,
-                                                uint16_t* __restrict__ val) {
+                                                uint16_t* __restrict__ val, int vec) {
   using U = typename Key<T>::U;
   const U t = sel->prefix;
   const unsigned long long take = sel->take;
   const int64_t i0 = blockIdx.x * (int64_t)kTile + threadIdx.x * kPer;
+  T v[kPer];
+  const int m = load_per<T>(x, i0, n, vec, v);
   uint32_t gt = 0, eq = 0;
+#pragma unroll
   for (int j = 0; j < kPer; ++j) {
-    if (i0 + j >= n) break;
-    const U k = Key<T>::of(x, i0 + j);
-    gt += k > t;
-    eq += k == t;
+    const U k = Key<T>::of_val(v[j]);
+    gt += (j < m) & (k > t);
+    eq += (j < m) & (k == t);
   }
   // block-exclusive prefix of (gt, eq) over threads
   __shared__ uint32_t sg[kT / 32], se[kT / 32];
@@ -389,10 +546,11 @@ __global__ void __launch_bounds__(kT) k_tk_write(const T* __restrict__ x, int64_
   for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) { wg += sg[w]; we += se[w]; }
   unsigned long long pg = cnt[2 * blockIdx.x] + wg + ig - gt;
   unsigned long long pe = cnt[2 * blockIdx.x + 1] + we + ie - eq;
+#pragma unroll
   for (int j = 0; j < kPer; ++j) {
     const int64_t i = i0 + j;
-    if (i >= n) break;
-    const U k = Key<T>::of(x, i);
+    if (j >= m) break;
+    const U k = Key<T>::of_val(v[j]);
     bool keep = false;
     if (k > t) {
       keep = true;
@@ -402,7 +560,7 @@ __global__ void __launch_bounds__(kT) k_tk_write(const T* __restrict__ x, int64_
     if (keep) {
       const unsigned long long pos = pg + (pe < take ? pe : take);
       idx[pos] = (uint32_t)i;
-      val[pos] = to_f16_bits<T>(x, i);
+      val[pos] = to_f16_bits<T>(v[j]);
     }
     pg += k > t;
     pe += k == t;
@@ -429,13 +587,32 @@ void ci_compress(const T* x, int64_t rows, int64_t C, int bits, uint16_t* scales
   using U = typename Key<T>::U;
   U* amax = reinterpret_cast<U*>(ws);
   cudaMemsetAsync(amax, 0, C * sizeof(U), st);
-  constexpr int RB = 32;
-  dim3 g((unsigned)((C + kT - 1) / kT), (unsigned)((rows + RB - 1) / RB));
-  k_ci_amax<T, RB><<<g, kT, 0, st>>>(x, rows, C, amax, nf);
+  const bool vec = C % 8 == 0 && ((uintptr_t)x % 16) == 0;
+  if (vec) {
+    constexpr int RB = 64;
+    dim3 g((unsigned)((C / 8 + 31) / 32), (unsigned)((rows + RB - 1) / RB));
+    k_ci_amax_v<T, RB><<<g, 256, 0, st>>>(x, rows, C, amax, nf);
+  } else {
+    constexpr int RB = 32;
+    dim3 g((unsigned)((C + kT - 1) / kT), (unsigned)((rows + RB - 1) / RB));
+    k_ci_amax<T, RB><<<g, kT, 0, st>>>(x, rows, C, amax, nf);
+  }
   k_ci_scale<U><<<(unsigned)((C + kT - 1) / kT), kT, 0, st>>>(amax, C, (1 << (bits - 1)) - 1,
                                                               scales);
   const int64_t n = rows * C, groups = (n + 7) / 8;
-  k_ci_quant<T><<<(unsigned)((groups + kT - 1) / kT), kT, 0, st>>>(x, n, C, scales, bits, codes);
+  const unsigned qg = (unsigned)((groups + kT - 1) / kT);
+  if (vec && ((uintptr_t)scales % 16) == 0) {
+    switch (bits) {
+      case 2: k_ci_quant_v<T, 2><<<qg, kT, 0, st>>>(x, n, C, scales, codes); break;
+      case 3: k_ci_quant_v<T, 3><<<qg, kT, 0, st>>>(x, n, C, scales, codes); break;
+      case 4: k_ci_quant_v<T, 4><<<qg, kT, 0, st>>>(x, n, C, scales, codes); break;
+      case 5: k_ci_quant_v<T, 5><<<qg, kT, 0, st>>>(x, n, C, scales, codes); break;
+      case 6: k_ci_quant_v<T, 6><<<qg, kT, 0, st>>>(x, n, C, scales, codes); break;
+      case 7: k_ci_quant_v<T, 7><<<qg, kT, 0, st>>>(x, n, C, scales, codes); break;
+      default: k_ci_quant_v<T, 8><<<qg, kT, 0, st>>>(x, n, C, scales, codes); break;
+    }
+  } else
+    k_ci_quant<T><<<(unsigned)((groups + kT - 1) / kT), kT, 0, st>>>(x, n, C, scales, bits, codes);
 }
 
 template <typename OutT>
@@ -456,6 +633,7 @@ void tk_compress(const T* x, int64_t n, int64_t k, uint32_t* idx, uint16_t* val,
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(
       reinterpret_cast<uint8_t*>(ws) + ((sizeof(Sel<U>) + 255) / 256) * 256);
   k_tk_init<U><<<1, 256, 0, st>>>(sel, (unsigned long long)k);  // graph-capturable
+  const int vec = ((uintptr_t)x % 16) == 0 && (8 * sizeof(T)) % 16 == 0;
   static thread_local int sms = 0;
   if (sms == 0) {
     int dev = 0;
@@ -465,13 +643,14 @@ void tk_compress(const T* x, int64_t n, int64_t k, uint32_t* idx, uint16_t* val,
   const unsigned hg = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>((int64_t)sms * 8, (n + kT * 8 - 1) / (kT * 8)));
   for (int shift = (int)(8 * sizeof(U)) - 8; shift >= low_shift; shift -= 8) {
-    k_tk_hist<T><<<hg, kT, 0, st>>>(x, n, sel, shift, shift == (int)(8 * sizeof(U)) - 8 ? nf : nullptr);
+    const bool top = shift == (int)(8 * sizeof(U)) - 8;
+    k_tk_hist<T><<<hg, kT, 0, st>>>(x, n, sel, shift, top ? nf : nullptr, vec, top ? 1 : 0);
     k_tk_select<U><<<1, 32, 0, st>>>(sel, shift);
   }
   const int64_t nb = tk_blocks(n);
-  k_tk_count<T><<<(unsigned)nb, kT, 0, st>>>(x, n, sel, cnt);
+  k_tk_count<T><<<(unsigned)nb, kT, 0, st>>>(x, n, sel, cnt, vec);
   k_tk_scan<<<1, 1024, 0, st>>>(cnt, nb);
-  k_tk_write<T><<<(unsigned)nb, kT, 0, st>>>(x, n, sel, cnt, idx, val);
+  k_tk_write<T><<<(unsigned)nb, kT, 0, st>>>(x, n, sel, cnt, idx, val, vec);
 }
 
 }  // namespace bl

@@ -170,8 +170,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_fused_oneshot(const FArgs F) {
 // decodes + sums them in rank order.  Quantise and dequant-sum of different
 // units overlap across warps instead of being separated by a grid barrier;
 // every warp owns one unit, the grid is sized to the work (several waves).
-template <typename OutT, int B, int ENC, int BITS>
-__global__ void __launch_bounds__(kThreads) k_fused_flow(const FArgs F) {
+template <typename OutT, int B, int ENC, int BITS, int TH = kThreads>
+__global__ void __launch_bounds__(TH) k_fused_flow(const FArgs F) {
   using InT = __nv_bfloat16;
   constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
   constexpr int NSB = Geo<B>::NSB;
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kThreads) k_fused_flow(const FArgs F) {
     __syncthreads();
   }
   const int lane = threadIdx.x & 31;
-  const uint32_t q = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint32_t q = blockIdx.x * (TH / 32) + (threadIdx.x >> 5);
   if (q >= (uint32_t)(F.n / kUnit)) return;
   const int nr = F.nranks;
   const size_t xoff = (size_t)q * kUnit + lane * kVPL;
@@ -241,13 +241,20 @@ __global__ void __launch_bounds__(kThreads) k_fused_flow(const FArgs F) {
 
 // ---------------------------------------------------------------------------
 // Multi-GPU fused one-shot over symmetric (peer-mapped) memory: the NVLink
-// form of the kernel above.  Rank r quantises its partial into ITS shard of
-// the symmetric buffer (slot = epoch parity), a system-scope release/acquire
-// flag exchange replaces the all-gather, and phase 2 decodes the N shards
-// straight out of the peers' memory over NVLink (rank order, fp32, +0.0
-// start) -- no gather buffer, no NCCL kernel, one launch.  Double buffering:
-// a rank writes slot e&1 at epoch e only after it has seen every peer's
-// epoch e-1 flag, i.e. after every peer finished reading slot e&1 at e-2.
+// form of k_fused_flow, with per-CTA dataflow instead of grid barriers.
+// CTA b owns the same 8 units on every rank.  It quantises its units of the
+// local partial into ITS shard slot (slot = epoch parity) of its symmetric
+// buffer, publishes "CTA b of rank r is ready at epoch e" by a system-scope
+// release store into every peer's flag array, waits (acquire) for the N
+// flags of CTA b, then decodes its units of the N shards straight out of
+// the peers' memory over NVLink in rank order (fp32 from +0.0).  No gather
+// buffer, no NCCL kernel, no grid-wide barrier: CTAs of different ranks
+// pipeline against each other.  Per-CTA epochs (local memory) make every
+// launch -- and every CUDA-graph replay -- use the next epoch.  Double
+// buffering: rank r writes slot e&1 at epoch e only after its epoch e-1
+// launch saw every peer's epoch e-1 flag for the same CTA, i.e. after every
+// peer had finished epoch e-2, the last reader of slot e&1.  A wait that
+// exceeds ~2 s sets *status and proceeds (no hang; the host reports it).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
   unsigned int v;
@@ -259,7 +266,7 @@ __device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) 
 }
 
 template <typename OutT, int B, int ENC, int BITS>
-__global__ void __launch_bounds__(kThreads, 3) k_symm_oneshot(const SArgs S) {
+__global__ void __launch_bounds__(kThreads) k_symm_flow(const SArgs S) {
   using InT = __nv_bfloat16;
   constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
   constexpr int NSB = Geo<B>::NSB;
@@ -267,130 +274,84 @@ __global__ void __launch_bounds__(kThreads, 3) k_symm_oneshot(const SArgs S) {
   constexpr int UBYTES = kUnit / 8 * BITS;
   constexpr int USCALES = kUnit / B;
   __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
+  __shared__ unsigned int s_e;
   const Fmt f = S.f;
   if constexpr (DEC != ENC_E2M1) fill_lut(s_lut, f);
+  const uint32_t b = blockIdx.x, G = gridDim.x;
+  if (threadIdx.x == 0) s_e = S.epoch[b] + 1u;
+  __syncthreads();
+  const unsigned int e = s_e;
   const int lane = threadIdx.x & 31;
-  const uint32_t nw = (uint32_t)(gridDim.x * kWarps);
-  const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const uint32_t nunits = (uint32_t)(S.n / kUnit);
+  const uint32_t q = b * kWarps + (threadIdx.x >> 5);
+  const bool live = q < (uint32_t)(S.n / kUnit);
   const int nr = S.nranks;
-  const unsigned int e = *S.epoch + 1u;
   const int64_t slot = (int64_t)(e & 1u) * S.slot_stride;
 
-  // ---- phase 1: quantise the local partial into my shard (slot e&1) -----
-  {
+  // ---- quantise my unit of the local partial into my shard slot ----------
+  if (live) {
+    Raw<InT> raw;
+    load_raw<InT>(reinterpret_cast<const InT*>(S.x) + (size_t)q * kUnit + lane * kVPL, raw);
+    int stored[NSB];
+    bool bad;
+    LaneCodes<BITS> c = quant_lane<InT, B, ENC, BITS>(raw, f, stored, bad);
+    if (bad) report_nonfinite_raw<InT>(raw, kVPL, (int64_t)q * kUnit + lane * kVPL, S.nonfinite);
     uint8_t* shard = S.bufs[S.rank] + slot;
-    auto quantise = [&](const Raw<InT>& raw, uint32_t q) {
-      int stored[NSB];
-      bool bad;
-      LaneCodes<BITS> c = quant_lane<InT, B, ENC, BITS>(raw, f, stored, bad);
-      if (bad)
-        report_nonfinite_raw<InT>(raw, kVPL, (int64_t)q * kUnit + lane * kVPL, S.nonfinite);
-      store_lane_codes<BITS>(shard + S.elem_off + (size_t)q * UBYTES + lane * (4 * BITS), c, kVPL);
-      uint8_t* sp = shard + S.scale_off + (size_t)q * USCALES + (lane / LPB) * NSB;
-      if constexpr (NSB == 4) {
-        *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
-                                           ((uint32_t)stored[2] << 16) |
-                                           ((uint32_t)stored[3] << 24);
-      } else if constexpr (NSB == 2) {
-        *reinterpret_cast<uint16_t*>(sp) = (uint16_t)(stored[0] | (stored[1] << 8));
-      } else {
-        if (lane % LPB == 0) *sp = (uint8_t)stored[0];
-      }
-    };
-    const InT* x = reinterpret_cast<const InT*>(S.x) + lane * kVPL;
-    Raw<InT> b0, b1;
-    uint32_t q = gw;
-    if (q < nunits) load_raw<InT>(x + (size_t)q * kUnit, b0);
-    while (q < nunits) {
-      uint32_t qn = q + nw;
-      if (qn < nunits) load_raw<InT>(x + (size_t)qn * kUnit, b1);
-      quantise(b0, q);
-      q = qn;
-      if (q >= nunits) break;
-      qn = q + nw;
-      if (qn < nunits) load_raw<InT>(x + (size_t)qn * kUnit, b0);
-      quantise(b1, q);
-      q = qn;
+    store_lane_codes<BITS>(shard + S.elem_off + (size_t)q * UBYTES + lane * (4 * BITS), c, kVPL);
+    uint8_t* sp = shard + S.scale_off + (size_t)q * USCALES + (lane / LPB) * NSB;
+    if constexpr (NSB == 4) {
+      *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
+                                         ((uint32_t)stored[2] << 16) | ((uint32_t)stored[3] << 24);
+    } else if constexpr (NSB == 2) {
+      *reinterpret_cast<uint16_t*>(sp) = (uint16_t)(stored[0] | (stored[1] << 8));
+    } else {
+      if (lane % LPB == 0) *sp = (uint8_t)stored[0];
     }
   }
-  __threadfence_system();  // my shard bytes, before any flag leaves this GPU
-  grid_barrier(S.bar);
+  __syncthreads();
 
-  // ---- flag exchange: "my shard for epoch e is ready" ---------------------
-  if (blockIdx.x == 0 && threadIdx.x < (unsigned)nr) {
+  // ---- publish to every peer, then wait for every peer's CTA b -----------
+  if ((int)threadIdx.x < nr) {
     const int j = threadIdx.x;
-    st_release_sys(S.sigs[j] + S.rank, e);              // peer j's pad, my slot
-    const unsigned int* mine = S.sigs[S.rank] + j;      // my pad, peer j's slot
-    while ((int)(ld_acquire_sys(mine) - e) < 0) __nanosleep(64);
+    __threadfence_system();  // this CTA's shard bytes before the flag leaves
+    st_release_sys(S.flags[j] + (size_t)S.rank * G + b, e);
+    const unsigned int* mine = S.flags[S.rank] + (size_t)j * G + b;
+    const long long t0 = clock64();
+    while ((int)(ld_acquire_sys(mine) - e) < 0) {
+      __nanosleep(32);
+      if (clock64() - t0 > 4000000000ll) {  // ~2 s: report, do not hang
+        atomicExch(S.status, 1u);
+        break;
+      }
+    }
+    __threadfence_system();
   }
-  grid_barrier(S.bar);
+  __syncthreads();
 
-  // ---- phase 2: pull-decode the N shards over NVLink, rank order ---------
-  {
+  // ---- pull-decode my unit of the N shards over NVLink, rank order -------
+  if (live) {
     using RL = RankLoad<B, BITS, kVPL>;
-    auto load_r = [&](RL& x, int r, uint32_t uu) {
-      load_rank<B, BITS, kVPL, true>(x, S.bufs[r] + slot, S.scale_off, S.elem_off,
-                                     (int64_t)uu * kUnit, lane, kVPL, 8);
-    };
-    auto reduce = [&](const RL& x0, const RL& x1, uint32_t uu) {
-      float acc[kVPL];
+    float acc[kVPL];
 #pragma unroll
-      for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
+    for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
+    for (int r = 0; r < nr; r += 2) {
+      RL x0, x1;
+      load_rank<B, BITS, kVPL, true>(x0, S.bufs[r] + slot, S.scale_off, S.elem_off,
+                                     (int64_t)q * kUnit, lane, kVPL, 8);
+      if (r + 1 < nr)
+        load_rank<B, BITS, kVPL, true>(x1, S.bufs[r + 1] + slot, S.scale_off, S.elem_off,
+                                       (int64_t)q * kUnit, lane, kVPL, 8);
       decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
-      if (nr > 1) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
-      for (int rk = 2; rk < nr; ++rk) {
-        RL rr;
-        load_r(rr, rk, uu);
-        decode_rank<B, DEC, BITS, kVPL>(rr, f, acc, false, s_lut);
-      }
-      store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(S.out) + (size_t)uu * kUnit +
-                                     lane * kVPL,
-                                 kVPL, acc);
-    };
-    uint32_t u = gw;
-    RL a0, a1, c0, c1;
-    if (u < nunits) {
-      load_r(a0, 0, u);
-      if (nr > 1) load_r(a1, 1, u);
+      if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
     }
-    while (u < nunits) {
-      uint32_t un = u + nw;
-      if (un < nunits) {
-        load_r(c0, 0, un);
-        if (nr > 1) load_r(c1, 1, un);
-      }
-      reduce(a0, a1, u);
-      u = un;
-      if (u >= nunits) break;
-      un = u + nw;
-      if (un < nunits) {
-        load_r(a0, 0, un);
-        if (nr > 1) load_r(a1, 1, un);
-      }
-      reduce(c0, c1, u);
-      u = un;
-    }
+    store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(S.out) + (size_t)q * kUnit + lane * kVPL,
+                               kVPL, acc);
   }
-  // every CTA read *epoch before the first barrier: safe to advance it
-  if (blockIdx.x == 0 && threadIdx.x == 0) *S.epoch = e;
+  if (threadIdx.x == 0) S.epoch[b] = e;
 }
 
 template <typename OutT, int B, int ENC, int BITS>
 void go_symm(const SArgs& a, cudaStream_t st) {
-  auto k = k_symm_oneshot<OutT, B, ENC, BITS>;
-  static thread_local int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, 0);
-  if (occ < 1) occ = 1;
-  const int64_t need = (a.n / kUnit + kWarps - 1) / kWarps;
-  k<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ, need)), kThreads, 0,
-      st>>>(a);
+  k_symm_flow<OutT, B, ENC, BITS><<<(unsigned)symm_ctas(a.n), kThreads, 0, st>>>(a);
 }
 
 template <typename InT, typename OutT, int B, int ENC, int BITS>

@@ -590,15 +590,31 @@ int mx_allreduce_fused(const void* const* partials, int32_t dtype, int32_t nrank
   return cuda_check("k_fused_oneshot");
 }
 
+int mx_symm_layout(int64_t n, const mx_scheme_t* s, int32_t nranks, int64_t* slot_stride,
+                   int64_t* flags_offset, int64_t* buffer_bytes, int64_t* ctas) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (n <= 0 || nranks < 1) return fail(MX_ERR_INVALID_ARGUMENT, "bad sizes");
+  int64_t so, eo, sbytes;
+  mx_shard_layout(n, s, &so, &eo, &sbytes);
+  const int64_t slot = (sbytes + 255) / 256 * 256;
+  const int64_t g = symm_ctas(n);
+  if (slot_stride) *slot_stride = slot;
+  if (flags_offset) *flags_offset = 2 * slot;
+  if (buffer_bytes) *buffer_bytes = 2 * slot + ((int64_t)nranks * g * 4 + 255) / 256 * 256;
+  if (ctas) *ctas = g;
+  return MX_OK;
+}
+
 int mx_allreduce_symm(const void* x, int32_t dtype, int64_t n, const mx_scheme_t* s,
-                      uint8_t* const* peer_bufs, uint32_t* const* peer_signals, int32_t rank,
+                      uint8_t* const* peer_bufs, uint32_t* const* peer_flags, int32_t rank,
                       int32_t nranks, int64_t slot_stride, void* out, int32_t out_dtype,
-                      uint32_t* barrier, uint32_t* epoch, uint64_t* nonfinite, void* stream) {
+                      uint32_t* status, uint32_t* epochs, uint64_t* nonfinite, void* stream) {
   int rc = check_scheme(s);
   if (rc) return rc;
   if (n <= 0 || nranks < 1 || rank < 0 || rank >= nranks)
     return fail(MX_ERR_INVALID_ARGUMENT, "bad sizes");
-  if (!x || !peer_bufs || !peer_signals || !out || !barrier || !epoch)
+  if (!x || !peer_bufs || !peer_flags || !out || !status || !epochs)
     return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
   int64_t so, eo, sbytes;
   mx_shard_layout(n, s, &so, &eo, &sbytes);
@@ -608,16 +624,17 @@ int mx_allreduce_symm(const void* x, int32_t dtype, int64_t n, const mx_scheme_t
       !aligned(out, 32))
     return fail(MX_ERR_UNSUPPORTED,
                 "symmetric path: bf16 in, bf16/f32 out, n %% 1024 == 0, E8M0, 32-B aligned");
+  if (nranks > kThreads) return fail(MX_ERR_UNSUPPORTED, "at most %d ranks", kThreads);
   SArgs a;
   a.x = x; a.n = n;
-  a.bufs = peer_bufs; a.sigs = reinterpret_cast<unsigned int* const*>(peer_signals);
+  a.bufs = peer_bufs; a.flags = reinterpret_cast<unsigned int* const*>(peer_flags);
   a.rank = rank; a.nranks = nranks; a.slot_stride = slot_stride;
-  a.scale_off = so; a.elem_off = eo; a.out = out; a.bar = barrier;
-  a.epoch = epoch; a.nonfinite = reinterpret_cast<unsigned long long*>(nonfinite); a.f = f;
+  a.scale_off = so; a.elem_off = eo; a.out = out; a.status = status;
+  a.epoch = epochs; a.nonfinite = reinterpret_cast<unsigned long long*>(nonfinite); a.f = f;
   if (!launch_symm_oneshot(a, out_dtype == MX_BF16, (int)s->block_size, enc_of(s), f.bits,
                            (cudaStream_t)stream))
     return fail(MX_ERR_UNSUPPORTED, "symmetric path: scheme not instantiated");
-  return cuda_check("k_symm_oneshot");
+  return cuda_check("k_symm_flow");
 }
 
 int mx_unpack_codes(const uint8_t* packed, int64_t count, int32_t width, uint8_t* codes, void* stream) {

@@ -1018,16 +1018,18 @@ struct SArgs {
   const void* x;                 // this rank's bf16 partial (n values)
   int64_t n;                     // multiple of 1024
   uint8_t* const* bufs;          // device array [nranks]: peer buffer bases
-  unsigned int* const* sigs;     // device array [nranks]: peer signal pads (u32 x nranks)
+  unsigned int* const* flags;    // device array [nranks]: peer flag arrays (u32 x nranks x ctas)
   int rank, nranks;
   int64_t slot_stride;           // bytes of one shard slot (2 slots per buffer)
   int64_t scale_off, elem_off;   // shard layout for n values
   void* out;
-  unsigned int* bar;             // local grid barrier {count, generation}
-  unsigned int* epoch;           // local, advanced once per call
+  unsigned int* status;          // local u32: set to 1 if a peer wait timed out
+  unsigned int* epoch;           // local u32 per CTA, advanced once per call
   unsigned long long* nonfinite;
   Fmt f;
 };
+// CTAs of the symmetric-memory kernel for n values (one 1024-value unit per warp)
+inline int64_t symm_ctas(int64_t n) { return (n / kUnit + kWarps - 1) / kWarps; }
 bool launch_symm_oneshot(const SArgs& a, int out_is_bf16, int block, int enc, int bits,
                          cudaStream_t st);
 

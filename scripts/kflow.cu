@@ -188,6 +188,12 @@ int main(int argc, char** argv) {
   bench("k_flow_pipe<minb" #MINB ",grid" #C "x148>", R, [&](int i, cudaStream_t s) {         \
     k_flow_pipe<32, ENC_E2M1, 4, MINB><<<sms * C, kThreads, 0, s>>>(args[i]); }, bytes, st); \
   check("pipe");
-  PIPE(2, 2) PIPE(3, 3) PIPE(4, 4) PIPE(4, 3) PIPE(3, 2)
+  PIPE(3, 3)
+#define FLOWT(TH)                                                                             \
+  bench("k_fused_flow<threads" #TH ">", R, [&](int i, cudaStream_t s) {                       \
+    fz::k_fused_flow<__nv_bfloat16, 32, ENC_E2M1, 4, TH>                                      \
+        <<<(unsigned)(n / kUnit / (TH / 32)), TH, 0, s>>>(args[i]); }, bytes, st);            \
+  check("flowT");
+  FLOWT(64) FLOWT(128) FLOWT(256) FLOWT(512) FLOWT(1024)
   return 0;
 }

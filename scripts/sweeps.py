@@ -133,6 +133,69 @@ def messages():
         torch.cuda.empty_cache()
 
 
+def codecs():
+    """Paper Table 4 on one B200: MX vs the comparison codecs (channel-wise
+    INT, TopK) vs fp16 on the 8B prefill partial, simulated TP=2.  Device
+    compress / decompress time of one rank's partial, wire payload, and the
+    error of the float64 rank-order sum of the decoded partials against the
+    exact sum (the tpsim report, mx/tpsim.py:234-302)."""
+    from paper_2411_09510_b200 import baselines as bl
+    from paper_2411_09510_b200.codec import (compress_tensor_device, decompress_tensor_device,
+                                             header_nbytes)
+
+    T, H = 2048, 4096
+    n = T * H
+    host = rank_partials((T, H), 2, seed=0)
+    exact = host[0].astype(np.float64) + host[1].astype(np.float64)
+    base = [torch.from_numpy(h).to("cuda", torch.bfloat16) for h in host]
+    R = max(2, -(-3 * L2 // (3 * n)))
+    xs = [(base[0].roll(i * 7, 0) * (-1) ** i).contiguous() for i in range(R)]
+
+    def mx_codec(spec):
+        sch = parse_scheme(spec, extensions=True)
+        enc = lambda x: compress_tensor_device(x, sch, check_finite=False)  # noqa: E731
+        dec = lambda c: decompress_tensor_device(c, torch.bfloat16)  # noqa: E731
+        sb, eb = _native.stream_nbytes(n, sch.to_c())
+        return enc, dec, header_nbytes(2) + sb + eb
+
+    def chan(bits):
+        enc = lambda x: bl.channelwise_int_compress_device(x, bits, check_finite=False)  # noqa: E731
+        dec = lambda c: bl.channelwise_int_decompress_device(c[0], c[1], c[2], bits,  # noqa: E731
+                                                             torch.bfloat16)
+        return enc, dec, header_nbytes(2) + 2 * H + (n * bits + 7) // 8
+
+    def topk(f):
+        k = bl.topk_budget(n, 2, f)
+        enc = lambda x: bl.topk_compress_device(x, k, check_finite=False)  # noqa: E731
+        dec = lambda c: bl.topk_decompress_device(c[0], c[1], n, torch.bfloat16)  # noqa: E731
+        return enc, dec, header_nbytes(2) + 6 * k
+
+    def fp16():
+        return (lambda x: x.to(torch.float16)), (lambda c: c.to(torch.bfloat16)), \
+            header_nbytes(2) + 2 * n
+
+    table = [("fp4_e2m1:32:e8m0", mx_codec("fp4_e2m1:32:e8m0")),
+             ("fp6_e2m3:32:e8m0", mx_codec("fp6_e2m3:32:e8m0")),
+             ("chanint:4", chan(4)), ("chanint:8", chan(8)),
+             ("topk:3", topk(3.0)), ("topk:10", topk(10.0)), ("fp16", fp16())]
+    for name, (enc, dec, payload) in table:
+        comp = [enc(x) for x in xs]
+        reps = 20
+        t_enc = graph_time(lambda: [enc(x) for x in xs], reps) / R
+        t_dec = graph_time(lambda: [dec(c) for c in comp], reps) / R
+        rec = [dec(enc(b)).double().cpu().numpy().reshape(T, H) for b in base]
+        err = rec[0] + rec[1] - exact
+        print(json.dumps({
+            "config": "codecs", "codec": name, "shape": [T, H], "tp": 2,
+            "compress_us": round(t_enc * 1e3, 3), "decompress_us": round(t_dec * 1e3, 3),
+            "payload_bytes": payload, "ratio_vs_bf16": round(2 * n / payload, 3),
+            "rel_frob_err": float(np.linalg.norm(err) / np.linalg.norm(exact)),
+            "sqnr_db": round(10 * math.log10(float((exact ** 2).sum() / (err ** 2).sum())), 3),
+            "max_abs_err": float(np.abs(err).max()),
+            "note": "decoded to bf16 for timing; errors from the float64 rank-order sum "
+                    "of the decoded partials (bf16 output rounding included)"}), flush=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "formats"
-    {"formats": formats, "messages": messages}[what]()
+    {"formats": formats, "messages": messages, "codecs": codecs}[what]()

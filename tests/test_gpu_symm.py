@@ -51,3 +51,4 @@ def test_symm_world1_matches_oneshot(pg, spec):
         assert np.array_equal(a, b), it
         assert np.array_equal(a, O.allreduce_oneshot([x64], O.scheme(spec))), it
     car.check_finite()
+    car.check_status()

@@ -139,11 +139,20 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
+_POOL = {}
+
+
+def _pool(threads):
+    from concurrent.futures import ThreadPoolExecutor
+
+    if threads not in _POOL:  # one pool per process: no per-step thread start-up
+        _POOL[threads] = ThreadPoolExecutor(threads)
+    return _POOL[threads]
+
+
 def cpu_oracle_step(partials64, spec, threads):
     """One simulated-TP compress+reduce cycle of the reference semantics
     (mx/netbench.py:323-334) on host cores, blocks split over threads."""
-    from concurrent.futures import ThreadPoolExecutor
-
     from oracle import mx_oracle as O
 
     sch = O.scheme(spec)
@@ -156,10 +165,9 @@ def cpu_oracle_step(partials64, spec, threads):
     def work(sl):
         return O.allreduce_oneshot([p.reshape(-1)[sl] for p in partials64], sch)
 
-    if threads == 1:
+    if threads == 1 or len(sls) == 1:
         return work(slice(0, n))
-    with ThreadPoolExecutor(threads) as ex:
-        return np.concatenate(list(ex.map(work, sls)))
+    return np.concatenate(list(_pool(threads).map(work, sls)))
 
 
 def cpu_baseline(spec, shape, nranks, budget_s=10.0):
@@ -195,15 +203,17 @@ def run_reference(args, shape, rank, world):
     T, H = shape
     nranks = args.sim_ranks if world == 1 else world
     threads = os.cpu_count() or 1
-    # calibrate: seconds per row for the full cycle
-    cal_rows = 64
+    # calibrate: seconds per row for the full cycle (pool warm, 128 rows)
+    cal_rows = 128
     cal = [p.astype(np.float64) for p in rank_partials((cal_rows, H), nranks, seed=0)]
+    cpu_oracle_step(cal, args.scheme, threads)
     t = time.perf_counter()
     cpu_oracle_step(cal, args.scheme, threads)
     per_row = (time.perf_counter() - t) / cal_rows
+    # each step: as many rows as a ~120 s run allows (at least 8)
     budget = 120.0
-    rows = int(max(8, min(T, budget / max(1, args.steps + args.warmup) / max(per_row, 1e-9))))
-    rows = max(8, (rows // 8) * 8)
+    rows = int(min(T, budget / max(1, args.steps + args.warmup) / max(per_row, 1e-9)))
+    rows = min(T, max(8, (rows // 8) * 8))
     parts = [p.astype(np.float64) for p in rank_partials((rows, H), nranks, seed=0)]
     for _ in range(args.warmup):
         cpu_oracle_step(parts, args.scheme, threads)

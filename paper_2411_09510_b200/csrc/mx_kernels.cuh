@@ -574,8 +574,9 @@ __device__ __forceinline__ void quant_full_unit(const QArgs& A, const Fmt& f, ui
   }
 }
 
-template <typename InT, int B, int ENC, int BITS>
+template <typename InT, int B_, int ENC, int BITS>
 __global__ void __launch_bounds__(kThreads) k_quant(const QArgs A) {
+  constexpr int B = B_;
   __shared__ __align__(16) uint8_t s_stage[kWarps][kUnit / 8];  // one byte per block (B >= 8)
   const Fmt f = A.f;
   const int lane = threadIdx.x & 31;
@@ -585,6 +586,29 @@ __global__ void __launch_bounds__(kThreads) k_quant(const QArgs A) {
   const bool one = total == upc;
   const uint32_t nw = (uint32_t)(gridDim.x * kWarps);
   const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (!one && f.kbits == 8 && A.cv % kUnit == 0 && A.n % A.cv == 0) {
+    // equal chunks of whole units (two-shot at 1024-multiple chunk sizes):
+    // unit u is flat unit u of x; its codes go to chunk u / upc
+    const uint32_t nfull = (uint32_t)(A.n / kUnit);
+    auto one_unit = [&](uint32_t u, const Raw<InT>& r) {
+      const uint32_t chunk = u / upc, q = u - chunk * upc;
+      QArgs B = A;
+      B.elem_base = A.elem_base + (size_t)chunk * A.chunk_stride;
+      B.scale_base = A.scale_base + (size_t)chunk * A.chunk_stride;
+      B.flat_off = A.flat_off + (int64_t)chunk * A.cv;
+      quant_full_unit<InT, B_, ENC, BITS>(B, f, q, r, lane);
+    };
+    for (uint32_t u0 = gw; u0 < nfull; u0 += kUPW * nw) {
+      const uint32_t u1 = u0 + nw;
+      const bool has1 = u1 < nfull;
+      Raw<InT> r0, r1;
+      load_raw<InT>(x + (size_t)u0 * kUnit + lane * kVPL, r0);
+      if (has1) load_raw<InT>(x + (size_t)u1 * kUnit + lane * kVPL, r1);
+      one_unit(u0, r0);
+      if (has1) one_unit(u1, r1);
+    }
+    return;
+  }
   if (one && f.kbits == 8) {
     // single chunk, E8M0 scales: full units in pairs with both units' loads
     // in flight before any math; pointers are plain multiples of u
@@ -917,8 +941,9 @@ __global__ void __launch_bounds__(kThreads) k_dqsum(const DArgs A) {
   }
 }
 
-// K2 lean form for the common case -- one chunk, E8M0 scales, n a multiple
-// of 1024, accumulate mode: one 1024-value unit per warp (32 values per
+// K2 lean form for the common case -- equal chunks of whole 1024-value
+// units (one chunk: n % 1024 == 0; two-shot: chunk size % 1024 == 0), E8M0
+// scales, accumulate mode: one 1024-value unit per warp (32 values per
 // lane, the quantiser's layout), no chunk / tail / generic-scale logic, the
 // ranks' codes loaded two at a time before their decode.  A flat grid of
 // one unit per warp lets the block scheduler balance the waves.
@@ -934,12 +959,15 @@ __global__ void __launch_bounds__(kThreads) k_dqsum_lean(const DArgs A) {
   const int lane = threadIdx.x & 31;
   const uint32_t u = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (u >= (uint32_t)(A.n / kUnit)) return;
-  const int64_t uoff = (int64_t)u * kUnit;
+  // equal chunks of whole units: unit u is flat unit u of the output
+  const uint32_t upc = (uint32_t)(A.cv / kUnit);
+  const uint32_t chunk = u / upc;
+  const int64_t uoff = (int64_t)(u - chunk * upc) * kUnit;
   const int nr = A.nranks;
   float acc[kVPL];
 #pragma unroll
   for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
-  const uint8_t* b = A.in;
+  const uint8_t* b = A.in + (size_t)chunk * A.chunk_stride;
   for (int r = 0; r < nr; r += 2, b += 2 * A.rank_stride) {
     RL x0, x1;
     load_rank<B, BITS, kVPL>(x0, b, A.scale_off, A.elem_off, uoff, lane, kVPL, 8);
@@ -949,7 +977,8 @@ __global__ void __launch_bounds__(kThreads) k_dqsum_lean(const DArgs A) {
     decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
     if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
   }
-  store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(A.out) + uoff + lane * kVPL, kVPL, acc);
+  store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(A.out) + (size_t)u * kUnit + lane * kVPL,
+                             kVPL, acc);
 }
 
 // ---------------------------------------------------------------------------

@@ -133,6 +133,63 @@ def messages():
         torch.cuda.empty_cache()
 
 
+def tp():
+    """Per-rank device cost of the compressed collective at TP = 2/4/8,
+    measured on one GPU with the real kernels (a rank's K1, and K2 over N
+    shards / the two-shot K1-chunked + K3 + K2 chain), next to the NVLink
+    wire time of its bytes at NVLINK_GBS (model; one GPU cannot measure the
+    exchange).  8B and 70B prefill shapes, fp4_e2m1:32:e8m0."""
+    from paper_2411_09510_b200.collective import chunk_len, twoshot_chunk_values
+
+    spec = "fp4_e2m1:32:e8m0"
+    sch = parse_scheme(spec, extensions=True)
+    be = NativeBackend(sch)
+    for T, H in ((2048, 4096), (4096, 8192)):
+        n = T * H
+        for N in (2, 4, 8):
+            R = max(2, -(-3 * L2 // ((N + 2) * n)))
+            g = torch.Generator(device="cuda").manual_seed(N)
+            xs = [torch.randn(n, device="cuda", generator=g).to(torch.bfloat16) for _ in range(R)]
+            ops1 = [SimulatedAllReduce(sch, n, N, "oneshot", torch.bfloat16, fused=False)
+                    for _ in range(R)]
+            for op, x in zip(ops1, xs):
+                op([x] * N)
+            reps = max(3, min(50, int(2e3 / R)))
+            k1 = graph_time(lambda: [be.quantize_into(x, op.gathered[:op.S], op.ws, op.flag)
+                                     for op, x in zip(ops1, xs)], reps) / R
+            k2 = graph_time(lambda: [op.reduce() for op in ops1], reps) / R
+            S = ops1[0].S
+            del ops1
+            ops2 = [SimulatedAllReduce(sch, n, N, "twoshot", torch.bfloat16) for _ in range(R)]
+            for op, x in zip(ops2, xs):
+                op([x] * N)
+            c, S2 = ops2[0].c, ops2[0].S
+            own = chunk_len(n, c, 0)
+            t_q = graph_time(lambda: [be.quantize_chunks(x, c, op.send[0], S2, op.ws, op.flag)
+                                      for op, x in zip(ops2, xs)], reps) / R
+            t_r = graph_time(lambda: [be.requant(op.recv[0], S2, N, own, c, op.gathered[:S2],
+                                                 op.ws, op.flag) for op in ops2], reps) / R
+            t_d = graph_time(lambda: [be.dequant_sum(op.gathered, 0, 1, n, c, S2, op.out)
+                                      for op in ops2], reps) / R
+            del ops2, xs
+            torch.cuda.empty_cache()
+            wm = wire_model(n, S, N)
+            one = (k1 + k2) * 1e3
+            two = (t_q + t_r + t_d) * 1e3
+            print(json.dumps({
+                "config": "tp", "scheme": spec, "shape": [T, H], "tp": N,
+                "oneshot_us": {"k1": round(k1 * 1e3, 3), "k2_nshards": round(k2 * 1e3, 3),
+                               "compute": round(one, 3), "wire_model": wm["oneshot_wire_us"],
+                               "total_model": round(one + wm["oneshot_wire_us"], 2)},
+                "twoshot_us": {"k1_chunked": round(t_q * 1e3, 3), "k3_requant": round(t_r * 1e3, 3),
+                               "k2_final": round(t_d * 1e3, 3), "compute": round(two, 3),
+                               "wire_model": wm["twoshot_wire_us"],
+                               "total_model": round(two + wm["twoshot_wire_us"], 2)},
+                "bf16_ring_wire_model_us": wm["bf16_ring_wire_us"],
+                "note": f"kernel times measured on one B200; wire = bytes / {NVLINK_GBS} GB/s "
+                        "(model, no overlap assumed)"}), flush=True)
+
+
 def codecs():
     """Paper Table 4 on one B200: MX vs the comparison codecs (channel-wise
     INT, TopK) vs fp16 on the 8B prefill partial, simulated TP=2.  Device
@@ -198,4 +255,4 @@ def codecs():
 
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "formats"
-    {"formats": formats, "messages": messages, "codecs": codecs}[what]()
+    {"formats": formats, "messages": messages, "codecs": codecs, "tp": tp}[what]()

@@ -161,6 +161,25 @@ def test_oneshot_and_twoshot_vs_oracle(mx, N, spec):
     assert np.all(np.abs(ref2.astype(np.float64) - one.cpu().numpy()) <= per * 1.0000001 + 1e-30)
 
 
+@pytest.mark.parametrize("N", [2, 4, 8])
+@pytest.mark.parametrize("spec", ["fp4_e2m1:32:e8m0", "fp6_e2m3:64:e8m0", "int8:16:e8m0"])
+def test_twoshot_whole_unit_chunks_vs_oracle(mx, N, spec):
+    """Chunk sizes that are multiples of 1024 take the chunked full-unit K1
+    path and the multi-chunk lean K2; both must stay bit-exact."""
+    from paper_2411_09510_b200.collective import simulate_allreduce
+
+    n = 1 << 18
+    x64 = [inputs.gauss_bf16(n, 3100 + r) for r in range(N)]
+    parts = [dev(x, "bf16") for x in x64]
+    osch = O.scheme(spec)
+    for out_dt in (torch.float32, torch.bfloat16):
+        two, _ = simulate_allreduce(parts, spec, "twoshot", out_dt)
+        ref = O.allreduce_twoshot(x64, osch)
+        got = two.float().cpu().numpy()
+        want = torch.from_numpy(ref).to(out_dt).float().numpy()
+        assert np.array_equal(got, want), (spec, N, out_dt)
+
+
 def test_large_prefill_shape_tp2(mx, golden):
     from paper_2411_09510_b200.collective import simulate_allreduce
     from paper_2411_09510_b200.synth import rank_partials

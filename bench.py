@@ -54,7 +54,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--scheme", default="fp4_e2m1:32:e8m0")
-    ap.add_argument("--algo", choices=["oneshot", "twoshot"], default="oneshot")
+    ap.add_argument("--algo", choices=["auto", "oneshot", "twoshot"], default="auto",
+                    help="auto: one-shot up to TP=2, two-shot from TP=4 (DESIGN.md (e))")
     ap.add_argument("--shape", default="2048,4096")
     ap.add_argument("--sim-ranks", type=int, default=2, help="simulated TP degree at N=1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -315,7 +316,8 @@ def run_ours(args, shape, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_2411_09510_b200 import _native
-    from paper_2411_09510_b200.collective import CompressedAllReduce, SimulatedAllReduce
+    from paper_2411_09510_b200.collective import (CompressedAllReduce, SimulatedAllReduce,
+                                                  twoshot_chunk_values)
     from paper_2411_09510_b200.formats import parse_scheme
     from paper_2411_09510_b200.synth import rank_partials
 
@@ -560,7 +562,10 @@ def run_ours(args, shape, rank, world, local_rank):
             "data": "synthetic (gaussian_with_outliers N(0,1) with 1% x100 outliers, "
                     "mx/synth.py), bf16 partial sums",
             "config": config_dict(args, shape, world),
-            "wire_bytes_per_rank": (nranks - 1) * S if args.algo == "oneshot" else None,
+            "wire_bytes_per_rank": ((nranks - 1) * S if args.algo == "oneshot" else
+                                    2 * (nranks - 1) * _native.shard_layout(
+                                        twoshot_chunk_values(n, nranks, sch.block_size),
+                                        sch.to_c())[2]),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
             "bf16_nccl_allreduce": bf16_ar, "symmetric_memory_fused": symm}
@@ -571,6 +576,9 @@ def main():
     args = parse()
     shape = tuple(int(v) for v in args.shape.split(","))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.algo == "auto":
+        tp = args.sim_ranks if world == 1 else world
+        args.algo = "oneshot" if tp <= 2 else "twoshot"
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":

@@ -194,6 +194,21 @@ int main(int argc, char** argv) {
     fz::k_fused_flow<__nv_bfloat16, 32, ENC_E2M1, 4, TH>                                      \
         <<<(unsigned)(n / kUnit / (TH / 32)), TH, 0, s>>>(args[i]); }, bytes, st);            \
   check("flowT");
-  FLOWT(64) FLOWT(128) FLOWT(256) FLOWT(512) FLOWT(1024)
+  FLOWT(256)
+  // result written straight to mapped pinned host memory (D2H by SM stores)
+  {
+    void* hout;
+    CK(cudaHostAlloc(&hout, xbytes, cudaHostAllocMapped));
+    FArgs a = args[0];
+    a.out = hout;
+    bench("k_fused_flow, device partials -> host result (SM stores over PCIe)", 1,
+          [&](int i, cudaStream_t s) {
+            fz::k_fused_flow<__nv_bfloat16, 32, ENC_E2M1, 4><<<flat, kThreads, 0, s>>>(a); },
+          xbytes, st);
+    void* dout;
+    CK(cudaMalloc(&dout, xbytes));
+    bench("cudaMemcpyAsync D2H 16.8 MB", 1, [&](int i, cudaStream_t s) {
+      CK(cudaMemcpyAsync(hout, dout, xbytes, cudaMemcpyDeviceToHost, s)); }, xbytes, st);
+  }
   return 0;
 }

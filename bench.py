@@ -518,29 +518,48 @@ def run_ours(args, shape, rank, world, local_rank):
         bf16_ar = {"us": round(ms_b * 1e3, 2), "value": round(world * 2 * n / (ms_b * 1e-3) / 1e9, 2),
                    "unit": UNIT, "speedup_of_compressed": round(ms_b / ms_step, 3)}
 
-    # ---- the NVLink-pull fused kernel over symmetric memory (N>1)
+    # ---- the NVLink-pull fused kernel over symmetric memory (N>1).  Every
+    # stage that can fail agrees across ranks first (all_reduce MIN of an
+    # ok flag), so one rank's failure can never leave the others waiting in
+    # a collective.
     symm = None
     if world > 1 and os.environ.get("MXB200_BENCH_SYMM", "1") == "1":
-        try:
-            from paper_2411_09510_b200.collective import SymmetricAllReduce
+        from paper_2411_09510_b200.collective import SymmetricAllReduce
 
+        def all_ok(ok):
+            t = torch.tensor([1 if ok else 0], device=dev, dtype=torch.int32)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            return bool(t.item())
+
+        err, sar, ms_s, exact = None, None, None, None
+        try:
             sar = SymmetricAllReduce(sch, n, out_dtype=torch.bfloat16, device=dev)
             x0 = sets[0][0][0]
             got = sar(x0).clone()
-            exact = None
-            if args.algo == "oneshot":
-                ref = sets[0][1](x0).clone()
-                exact = bool(torch.equal(got.view(torch.int16), ref.view(torch.int16)))
-            gss = [capture(torch, (lambda x=s_[0][0]: sar(x))) for s_ in sets]
-            for i in range(args.warmup):
-                gss[i % R].replay()
-            dist.barrier()
-            gss_all = capture(torch, lambda: [sar(s_[0][0]) for s_ in sets])
-            ms_s = time_steps(torch, gss_all, gss, args.steps) / args.steps
+            torch.cuda.synchronize()
+            sar.check_status()
+        except Exception as exc:  # noqa: BLE001
+            err = exc
+        ok = all_ok(err is None)  # identical on every rank
+        if ok:
+            one = CompressedAllReduce(sch, n, algo="oneshot", out_dtype=torch.bfloat16, device=dev)
+            ref = one(x0).clone()
+            exact = bool(torch.equal(got.view(torch.int16), ref.view(torch.int16)))
+            try:
+                gss = [capture(torch, (lambda x=s_[0][0]: sar(x))) for s_ in sets]
+                for i in range(args.warmup):
+                    gss[i % R].replay()
+                torch.cuda.synchronize()
+                gss_all = capture(torch, lambda: [sar(s_[0][0]) for s_ in sets])
+                ms_s = time_steps(torch, gss_all, gss, args.steps) / args.steps
+                sar.check_status()  # a timed-out peer wait invalidates the number
+            except Exception as exc:  # noqa: BLE001
+                err = exc
+            ok = all_ok(err is None)
+        if ok:
             tt = torch.tensor([ms_s], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ms_s = float(tt.item())
-            sar.check_status()  # a timed-out peer wait invalidates the number
             symm = {"us": round(ms_s * 1e3, 2),
                     "value": round(world * 2 * n / (ms_s * 1e-3) / 1e9, 2), "unit": UNIT,
                     "bit_exact_vs_nccl_oneshot": exact,
@@ -549,8 +568,9 @@ def run_ours(args, shape, rank, world, local_rank):
                               "rank, no grid barrier)"}
             if bf16_ar:
                 symm["speedup_vs_bf16_allreduce"] = round(bf16_ar["us"] / symm["us"], 3)
-        except Exception as exc:  # reported, never fatal for the main measurement
-            symm = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        else:
+            symm = {"error": (f"{type(err).__name__}: {err}"[:300] if err is not None
+                              else "failed on another rank")}
 
     if rank != 0:
         return

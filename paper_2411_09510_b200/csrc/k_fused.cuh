@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_fused_oneshot(const FArgs F) {
 // units overlap across warps instead of being separated by a grid barrier;
 // every warp owns one unit, the grid is sized to the work (several waves).
 template <typename OutT, int B, int ENC, int BITS, int TH = kThreads>
-__global__ void __launch_bounds__(TH) k_fused_flow(const FArgs F) {
+__device__ __forceinline__ void k_fused_flow_body(const FArgs& F) {
   using InT = __nv_bfloat16;
   constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
   constexpr int NSB = Geo<B>::NSB;
@@ -237,6 +237,11 @@ __global__ void __launch_bounds__(TH) k_fused_flow(const FArgs F) {
     if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
   }
   store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(F.out) + xoff, kVPL, acc);
+}
+
+template <typename OutT, int B, int ENC, int BITS, int TH = kThreads>
+__global__ void __launch_bounds__(TH) k_fused_flow(const FArgs F) {
+  k_fused_flow_body<OutT, B, ENC, BITS, TH>(F);
 }
 
 // ---------------------------------------------------------------------------

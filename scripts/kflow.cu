@@ -105,6 +105,18 @@ __global__ void __launch_bounds__(kThreads, MINB) k_flow_pipe(const FArgs F) {
   }
 }
 
+// PDL form: identical body behind griddepcontrol.wait; the next launch is
+// released at our start (launch_dependents), so its CTAs are scheduled and
+// parked while this grid drains.
+template <int WHERE>
+__global__ void __launch_bounds__(kThreads) k_flow_pdl(const FArgs F) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (WHERE == 0) asm volatile("griddepcontrol.launch_dependents;");
+  // same per-warp work as k_fused_flow (one unit per warp)
+  fz::k_fused_flow_body<__nv_bfloat16, 32, ENC_E2M1, 4, kThreads>(F);
+  if (WHERE == 1) asm volatile("griddepcontrol.launch_dependents;");
+}
+
 template <typename F>
 static double bench(const char* name, int R, F launch, double bytes, cudaStream_t st) {
   cudaGraph_t g;
@@ -195,6 +207,23 @@ int main(int argc, char** argv) {
         <<<(unsigned)(n / kUnit / (TH / 32)), TH, 0, s>>>(args[i]); }, bytes, st);            \
   check("flowT");
   FLOWT(256)
+  for (int where = 0; where < 2; ++where) {
+    auto k = where == 0 ? k_flow_pdl<0> : k_flow_pdl<1>;
+    bench(where == 0 ? "k_flow_pdl(launch_dependents at start)" : "k_flow_pdl(launch_dependents at end)",
+          R, [&](int i, cudaStream_t s) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(flat);
+            cfg.blockDim = dim3(kThreads);
+            cfg.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            CK(cudaLaunchKernelEx(&cfg, k, args[i]));
+          }, bytes, st);
+    check("pdl");
+  }
   // result written straight to mapped pinned host memory (D2H by SM stores)
   {
     void* hout;

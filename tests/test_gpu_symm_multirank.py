@@ -1,0 +1,97 @@
+"""The NVLink kernel's multi-rank protocol on ONE device.
+
+k_symm_flow does not care whether its peer pointers are remote: N "ranks"
+are N concurrent launches on N streams of the same GPU, each with its own
+symmetric-layout buffer, the peers' buffers passed as plain device
+pointers.  Sizes are small enough that every rank's CTAs are co-resident
+(the kernels spin on each other's flags).  This exercises the real
+cross-rank flag publish/acquire, per-CTA epochs and slot double-buffering
+over repeated calls at N = 2..8, bit-exact against the oracle and
+identical on every rank (mx/netbench.py:415-419)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import mx_oracle as O  # noqa: E402
+from tests.golden import inputs  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2411_09510_b200 import _native
+
+    return _native
+
+
+def run_ranks(_native, spec, parts, calls, out_dtype=torch.float32):
+    from paper_2411_09510_b200.formats import parse_scheme
+
+    sch = parse_scheme(spec, extensions=True)
+    cs = sch.to_c()
+    sets = parts if isinstance(parts[0], list) else [parts]
+    N, n = len(sets[0]), sets[0][0].numel()
+    slot, flags_off, total, ctas = _native.symm_layout(n, cs, N)
+    bufs = [torch.zeros(total, dtype=torch.uint8, device="cuda") for _ in range(N)]
+    bptr = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    fptr = torch.tensor([b.data_ptr() + flags_off for b in bufs], dtype=torch.int64, device="cuda")
+    state = [torch.zeros(1 + ctas, dtype=torch.int32, device="cuda") for _ in range(N)]
+    flag = [torch.empty(1, dtype=torch.int64, device="cuda") for _ in range(N)]
+    lib = _native.load()
+    for f in flag:
+        lib.mx_nonfinite_reset(ctypes.c_void_p(f.data_ptr()), None)
+    outs = [torch.empty(n, dtype=out_dtype, device="cuda") for _ in range(N)]
+    streams = [torch.cuda.Stream() for _ in range(N)]
+    torch.cuda.synchronize()
+    results = []
+    for c in range(calls):
+        xs = sets[c % len(sets)]
+        for r in range(N):
+            st = streams[r]
+            rc = lib.mx_allreduce_symm(
+                ctypes.c_void_p(xs[r].data_ptr()), _native.MX_BF16, n, ctypes.byref(cs),
+                ctypes.c_void_p(bptr.data_ptr()), ctypes.c_void_p(fptr.data_ptr()), r, N, slot,
+                ctypes.c_void_p(outs[r].data_ptr()),
+                _native.MX_F32 if out_dtype == torch.float32 else _native.MX_BF16,
+                ctypes.c_void_p(state[r].data_ptr()), ctypes.c_void_p(state[r].data_ptr() + 4),
+                ctypes.c_void_p(flag[r].data_ptr()), ctypes.c_void_p(st.cuda_stream))
+            _native.check(rc, "mx_allreduce_symm")
+        torch.cuda.synchronize()
+        assert all(int(s[0].item()) == 0 for s in state), "peer wait timed out"
+        results.append([o.clone() for o in outs])
+    return results
+
+
+@pytest.mark.parametrize("N", [2, 3, 4, 8])
+@pytest.mark.parametrize("spec", ["fp4_e2m1:32:e8m0", "fp6_e3m2:16:e8m0", "int8:64:e8m0"])
+def test_symm_multirank_bit_exact(lib, N, spec):
+    n = 32 * 1024  # 4 CTAs per rank: all ranks co-resident
+    sets = []
+    x64s = []
+    for it in range(3):
+        x64 = [inputs.gauss_bf16(n, 4000 + 17 * it + r) for r in range(N)]
+        x64s.append(x64)
+        sets.append([torch.from_numpy(x).to("cuda", torch.bfloat16) for x in x64])
+    # 5 calls cycle through 3 input sets: epochs 1..5, both slots, twice
+    out = run_ranks(lib, spec, sets, 5)
+    for c, outs in enumerate(out):
+        ref = O.allreduce_oneshot(x64s[c % 3], O.scheme(spec))
+        for r in range(N):
+            assert np.array_equal(outs[r].cpu().numpy(), ref), (spec, N, c, r)
+
+
+def test_symm_multirank_bf16_out(lib):
+    N, n = 4, 16 * 1024
+    x64 = [inputs.gauss_bf16(n, 77 + r) for r in range(N)]
+    xs = [torch.from_numpy(x).to("cuda", torch.bfloat16) for x in x64]
+    outs = run_ranks(lib, "fp4_e2m1:32:e8m0", xs, 3, out_dtype=torch.bfloat16)
+    ref = torch.from_numpy(O.allreduce_oneshot(x64, O.scheme("fp4_e2m1:32:e8m0"))).to(torch.bfloat16)
+    for call in outs:
+        for o in call:
+            assert torch.equal(o.cpu(), ref)

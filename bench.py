@@ -533,7 +533,7 @@ def run_ours(args, shape, rank, world, local_rank):
 
         err, sar, ms_s, exact = None, None, None, None
         try:
-            sar = SymmetricAllReduce(sch, n, out_dtype=torch.bfloat16, device=dev)
+            sar = SymmetricAllReduce(sch, n, out_dtype=torch.bfloat16, device=dev, algo=args.algo)
             x0 = sets[0][0][0]
             got = sar(x0).clone()
             torch.cuda.synchronize()
@@ -542,7 +542,7 @@ def run_ours(args, shape, rank, world, local_rank):
             err = exc
         ok = all_ok(err is None)  # identical on every rank
         if ok:
-            one = CompressedAllReduce(sch, n, algo="oneshot", out_dtype=torch.bfloat16, device=dev)
+            one = CompressedAllReduce(sch, n, algo=args.algo, out_dtype=torch.bfloat16, device=dev)
             ref = one(x0).clone()
             exact = bool(torch.equal(got.view(torch.int16), ref.view(torch.int16)))
             try:
@@ -562,10 +562,13 @@ def run_ours(args, shape, rank, world, local_rank):
             ms_s = float(tt.item())
             symm = {"us": round(ms_s * 1e3, 2),
                     "value": round(world * 2 * n / (ms_s * 1e-3) / 1e9, 2), "unit": UNIT,
-                    "bit_exact_vs_nccl_oneshot": exact,
-                    "kernel": "k_symm_flow (per-CTA: quantise -> release flag to every peer "
-                              "-> acquire N flags -> NVLink pull dequant-sum; one launch per "
-                              "rank, no grid barrier)"}
+                    f"bit_exact_vs_nccl_{args.algo}": exact,
+                    "kernel": ("k_symm_flow (per-CTA: quantise -> release flag to every peer "
+                               "-> acquire N flags -> NVLink pull dequant-sum; one launch per "
+                               "rank, no grid barrier)" if args.algo == "oneshot" else
+                               "k_symm2_flow (per-CTA: quantise N chunks -> flag -> pull my "
+                               "chunk from N peers, fp32 sum, requantise -> flag -> pull N "
+                               "reduced chunks, decode; one launch per rank)")}
             if bf16_ar:
                 symm["speedup_vs_bf16_allreduce"] = round(bf16_ar["us"] / symm["us"], 3)
         else:

@@ -190,6 +190,30 @@ int mx_allreduce_symm(const void* x, int32_t dtype, int64_t n, const mx_scheme_t
                       int32_t nranks, int64_t slot_stride, void* out, int32_t out_dtype,
                       uint32_t* status, uint32_t* epochs, uint64_t* nonfinite, void* stream);
 
+/* Sizes of the two-shot symmetric-memory collective (n % (1024*nranks) == 0):
+ * one buffer per rank of *buffer_bytes = two slots of *slot_stride bytes
+ * (each: nranks send chunk shards + one reduced chunk shard, *shard_stride
+ * bytes apiece) followed, at *flags_offset, by 2 x nranks x *ctas u32 flags
+ * (zero-initialised); local epochs are *ctas u32. */
+int mx_symm_twoshot_layout(int64_t n, const mx_scheme_t* scheme, int32_t nranks,
+                           int64_t* slot_stride, int64_t* shard_stride, int64_t* flags_offset,
+                           int64_t* buffer_bytes, int64_t* ctas);
+
+/* Two-shot compressed all-reduce over NVLink peer memory, ONE launch per
+ * rank, per-CTA dataflow: quantise the local partial's N chunks into this
+ * rank's send shards -> flag -> pull the N peers' shards of this rank's
+ * chunk, fp32 rank-order sum, re-quantise into the reduced shard -> flag ->
+ * pull every owner's reduced shard and decode into `out`.  Bit-identical
+ * to quantise_chunks -> all_to_all -> dequant_sum_requant -> all_gather ->
+ * dequant_sum.  Arguments as mx_allreduce_symm, sizes from
+ * mx_symm_twoshot_layout.  MX_ERR_UNSUPPORTED outside bf16 in,
+ * n % (1024*nranks) == 0, E8M0, B in {16,32,64}. */
+int mx_allreduce_symm_twoshot(const void* x, int32_t dtype, int64_t n,
+                              const mx_scheme_t* scheme, uint8_t* const* peer_bufs,
+                              uint32_t* const* peer_flags, int32_t rank, int32_t nranks,
+                              void* out, int32_t out_dtype, uint32_t* status, uint32_t* epochs,
+                              uint64_t* nonfinite, void* stream);
+
 /* unpack_bits (mx/bitpack.py:37-58) on the device: `count` codes of
  * `width` bits -> one uint8 per code (quantize_block's return value). */
 int mx_unpack_codes(const uint8_t* packed, int64_t count, int32_t width, uint8_t* codes,

@@ -52,6 +52,10 @@ SIGNATURES = {
                                        c_i64, c_vp]),
     "mx_allreduce_fused": (c_i32, [c_vp, c_i32, c_i32, c_i64, _SP, c_vp, c_i64, c_vp, c_i32,
                                    c_vp, c_vp, c_vp]),
+    "mx_symm_twoshot_layout": (c_i32, [c_i64, _SP, c_i32, c_i64p, c_i64p, c_i64p, c_i64p,
+                                       c_i64p]),
+    "mx_allreduce_symm_twoshot": (c_i32, [c_vp, c_i32, c_i64, _SP, c_vp, c_vp, c_i32, c_i32,
+                                          c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "mx_symm_layout": (c_i32, [c_i64, _SP, c_i32, c_i64p, c_i64p, c_i64p, c_i64p]),
     "mx_allreduce_symm": (c_i32, [c_vp, c_i32, c_i64, _SP, c_vp, c_vp, c_i32, c_i32, c_i64, c_vp,
                                   c_i32, c_vp, c_vp, c_vp, c_vp]),
@@ -134,6 +138,16 @@ def symm_layout(n: int, cs: MxScheme, nranks: int) -> tuple[int, int, int, int]:
     check(lib.mx_symm_layout(n, ctypes.byref(cs), nranks, ctypes.byref(a), ctypes.byref(b),
                              ctypes.byref(c), ctypes.byref(d)), "mx_symm_layout")
     return a.value, b.value, c.value, d.value
+
+
+def symm_twoshot_layout(n: int, cs: MxScheme, nranks: int):
+    """(slot_stride, shard_stride, flags_offset, buffer_bytes, ctas) of the
+    two-shot symmetric-memory collective."""
+    lib = load()
+    v = [c_i64() for _ in range(5)]
+    check(lib.mx_symm_twoshot_layout(n, ctypes.byref(cs), nranks, *[ctypes.byref(x) for x in v]),
+          "mx_symm_twoshot_layout")
+    return tuple(x.value for x in v)
 
 
 def require_cuda():

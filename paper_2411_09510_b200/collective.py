@@ -270,17 +270,25 @@ class SymmetricAllReduce:
     NCCL kernel and no grid-wide barrier; the result is bit-identical to the
     NCCL one-shot (same codes, same sum order).  A peer wait longer than
     ~2 s sets a status word instead of hanging (:meth:`check_status`).
-    Requirements: bf16 partial, n % 1024 == 0, E8M0 scales, B in {16,32,64}.
+    ``algo="twoshot"`` runs k_symm2_flow instead (the TP >= 4 algorithm:
+    reduce-scatter leg as peer pulls of this rank's chunk, fp32 sum and
+    re-quantisation, then pulls of every owner's reduced chunk), bit-identical
+    to the NCCL two-shot.
+    Requirements: bf16 partial, n % 1024 == 0 (two-shot: n % (1024*N) == 0),
+    E8M0 scales, B in {16,32,64}.
     """
 
-    def __init__(self, scheme, n: int, group=None, out_dtype=None, device=None):
+    def __init__(self, scheme, n: int, group=None, out_dtype=None, device=None,
+                 algo: str = "oneshot"):
         import torch
         import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm_mem
 
         if isinstance(scheme, str):
             scheme = parse_scheme(scheme, extensions=True)
-        self.scheme, self.n = scheme, int(n)
+        if algo not in ALGOS:
+            raise ValueError(f"algo must be one of {ALGOS}")
+        self.scheme, self.n, self.algo = scheme, int(n), algo
         self.group = group or dist.group.WORLD
         self.world = dist.get_world_size(self.group)
         self.rank = dist.get_rank(self.group)
@@ -288,8 +296,12 @@ class SymmetricAllReduce:
             "cuda", torch.cuda.current_device())
         self.out_dtype = out_dtype or torch.bfloat16
         self.backend = NativeBackend(scheme)
-        self.slot, flags_off, total, ctas = _native.symm_layout(self.n, self.backend.cs,
-                                                                self.world)
+        if algo == "oneshot":
+            self.slot, flags_off, total, ctas = _native.symm_layout(self.n, self.backend.cs,
+                                                                    self.world)
+        else:  # k_symm2_flow: n % (1024 * world) == 0
+            self.slot, _, flags_off, total, ctas = _native.symm_twoshot_layout(
+                self.n, self.backend.cs, self.world)
         self.buf = symm_mem.empty(total, dtype=torch.uint8, device=self.device)
         self.hdl = symm_mem.rendezvous(self.buf, self.group)
         # flags start at zero on every rank before anyone can signal
@@ -311,12 +323,20 @@ class SymmetricAllReduce:
         o = self.out if out is None else out.reshape(-1)
         be = self.backend
         base = self.state.data_ptr()
-        rc = be.lib.mx_allreduce_symm(
-            ctypes.c_void_p(x.data_ptr()), _native.MX_BF16, self.n, ctypes.byref(be.cs),
-            ctypes.c_void_p(self.hdl.buffer_ptrs_dev), ctypes.c_void_p(self.flag_ptrs.data_ptr()),
-            self.rank, self.world, self.slot, ctypes.c_void_p(o.data_ptr()), be._dt(o),
-            ctypes.c_void_p(base), ctypes.c_void_p(base + 4), ctypes.c_void_p(self.flag.data_ptr()),
-            be._st())
+        if self.algo == "oneshot":
+            rc = be.lib.mx_allreduce_symm(
+                ctypes.c_void_p(x.data_ptr()), _native.MX_BF16, self.n, ctypes.byref(be.cs),
+                ctypes.c_void_p(self.hdl.buffer_ptrs_dev),
+                ctypes.c_void_p(self.flag_ptrs.data_ptr()), self.rank, self.world, self.slot,
+                ctypes.c_void_p(o.data_ptr()), be._dt(o), ctypes.c_void_p(base),
+                ctypes.c_void_p(base + 4), ctypes.c_void_p(self.flag.data_ptr()), be._st())
+        else:
+            rc = be.lib.mx_allreduce_symm_twoshot(
+                ctypes.c_void_p(x.data_ptr()), _native.MX_BF16, self.n, ctypes.byref(be.cs),
+                ctypes.c_void_p(self.hdl.buffer_ptrs_dev),
+                ctypes.c_void_p(self.flag_ptrs.data_ptr()), self.rank, self.world,
+                ctypes.c_void_p(o.data_ptr()), be._dt(o), ctypes.c_void_p(base),
+                ctypes.c_void_p(base + 4), ctypes.c_void_p(self.flag.data_ptr()), be._st())
         _native.check(rc, "mx_allreduce_symm")
         return o.view(x.shape)
 

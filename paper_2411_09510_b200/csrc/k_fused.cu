@@ -1,5 +1,5 @@
-// Dispatch of the fused one-shot kernels (k_fused.cuh) to the slices
-// instantiated by k_fused_inst.cu.
+// Dispatch of the fused kernels (k_fused.cuh) to the slices instantiated by
+// k_fused_inst.cu.
 #include "mx_kernels.cuh"
 
 namespace mxb {
@@ -8,6 +8,8 @@ template <typename InT, typename OutT, int B>
 void by_enc(const FArgs& a, int enc, int bits, cudaStream_t st);
 template <typename OutT, int B>
 bool symm_by_enc(const SArgs& a, int enc, int bits, cudaStream_t st);
+template <typename OutT, int B>
+bool symm2_by_enc(const S2Args& a, int enc, int bits, cudaStream_t st);
 
 template <typename OutT>
 void by_block(const FArgs& a, int block, int enc, int bits, cudaStream_t st) {
@@ -30,6 +32,20 @@ bool launch_symm_oneshot(const SArgs& a, int out_is_bf16, int block, int enc, in
                                 : symm_by_enc<float, 32>(a, enc, bits, st);
     case 64: return out_is_bf16 ? symm_by_enc<__nv_bfloat16, 64>(a, enc, bits, st)
                                 : symm_by_enc<float, 64>(a, enc, bits, st);
+  }
+  return false;
+}
+
+bool launch_symm_twoshot(const S2Args& a, int out_is_bf16, int block, int enc, int bits,
+                         cudaStream_t st) {
+  using namespace fz;
+  switch (block) {
+    case 16: return out_is_bf16 ? symm2_by_enc<__nv_bfloat16, 16>(a, enc, bits, st)
+                                : symm2_by_enc<float, 16>(a, enc, bits, st);
+    case 32: return out_is_bf16 ? symm2_by_enc<__nv_bfloat16, 32>(a, enc, bits, st)
+                                : symm2_by_enc<float, 32>(a, enc, bits, st);
+    case 64: return out_is_bf16 ? symm2_by_enc<__nv_bfloat16, 64>(a, enc, bits, st)
+                                : symm2_by_enc<float, 64>(a, enc, bits, st);
   }
   return false;
 }

@@ -354,6 +354,168 @@ __global__ void __launch_bounds__(kThreads) k_symm_flow(const SArgs S) {
   if (threadIdx.x == 0) S.epoch[b] = e;
 }
 
+// ---------------------------------------------------------------------------
+// Two-shot over NVLink peer memory (the TP >= 4 algorithm), one launch per
+// rank, per-CTA dataflow.  Chunk j (c = n/N values) is owned by rank j.
+// CTA b owns units [8b, 8b+8) of EVERY chunk:
+//   A1  quantise those units of the local partial, chunk by chunk, into this
+//       rank's send shards (slot e&1: N chunk shards);  publish flag A(b)
+//   A2  wait for A(b) of every peer; pull the N peers' send shards of MY
+//       chunk over NVLink, fp32 rank-order sum from +0.0, re-quantise into
+//       this rank's reduced shard (k_requant's arithmetic);  publish B(b)
+//   B   wait for B(b) of every peer; pull each owner's reduced shard of its
+//       chunk and decode it (one rank, +0.0 start) into out.
+// Same bytes and same arithmetic as quantise -> all_to_all -> K3 ->
+// all_gather -> K2 (collective.py two-shot), so the result is bit-identical
+// to it; no NCCL kernel, no grid barrier.
+// ---------------------------------------------------------------------------
+
+template <typename OutT, int B, int ENC, int BITS>
+__global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
+  using InT = __nv_bfloat16;
+  constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
+  constexpr int NSB = Geo<B>::NSB;
+  constexpr int LPB = Geo<B>::LPB;
+  constexpr int UBYTES = kUnit / 8 * BITS;
+  constexpr int USCALES = kUnit / B;
+  using RL = RankLoad<B, BITS, kVPL>;
+  __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
+  __shared__ unsigned int s_e;
+  const Fmt f = S.f;
+  if constexpr (DEC != ENC_E2M1) fill_lut(s_lut, f);
+  const uint32_t b = blockIdx.x, G = gridDim.x;
+  if (threadIdx.x == 0) s_e = S.epoch[b] + 1u;
+  __syncthreads();
+  const unsigned int e = s_e;
+  const int lane = threadIdx.x & 31;
+  const uint32_t q = b * kWarps + (threadIdx.x >> 5);  // unit inside every chunk
+  const bool live = q < (uint32_t)(S.c / kUnit);
+  const int nr = S.nranks, me = S.rank;
+  const int64_t slot = (int64_t)(e & 1u) * S.slot_stride;
+  uint8_t* const mine = S.bufs[me] + slot;
+
+  auto put = [&](uint8_t* shard, const LaneCodes<BITS>& cc, const int* stored) {
+    store_lane_codes<BITS>(shard + S.elem_off + (size_t)q * UBYTES + lane * (4 * BITS), cc, kVPL);
+    uint8_t* sp = shard + S.scale_off + (size_t)q * USCALES + (lane / LPB) * NSB;
+    if constexpr (NSB == 4) {
+      *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
+                                         ((uint32_t)stored[2] << 16) | ((uint32_t)stored[3] << 24);
+    } else if constexpr (NSB == 2) {
+      *reinterpret_cast<uint16_t*>(sp) = (uint16_t)(stored[0] | (stored[1] << 8));
+    } else {
+      if (lane % LPB == 0) *sp = (uint8_t)stored[0];
+    }
+  };
+  auto publish_wait = [&](int which) {
+    __syncthreads();
+    if ((int)threadIdx.x < nr) {
+      const int j = threadIdx.x;
+      __threadfence_system();
+      st_release_sys(S.flags[j] + ((size_t)which * nr + me) * G + b, e);
+      const unsigned int* w = S.flags[me] + ((size_t)which * nr + j) * G + b;
+      const long long t0 = clock64();
+      while ((int)(ld_acquire_sys(w) - e) < 0) {
+        __nanosleep(32);
+        if (clock64() - t0 > 4000000000ll) {
+          atomicExch(S.status, 1u);
+          break;
+        }
+      }
+      __threadfence_system();
+    }
+    __syncthreads();
+  };
+
+  // ---- A1: my partial's unit q of every chunk -> my send shards ----------
+  if (live) {
+    const InT* x = reinterpret_cast<const InT*>(S.x) + (size_t)q * kUnit + lane * kVPL;
+    for (int j = 0; j < nr; j += 2) {
+      Raw<InT> r0, r1;
+      load_raw<InT>(x + (size_t)j * S.c, r0);
+      if (j + 1 < nr) load_raw<InT>(x + (size_t)(j + 1) * S.c, r1);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (j + h >= nr) break;
+        int stored[NSB];
+        bool bad;
+        LaneCodes<BITS> cc = quant_lane<InT, B, ENC, BITS>(h ? r1 : r0, f, stored, bad);
+        if (bad)
+          report_nonfinite_raw<InT>(h ? r1 : r0, kVPL,
+                                    (int64_t)(j + h) * S.c + (int64_t)q * kUnit + lane * kVPL,
+                                    S.nonfinite);
+        put(mine + (size_t)(j + h) * S.shard_stride, cc, stored);
+      }
+    }
+  }
+  publish_wait(0);
+
+  // ---- A2: sum my chunk's N send shards (NVLink), re-quantise -----------
+  if (live) {
+    float acc[kVPL];
+#pragma unroll
+    for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
+    for (int r = 0; r < nr; r += 2) {
+      RL a0, a1;
+      load_rank<B, BITS, kVPL, true>(a0, S.bufs[r] + slot + (size_t)me * S.shard_stride,
+                                     S.scale_off, S.elem_off, (int64_t)q * kUnit, lane, kVPL, 8);
+      if (r + 1 < nr)
+        load_rank<B, BITS, kVPL, true>(a1, S.bufs[r + 1] + slot + (size_t)me * S.shard_stride,
+                                       S.scale_off, S.elem_off, (int64_t)q * kUnit, lane, kVPL,
+                                       8);
+      decode_rank<B, DEC, BITS, kVPL>(a0, f, acc, false, s_lut);
+      if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(a1, f, acc, false, s_lut);
+    }
+    Raw<float> raw;
+#pragma unroll
+    for (int i = 0; i < kVPL; ++i) raw.w[i] = __float_as_uint(acc[i]);
+    int stored[NSB];
+    bool bad;
+    LaneCodes<BITS> cc = quant_lane<float, B, ENC, BITS>(raw, f, stored, bad);
+    if (bad)
+      report_nonfinite_raw<float>(raw, kVPL, (int64_t)me * S.c + (int64_t)q * kUnit + lane * kVPL,
+                                  S.nonfinite);
+    put(mine + (size_t)nr * S.shard_stride, cc, stored);
+  }
+  publish_wait(1);
+
+  // ---- B: every owner's reduced shard -> out ------------------------------
+  if (live) {
+    for (int j = 0; j < nr; ++j) {
+      RL a;
+      load_rank<B, BITS, kVPL, true>(a, S.bufs[j] + slot + (size_t)nr * S.shard_stride,
+                                     S.scale_off, S.elem_off, (int64_t)q * kUnit, lane, kVPL, 8);
+      float acc[kVPL];
+#pragma unroll
+      for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;
+      decode_rank<B, DEC, BITS, kVPL>(a, f, acc, false, s_lut);
+      store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(S.out) + (size_t)j * S.c +
+                                     (size_t)q * kUnit + lane * kVPL,
+                                 kVPL, acc);
+    }
+  }
+  if (threadIdx.x == 0) S.epoch[b] = e;
+}
+
+template <typename OutT, int B, int ENC, int BITS>
+void go_symm2(const S2Args& a, cudaStream_t st) {
+  const int64_t g = (a.c / kUnit + kWarps - 1) / kWarps;
+  k_symm2_flow<OutT, B, ENC, BITS><<<(unsigned)g, kThreads, 0, st>>>(a);
+}
+
+template <typename OutT, int B>
+bool symm2_by_enc(const S2Args& a, int enc, int bits, cudaStream_t st) {
+  switch (enc) {
+    case ENC_E2M1: go_symm2<OutT, B, ENC_E2M1, 4>(a, st); return true;
+    case ENC_E2M3: go_symm2<OutT, B, ENC_E2M3, 6>(a, st); return true;
+    case ENC_E3M2: go_symm2<OutT, B, ENC_E3M2, 6>(a, st); return true;
+    case ENC_INT:
+      if (bits == 8) { go_symm2<OutT, B, ENC_INT, 8>(a, st); return true; }
+      return false;
+  }
+  if (bits == 5) { go_symm2<OutT, B, ENC_GEN, 5>(a, st); return true; }
+  return false;
+}
+
 template <typename OutT, int B, int ENC, int BITS>
 void go_symm(const SArgs& a, cudaStream_t st) {
   k_symm_flow<OutT, B, ENC, BITS><<<(unsigned)symm_ctas(a.n), kThreads, 0, st>>>(a);

@@ -17,6 +17,7 @@ using OutT = float;
 template void by_enc<__nv_bfloat16, OutT, MXB_B>(const FArgs&, int, int, cudaStream_t);
 #if MXB_B != 8
 template bool symm_by_enc<OutT, MXB_B>(const SArgs&, int, int, cudaStream_t);
+template bool symm2_by_enc<OutT, MXB_B>(const S2Args&, int, int, cudaStream_t);
 #endif
 }  // namespace fz
 }  // namespace mxb

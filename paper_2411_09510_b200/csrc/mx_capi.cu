@@ -637,6 +637,57 @@ int mx_allreduce_symm(const void* x, int32_t dtype, int64_t n, const mx_scheme_t
   return cuda_check("k_symm_flow");
 }
 
+int mx_symm_twoshot_layout(int64_t n, const mx_scheme_t* s, int32_t nranks,
+                           int64_t* slot_stride, int64_t* shard_stride, int64_t* flags_offset,
+                           int64_t* buffer_bytes, int64_t* ctas) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (n <= 0 || nranks < 1 || n % (1024 * (int64_t)nranks) != 0)
+    return fail(MX_ERR_UNSUPPORTED, "two-shot symmetric path needs n %% (1024*nranks) == 0");
+  const int64_t c = n / nranks;
+  int64_t so, eo, sc;
+  mx_shard_layout(c, s, &so, &eo, &sc);
+  const int64_t slot = ((nranks + 1) * sc + 255) / 256 * 256;
+  const int64_t g = (c / kUnit + kWarps - 1) / kWarps;
+  if (slot_stride) *slot_stride = slot;
+  if (shard_stride) *shard_stride = sc;
+  if (flags_offset) *flags_offset = 2 * slot;
+  if (buffer_bytes) *buffer_bytes = 2 * slot + (2 * (int64_t)nranks * g * 4 + 255) / 256 * 256;
+  if (ctas) *ctas = g;
+  return MX_OK;
+}
+
+int mx_allreduce_symm_twoshot(const void* x, int32_t dtype, int64_t n, const mx_scheme_t* s,
+                              uint8_t* const* peer_bufs, uint32_t* const* peer_flags,
+                              int32_t rank, int32_t nranks, void* out, int32_t out_dtype,
+                              uint32_t* status, uint32_t* epochs, uint64_t* nonfinite,
+                              void* stream) {
+  int64_t slot, sc, foff, total, g;
+  int rc = mx_symm_twoshot_layout(n, s, nranks, &slot, &sc, &foff, &total, &g);
+  if (rc) return rc;
+  if (rank < 0 || rank >= nranks) return fail(MX_ERR_INVALID_ARGUMENT, "bad rank");
+  if (!x || !peer_bufs || !peer_flags || !out || !status || !epochs)
+    return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
+  Fmt f = make_fmt(s);
+  if (dtype != MX_BF16 || (out_dtype != MX_BF16 && out_dtype != MX_F32) || f.kbits != 8 ||
+      !aligned(x, 32) || !aligned(out, 32))
+    return fail(MX_ERR_UNSUPPORTED, "two-shot symmetric path: bf16 in, bf16/f32 out, E8M0");
+  if (nranks > kThreads) return fail(MX_ERR_UNSUPPORTED, "at most %d ranks", kThreads);
+  const int64_t c = n / nranks;
+  int64_t so, eo, sb;
+  mx_shard_layout(c, s, &so, &eo, &sb);
+  S2Args a;
+  a.x = x; a.n = n; a.c = c;
+  a.bufs = peer_bufs; a.flags = reinterpret_cast<unsigned int* const*>(peer_flags);
+  a.rank = rank; a.nranks = nranks; a.slot_stride = slot; a.shard_stride = sc;
+  a.scale_off = so; a.elem_off = eo; a.out = out; a.status = status; a.epoch = epochs;
+  a.nonfinite = reinterpret_cast<unsigned long long*>(nonfinite); a.f = f;
+  if (!launch_symm_twoshot(a, out_dtype == MX_BF16, (int)s->block_size, enc_of(s), f.bits,
+                           (cudaStream_t)stream))
+    return fail(MX_ERR_UNSUPPORTED, "two-shot symmetric path: scheme not instantiated");
+  return cuda_check("k_symm2_flow");
+}
+
 int mx_unpack_codes(const uint8_t* packed, int64_t count, int32_t width, uint8_t* codes, void* stream) {
   if (width < 1 || width > 8) return fail(MX_ERR_INVALID_ARGUMENT, "width %d outside [1, 8]", width);
   if (count <= 0) return MX_OK;

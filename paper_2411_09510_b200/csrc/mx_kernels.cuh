@@ -1057,6 +1057,24 @@ struct SArgs {
   unsigned long long* nonfinite;
   Fmt f;
 };
+// two-shot over symmetric memory (k_fused.cuh, k_symm2_flow)
+struct S2Args {
+  const void* x;                 // this rank's bf16 partial (n values)
+  int64_t n, c;                  // c = n / nranks, multiple of 1024
+  uint8_t* const* bufs;          // device array [nranks]: peer buffer bases
+  unsigned int* const* flags;    // device array [nranks]: peer flag arrays (2 x nranks x ctas)
+  int rank, nranks;
+  int64_t slot_stride;           // bytes of one slot: (nranks + 1) chunk shards
+  int64_t shard_stride;          // bytes of one chunk shard
+  int64_t scale_off, elem_off;   // chunk shard layout (c values)
+  void* out;
+  unsigned int* status;
+  unsigned int* epoch;           // local u32 per CTA
+  unsigned long long* nonfinite;
+  Fmt f;
+};
+bool launch_symm_twoshot(const S2Args& a, int out_is_bf16, int block, int enc, int bits,
+                         cudaStream_t st);
 // CTAs of the symmetric-memory kernel for n values (one 1024-value unit per warp)
 inline int64_t symm_ctas(int64_t n) { return (n / kUnit + kWarps - 1) / kWarps; }
 bool launch_symm_oneshot(const SArgs& a, int out_is_bf16, int block, int enc, int bits,

@@ -52,3 +52,20 @@ def test_symm_world1_matches_oneshot(pg, spec):
         assert np.array_equal(a, O.allreduce_oneshot([x64], O.scheme(spec))), it
     car.check_finite()
     car.check_status()
+
+
+@pytest.mark.parametrize("spec", ["fp4_e2m1:32:e8m0", "int8:16:e8m0"])
+def test_symm_twoshot_world1_real_symmetric_memory(pg, spec):
+    """k_symm2_flow through torch symmetric memory (world size 1)."""
+    from oracle import mx_oracle as O
+    from paper_2411_09510_b200.collective import SymmetricAllReduce
+    from tests.golden import inputs
+
+    n = 1 << 18
+    car = SymmetricAllReduce(spec, n, out_dtype=torch.float32, algo="twoshot")
+    for it in range(4):
+        x64 = inputs.gauss_bf16(n, 3300 + it)
+        x = torch.from_numpy(x64).to("cuda", torch.bfloat16)
+        a = car(x).cpu().numpy().copy()
+        assert np.array_equal(a, O.allreduce_twoshot([x64], O.scheme(spec))), it
+    car.check_status()

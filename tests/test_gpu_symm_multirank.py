@@ -30,14 +30,17 @@ def lib():
     return _native
 
 
-def run_ranks(_native, spec, parts, calls, out_dtype=torch.float32):
+def run_ranks(_native, spec, parts, calls, out_dtype=torch.float32, algo="oneshot"):
     from paper_2411_09510_b200.formats import parse_scheme
 
     sch = parse_scheme(spec, extensions=True)
     cs = sch.to_c()
     sets = parts if isinstance(parts[0], list) else [parts]
     N, n = len(sets[0]), sets[0][0].numel()
-    slot, flags_off, total, ctas = _native.symm_layout(n, cs, N)
+    if algo == "oneshot":
+        slot, flags_off, total, ctas = _native.symm_layout(n, cs, N)
+    else:
+        slot, _, flags_off, total, ctas = _native.symm_twoshot_layout(n, cs, N)
     bufs = [torch.zeros(total, dtype=torch.uint8, device="cuda") for _ in range(N)]
     bptr = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
     fptr = torch.tensor([b.data_ptr() + flags_off for b in bufs], dtype=torch.int64, device="cuda")
@@ -54,13 +57,19 @@ def run_ranks(_native, spec, parts, calls, out_dtype=torch.float32):
         xs = sets[c % len(sets)]
         for r in range(N):
             st = streams[r]
-            rc = lib.mx_allreduce_symm(
-                ctypes.c_void_p(xs[r].data_ptr()), _native.MX_BF16, n, ctypes.byref(cs),
-                ctypes.c_void_p(bptr.data_ptr()), ctypes.c_void_p(fptr.data_ptr()), r, N, slot,
-                ctypes.c_void_p(outs[r].data_ptr()),
-                _native.MX_F32 if out_dtype == torch.float32 else _native.MX_BF16,
-                ctypes.c_void_p(state[r].data_ptr()), ctypes.c_void_p(state[r].data_ptr() + 4),
-                ctypes.c_void_p(flag[r].data_ptr()), ctypes.c_void_p(st.cuda_stream))
+            odt = _native.MX_F32 if out_dtype == torch.float32 else _native.MX_BF16
+            common = (ctypes.c_void_p(state[r].data_ptr()), ctypes.c_void_p(state[r].data_ptr() + 4),
+                      ctypes.c_void_p(flag[r].data_ptr()), ctypes.c_void_p(st.cuda_stream))
+            if algo == "oneshot":
+                rc = lib.mx_allreduce_symm(
+                    ctypes.c_void_p(xs[r].data_ptr()), _native.MX_BF16, n, ctypes.byref(cs),
+                    ctypes.c_void_p(bptr.data_ptr()), ctypes.c_void_p(fptr.data_ptr()), r, N,
+                    slot, ctypes.c_void_p(outs[r].data_ptr()), odt, *common)
+            else:
+                rc = lib.mx_allreduce_symm_twoshot(
+                    ctypes.c_void_p(xs[r].data_ptr()), _native.MX_BF16, n, ctypes.byref(cs),
+                    ctypes.c_void_p(bptr.data_ptr()), ctypes.c_void_p(fptr.data_ptr()), r, N,
+                    ctypes.c_void_p(outs[r].data_ptr()), odt, *common)
             _native.check(rc, "mx_allreduce_symm")
         torch.cuda.synchronize()
         assert all(int(s[0].item()) == 0 for s in state), "peer wait timed out"
@@ -95,3 +104,21 @@ def test_symm_multirank_bf16_out(lib):
     for call in outs:
         for o in call:
             assert torch.equal(o.cpu(), ref)
+
+
+@pytest.mark.parametrize("N", [2, 3, 4, 8])
+@pytest.mark.parametrize("spec", ["fp4_e2m1:32:e8m0", "fp6_e2m3:64:e8m0", "int8:16:e8m0"])
+def test_symm_twoshot_multirank_bit_exact(lib, N, spec):
+    """k_symm2_flow == the NCCL two-shot semantics (oracle allreduce_twoshot)."""
+    n = N * 16 * 1024  # chunks of 16 units: 2 CTAs per rank
+    sets, x64s = [], []
+    for it in range(3):
+        x64 = [inputs.gauss_bf16(n, 6000 + 31 * it + r) for r in range(N)]
+        x64s.append(x64)
+        sets.append([torch.from_numpy(x).to("cuda", torch.bfloat16) for x in x64])
+    for out_dtype in (torch.float32, torch.bfloat16):
+        out = run_ranks(lib, spec, sets, 5, out_dtype=out_dtype, algo="twoshot")
+        for c, outs in enumerate(out):
+            ref = torch.from_numpy(O.allreduce_twoshot(x64s[c % 3], O.scheme(spec))).to(out_dtype)
+            for r in range(N):
+                assert torch.equal(outs[r].cpu(), ref), (spec, N, c, r, out_dtype)

@@ -160,6 +160,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_fused_oneshot(const FArgs F) {
   }
 }
 
+// Units per warp of k_fused_flow: enough that a warp's E8M0 scale bytes of
+// one shard fill a 32-byte sector (B = 64: 16 bytes per unit), so its
+// read-back never hits a partially written sector.
+// (measured: helps FP4 only; the heavier formats keep one unit per warp)
+__host__ __device__ constexpr int flow_units_per_warp(int B, int ENC) {
+  return (B >= 64 && ENC == ENC_E2M1) ? 32 * B / kUnit : 1;
+}
+
 // Dataflow variant for the common case (bf16 partials, n % 1024 == 0, E8M0
 // scales): no grid barrier.  The reduction of unit u depends only on unit u
 // of every rank's shard, and on one device the warp that quantises unit u of
@@ -171,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_fused_oneshot(const FArgs F) {
 // units overlap across warps instead of being separated by a grid barrier;
 // every warp owns one unit, the grid is sized to the work (several waves).
 template <typename OutT, int B, int ENC, int BITS, int TH = kThreads>
-__device__ __forceinline__ void k_fused_flow_body(const FArgs& F) {
+__device__ __forceinline__ void k_flow_one_unit(const FArgs& F) {
   using InT = __nv_bfloat16;
   constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
   constexpr int NSB = Geo<B>::NSB;
@@ -240,7 +248,95 @@ __device__ __forceinline__ void k_fused_flow_body(const FArgs& F) {
 }
 
 template <typename OutT, int B, int ENC, int BITS, int TH = kThreads>
-__global__ void __launch_bounds__(TH) k_fused_flow(const FArgs F) {
+__device__ __forceinline__ void k_flow_multi_unit(const FArgs& F) {
+  using InT = __nv_bfloat16;
+  constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
+  constexpr int NSB = Geo<B>::NSB;
+  constexpr int LPB = Geo<B>::LPB;
+  constexpr int UBYTES = kUnit / 8 * BITS;  // element-stream bytes per unit
+  constexpr int USCALES = kUnit / B;         // scale bytes per unit (k = 8)
+  __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
+  const Fmt f = F.f;
+  if constexpr (DEC != ENC_E2M1) {
+    fill_lut(s_lut, f);
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  constexpr int UPW = flow_units_per_warp(B, ENC);
+  const uint32_t nunits = (uint32_t)(F.n / kUnit);
+  const uint32_t q0 = (blockIdx.x * (TH / 32) + (threadIdx.x >> 5)) * UPW;
+  if (q0 >= nunits) return;
+  const int nr = F.nranks;
+
+  auto quantise = [&](const Raw<InT>& raw, int r, uint32_t q) {
+    int stored[NSB];
+    bool bad;
+    LaneCodes<BITS> c = quant_lane<InT, B, ENC, BITS>(raw, f, stored, bad);
+    if (bad)
+      report_nonfinite_raw<InT>(raw, kVPL, (int64_t)q * kUnit + lane * kVPL, F.nonfinite);
+    uint8_t* shard = F.shards + (size_t)r * F.shard_stride;
+    store_lane_codes<BITS>(shard + F.elem_off + (size_t)q * UBYTES + lane * (4 * BITS), c, kVPL);
+    uint8_t* sp = shard + F.scale_off + (size_t)q * USCALES + (lane / LPB) * NSB;
+    if constexpr (NSB == 4) {
+      *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
+                                         ((uint32_t)stored[2] << 16) |
+                                         ((uint32_t)stored[3] << 24);
+    } else if constexpr (NSB == 2) {
+      *reinterpret_cast<uint16_t*>(sp) = (uint16_t)(stored[0] | (stored[1] << 8));
+    } else {
+      if (lane % LPB == 0) *sp = (uint8_t)stored[0];
+    }
+  };
+
+  // ---- quantise the warp's units of every partial, two ranks in flight ---
+#pragma unroll
+  for (int u = 0; u < UPW; ++u) {
+    const uint32_t q = q0 + u;
+    if (UPW > 1 && q >= nunits) break;
+    const size_t xoff = (size_t)q * kUnit + lane * kVPL;
+    for (int r = 0; r < nr; r += 2) {
+      Raw<InT> a, b;
+      load_raw<InT>(reinterpret_cast<const InT*>(F.partials[r]) + xoff, a);
+      if (r + 1 < nr) load_raw<InT>(reinterpret_cast<const InT*>(F.partials[r + 1]) + xoff, b);
+      quantise(a, r, q);
+      if (r + 1 < nr) quantise(b, r + 1, q);
+    }
+  }
+  __syncwarp();
+
+  // ---- read the N shard slices back, decode, fp32 rank-order sum ---------
+  using RL = RankLoad<B, BITS, kVPL>;
+#pragma unroll
+  for (int u = 0; u < UPW; ++u) {
+    const uint32_t q = q0 + u;
+    if (UPW > 1 && q >= nunits) break;
+    float acc[kVPL];
+#pragma unroll
+    for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
+    for (int r = 0; r < nr; r += 2) {
+      RL x0, x1;
+      load_rank<B, BITS, kVPL, true>(x0, F.shards + (size_t)r * F.shard_stride, F.scale_off,
+                                     F.elem_off, (int64_t)q * kUnit, lane, kVPL, 8);
+      if (r + 1 < nr)
+        load_rank<B, BITS, kVPL, true>(x1, F.shards + (size_t)(r + 1) * F.shard_stride,
+                                       F.scale_off, F.elem_off, (int64_t)q * kUnit, lane, kVPL,
+                                       8);
+      decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
+      if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
+    }
+    store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(F.out) + (size_t)q * kUnit + lane * kVPL,
+                               kVPL, acc);
+  }
+}
+
+template <typename OutT, int B, int ENC, int BITS, int TH = kThreads>
+__device__ __forceinline__ void k_fused_flow_body(const FArgs& F) {
+  if constexpr (flow_units_per_warp(B, ENC) == 1) k_flow_one_unit<OutT, B, ENC, BITS, TH>(F);
+  else k_flow_multi_unit<OutT, B, ENC, BITS, TH>(F);
+}
+
+template <typename OutT, int B, int ENC, int BITS, int TH = kThreads>
+__global__ void __launch_bounds__(TH, (ENC == ENC_E2M1 && B == 64) ? 1024 / TH : 0) k_fused_flow(const FArgs F) {
   k_fused_flow_body<OutT, B, ENC, BITS, TH>(F);
 }
 
@@ -525,9 +621,10 @@ template <typename InT, typename OutT, int B, int ENC, int BITS>
 void go(const FArgs& a, cudaStream_t st) {
   if (a.n % kUnit == 0 && a.f.kbits == 8) {
     // dataflow kernel: one warp per unit, no grid barrier
+    constexpr int UPW = flow_units_per_warp(B, ENC);
     const int64_t units = a.n / kUnit;
-    k_fused_flow<OutT, B, ENC, BITS><<<(unsigned)((units + kWarps - 1) / kWarps), kThreads, 0,
-                                       st>>>(a);
+    k_fused_flow<OutT, B, ENC, BITS>
+        <<<(unsigned)((units + kWarps * UPW - 1) / (kWarps * UPW)), kThreads, 0, st>>>(a);
     return;
   }
   auto k = k_fused_oneshot<InT, OutT, B, ENC, BITS>;

@@ -742,6 +742,11 @@ __device__ __forceinline__ void load_rank(RankLoad<B, BITS, VPL>& r,
       uint32_t v = ldro<CG>(reinterpret_cast<const unsigned short*>(sc + blk0));
       r.st[0] = v & 0xff;
       r.st[1] = v >> 8;
+    } else if constexpr (CG && LPB > 1) {
+      // shard bytes written in this kernel: only the lane that stored the
+      // shared scale byte reads it back; its pair partner gets it by shuffle
+      int v = lane % LPB == 0 ? (int)ldro<CG>(sc + blk0) : 0;
+      r.st[0] = __shfl_sync(0xffffffffu, v, lane & ~(LPB - 1));
     } else {
       r.st[0] = ldro<CG>(sc + blk0);
     }

@@ -207,6 +207,17 @@ int main(int argc, char** argv) {
         <<<(unsigned)(n / kUnit / (TH / 32)), TH, 0, s>>>(args[i]); }, bytes, st);            \
   check("flowT");
   FLOWT(256)
+  {
+    // block 64 (two lanes per block): one E8M0 byte per 64 values
+    std::vector<FArgs> a64 = args;
+    for (auto& a : a64) { a.f.block = 64; a.scale_off = 0; a.elem_off = n / 64 + ((32 - (n / 64) % 32) % 32); }
+    bench("k_fused_flow<B=64>", R, [&](int i, cudaStream_t s) {
+      fz::k_fused_flow<__nv_bfloat16, 64, ENC_E2M1, 4><<<flat / fz::flow_units_per_warp(64, ENC_E2M1), kThreads, 0, s>>>(a64[i]); },
+      bytes, st);
+    bench("k_fused_flow<B=16>", R, [&](int i, cudaStream_t s) {
+      fz::k_fused_flow<__nv_bfloat16, 16, ENC_E2M1, 4><<<flat, kThreads, 0, s>>>(args[i]); },
+      bytes, st);
+  }
   for (int where = 0; where < 2; ++where) {
     auto k = where == 0 ? k_flow_pdl<0> : k_flow_pdl<1>;
     bench(where == 0 ? "k_flow_pdl(launch_dependents at start)" : "k_flow_pdl(launch_dependents at end)",

@@ -18,6 +18,9 @@ void by_dec(const DArgs& a, int enc, int bits, cudaStream_t st) {
     go<B, ENC_E2M1, 4>(a, st);
     return;
   }
+  if (enc == ENC_E2M3) { go<B, ENC_E2M3, 6>(a, st); return; }
+  if (enc == ENC_E3M2) { go<B, ENC_E3M2, 6>(a, st); return; }
+  if (enc == ENC_INT && bits == 8) { go<B, ENC_INT, 8>(a, st); return; }
   switch (bits) {
     case 2: go<B, ENC_GEN, 2>(a, st); return;
     case 3: go<B, ENC_GEN, 3>(a, st); return;

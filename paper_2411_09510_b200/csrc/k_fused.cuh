@@ -44,7 +44,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar) {
 
 template <typename InT, typename OutT, int B, int ENC, int BITS>
 __global__ void __launch_bounds__(kThreads, 3) k_fused_oneshot(const FArgs F) {
-  constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
+  constexpr int DEC = dec_of(ENC, BITS);
   __shared__ __align__(16) uint8_t s_stage[kWarps][kUnit / 8];
   __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
   const Fmt f = F.f;
@@ -181,7 +181,7 @@ __host__ __device__ constexpr int flow_units_per_warp(int B, int ENC) {
 template <typename OutT, int B, int ENC, int BITS, int TH = kThreads>
 __device__ __forceinline__ void k_flow_one_unit(const FArgs& F) {
   using InT = __nv_bfloat16;
-  constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
+  constexpr int DEC = dec_of(ENC, BITS);
   constexpr int NSB = Geo<B>::NSB;
   constexpr int LPB = Geo<B>::LPB;
   constexpr int UBYTES = kUnit / 8 * BITS;  // element-stream bytes per unit
@@ -250,7 +250,7 @@ __device__ __forceinline__ void k_flow_one_unit(const FArgs& F) {
 template <typename OutT, int B, int ENC, int BITS, int TH = kThreads>
 __device__ __forceinline__ void k_flow_multi_unit(const FArgs& F) {
   using InT = __nv_bfloat16;
-  constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
+  constexpr int DEC = dec_of(ENC, BITS);
   constexpr int NSB = Geo<B>::NSB;
   constexpr int LPB = Geo<B>::LPB;
   constexpr int UBYTES = kUnit / 8 * BITS;  // element-stream bytes per unit
@@ -369,7 +369,7 @@ __device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) 
 template <typename OutT, int B, int ENC, int BITS>
 __global__ void __launch_bounds__(kThreads) k_symm_flow(const SArgs S) {
   using InT = __nv_bfloat16;
-  constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
+  constexpr int DEC = dec_of(ENC, BITS);
   constexpr int NSB = Geo<B>::NSB;
   constexpr int LPB = Geo<B>::LPB;
   constexpr int UBYTES = kUnit / 8 * BITS;
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(kThreads) k_symm_flow(const SArgs S) {
 template <typename OutT, int B, int ENC, int BITS>
 __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
   using InT = __nv_bfloat16;
-  constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
+  constexpr int DEC = dec_of(ENC, BITS);
   constexpr int NSB = Geo<B>::NSB;
   constexpr int LPB = Geo<B>::LPB;
   constexpr int UBYTES = kUnit / 8 * BITS;

@@ -34,6 +34,14 @@ namespace mxb {
 
 enum Enc { ENC_GEN = 0, ENC_E2M1 = 1, ENC_E2M3 = 2, ENC_E3M2 = 3, ENC_INT = 4 };
 
+// Decoder of an encoding: hardware f16 conversions for E2M1 / E2M3 / E3M2,
+// integer->f16 for INT8; everything else decodes through the smem LUT.
+__host__ __device__ constexpr int dec_of(int enc, int bits) {
+  return (enc == ENC_E2M1 || enc == ENC_E2M3 || enc == ENC_E3M2 || (enc == ENC_INT && bits == 8))
+             ? enc
+             : ENC_GEN;
+}
+
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kVPL = 32;          // values per lane
@@ -779,6 +787,44 @@ __device__ __forceinline__ void e2m1_word_fma(uint32_t w, uint16_t F16, float* a
       : "r"(w), "h"(F16));
 }
 
+__device__ __forceinline__ void fma2_f16(uint32_t h2, uint16_t F16, float& a0, float& a1) {
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
+      "fma.rn.f32.f16 %0, l, %3, %0;\n\tfma.rn.f32.f16 %1, h, %3, %1;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "r"(h2), "h"(F16));
+}
+
+// 8 FP6 codes (48 bits, value i at bit 6i) -> acc += grid * 2^s: the OCP
+// E2M3 / E3M2 code points equal the reference's sign|index codes, so the
+// hardware f16x2 conversion yields the exact grid values (f16-exact), and
+// FHFMA adds g * 2^s with one rounding.
+template <int DEC>
+__device__ __forceinline__ void fp6_group_fma(uint64_t w, uint16_t F16, float* a) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t b = (uint32_t)((w >> (12 * i)) & 63u) | ((uint32_t)((w >> (12 * i + 6)) & 63u) << 8);
+    uint32_t h2;
+    if constexpr (DEC == ENC_E2M3)
+      asm("cvt.rn.f16x2.e2m3x2 %0, %1;" : "=r"(h2) : "h"((uint16_t)b));
+    else
+      asm("cvt.rn.f16x2.e3m2x2 %0, %1;" : "=r"(h2) : "h"((uint16_t)b));
+    fma2_f16(h2, F16, a[2 * i], a[2 * i + 1]);
+  }
+}
+
+// 8 sign-magnitude INT8 codes -> acc += (+-mag) * 2^s (mag <= 127: f16-exact)
+__device__ __forceinline__ void int8_group_fma(uint64_t w, uint16_t F16, float* a) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t c0 = (uint32_t)(w >> (16 * i)) & 0xffu, c1 = (uint32_t)(w >> (16 * i + 8)) & 0xffu;
+    uint16_t h0, h1;
+    asm("cvt.rn.f16.u32 %0, %1;" : "=h"(h0) : "r"(c0 & 127u));
+    asm("cvt.rn.f16.u32 %0, %1;" : "=h"(h1) : "r"(c1 & 127u));
+    const uint32_t h2 = ((uint32_t)h0 | ((c0 & 128u) << 8)) | (((uint32_t)h1 | ((c1 & 128u) << 8)) << 16);
+    fma2_f16(h2, F16, a[2 * i], a[2 * i + 1]);
+  }
+}
+
 // 2^s as f16 bits, s in [-24, 15]
 __device__ __forceinline__ uint16_t pow2_f16(int s) {
   return (uint16_t)(s >= -14 ? (uint32_t)(s + 15) << 10 : 1u << (s + 24));
@@ -793,15 +839,19 @@ __device__ __forceinline__ void decode_rank(const RankLoad<B, BITS, VPL>& r, con
   for (int sb = 0; sb < NSB; ++sb) {
     const int stored = r.st[sb];
     const int s = stored - f.sbias;
-    if constexpr (DEC == ENC_E2M1) {
-      // FP4 fast path: 2^s representable in f16 (|s| covers every block of
+    if constexpr (DEC == ENC_E2M1 || DEC == ENC_E2M3 || DEC == ENC_E3M2 || DEC == ENC_INT) {
+      // f16 fast path: 2^s representable in f16 (|s| covers every block of
       // real activations); g*2^s is then always an exact f32
       if (!plain && stored != 0 && s >= -24 && s <= 15) {
         const uint16_t F16 = pow2_f16(s);
 #pragma unroll
-        for (int g = 0; g < GPB; ++g)
-          e2m1_word_fma((uint32_t)get_group<BITS, VPL>(r.c, sb * GPB + g), F16,
-                        acc + 8 * (sb * GPB + g));
+        for (int g = 0; g < GPB; ++g) {
+          const uint64_t w = get_group<BITS, VPL>(r.c, sb * GPB + g);
+          float* a = acc + 8 * (sb * GPB + g);
+          if constexpr (DEC == ENC_E2M1) e2m1_word_fma((uint32_t)w, F16, a);
+          else if constexpr (DEC == ENC_INT) int8_group_fma(w, F16, a);
+          else fp6_group_fma<DEC>(w, F16, a);
+        }
         continue;
       }
     }
@@ -991,7 +1041,7 @@ __global__ void __launch_bounds__(kThreads) k_dqsum_lean(const DArgs A) {
 // ---------------------------------------------------------------------------
 template <int B, int ENC, int BITS>
 __global__ void __launch_bounds__(kThreads) k_requant(const RArgs A) {
-  constexpr int DEC = ENC == ENC_E2M1 ? ENC_E2M1 : ENC_GEN;
+  constexpr int DEC = dec_of(ENC, BITS);
   __shared__ __align__(16) uint8_t s_stage[kWarps][kUnit / 8];  // one byte per block (B >= 8)
   __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
   const Fmt f = A.f;

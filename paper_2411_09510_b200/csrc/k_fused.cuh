@@ -608,6 +608,7 @@ bool symm2_by_enc(const S2Args& a, int enc, int bits, cudaStream_t st) {
       if (bits == 8) { go_symm2<OutT, B, ENC_INT, 8>(a, st); return true; }
       return false;
   }
+  if (enc == ENC_E2M2) { go_symm2<OutT, B, ENC_E2M2, 5>(a, st); return true; }
   if (bits == 5) { go_symm2<OutT, B, ENC_GEN, 5>(a, st); return true; }
   return false;
 }
@@ -652,6 +653,7 @@ void by_enc(const FArgs& a, int enc, int bits, cudaStream_t st) {
     case ENC_E2M1: go<InT, OutT, B, ENC_E2M1, 4>(a, st); return;
     case ENC_E2M3: go<InT, OutT, B, ENC_E2M3, 6>(a, st); return;
     case ENC_E3M2: go<InT, OutT, B, ENC_E3M2, 6>(a, st); return;
+    case ENC_E2M2: go<InT, OutT, B, ENC_E2M2, 5>(a, st); return;
     case ENC_INT:
       if (bits == 4) go<InT, OutT, B, ENC_INT, 4>(a, st);
       else if (bits == 5) go<InT, OutT, B, ENC_INT, 5>(a, st);
@@ -676,6 +678,7 @@ bool symm_by_enc(const SArgs& a, int enc, int bits, cudaStream_t st) {
       if (bits == 8) { go_symm<OutT, B, ENC_INT, 8>(a, st); return true; }
       return false;
   }
+  if (enc == ENC_E2M2) { go_symm<OutT, B, ENC_E2M2, 5>(a, st); return true; }
   if (bits == 5) { go_symm<OutT, B, ENC_GEN, 5>(a, st); return true; }
   return false;
 }

@@ -14,6 +14,7 @@ void by_enc(const QArgs& a, int enc, int bits, cudaStream_t st) {
     case ENC_E2M1: go<B, ENC_E2M1, 4>(a, st); return;
     case ENC_E2M3: go<B, ENC_E2M3, 6>(a, st); return;
     case ENC_E3M2: go<B, ENC_E3M2, 6>(a, st); return;
+    case ENC_E2M2: go<B, ENC_E2M2, 5>(a, st); return;
     case ENC_INT:
       switch (bits) {
         case 3: go<B, ENC_INT, 3>(a, st); return;

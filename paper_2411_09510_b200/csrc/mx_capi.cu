@@ -267,6 +267,7 @@ int enc_of(const mx_scheme_t* s) {
     if (s->exponent_bits == 2 && s->mantissa_bits == 1) return ENC_E2M1;
     if (s->exponent_bits == 2 && s->mantissa_bits == 3) return ENC_E2M3;
     if (s->exponent_bits == 3 && s->mantissa_bits == 2) return ENC_E3M2;
+    if (s->exponent_bits == 2 && s->mantissa_bits == 2) return ENC_E2M2;
     return ENC_GEN;
   }
   int b = 1 + s->mantissa_bits;  // sign-magnitude INTb with a compiled width

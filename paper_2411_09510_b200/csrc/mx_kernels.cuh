@@ -32,7 +32,7 @@
 
 namespace mxb {
 
-enum Enc { ENC_GEN = 0, ENC_E2M1 = 1, ENC_E2M3 = 2, ENC_E3M2 = 3, ENC_INT = 4 };
+enum Enc { ENC_GEN = 0, ENC_E2M1 = 1, ENC_E2M3 = 2, ENC_E3M2 = 3, ENC_INT = 4, ENC_E2M2 = 5 };
 
 // Decoder of an encoding: hardware f16 conversions for E2M1 / E2M3 / E3M2,
 // integer->f16 for INT8; everything else decodes through the smem LUT.
@@ -216,6 +216,20 @@ __device__ __forceinline__ uint64_t encode8(const float* x, const Fmt& f) {
                                    : cvt_e3m2x2(x[2 * i], x[2 * i + 1]);
       w |= (uint64_t)(p & 0x3fu) << (12 * i);
       w |= (uint64_t)((p >> 8) & 0x3fu) << (12 * i + 6);
+    }
+  } else if constexpr (ENC == ENC_E2M2) {
+    // FP5 E2M2 (no hardware conversion): encode_gen's closed form with the
+    // format folded in -- lowest normal exponent 0, 2 mantissa bits, grid
+    // max 7; a mantissa-bearing format needs no explicit tie fix
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t sign = __float_as_uint(x[i]) >> 31;
+      const float a = fminf(fabsf(x[i]), 7.0f);
+      const int q = max((int)(__float_as_uint(a) >> 23) - 127, 0);
+      const float C = __uint_as_float(((uint32_t)(q - 2 + 150) << 23) | 0x400000u);
+      const float sum = __fadd_rn(a, C);
+      const uint32_t idx = (__float_as_uint(sum) - __float_as_uint(C)) + ((uint32_t)q << 2);
+      w |= (uint64_t)((sign << 4) | idx) << (i * 5);
     }
   } else if constexpr (ENC == ENC_INT) {
     // sign-magnitude INTb: RNE to an integer by the 1.5*2^23 magic add, the

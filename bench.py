@@ -469,8 +469,9 @@ def run_ours(args, shape, rank, world, local_rank):
             pipe = HostPipeline.simulated(sch, n, nranks, args.algo, torch.bfloat16, dev,
                                           chunks=args.e2e_chunks)
         else:
+            # eager issue across ranks: no NCCL inside a multi-stream graph capture
             pipe = HostPipeline.compressed(sch, n, algo=args.algo, out_dtype=torch.bfloat16,
-                                           device=dev, chunks=args.e2e_chunks)
+                                           device=dev, chunks=args.e2e_chunks, graph=False)
         ke = max(3, min(args.steps, 100))
         for _ in range(3):
             pipe(host_in, host_out)

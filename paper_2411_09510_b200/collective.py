@@ -485,6 +485,8 @@ class HostPipeline:
     partial, NCCL exchange).
     """
 
+    MAX_GRAPHS = 8  # captured host-buffer sets kept (LRU)
+
     def __init__(self, make_op, n: int, ninputs: int, in_dtype=None, out_dtype=None,
                  device="cuda", chunks: int = 4, graph: bool = True, h2d_streams: int = 1):
         import torch
@@ -537,14 +539,16 @@ class HostPipeline:
             self._issue(hin, hout)
             return host_out
         key = tuple(h.data_ptr() for h in hin) + (hout.data_ptr(),)
-        g = self._graphs.get(key)
+        g = self._graphs.pop(key, None)
         if g is None:
             self._issue(hin, hout)  # first-call allocations happen eagerly
             torch.cuda.synchronize(self.device)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 self._issue(hin, hout)
-            self._graphs[key] = g
+            while len(self._graphs) >= self.MAX_GRAPHS:  # least recently used out
+                self._graphs.pop(next(iter(self._graphs)))
+        self._graphs[key] = g  # (re)inserted last: most recently used
         g.replay()
         return host_out
 

@@ -73,3 +73,19 @@ def test_flow_kernel_nonfinite_flag(coll):
     sim(parts)
     torch.cuda.synchronize()
     assert sim.fused and int(sim.flag.item()) == 40000
+
+
+def test_host_pipeline_graph_cache_is_bounded(coll):
+    n, N = 8 * 1024, 2
+    x64 = [inputs.gauss_bf16(n, 300 + r) for r in range(N)]
+    host = [_bf16(x).pin_memory() for x in x64]
+    pipe = coll.HostPipeline.simulated("fp4_e2m1:32:e8m0", n, N, "oneshot", torch.float32,
+                                       "cuda", 2)
+    ref = O.allreduce_oneshot(x64, O.scheme("fp4_e2m1:32:e8m0"))
+    outs = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(pipe.MAX_GRAPHS + 3)]
+    for o in outs + outs[:2]:
+        pipe(host, o)
+    torch.cuda.synchronize()
+    assert len(pipe._graphs) == pipe.MAX_GRAPHS
+    for o in outs:
+        assert np.array_equal(o.numpy(), ref)

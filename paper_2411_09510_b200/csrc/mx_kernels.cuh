@@ -826,16 +826,24 @@ __device__ __forceinline__ void fp6_group_fma(uint64_t w, uint16_t F16, float* a
   }
 }
 
-// 8 sign-magnitude INT8 codes -> acc += (+-mag) * 2^s (mag <= 127: f16-exact)
+// 8 sign-magnitude INT8 codes -> acc += (+-mag) * 2^s (mag <= 127: f16-exact).
+// Per 4 codes: the magnitudes become f16 0x64XX = 1024 + mag by one byte
+// permute per pair, one HADD2 removes the 1024 exactly, and the code's sign
+// bit is permuted into bit 15 of its half.
 __device__ __forceinline__ void int8_group_fma(uint64_t w, uint16_t F16, float* a) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t c0 = (uint32_t)(w >> (16 * i)) & 0xffu, c1 = (uint32_t)(w >> (16 * i + 8)) & 0xffu;
-    uint16_t h0, h1;
-    asm("cvt.rn.f16.u32 %0, %1;" : "=h"(h0) : "r"(c0 & 127u));
-    asm("cvt.rn.f16.u32 %0, %1;" : "=h"(h1) : "r"(c1 & 127u));
-    const uint32_t h2 = ((uint32_t)h0 | ((c0 & 128u) << 8)) | (((uint32_t)h1 | ((c1 & 128u) << 8)) << 16);
-    fma2_f16(h2, F16, a[2 * i], a[2 * i + 1]);
+  for (int k = 0; k < 2; ++k) {
+    const uint32_t v = (uint32_t)(w >> (32 * k));
+    const uint32_t m = v & 0x7f7f7f7fu;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      // bytes [c(2p), 0x64, c(2p+1), 0x64] and [0, c(2p), 0, c(2p+1)]
+      const uint32_t biased = __byte_perm(m, 0x64646464u, p ? 0x4342u : 0x4140u);
+      const uint32_t signs = __byte_perm(v, 0u, p ? 0x3424u : 0x1404u) & 0x80008000u;
+      uint32_t h2;
+      asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(h2) : "r"(biased), "r"(0x64006400u));
+      fma2_f16(h2 ^ signs, F16, a[4 * k + 2 * p], a[4 * k + 2 * p + 1]);
+    }
   }
 }
 

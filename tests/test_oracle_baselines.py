@@ -79,3 +79,55 @@ def test_prefill_shape(gold):
     idx, vals = BO.topk_compress(x, factor=3.0)
     g = gold["topk"]["prefill_bf16_2048x4096|f3"]
     assert sha(idx.astype("<u4")) == g["indices"] and sha(vals.astype("<f2")) == g["values"]
+
+
+@pytest.mark.parametrize("case", SMALL)
+def test_host_containers_match_reference(gold, case):
+    """The product package's MXC1 container formatting for the comparison
+    codecs (host code, no GPU) reproduces the reference's bytes."""
+    from paper_2411_09510_b200 import baselines as bl
+
+    x = inputs.baseline_case(case)
+    for bits in (2, 4, 8):
+        s16, _, stream = BO.chanint_compress(x, bits)
+        p = bl.ChannelIntPacket(shape=tuple(x.shape) or (1,), bits=bits, scales=s16,
+                                code_stream=stream)
+        blob = bl.serialize_channel_int(p)
+        assert sha(blob) == gold["chanint"][f"{case}|{bits}"]["container"]
+        q = bl.deserialize_channel_int(blob)
+        assert q.code_stream == stream and np.array_equal(q.scales, s16) and q.bits == bits
+        assert p.nbytes == gold["chanint"][f"{case}|{bits}"]["nbytes"]
+    for key, g in gold["topk"].items():
+        name, arg = key.split("|")
+        if name != case or "error" in g:
+            continue
+        if arg.startswith("f"):
+            k = bl.topk_budget(x.size, x.ndim, float(arg[1:]))
+        else:
+            k = int(arg[1:])
+        idx, vals = BO.topk_compress(x, k=k)
+        p = bl.TopKPacket(shape=tuple(x.shape), indices=idx, values=vals)
+        blob = bl.serialize_topk(p)
+        assert sha(blob) == g["container"], key
+        q = bl.deserialize_topk(blob)
+        assert np.array_equal(q.indices, idx) and np.array_equal(q.values.view(np.uint16),
+                                                               vals.view(np.uint16))
+
+
+def test_host_container_errors():
+    from paper_2411_09510_b200 import baselines as bl
+    from paper_2411_09510_b200.errors import MalformedHeader, TruncatedStream
+
+    p = bl.TopKPacket(shape=(4, 4), indices=np.array([1, 5], np.uint32),
+                      values=np.array([1.0, -2.0], np.float16))
+    blob = bl.serialize_topk(p)
+    with pytest.raises(TruncatedStream):
+        bl.deserialize_topk(blob[:-1])
+    with pytest.raises(MalformedHeader):
+        bl.deserialize_channel_int(blob)
+    c = bl.ChannelIntPacket(shape=(2, 3), bits=4, scales=np.ones(3, np.float16),
+                            code_stream=bytes(3))
+    with pytest.raises(MalformedHeader):
+        bl.deserialize_topk(bl.serialize_channel_int(c))
+    with pytest.raises(TruncatedStream):
+        bl.deserialize_channel_int(bl.serialize_channel_int(c)[:-1])

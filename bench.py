@@ -415,9 +415,49 @@ def run_ours(args, shape, rank, world, local_rank):
             kernels[name] = {"us": round(ms * 1e3, 3), "bytes": bytes_per,
                              "gbs": round(bytes_per / (ms * 1e-3) / 1e9, 1),
                              "launches_timed": reps * R}
+    if not sim and args.algo == "oneshot":
+        # N>1: this rank's K1 and its K2 over the N gathered shards, timed on
+        # the rank's own buffers (local launches only, no collective)
+        try:
+            def q_all():
+                for parts, op in sets:
+                    S_ = op.plan.shard_bytes
+                    op.backend.quantize_into(parts[0].reshape(-1),
+                                             op.gathered[rank * S_:(rank + 1) * S_], op.ws,
+                                             op.flag)
+
+            def d_all():
+                for parts, op in sets:
+                    S_ = op.plan.shard_bytes
+                    op.backend.dequant_sum(op.gathered, S_, world, n, n, 0, op.out)
+
+            for name, fn, bytes_per in (("k_quant", q_all, 2 * n + sb + eb),
+                                        ("k_dqsum", d_all, world * (sb + eb) + 2 * n)):
+                g = capture(torch, fn)
+                for _ in range(3):
+                    g.replay()
+                reps = max(4, min(100, args.steps // 20))
+                ms = time_graph_replays(torch, [g], reps) / (reps * R)
+                kernels[name] = {"us": round(ms * 1e3, 3), "bytes": bytes_per,
+                                 "gbs": round(bytes_per / (ms * 1e-3) / 1e9, 1),
+                                 "launches_timed": reps * R}
+        except Exception as exc:  # noqa: BLE001  (reported, never fatal)
+            kernels = {"error": f"{type(exc).__name__}: {exc}"[:200]}
     peak, peak_kind = peaks()
     roof = None
-    if fused and "k_quant" in kernels:
+    if not sim and "k_dqsum" in kernels:
+        kd = kernels["k_dqsum"]
+        roof = {"bound": "hbm",
+                "kernel": f"k_dqsum_lean<bf16,B={sch.block_size},{sch.element.name}> "
+                          f"(K2: {world} gathered shards -> bf16, this rank)",
+                "achieved": kd["gbs"], "peak": peak, "unit": "GB/s",
+                "frac": round(kd["gbs"] / peak, 4), "traffic": None,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",
+                "algorithmic_bytes_per_launch": kd["bytes"], "launch_us": kd["us"],
+                "share_of_step": round(kd["us"] / (ms_step * 1e3), 3),
+                "other_kernels": {k: v for k, v in kernels.items() if k != "k_dqsum"},
+                "note": "rank 0's device time; the NCCL all-gather is the rest of the step"}
+    elif fused and "k_quant" in kernels:
         # the step IS one kernel (k_fused_flow): it must read the N partials
         # from HBM, write the N shards into the gather buffer (the bytes an
         # all-gather delivers) and write the bf16 sum.  Each warp reads its

@@ -391,6 +391,9 @@ def _torch():
     return torch
 
 
+_SYMM_CACHE = {}  # (group, scheme, n, dtype, algo) -> SymmetricAllReduce shared by layers
+
+
 def make_module_classes():
     """Build the nn.Module classes lazily (torch import stays optional for
     the pure-host parts of the package)."""
@@ -402,7 +405,10 @@ def make_module_classes():
         """y = all_reduce(x_local @ W_r): the hook of mx/tpsim.py:263-281.
 
         ``scheme`` None -> uncompressed NCCL bf16 all-reduce; otherwise the
-        MX-compressed all-reduce (one-shot or two-shot)."""
+        MX-compressed all-reduce: ``algo`` "oneshot" / "twoshot" over NCCL,
+        "symm" / "symm2" for the one-kernel NVLink forms (K5 / K5b, one
+        symmetric buffer shared by every layer of the same shape), "auto"
+        for one-shot up to TP=2 and two-shot beyond."""
 
         def __init__(self, d_in_local, d_out, group=None, scheme=None, algo="oneshot",
                      tokens=None, device="cuda", dtype=torch.bfloat16, std=0.02):
@@ -419,18 +425,30 @@ def make_module_classes():
                 if dist.is_initialized() and dist.get_world_size(self.group) > 1:
                     dist.all_reduce(y, group=self.group)
                 return y
-            from .collective import CompressedAllReduce
+            from .collective import CompressedAllReduce, SymmetricAllReduce
 
             key = (y.numel(), y.dtype)
             car = self._car.get(key)
             if car is None:
                 ws = dist.get_world_size(self.group) if dist.is_initialized() else 1
                 rk = dist.get_rank(self.group) if dist.is_initialized() else 0
-                car = CompressedAllReduce(self.scheme, y.numel(), group=self.group,
-                                          algo=self.algo, out_dtype=y.dtype, device=y.device,
-                                          world_size=ws, rank=rk)
+                algo = self.algo
+                if algo == "auto":
+                    algo = "oneshot" if ws <= 2 else "twoshot"
+                if algo in ("symm", "symm2"):
+                    skey = (id(self.group), str(self.scheme), y.numel(), y.dtype, algo)
+                    car = _SYMM_CACHE.get(skey)
+                    if car is None:
+                        car = SymmetricAllReduce(self.scheme, y.numel(), group=self.group,
+                                                 out_dtype=y.dtype, device=y.device,
+                                                 algo="oneshot" if algo == "symm" else "twoshot")
+                        _SYMM_CACHE[skey] = car
+                else:
+                    car = CompressedAllReduce(self.scheme, y.numel(), group=self.group,
+                                              algo=algo, out_dtype=y.dtype, device=y.device,
+                                              world_size=ws, rank=rk)
                 self._car[key] = car
-            return car(y)
+            return car(y.contiguous())
 
         def forward(self, x):
             return self.reduce(F.linear(x, self.weight))

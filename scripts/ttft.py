@@ -29,7 +29,8 @@ def main():
     ap.add_argument("--layers", type=int, default=None, help="truncate the stack (memory)")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--schemes", default="none,fp4_e2m1:32:e8m0")
-    ap.add_argument("--algos", default="oneshot,twoshot")
+    ap.add_argument("--algos", default="oneshot,twoshot",
+                    help="oneshot,twoshot (NCCL), symm,symm2 (one-kernel NVLink), auto")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -69,3 +69,19 @@ def test_symm_twoshot_world1_real_symmetric_memory(pg, spec):
         a = car(x).cpu().numpy().copy()
         assert np.array_equal(a, O.allreduce_twoshot([x64], O.scheme(spec))), it
     car.check_status()
+
+
+def test_row_parallel_linear_symm_algos(pg):
+    """The TP hook with the one-kernel NVLink collectives equals the NCCL
+    one-shot / two-shot hook bit for bit (world size 1)."""
+    from paper_2411_09510_b200 import tp
+
+    RowParallelLinear, _, _, _ = tp.make_module_classes()
+    torch.manual_seed(0)
+    x = torch.randn(2, 64, 512, device="cuda", dtype=torch.bfloat16)
+    for nccl, symm in (("oneshot", "symm"), ("twoshot", "symm2")):
+        a = RowParallelLinear(512, 256, scheme="fp4_e2m1:32:e8m0", algo=nccl)
+        b = RowParallelLinear(512, 256, scheme="fp4_e2m1:32:e8m0", algo=symm)
+        b.weight.data.copy_(a.weight.data)
+        for _ in range(3):
+            assert torch.equal(a(x), b(x)), (nccl, symm)

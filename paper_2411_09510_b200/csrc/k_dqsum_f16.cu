@@ -5,7 +5,7 @@ namespace mxb {
 namespace {
 template <int B, int DEC, int BITS>
 void go(const DArgs& a, cudaStream_t st) {
-  if (!a.plain && a.f.kbits == 8 && a.cv % kUnit == 0 && a.n % a.cv == 0) {
+  if (a.f.kbits == 8 && a.cv % kUnit == 0 && a.n % a.cv == 0 && (!a.plain || a.nranks == 1)) {
     k_dqsum_lean<__half, B, DEC, BITS><<<(unsigned)(a.n / kUnit / kWarps), kThreads, 0, st>>>(a);
     return;
   }

@@ -1020,7 +1020,7 @@ __global__ void __launch_bounds__(kThreads) k_dqsum(const DArgs A) {
 
 // K2 lean form for the common case -- equal chunks of whole 1024-value
 // units (one chunk: n % 1024 == 0; two-shot: chunk size % 1024 == 0), E8M0
-// scales, accumulate mode: one 1024-value unit per warp (32 values per
+// scales (accumulate mode, or plain decode as accumulation from -0.0): one 1024-value unit per warp (32 values per
 // lane, the quantiser's layout), no chunk / tail / generic-scale logic, the
 // ranks' codes loaded two at a time before their decode.  A flat grid of
 // one unit per warp lets the block scheduler balance the waves.
@@ -1041,9 +1041,13 @@ __global__ void __launch_bounds__(kThreads) k_dqsum_lean(const DArgs A) {
   const uint32_t chunk = u / upc;
   const int64_t uoff = (int64_t)(u - chunk * upc) * kUnit;
   const int nr = A.nranks;
+  // sums start at +0.0 (mx/netbench.py:332); a plain decode (one shard,
+  // decompress_tensor) starts at -0.0, which makes acc + v == v for every v
+  // including -0, so it shares the accumulate code paths exactly
+  const float z = A.plain ? -0.f : 0.f;
   float acc[kVPL];
 #pragma unroll
-  for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
+  for (int i = 0; i < kVPL; ++i) acc[i] = z;
   const uint8_t* b = A.in + (size_t)chunk * A.chunk_stride;
   for (int r = 0; r < nr; r += 2, b += 2 * A.rank_stride) {
     RL x0, x1;

@@ -288,3 +288,33 @@ def test_fused_oneshot_bit_identical(mx, spec, N):
         assert fused.fused, "fused kernel not taken"
         assert np.array_equal(a, b) and np.array_equal(a, a2)
         assert np.array_equal(a, O.allreduce_oneshot(x64, O.scheme(spec)))
+
+
+def test_tma_quantiser_opt_in_bit_exact(mx):
+    """K1's opt-in TMA pipeline (MXB200_TMA=1; read once per process, so a
+    subprocess) writes the same streams as the oracle, whole tiles plus a
+    register-path remainder."""
+    import os
+    import subprocess
+    import sys
+
+    code = r"""
+import numpy as np, torch
+from oracle import mx_oracle as O
+from tests.golden import inputs
+import paper_2411_09510_b200 as mx
+for n, spec in [(8192 * 3 + 1000, "fp4_e2m1:32:e8m0"), (8192 * 5, "fp6_e2m3:16:e8m0"),
+                (8192 * 2 + 64, "int8:64:e8m0")]:
+    x64 = inputs.gauss_bf16(n, 77)
+    d = mx.compress_tensor_device(torch.from_numpy(x64).to("cuda", torch.bfloat16),
+                                  mx.parse_scheme(spec, extensions=True))
+    ss, es = O.compress(x64, O.scheme(spec))
+    assert d.scale.cpu().numpy().tobytes() == ss, spec
+    assert d.elements.cpu().numpy().tobytes() == es, spec
+print("tma ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MXB200_TMA="1", PYTHONPATH=root)
+    p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=300)
+    assert p.returncode == 0 and "tma ok" in p.stdout, p.stderr[-2000:]

@@ -616,6 +616,20 @@ def run_ours(args, shape, rank, world, local_rank):
             symm = {"error": (f"{type(err).__name__}: {err}"[:300] if err is not None
                               else "failed on another rank")}
 
+    # the collective against NVLink (N>1): effective (uncompressed-equivalent,
+    # nccl-tests "algbw") and wire GB/s per rank, against 900 GB/s/direction
+    coll = None
+    if world > 1:
+        wire = ((world - 1) * S if args.algo == "oneshot" else
+                2 * (world - 1) * _native.shard_layout(
+                    twoshot_chunk_values(n, world, sch.block_size), sch.to_c())[2])
+        t = ms_step * 1e-3
+        coll = {"effective_algbw_gbs": round(2 * n / t / 1e9, 1),
+                "busbw_gbs": round(2 * n / t / 1e9 * 2 * (world - 1) / world, 1),
+                "wire_bytes_per_rank": wire, "wire_gbs_per_rank": round(wire / t / 1e9, 1),
+                "nvlink_gbs_per_direction": 900.0,
+                "wire_frac_of_nvlink": round(wire / t / 1e9 / 900.0, 4)}
+
     if rank != 0:
         return
     cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(args.scheme, shape, nranks)
@@ -632,7 +646,8 @@ def run_ours(args, shape, rank, world, local_rank):
                                         sch.to_c())[2]),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
-            "bf16_nccl_allreduce": bf16_ar, "symmetric_memory_fused": symm}
+            "bf16_nccl_allreduce": bf16_ar, "symmetric_memory_fused": symm,
+            "collective": coll}
     print(json.dumps(line), flush=True)
 
 

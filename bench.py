@@ -60,7 +60,8 @@ def parse():
     ap.add_argument("--sim-ranks", type=int, default=2, help="simulated TP degree at N=1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=4)
+    ap.add_argument("--e2e-pieces", default="1,3,3,1",
+                    help="HostPipeline piece weights (or one integer: equal pieces)")
     ap.add_argument("--profile", action="store_true",
                     help="ncu mode: a few eager launches, no timing, no JSON")
     return ap.parse_args()
@@ -505,13 +506,15 @@ def run_ours(args, shape, rank, world, local_rank):
 
         host_in = [torch.from_numpy(host_parts[r]).to(torch.bfloat16).pin_memory() for r in mine]
         host_out = torch.empty(n, dtype=torch.bfloat16).pin_memory()
+        w = [int(v) for v in args.e2e_pieces.split(",")]
+        pieces = w[0] if len(w) == 1 else tuple(w)
         if sim:
             pipe = HostPipeline.simulated(sch, n, nranks, args.algo, torch.bfloat16, dev,
-                                          chunks=args.e2e_chunks)
+                                          chunks=pieces)
         else:
             # eager issue across ranks: no NCCL inside a multi-stream graph capture
             pipe = HostPipeline.compressed(sch, n, algo=args.algo, out_dtype=torch.bfloat16,
-                                           device=dev, chunks=args.e2e_chunks, graph=False)
+                                           device=dev, chunks=pieces, graph=False)
         ke = max(3, min(args.steps, 100))
         for _ in range(3):
             pipe(host_in, host_out)
@@ -539,7 +542,8 @@ def run_ours(args, shape, rank, world, local_rank):
             ms_e = float(tt.item())
         e2e = {"value": round(nranks * 2 * n / (ms_e * 1e-3) / 1e9, 3), "unit": UNIT,
                "h2d_bytes_per_step": pipe.h2d_bytes, "d2h_bytes_per_step": pipe.d2h_bytes,
-               "ms_per_step": round(ms_e, 4), "steps": ke, "chunks": pipe.k,
+               "ms_per_step": round(ms_e, 4), "steps": ke, "pieces": pipe.k,
+               "piece_values": [b1 - b0 for b0, b1 in zip(pipe.bounds, pipe.bounds[1:])],
                "bit_exact_vs_device_call": exact,
                "api": "HostPipeline.__call__ (pinned host partials -> pinned host result)"}
 

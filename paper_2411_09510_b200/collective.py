@@ -488,20 +488,36 @@ class HostPipeline:
     MAX_GRAPHS = 8  # captured host-buffer sets kept (LRU)
 
     def __init__(self, make_op, n: int, ninputs: int, in_dtype=None, out_dtype=None,
-                 device="cuda", chunks: int = 4, graph: bool = True, h2d_streams: int = 1):
+                 device="cuda", chunks=4, graph: bool = True, h2d_streams: int = 1):
         import torch
 
         self.n, self.nin = int(n), int(ninputs)
         self.use_graph = graph
         self._graphs = {}
-        k = max(1, int(chunks))
-        while k > 1 and (self.n % k or (self.n // k) % 1024):
-            k -= 1
-        self.k, self.c = k, self.n // k
+        if isinstance(chunks, (list, tuple)):
+            # explicit piece weights, e.g. (1, 3, 3, 1): small first and last
+            # pieces shorten the un-overlapped head (H2D) and tail (D2H)
+            units, tot = self.n // 1024, float(sum(chunks))
+            cuts = [0]
+            for wgt in chunks[:-1]:
+                cuts.append(min(units, cuts[-1] + max(1, round(units * wgt / tot))))
+            cuts.append(units)
+            bounds = [c * 1024 for c in cuts]
+            if self.n % 1024 or any(b1 <= b0 for b0, b1 in zip(bounds, bounds[1:])):
+                bounds = [0, self.n]
+        else:
+            k = max(1, int(chunks))
+            while k > 1 and (self.n % k or (self.n // k) % 1024):
+                k -= 1
+            bounds = [j * (self.n // k) for j in range(k + 1)]
+        self.bounds = bounds
+        self.k = len(bounds) - 1
+        self.c = bounds[1] - bounds[0]
         self.device = torch.device(device)
         in_dtype = in_dtype or torch.bfloat16
         self.out_dtype = out_dtype or torch.bfloat16
-        self.ops = [make_op(self.c) for _ in range(k)]
+        self.ops = [make_op(b1 - b0) for b0, b1 in zip(bounds, bounds[1:])]
+        k = self.k
         self.dev_in = [torch.empty(self.n, dtype=in_dtype, device=self.device)
                        for _ in range(self.nin)]
         self.dev_out = torch.empty(self.n, dtype=self.out_dtype, device=self.device)
@@ -559,9 +575,8 @@ class HostPipeline:
         s_red, s_out, s_ins = self.streams[0], self.streams[1], self.streams[2:]
         for s in self.streams:
             s.wait_stream(cur)
-        c = self.c
         for j in range(self.k):
-            sl = slice(j * c, (j + 1) * c)
+            sl = slice(self.bounds[j], self.bounds[j + 1])
             for i, (d, h) in enumerate(zip(self.dev_in, hin)):
                 s_in = s_ins[i % len(s_ins)]
                 with torch.cuda.stream(s_in):

@@ -31,9 +31,13 @@ def main():
     h_out = torch.empty(n, dtype=torch.bfloat16).pin_memory()
     res = {}
     for hs in (1, 2):
-        for k in (1, 2, 3, 4, 6, 8, 16):
+        for k in (2, 4, 8):
             pipe = HostPipeline.simulated("fp4_e2m1:32:e8m0", n, 2, chunks=k, h2d_streams=hs)
             res[f"h2d{hs}_chunks{pipe.k}"] = round(timed(lambda: pipe(h_in, h_out)), 4)
+    for w in ((1, 3, 3, 1), (1, 2, 2, 2, 1), (1, 4, 1), (2, 3, 2, 1), (1, 2, 4, 1), (3, 3, 1, 1),
+              (1, 6, 1), (2, 5, 1)):
+        pipe = HostPipeline.simulated("fp4_e2m1:32:e8m0", n, 2, chunks=w)
+        res["pieces" + "-".join(map(str, w))] = round(timed(lambda: pipe(h_in, h_out)), 4)
     pe = HostPipeline.simulated("fp4_e2m1:32:e8m0", n, 2, chunks=4, graph=False)
     res["eager_chunks4"] = round(timed(lambda: pe(h_in, h_out)), 4)
     print(json.dumps(res))

@@ -89,3 +89,16 @@ def test_host_pipeline_graph_cache_is_bounded(coll):
     assert len(pipe._graphs) == pipe.MAX_GRAPHS
     for o in outs:
         assert np.array_equal(o.numpy(), ref)
+
+
+def test_host_pipeline_weighted_pieces(coll):
+    n, N = 64 * 1024, 2
+    x64 = [inputs.gauss_bf16(n, 900 + r) for r in range(N)]
+    host = [_bf16(x).pin_memory() for x in x64]
+    out = torch.empty(n, dtype=torch.float32).pin_memory()
+    pipe = coll.HostPipeline.simulated("fp4_e2m1:32:e8m0", n, N, "oneshot", torch.float32,
+                                       "cuda", (1, 3, 3, 1))
+    assert pipe.bounds == [0, 8192, 32768, 57344, 65536]
+    pipe(host, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.numpy(), O.allreduce_oneshot(x64, O.scheme("fp4_e2m1:32:e8m0")))

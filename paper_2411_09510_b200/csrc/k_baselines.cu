@@ -151,13 +151,22 @@ __global__ void __launch_bounds__(256) k_ci_amax_v(const T* __restrict__ x, int6
   for (int j = 0; j < 8; ++j) m[j] = 0;
   unsigned long long bad = ~0ull;
   if (live) {
-    const int64_t r1 = min(rows, (int64_t)(blockIdx.y + 1) * RB);
-    for (int64_t r = (int64_t)blockIdx.y * RB + ty; r < r1; r += 8) {
-      T v[8];
-      ldv<T, 8>(x + r * C + c0, v);
+    // the thread's RB/8 rows: every load in flight before the reduction
+    constexpr int NR = RB / 8;
+    const int64_t rb = (int64_t)blockIdx.y * RB + ty;
+    T v[NR][8];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const int64_t r = rb + 8 * i;
+      if (r < rows) ldv<T, 8>(x + r * C + c0, v[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const int64_t r = rb + 8 * i;
+      if (r >= rows) break;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const U k = Key<T>::of_val(v[j]);
+        const U k = Key<T>::of_val(v[i][j]);
         if (Key<T>::bad(k)) bad = min(bad, (unsigned long long)(r * C + c0 + j));
         else m[j] = k > m[j] ? k : m[j];
       }
@@ -208,6 +217,19 @@ __device__ __forceinline__ int level_f32(float mag, float s, float rs, int qmax)
   return min(l, qmax);
 }
 
+// Fast form: floor/fraction of the approximate quotient decide directly
+// unless the fraction is within 1e-3 of one half (the approximation error is
+// < 1e-4 for quotients up to 2^8), where the exact test above decides.
+__device__ __forceinline__ int level_f32_fast(float mag, float s, float rs, int qmax) {
+  const float r = mag * rs;
+  const float fl = floorf(r);
+  const float t = r - fl;
+  int l;
+  if (fabsf(t - 0.5f) > 1e-3f) l = (int)fl + (t > 0.5f ? 1 : 0);
+  else l = level_f32(mag, s, rs, qmax);
+  return min(l, qmax);
+}
+
 __device__ __forceinline__ float rcp_approx(float s) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s));
@@ -228,7 +250,7 @@ __device__ __forceinline__ uint32_t ci_code(const T* x, int64_t i, uint16_t sb, 
   } else {
     const float v = InTraits<T>::to_f32(x[i]);
     const float sf = __half2float(__ushort_as_half(sb));
-    l = level_f32(fabsf(v), sf, rcp_approx(sf), qmax);
+    l = level_f32_fast(fabsf(v), sf, rcp_approx(sf), qmax);
     neg = v < 0.f && l > 0;
   }
   return (uint32_t)l | (neg ? (1u << (bits - 1)) : 0u);
@@ -286,6 +308,51 @@ __global__ void __launch_bounds__(kT) k_ci_quant_v(const T* __restrict__ x, int6
   } else {
 #pragma unroll
     for (int b = 0; b < BITS; ++b) p[b] = (uint8_t)(w >> (8 * b));
+  }
+}
+
+// C % 8 == 0, f32 / bf16 output: level * scale is exact in f32 (a 7-bit
+// level times an f16 scale), so the float64 product of the reference rounds
+// to the same f32 / bf16; vector loads of codes and scales, one 16/32-byte
+// store per 8 values.
+template <typename OutT, int BITS>
+__global__ void __launch_bounds__(kT) k_ci_dequant_v(const uint8_t* __restrict__ codes,
+                                                    const uint16_t* __restrict__ scales,
+                                                    int64_t n, int64_t C, OutT* __restrict__ out) {
+  const int64_t g = blockIdx.x * (int64_t)kT + threadIdx.x;
+  const int64_t i0 = g * 8;
+  if (i0 >= n) return;
+  const uint8_t* p = codes + g * BITS;
+  unsigned long long w = 0;
+  if constexpr (BITS == 4) w = *reinterpret_cast<const uint32_t*>(p);
+  else if constexpr (BITS == 8) w = *reinterpret_cast<const unsigned long long*>(p);
+  else if constexpr (BITS == 2) w = *reinterpret_cast<const uint16_t*>(p);
+  else {
+#pragma unroll
+    for (int b = 0; b < BITS; ++b) w |= (unsigned long long)p[b] << (8 * b);
+  }
+  const int64_t c0 = (n < 0x100000000ll) ? (int64_t)((uint32_t)i0 % (uint32_t)C) : i0 % C;
+  const uint4 sw = __ldg(reinterpret_cast<const uint4*>(scales + c0));
+  const uint32_t sv[4] = {sw.x, sw.y, sw.z, sw.w};
+  constexpr uint32_t MM = (1u << (BITS - 1)) - 1u;
+  float v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t code = (uint32_t)(w >> (j * BITS)) & ((1u << BITS) - 1u);
+    const float sc = __half2float(__ushort_as_half((uint16_t)(sv[j >> 1] >> (16 * (j & 1)))));
+    const float lev = (float)(code & MM);
+    v[j] = ((code >> (BITS - 1)) ? -lev : lev) * sc;  // exact (or inf/nan, like numpy)
+  }
+  if constexpr (std::is_same<OutT, float>::value) {
+    reinterpret_cast<float4*>(out + i0)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(out + i0)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  } else {
+    uint4 o;
+    o.x = pack2<__nv_bfloat16>(v[0], v[1]);
+    o.y = pack2<__nv_bfloat16>(v[2], v[3]);
+    o.z = pack2<__nv_bfloat16>(v[4], v[5]);
+    o.w = pack2<__nv_bfloat16>(v[6], v[7]);
+    *reinterpret_cast<uint4*>(out + i0) = o;
   }
 }
 
@@ -619,8 +686,23 @@ template <typename OutT>
 void ci_decompress(const uint16_t* scales, const uint8_t* codes, int64_t n, int64_t C, int bits,
                    void* out, cudaStream_t st) {
   const int64_t groups = (n + 7) / 8;
-  k_ci_dequant<OutT><<<(unsigned)((groups + kT - 1) / kT), kT, 0, st>>>(
-      codes, scales, n, C, bits, reinterpret_cast<OutT*>(out));
+  const unsigned gg = (unsigned)((groups + kT - 1) / kT);
+  if constexpr (!std::is_same<OutT, double>::value) {
+    if (C % 8 == 0 && ((uintptr_t)scales % 16) == 0 && ((uintptr_t)out % 32) == 0 &&
+        ((uintptr_t)codes % 8) == 0) {
+      OutT* o = reinterpret_cast<OutT*>(out);
+      switch (bits) {
+        case 2: k_ci_dequant_v<OutT, 2><<<gg, kT, 0, st>>>(codes, scales, n, C, o); return;
+        case 3: k_ci_dequant_v<OutT, 3><<<gg, kT, 0, st>>>(codes, scales, n, C, o); return;
+        case 4: k_ci_dequant_v<OutT, 4><<<gg, kT, 0, st>>>(codes, scales, n, C, o); return;
+        case 5: k_ci_dequant_v<OutT, 5><<<gg, kT, 0, st>>>(codes, scales, n, C, o); return;
+        case 6: k_ci_dequant_v<OutT, 6><<<gg, kT, 0, st>>>(codes, scales, n, C, o); return;
+        case 7: k_ci_dequant_v<OutT, 7><<<gg, kT, 0, st>>>(codes, scales, n, C, o); return;
+        default: k_ci_dequant_v<OutT, 8><<<gg, kT, 0, st>>>(codes, scales, n, C, o); return;
+      }
+    }
+  }
+  k_ci_dequant<OutT><<<gg, kT, 0, st>>>(codes, scales, n, C, bits, reinterpret_cast<OutT*>(out));
 }
 
 inline int64_t tk_blocks(int64_t n) { return (n + kTile - 1) / kTile; }

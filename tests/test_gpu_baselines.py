@@ -153,3 +153,20 @@ def test_tpsim_baseline_codecs(gold):
         assert float(rep.sqnr_db).hex() == g["sqnr_db"], g["scheme"]
         assert (rep.bytes_compressed, rep.bytes_uncompressed, rep.padding) == (
             g["bytes_compressed"], g["bytes_uncompressed"], g["padding"])
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4, 5, 8])
+def test_chanint_decompress_f32_bf16_vector_path(bl, bits):
+    """f32 / bf16 outputs (vectorised decoder) equal the float64 decode
+    rounded once (level * scale is exact in f32)."""
+    rng = np.random.default_rng(40 + bits)
+    x = rng.standard_normal((96, 256)) * 10.0 ** rng.uniform(-2, 2, size=256)
+    x[:, 7] = 0.0
+    s, c, shape = bl.channelwise_int_compress_device(torch.from_numpy(x).to("cuda", torch.float32),
+                                                     bits)
+    d64 = bl.channelwise_int_decompress_device(s, c, shape, bits, torch.float64).cpu().numpy()
+    for dt in (torch.float32, torch.bfloat16):
+        got = bl.channelwise_int_decompress_device(s, c, shape, bits, dt).cpu()
+        want = torch.from_numpy(d64).to(dt)
+        assert torch.equal(got.view(torch.int16 if dt == torch.bfloat16 else torch.int32),
+                           want.view(torch.int16 if dt == torch.bfloat16 else torch.int32)), (bits, dt)

@@ -707,6 +707,91 @@ void ci_decompress(const uint16_t* scales, const uint8_t* codes, int64_t n, int6
 
 inline int64_t tk_blocks(int64_t n) { return (n + kTile - 1) / kTile; }
 
+// 16-bit inputs (bf16 / f16): the 15-bit magnitude IS an order-preserving
+// key, so one pass builds the full 32768-bin histogram (per-block bins in
+// shared memory, non-zero bins flushed to global) and one block picks the
+// threshold -- instead of two 8-bit radix passes over the data.
+constexpr int kBins16 = 32768;
+
+template <typename T>
+__global__ void __launch_bounds__(1024) k_tk_hist16(const T* __restrict__ x, int64_t n, int vec,
+                                                   unsigned int* __restrict__ ghist,
+                                                   unsigned long long* nonfinite) {
+  extern __shared__ unsigned int h16[];
+  for (int i = threadIdx.x; i < kBins16; i += 1024) h16[i] = 0;
+  __syncthreads();
+  const uint32_t bad_key = std::is_same<T, __half>::value ? 0x7c00u : 0x7f80u;
+  const int64_t stride = (int64_t)gridDim.x * 1024 * 8;
+  for (int64_t i0 = ((int64_t)blockIdx.x * 1024 + threadIdx.x) * 8; i0 < n; i0 += stride) {
+    T v[8];
+    if (vec && i0 + 8 <= n) {
+      ldv<T, 8>(x + i0, v);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = i0 + j < n ? x[i0 + j] : T(0);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (i0 + j >= n) break;
+      const uint32_t k = (uint32_t)(*reinterpret_cast<const uint16_t*>(&v[j])) & 0x7fffu;
+      if (k >= bad_key && nonfinite) atomicMin(nonfinite, (unsigned long long)(i0 + j));
+      atomicAdd(&h16[k], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBins16; i += 1024)
+    if (h16[i]) atomicAdd(&ghist[i], h16[i]);
+}
+
+// one block: thread t owns bins 32767-32t .. 32736-32t (descending); a block
+// scan of the thread sums finds the threshold bin; writes the f32-domain
+// key of that bin and the number of equal keys to keep into *sel
+template <typename T>
+__global__ void __launch_bounds__(1024) k_tk_select16(const unsigned int* __restrict__ ghist,
+                                                     Sel<uint32_t>* sel) {
+  extern __shared__ unsigned int hs[];  // the histogram, loaded coalesced
+  __shared__ unsigned long long wsum[32];
+  __shared__ unsigned long long s_take;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  for (int i = t; i < kBins16 / 4; i += 1024)
+    reinterpret_cast<uint4*>(hs)[i] = reinterpret_cast<const uint4*>(ghist)[i];
+  __syncthreads();
+  unsigned long long tot = 0;
+#pragma unroll 8
+  for (int i = 0; i < 32; ++i) tot += hs[kBins16 - 1 - 32 * t - ((i + lane) & 31)];
+  unsigned long long incl = tot;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[w] = incl;
+  if (t == 0) s_take = sel->take;
+  __syncthreads();
+  unsigned long long before = 0;
+  for (int j = 0; j < w; ++j) before += wsum[j];
+  const unsigned long long take = s_take;
+  const unsigned long long excl = before + incl - tot;
+  if (excl < take && excl + tot >= take) {  // exactly one thread
+    unsigned long long above = excl;
+    int b = kBins16 - 1 - 32 * t;
+    for (int i = 0; i < 32; ++i, --b) {
+      const unsigned int c = hs[b];
+      if (above + c >= take || b == 0) break;
+      above += c;
+    }
+    uint32_t key32;
+    if constexpr (std::is_same<T, __half>::value)
+      key32 = __float_as_uint(__half2float(__ushort_as_half((unsigned short)b)));
+    else
+      key32 = (uint32_t)b << 16;
+    sel->prefix = key32;
+    sel->mask = 0xffffffffu;
+    sel->take = take - above;
+  }
+}
+
+
+
 template <typename T>
 void tk_compress(const T* x, int64_t n, int64_t k, uint32_t* idx, uint16_t* val, void* ws,
                  unsigned long long* nf, int low_shift, cudaStream_t st) {
@@ -724,6 +809,27 @@ void tk_compress(const T* x, int64_t n, int64_t k, uint32_t* idx, uint16_t* val,
   }
   const unsigned hg = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>((int64_t)sms * 8, (n + kT * 8 - 1) / (kT * 8)));
+  if constexpr (sizeof(T) == 2) {
+    unsigned int* gh = reinterpret_cast<unsigned int*>(
+        reinterpret_cast<uint8_t*>(cnt) + ((16 * tk_blocks(n) + 255) / 256) * 256);
+    cudaMemsetAsync(gh, 0, kBins16 * sizeof(unsigned int), st);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_tk_hist16<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kBins16 * 4);
+      attr = true;
+    }
+    const unsigned g16 = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)sms, (n + 8191) / 8192));
+    k_tk_hist16<T><<<g16, 1024, kBins16 * 4, st>>>(x, n, vec, gh, nf);
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(k_tk_select16<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kBins16 * 4);
+      attr2 = true;
+    }
+    k_tk_select16<T><<<1, 1024, kBins16 * 4, st>>>(gh, reinterpret_cast<Sel<uint32_t>*>(sel));
+  } else
   for (int shift = (int)(8 * sizeof(U)) - 8; shift >= low_shift; shift -= 8) {
     const bool top = shift == (int)(8 * sizeof(U)) - 8;
     k_tk_hist<T><<<hg, kT, 0, st>>>(x, n, sel, shift, top ? nf : nullptr, vec, top ? 1 : 0);
@@ -740,7 +846,7 @@ void tk_compress(const T* x, int64_t n, int64_t k, uint32_t* idx, uint16_t* val,
 // dtype codes as in mxb200.h
 int64_t topk_workspace_bytes(int64_t n) {
   return ((int64_t)sizeof(bl::Sel<unsigned long long>) + 255) / 256 * 256 +
-         16 * bl::tk_blocks(n) + 256;
+         (16 * bl::tk_blocks(n) + 255) / 256 * 256 + 4 * bl::kBins16 + 256;
 }
 
 void launch_chanint_compress(const void* x, int dtype, int64_t rows, int64_t C, int bits,

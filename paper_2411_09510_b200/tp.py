@@ -539,8 +539,11 @@ def make_module_classes():
 
 
 def measure_ttft(cfg: LlamaConfig, batch: int, seq: int, tp: int = 1, group=None, scheme=None,
-                 algo="oneshot", layers=None, reps: int = 5, warmup: int = 2, seed: int = 0):
-    """Prefill latency (ms, max over ranks) of the TP body on random data."""
+                 algo="oneshot", layers=None, reps: int = 5, warmup: int = 2, seed: int = 0,
+                 graph: bool = False):
+    """Prefill latency (ms, max over ranks) of the TP body on random data.
+    ``graph`` replays the whole forward as one captured CUDA graph (how a
+    serving engine runs it: no per-kernel host launch cost)."""
     torch = _torch()
     import torch.distributed as dist
 
@@ -552,13 +555,25 @@ def measure_ttft(cfg: LlamaConfig, batch: int, seq: int, tp: int = 1, group=None
         for _ in range(warmup):
             model(h)
         torch.cuda.synchronize()
+        run = lambda: model(h)  # noqa: E731
+        if graph:
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                model(h)
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g):
+                model(h)
+            run = g.replay
         if dist.is_initialized():
             dist.barrier(group)
         times = []
         for _ in range(reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            model(h)
+            run()
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--layers", type=int, default=None, help="truncate the stack (memory)")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--schemes", default="none,fp4_e2m1:32:e8m0")
+    ap.add_argument("--graph", action="store_true", help="replay the forward as one CUDA graph")
     ap.add_argument("--algos", default="oneshot,twoshot",
                     help="oneshot,twoshot (NCCL), symm,symm2 (one-kernel NVLink), auto")
     args = ap.parse_args()
@@ -44,7 +45,7 @@ def main():
         for algo in (["oneshot"] if spec == "none" else args.algos.split(",")):
             scheme = None if spec == "none" else spec
             ms = tp.measure_ttft(cfg, args.batch, args.seq, tp=world, scheme=scheme, algo=algo,
-                                 layers=args.layers, reps=args.reps)
+                                 layers=args.layers, reps=args.reps, graph=args.graph)
             if scheme is None:
                 base = ms
             if rank == 0:
@@ -52,7 +53,7 @@ def main():
                                   "batch": args.batch, "seq": args.seq,
                                   "layers": args.layers or cfg.layers,
                                   "allreduce": "bf16 NCCL" if scheme is None else f"{spec} {algo}",
-                                  "ttft_ms": round(ms, 3),
+                                  "ttft_ms": round(ms, 3), "cuda_graph": args.graph,
                                   "speedup_vs_bf16": None if base is None else round(base / ms, 3)}),
                       flush=True)
             torch.cuda.empty_cache()

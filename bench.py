@@ -497,6 +497,33 @@ def run_ours(args, shape, rank, world, local_rank):
                 "share_of_step": round(nranks * kq["us"] / (ms_step * 1e3), 3),
                 "other_kernels": {k: v for k, v in kernels.items() if k != "k_quant"}}
 
+    # ---- simulated TP=4 and TP=8 on this GPU (N=1): the fused one-kernel
+    # step with 4 / 8 rank partials (inputs rotated > 3x L2), informational
+    sim_more = None
+    if sim and args.algo == "oneshot" and args.sim_ranks == 2:
+        sim_more = {}
+        try:
+            for N_ in (4, 8):
+                per = N_ * 2 * n + N_ * S + 2 * n
+                R_ = max(2, -(-3 * L2_BYTES // per))
+                ps = [[(base[r % len(base)].roll(7 * (i + r), 0) * (-1) ** (i + r)).contiguous()
+                       for r in range(N_)] for i in range(R_)]
+                ops = [SimulatedAllReduce(sch, n, N_, "oneshot", torch.bfloat16, dev)
+                       for _ in range(R_)]
+                g = capture(torch, lambda: [op(pp) for op, pp in zip(ops, ps)])
+                for _ in range(3):
+                    g.replay()
+                reps = max(3, min(50, args.steps // 40))
+                ms = time_graph_replays(torch, [g], reps) / (reps * R_)
+                sim_more[f"tp{N_}"] = {"us": round(ms * 1e3, 3),
+                                       "value": round(N_ * 2 * n / (ms * 1e-3) / 1e9, 1),
+                                       "unit": UNIT,
+                                       "hbm_gbs": round(per / (ms * 1e-3) / 1e9, 1)}
+                del ps, ops, g
+                torch.cuda.empty_cache()
+        except Exception as exc:  # noqa: BLE001  (informational only)
+            sim_more = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
     # ---- end to end through the public API with pinned host buffers:
     # HostPipeline (chunked H2D -> compressed all-reduce -> D2H on three
     # streams), the host-array-in / host-array-out shape of the reference API
@@ -651,7 +678,7 @@ def run_ours(args, shape, rank, world, local_rank):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
             "bf16_nccl_allreduce": bf16_ar, "symmetric_memory_fused": symm,
-            "collective": coll}
+            "collective": coll, "simulated_tp_fused_step": sim_more}
     print(json.dumps(line), flush=True)
 
 

@@ -105,8 +105,11 @@ __device__ __forceinline__ void ldg256(const void* p, uint32_t* r) {
                  "=r"(r[6]), "=r"(r[7])
                : "l"(p));
 }
+#ifndef MXB_STG_HINT
+#define MXB_STG_HINT ""
+#endif
 __device__ __forceinline__ void stg256(void* p, const uint32_t* r) {
-  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]),
+  asm volatile("st.global" MXB_STG_HINT ".v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]),
                "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                : "memory");
 }

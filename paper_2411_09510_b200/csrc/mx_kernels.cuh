@@ -260,7 +260,9 @@ struct LaneCodes {
   uint32_t w[NW];
 };
 
-// Put group g (values 8g..8g+7; 8b bits = b bytes) into the lane words.
+// Put group g (values 8g..8g+7; 8b bits at bit offset 8bg) into the lane
+// words.  g and BITS are compile-time after unrolling, so the word index and
+// the funnel shifts fold to constants (2-3 shifts per group for odd widths).
 template <int BITS, int VPL = kVPL>
 __device__ __forceinline__ void put_group(LaneCodes<BITS, VPL>& c, int g, uint64_t v) {
   if constexpr (BITS == 4) {
@@ -269,11 +271,10 @@ __device__ __forceinline__ void put_group(LaneCodes<BITS, VPL>& c, int g, uint64
     c.w[2 * g] = (uint32_t)v;
     c.w[2 * g + 1] = (uint32_t)(v >> 32);
   } else {
-#pragma unroll
-    for (int t = 0; t < BITS; ++t) {
-      const int byte = g * BITS + t;  // compile-time after unrolling
-      c.w[byte >> 2] |= (uint32_t)((v >> (8 * t)) & 0xffu) << (8 * (byte & 3));
-    }
+    const int o = g * 8 * BITS, wi = o >> 5, sh = o & 31;
+    c.w[wi] |= (uint32_t)(v << sh);
+    if (sh + 8 * BITS > 32) c.w[wi + 1] |= (uint32_t)(v >> (32 - sh));
+    if (sh + 8 * BITS > 64) c.w[wi + 2] |= (uint32_t)(v >> (64 - sh));
   }
 }
 
@@ -284,13 +285,11 @@ __device__ __forceinline__ uint64_t get_group(const LaneCodes<BITS, VPL>& c, int
   } else if constexpr (BITS == 8) {
     return (uint64_t)c.w[2 * g] | ((uint64_t)c.w[2 * g + 1] << 32);
   } else {
-    uint64_t v = 0;
-#pragma unroll
-    for (int t = 0; t < BITS; ++t) {
-      const int byte = g * BITS + t;
-      v |= (uint64_t)((c.w[byte >> 2] >> (8 * (byte & 3))) & 0xffu) << (8 * t);
-    }
-    return v;
+    const int o = g * 8 * BITS, wi = o >> 5, sh = o & 31;
+    uint64_t v = (uint64_t)c.w[wi] >> sh;
+    if (sh + 8 * BITS > 32) v |= (uint64_t)c.w[wi + 1] << (32 - sh);
+    if (sh + 8 * BITS > 64) v |= (uint64_t)c.w[wi + 2] << (64 - sh);
+    return v & ((1ull << (8 * BITS)) - 1ull);
   }
 }
 

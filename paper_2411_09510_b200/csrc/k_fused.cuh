@@ -337,6 +337,9 @@ __device__ __forceinline__ void k_fused_flow_body(const FArgs& F) {
 
 template <typename OutT, int B, int ENC, int BITS, int TH = kThreads>
 __global__ void __launch_bounds__(TH, (ENC == ENC_E2M1 && B == 64) ? 1024 / TH : 0) k_fused_flow(const FArgs F) {
+  // programmatic dependent launch: the producer grid (e.g. the o_proj GEMM
+  // writing the partials) completes and flushes before any partial is read
+  pdl_prologue();
   k_fused_flow_body<OutT, B, ENC, BITS, TH>(F);
 }
 
@@ -624,8 +627,9 @@ void go(const FArgs& a, cudaStream_t st) {
     // dataflow kernel: one warp per unit, no grid barrier
     constexpr int UPW = flow_units_per_warp(B, ENC);
     const int64_t units = a.n / kUnit;
-    k_fused_flow<OutT, B, ENC, BITS>
-        <<<(unsigned)((units + kWarps * UPW - 1) / (kWarps * UPW)), kThreads, 0, st>>>(a);
+    launch_pdl(k_fused_flow<OutT, B, ENC, BITS>,
+               dim3((unsigned)((units + kWarps * UPW - 1) / (kWarps * UPW))), dim3(kThreads), 0,
+               st, a);
     return;
   }
   auto k = k_fused_oneshot<InT, OutT, B, ENC, BITS>;

@@ -96,6 +96,31 @@ struct Geo {
   static constexpr int SBV = VPL / NSB;               // values per owned block
 };
 
+// Programmatic dependent launch: a kernel launched with launch_pdl may be
+// scheduled while its predecessor on the stream drains; pdl_prologue() waits
+// for that predecessor to complete (memory flushed) before any input is read
+// and releases this kernel's own dependents.  No-ops without the attribute.
+__device__ __forceinline__ void pdl_prologue() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 // ---------------------------------------------------------------------------
 // 256-bit global accesses (sm_100)
 // ---------------------------------------------------------------------------
@@ -601,6 +626,7 @@ __device__ __forceinline__ void quant_full_unit(const QArgs& A, const Fmt& f, ui
 template <typename InT, int B_, int ENC, int BITS>
 __global__ void __launch_bounds__(kThreads) k_quant(const QArgs A) {
   constexpr int B = B_;
+  pdl_prologue();
   __shared__ __align__(16) uint8_t s_stage[kWarps][kUnit / 8];  // one byte per block (B >= 8)
   const Fmt f = A.f;
   const int lane = threadIdx.x & 31;
@@ -1029,6 +1055,7 @@ __global__ void __launch_bounds__(kThreads) k_dqsum(const DArgs A) {
 template <typename OutT, int B, int DEC, int BITS>
 __global__ void __launch_bounds__(kThreads) k_dqsum_lean(const DArgs A) {
   using RL = RankLoad<B, BITS, kVPL>;
+  pdl_prologue();
   __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
   const Fmt f = A.f;
   if constexpr (DEC != ENC_E2M1) {
@@ -1070,6 +1097,7 @@ __global__ void __launch_bounds__(kThreads) k_dqsum_lean(const DArgs A) {
 template <int B, int ENC, int BITS>
 __global__ void __launch_bounds__(kThreads) k_requant(const RArgs A) {
   constexpr int DEC = dec_of(ENC, BITS);
+  pdl_prologue();
   __shared__ __align__(16) uint8_t s_stage[kWarps][kUnit / 8];  // one byte per block (B >= 8)
   __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
   const Fmt f = A.f;

@@ -471,9 +471,11 @@ class HostPipeline:
     ``decompress_tensor`` mx/codec.py:266, the exchange of
     mx/netbench.py:323-334).
 
-    The flat tensor is cut into ``chunks`` equal pieces whose length is a
-    multiple of 1024 values, so no MX block straddles a piece and every
-    value's reduction is identical to the whole-tensor call.  Piece j's
+    The flat tensor is cut into pieces whose lengths are multiples of 1024
+    values (``chunks`` equal pieces, or a tuple of piece weights such as
+    ``(1, 3, 3, 1)`` whose small head and tail pieces shorten the parts of
+    the transfer that cannot overlap), so no MX block straddles a piece and
+    every value's reduction is identical to the whole-tensor call.  Piece j's
     pinned host->device copies, its compressed all-reduce (one persistent
     op per piece, so its device pointers stay fixed) and its device->host
     copy are issued on three streams ordered by events: the PCIe traffic in

@@ -17,7 +17,6 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-from paper_2411_09510_b200 import _native  # noqa: E402
 from paper_2411_09510_b200.collective import NativeBackend  # noqa: E402
 from paper_2411_09510_b200.formats import parse_scheme  # noqa: E402
 

@@ -1,4 +1,4 @@
-"""Multi-process (gloo, world_size 2 and 3) test of the collective's
+"""Multi-process (gloo, world_size 2, 3 and 4) test of the collective's
 orchestration on CPU: shard layout, chunking, all_to_all / all_gather order
 and the rank-order reduction, with the oracle standing in for the kernels."""
 
@@ -56,7 +56,7 @@ def _worker(rank, world, port, specs, n, q):
         q.put((rank, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_collective_orchestration_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

@@ -370,13 +370,24 @@ def run_ours(args, shape, rank, world, local_rank):
     else:  # two-shot: K1 x ranks, K3 x owned chunks, K2
         launches_per_step = (nranks if sim else 1) + (nranks if sim else 1) + 1
 
-    # warm-up (>= W replays and >= 0.3 s so clocks settle), timed region
+    # warm-up (>= W replays and >= 0.3 s so clocks settle), timed region.
+    # The replay count is agreed across ranks (each replay may hold NCCL
+    # collectives, so every rank must run exactly as many).
     with ClockSampler(local_rank) as clk:
         t = time.perf_counter()
-        i = 0
-        while i < args.warmup or time.perf_counter() - t < 0.3:
+        for i in range(args.warmup):
             graphs[i % R].replay()
-            i += 1
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t
+        extra = 0
+        if el < 0.3:
+            extra = int(min(1e6, (0.3 - el) / max(el / max(1, args.warmup), 1e-6))) + 1
+        if world > 1:
+            te = torch.tensor([extra], device=dev, dtype=torch.int64)
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            extra = int(te.item())
+        for i in range(extra):
+            graphs[i % R].replay()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()

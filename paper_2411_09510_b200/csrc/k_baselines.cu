@@ -611,26 +611,35 @@ __global__ void __launch_bounds__(kT) k_tk_write(const T* __restrict__ x, int64_
   __syncthreads();
   uint32_t wg = 0, we = 0;
   for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) { wg += sg[w]; we += se[w]; }
-  unsigned long long pg = cnt[2 * blockIdx.x] + wg + ig - gt;
-  unsigned long long pe = cnt[2 * blockIdx.x + 1] + we + ie - eq;
+  // block-local (32-bit) positions: the block's kept entries form one
+  // contiguous output range starting at base; equal keys are kept while
+  // fewer than `rem` equal keys of earlier blocks and threads precede them
+  const unsigned long long e0 = cnt[2 * blockIdx.x + 1];
+  const unsigned long long base = cnt[2 * blockIdx.x] + (e0 < take ? e0 : take);
+  const uint32_t rem = e0 < take ? (uint32_t)min(take - e0, 0x7fffffffull) : 0u;
+  uint32_t lg = wg + ig - gt, le = we + ie - eq;
+  __shared__ uint32_t s_idx[kTile];
+  __shared__ uint16_t s_val[kTile];
+  __shared__ uint32_t s_cnt;
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
-    const int64_t i = i0 + j;
     if (j >= m) break;
     const U k = Key<T>::of_val(v[j]);
-    bool keep = false;
-    if (k > t) {
-      keep = true;
-    } else if (k == t) {
-      keep = pe < take;
+    const bool g1 = k > t, e1 = k == t;
+    if (g1 || (e1 && le < rem)) {
+      const uint32_t pos = lg + min(le, rem);
+      s_idx[pos] = (uint32_t)(i0 + j);
+      s_val[pos] = to_f16_bits<T>(v[j]);
     }
-    if (keep) {
-      const unsigned long long pos = pg + (pe < take ? pe : take);
-      idx[pos] = (uint32_t)i;
-      val[pos] = to_f16_bits<T>(v[j]);
-    }
-    pg += k > t;
-    pe += k == t;
+    lg += g1;
+    le += e1;
+  }
+  if (threadIdx.x == kT - 1) s_cnt = lg + min(le, rem);  // the block's kept count
+  __syncthreads();
+  const uint32_t cntb = s_cnt;
+  for (uint32_t q = threadIdx.x; q < cntb; q += kT) {
+    idx[base + q] = s_idx[q];
+    val[base + q] = s_val[q];
   }
 }
 

@@ -333,7 +333,9 @@ def twoshot_chunks(n: int, nranks: int, block: int, align: int = 8):
 
 def allreduce_twoshot(partials, sch: OScheme, chunk_align: int = 8) -> np.ndarray:
     """Reduce-scatter of quantised chunks, fp32 rank-order sum per chunk,
-    requantise the sum, all-gather, decode (restatement; not in the reference)."""
+    requantise the sum, all-gather, decode (restatement; not in the reference).
+    Like every one-shot output value, the decoded value is accumulated into a
+    +0.0 float32 accumulator (mx/netbench.py:332), so a -0 code yields +0."""
     flats = [np.asarray(p, dtype=np.float64).ravel() for p in partials]
     n = flats[0].size
     out = np.zeros(n, dtype=np.float32)
@@ -343,7 +345,7 @@ def allreduce_twoshot(partials, sch: OScheme, chunk_align: int = 8) -> np.ndarra
         acc = np.zeros(hi - lo, dtype=np.float32)
         for f in flats:
             acc += roundtrip_f32(f[lo:hi], sch)
-        out[lo:hi] = roundtrip_f32(acc, sch)
+        out[lo:hi] = np.float32(0.0) + roundtrip_f32(acc, sch)
     return out
 
 

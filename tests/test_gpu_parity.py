@@ -318,3 +318,26 @@ print("tma ok")
     p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                        text=True, timeout=300)
     assert p.returncode == 0 and "tma ok" in p.stdout, p.stderr[-2000:]
+
+
+@pytest.mark.parametrize("spec", ["fp4_e2m1:32:e8m0", "fp3_e1m1:32:e8m0", "int5:16:e8m0",
+                                  "fp6_e3m2:64:e8m0"])
+@pytest.mark.parametrize("n", [1024, 4096, 5 * 1024, 12288])
+@pytest.mark.parametrize("fused", [True, False])
+def test_unit_counts_not_multiple_of_cta(mx, spec, n, fused):
+    """Sizes whose 1024-value unit count is not a multiple of the 8 warps of
+    a CTA (the lean kernels' grid must round up); bit-level comparison,
+    including the sign of zero, one-shot and two-shot."""
+    from paper_2411_09510_b200.collective import SimulatedAllReduce
+
+    for N, algo in ((2, "oneshot"), (3, "oneshot"), (2, "twoshot"), (4, "twoshot")):
+        x64 = [inputs.gauss_bf16(n, 7100 + N + r) for r in range(N)]
+        for x in x64:
+            x[::97] = 0.0
+        parts = [dev(x, "bf16") for x in x64]
+        op = SimulatedAllReduce(spec, n, N, algo, torch.float32,
+                                fused=fused and algo == "oneshot")
+        got = op(parts).cpu().numpy()
+        ref = (O.allreduce_oneshot if algo == "oneshot" else O.allreduce_twoshot)(
+            x64, O.scheme(spec))
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), (spec, n, N, algo)

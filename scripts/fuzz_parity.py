@@ -17,7 +17,10 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from oracle import mx_oracle as O  # noqa: E402
-from paper_2411_09510_b200 import compress_tensor_device, parse_scheme  # noqa: E402
+from oracle import baselines_oracle as BO  # noqa: E402
+from paper_2411_09510_b200 import baselines as BL  # noqa: E402
+from paper_2411_09510_b200 import (compress_tensor_device, decompress_tensor_device,  # noqa: E402
+                                   parse_scheme)
 from paper_2411_09510_b200.collective import SimulatedAllReduce  # noqa: E402
 from paper_2411_09510_b200.synth import bf16_round  # noqa: E402
 
@@ -62,12 +65,22 @@ def main():
         parts = [torch.from_numpy(x).to("cuda", torch.bfloat16) for x in x64]
         osch = O.scheme(spec)
         try:
-            # codec streams of rank 0
-            d = compress_tensor_device(parts[0], parse_scheme(spec, extensions=True),
+            # codec streams of rank 0, fed as bf16 / f16 / f32 (values are
+            # bf16-exact, so all three must give the same streams)
+            in_dt = [torch.bfloat16, torch.float16, torch.float32][int(rng.integers(0, 3))]
+            xin = torch.from_numpy(x64[0]).to("cuda", in_dt)
+            x0 = xin.double().cpu().numpy()  # f16 may round/overflow: the fed values
+            d = compress_tensor_device(xin, parse_scheme(spec, extensions=True),
                                        check_finite=False)
-            ss, es = O.compress(x64[0], osch)
-            ok = (d.scale.cpu().numpy().tobytes() == ss and d.elements.cpu().numpy().tobytes() == es)
+            ss, es = O.compress(x0, osch) if np.isfinite(x0).all() else (None, None)
+            ok = ss is None or (d.scale.cpu().numpy().tobytes() == ss and
+                                d.elements.cpu().numpy().tobytes() == es)
             stage = "codec" if not ok else None
+            if ok and ss is not None:  # plain decode (decompress_tensor) to f32
+                dec = decompress_tensor_device(d, torch.float32).cpu().numpy().ravel()
+                ref_dec = O.decompress(ss, es, n, osch, np.float32)
+                if not np.array_equal(dec.view(np.uint32), np.asarray(ref_dec, np.float32).view(np.uint32)):
+                    ok, stage = False, "decompress"
             # the all-reduce (fused where eligible)
             op = SimulatedAllReduce(spec, n, N, algo, out_dt)
             got = op(parts).float().cpu().numpy()
@@ -82,6 +95,27 @@ def main():
         except Exception as exc:  # noqa: BLE001
             ok = False
             spec += f" EXC {type(exc).__name__}: {exc}"[:200]
+        # comparison codecs on a 2-D view of rank 0's partial
+        if ok and rng.random() < 0.3:
+            try:
+                C = min(n, int(rng.choice([8, 16, 24, 40, 64, 128, 1000])))
+                rows = max(1, n // C)
+                xm = x64[0][: rows * C].reshape(rows, C)
+                dt = [torch.bfloat16, torch.float32][int(rng.integers(0, 2))]
+                xt = torch.from_numpy(xm).to("cuda", dt)
+                xv = xt.double().cpu().numpy()
+                bits = int(rng.integers(2, 9))
+                p = BL.channelwise_int_compress(xt, bits)
+                s16, _, stream = BO.chanint_compress(xv, bits)
+                k = int(rng.integers(1, xv.size + 1))
+                q = BL.topk_compress(xt, k=k)
+                ri, rv = BO.topk_compress(xv, k=k)
+                if not (p.code_stream == stream and np.array_equal(p.scales.view(np.uint16), s16.view(np.uint16))):
+                    ok, stage = False, f"chanint bits={bits} C={C}"
+                elif not (np.array_equal(q.indices, ri) and np.array_equal(q.values.view(np.uint16), rv.view(np.uint16))):
+                    ok, stage = False, f"topk k={k}"
+            except Exception as exc:  # noqa: BLE001
+                ok, stage = False, f"baselines EXC {type(exc).__name__}: {exc}"[:200]
         cases += 1
         if not ok:
             fails.append({"spec": spec, "n": n, "N": N, "algo": algo, "out": str(out_dt),

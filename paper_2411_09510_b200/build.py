@@ -54,7 +54,7 @@ def _digest(deps) -> str:
 
     h = hashlib.sha256(repr((ARCH, FLAGS, sorted(LINEINFO), VARIANTS)).encode())
     for d in sorted(deps):
-        h.update(d.encode())
+        h.update(os.path.relpath(d, ROOT).encode())  # checkout-independent
         with open(d, "rb") as f:
             h.update(f.read())
     return h.hexdigest()

@@ -381,18 +381,23 @@ __global__ void __launch_bounds__(kThreads) k_symm_flow(const SArgs S) {
   __shared__ unsigned int s_e;
   const Fmt f = S.f;
   if constexpr (DEC != ENC_E2M1) fill_lut(s_lut, f);
+  pdl_prologue();  // the previous call's epochs, flags and outputs are final
   const uint32_t b = blockIdx.x, G = gridDim.x;
   if (threadIdx.x == 0) s_e = S.epoch[b] + 1u;
   __syncthreads();
   const unsigned int e = s_e;
   const int lane = threadIdx.x & 31;
-  const uint32_t q = b * kWarps + (threadIdx.x >> 5);
-  const bool live = q < (uint32_t)(S.n / kUnit);
+  // CTA b owns unit rows b*U .. b*U+U-1 (kWarps units each): one flag
+  // exchange (one release fence) per U*kWarps units.
+  const uint32_t units = (uint32_t)(S.n / kUnit);
+  const uint32_t U = (units + G * kWarps - 1) / (G * kWarps);
   const int nr = S.nranks;
   const int64_t slot = (int64_t)(e & 1u) * S.slot_stride;
 
-  // ---- quantise my unit of the local partial into my shard slot ----------
-  if (live) {
+  // ---- quantise my units of the local partial into my shard slot ---------
+  for (uint32_t u = 0; u < U; ++u) {
+    const uint32_t q = (b * U + u) * kWarps + (threadIdx.x >> 5);
+    if (q >= units) break;
     Raw<InT> raw;
     load_raw<InT>(reinterpret_cast<const InT*>(S.x) + (size_t)q * kUnit + lane * kVPL, raw);
     int stored[NSB];
@@ -416,7 +421,10 @@ __global__ void __launch_bounds__(kThreads) k_symm_flow(const SArgs S) {
   // ---- publish to every peer, then wait for every peer's CTA b -----------
   if ((int)threadIdx.x < nr) {
     const int j = threadIdx.x;
-    __threadfence_system();  // this CTA's shard bytes before the flag leaves
+    // The release store is cumulative over the CTA's shard writes ordered
+    // before it by __syncthreads (the acquire side mirrors it), so no
+    // fence.sc.sys is needed; MXB200_SYMM_FENCE=1 adds one on both sides.
+    if (S.full_fence) __threadfence_system();
     st_release_sys(S.flags[j] + (size_t)S.rank * G + b, e);
     const unsigned int* mine = S.flags[S.rank] + (size_t)j * G + b;
     const long long t0 = clock64();
@@ -427,12 +435,14 @@ __global__ void __launch_bounds__(kThreads) k_symm_flow(const SArgs S) {
         break;
       }
     }
-    __threadfence_system();
+    if (S.full_fence) __threadfence_system();
   }
   __syncthreads();
 
-  // ---- pull-decode my unit of the N shards over NVLink, rank order -------
-  if (live) {
+  // ---- pull-decode my units of the N shards over NVLink, rank order ------
+  for (uint32_t u = 0; u < U; ++u) {
+    const uint32_t q = (b * U + u) * kWarps + (threadIdx.x >> 5);
+    if (q >= units) break;
     using RL = RankLoad<B, BITS, kVPL>;
     float acc[kVPL];
 #pragma unroll
@@ -482,6 +492,7 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
   __shared__ unsigned int s_e;
   const Fmt f = S.f;
   if constexpr (DEC != ENC_E2M1) fill_lut(s_lut, f);
+  pdl_prologue();  // the previous call's epochs, flags and outputs are final
   const uint32_t b = blockIdx.x, G = gridDim.x;
   if (threadIdx.x == 0) s_e = S.epoch[b] + 1u;
   __syncthreads();
@@ -509,7 +520,7 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
     __syncthreads();
     if ((int)threadIdx.x < nr) {
       const int j = threadIdx.x;
-      __threadfence_system();
+      if (S.full_fence) __threadfence_system();
       st_release_sys(S.flags[j] + ((size_t)which * nr + me) * G + b, e);
       const unsigned int* w = S.flags[me] + ((size_t)which * nr + j) * G + b;
       const long long t0 = clock64();
@@ -520,7 +531,7 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
           break;
         }
       }
-      __threadfence_system();
+      if (S.full_fence) __threadfence_system();
     }
     __syncthreads();
   };
@@ -598,7 +609,7 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
 template <typename OutT, int B, int ENC, int BITS>
 void go_symm2(const S2Args& a, cudaStream_t st) {
   const int64_t g = (a.c / kUnit + kWarps - 1) / kWarps;
-  k_symm2_flow<OutT, B, ENC, BITS><<<(unsigned)g, kThreads, 0, st>>>(a);
+  launch_pdl(k_symm2_flow<OutT, B, ENC, BITS>, dim3((unsigned)g), dim3(kThreads), 0, st, a);
 }
 
 template <typename OutT, int B>
@@ -618,7 +629,8 @@ bool symm2_by_enc(const S2Args& a, int enc, int bits, cudaStream_t st) {
 
 template <typename OutT, int B, int ENC, int BITS>
 void go_symm(const SArgs& a, cudaStream_t st) {
-  k_symm_flow<OutT, B, ENC, BITS><<<(unsigned)symm_ctas(a.n), kThreads, 0, st>>>(a);
+  launch_pdl(k_symm_flow<OutT, B, ENC, BITS>, dim3((unsigned)symm_ctas(a.n)), dim3(kThreads), 0, st,
+             a);
 }
 
 template <typename InT, typename OutT, int B, int ENC, int BITS>

@@ -286,6 +286,18 @@ bool use_tma() {
   return v == 1;
 }
 
+// MXB200_SYMM_FENCE=1 adds fence.sc.sys beside the release/acquire flag
+// operations of the NVLink kernels (k_fused.cuh); off by default -- the
+// release/acquire pair alone orders the shard bytes.
+int symm_full_fence() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MXB200_SYMM_FENCE");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v;
+}
+
 // block sizes with a fast (template) kernel
 bool fast_block(int64_t block) { return block == 8 || block == 16 || block == 32 || block == 64; }
 
@@ -632,6 +644,7 @@ int mx_allreduce_symm(const void* x, int32_t dtype, int64_t n, const mx_scheme_t
   a.rank = rank; a.nranks = nranks; a.slot_stride = slot_stride;
   a.scale_off = so; a.elem_off = eo; a.out = out; a.status = status;
   a.epoch = epochs; a.nonfinite = reinterpret_cast<unsigned long long*>(nonfinite); a.f = f;
+  a.full_fence = symm_full_fence();
   if (!launch_symm_oneshot(a, out_dtype == MX_BF16, (int)s->block_size, enc_of(s), f.bits,
                            (cudaStream_t)stream))
     return fail(MX_ERR_UNSUPPORTED, "symmetric path: scheme not instantiated");
@@ -683,6 +696,7 @@ int mx_allreduce_symm_twoshot(const void* x, int32_t dtype, int64_t n, const mx_
   a.rank = rank; a.nranks = nranks; a.slot_stride = slot; a.shard_stride = sc;
   a.scale_off = so; a.elem_off = eo; a.out = out; a.status = status; a.epoch = epochs;
   a.nonfinite = reinterpret_cast<unsigned long long*>(nonfinite); a.f = f;
+  a.full_fence = symm_full_fence();
   if (!launch_symm_twoshot(a, out_dtype == MX_BF16, (int)s->block_size, enc_of(s), f.bits,
                            (cudaStream_t)stream))
     return fail(MX_ERR_UNSUPPORTED, "two-shot symmetric path: scheme not instantiated");

@@ -1181,6 +1181,7 @@ struct SArgs {
   unsigned int* epoch;           // local u32 per CTA, advanced once per call
   unsigned long long* nonfinite;
   Fmt f;
+  int full_fence;                // 1: extra fence.sc.sys around the flags (MXB200_SYMM_FENCE=1)
 };
 // two-shot over symmetric memory (k_fused.cuh, k_symm2_flow)
 struct S2Args {
@@ -1197,11 +1198,23 @@ struct S2Args {
   unsigned int* epoch;           // local u32 per CTA
   unsigned long long* nonfinite;
   Fmt f;
+  int full_fence;
 };
 bool launch_symm_twoshot(const S2Args& a, int out_is_bf16, int block, int enc, int bits,
                          cudaStream_t st);
 // CTAs of the symmetric-memory kernel for n values (one 1024-value unit per warp)
-inline int64_t symm_ctas(int64_t n) { return (n / kUnit + kWarps - 1) / kWarps; }
+// (capped: each CTA then loops over several unit rows, so one flag exchange
+// -- one system-scope release -- covers more bytes; MXB200_SYMM_CTAS overrides)
+inline int64_t symm_ctas(int64_t n) {
+  static int64_t cap = -1;
+  if (cap < 0) {
+    const char* e = getenv("MXB200_SYMM_CTAS");
+    cap = e ? atoll(e) : 592;  // 148 SMs x 4 resident CTAs of k_symm_flow
+    if (cap < 1) cap = 1;
+  }
+  const int64_t g = (n / kUnit + kWarps - 1) / kWarps;
+  return g < cap ? g : cap;
+}
 bool launch_symm_oneshot(const SArgs& a, int out_is_bf16, int block, int enc, int bits,
                          cudaStream_t st);
 

@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(kThreads) k_symm_flow(const SArgs S) {
 // ---------------------------------------------------------------------------
 // Two-shot over NVLink peer memory (the TP >= 4 algorithm), one launch per
 // rank, per-CTA dataflow.  Chunk j (c = n/N values) is owned by rank j.
-// CTA b owns units [8b, 8b+8) of EVERY chunk:
+// CTA b owns unit rows [b*U, b*U+U) (8 units each) of EVERY chunk:
 //   A1  quantise those units of the local partial, chunk by chunk, into this
 //       rank's send shards (slot e&1: N chunk shards);  publish flag A(b)
 //   A2  wait for A(b) of every peer; pull the N peers' send shards of MY
@@ -498,13 +498,14 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
   __syncthreads();
   const unsigned int e = s_e;
   const int lane = threadIdx.x & 31;
-  const uint32_t q = b * kWarps + (threadIdx.x >> 5);  // unit inside every chunk
-  const bool live = q < (uint32_t)(S.c / kUnit);
+  // CTA b owns unit rows b*U .. b*U+U-1 (kWarps units each) of every chunk
+  const uint32_t cu = (uint32_t)(S.c / kUnit);
+  const uint32_t U = (cu + G * kWarps - 1) / (G * kWarps);
   const int nr = S.nranks, me = S.rank;
   const int64_t slot = (int64_t)(e & 1u) * S.slot_stride;
   uint8_t* const mine = S.bufs[me] + slot;
 
-  auto put = [&](uint8_t* shard, const LaneCodes<BITS>& cc, const int* stored) {
+  auto put = [&](uint8_t* shard, uint32_t q, const LaneCodes<BITS>& cc, const int* stored) {
     store_lane_codes<BITS>(shard + S.elem_off + (size_t)q * UBYTES + lane * (4 * BITS), cc, kVPL);
     uint8_t* sp = shard + S.scale_off + (size_t)q * USCALES + (lane / LPB) * NSB;
     if constexpr (NSB == 4) {
@@ -537,7 +538,9 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
   };
 
   // ---- A1: my partial's unit q of every chunk -> my send shards ----------
-  if (live) {
+  for (uint32_t u = 0; u < U; ++u) {
+    const uint32_t q = (b * U + u) * kWarps + (threadIdx.x >> 5);  // unit inside every chunk
+    if (q >= cu) break;
     const InT* x = reinterpret_cast<const InT*>(S.x) + (size_t)q * kUnit + lane * kVPL;
     for (int j = 0; j < nr; j += 2) {
       Raw<InT> r0, r1;
@@ -553,14 +556,16 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
           report_nonfinite_raw<InT>(h ? r1 : r0, kVPL,
                                     (int64_t)(j + h) * S.c + (int64_t)q * kUnit + lane * kVPL,
                                     S.nonfinite);
-        put(mine + (size_t)(j + h) * S.shard_stride, cc, stored);
+        put(mine + (size_t)(j + h) * S.shard_stride, q, cc, stored);
       }
     }
   }
   publish_wait(0);
 
   // ---- A2: sum my chunk's N send shards (NVLink), re-quantise -----------
-  if (live) {
+  for (uint32_t u = 0; u < U; ++u) {
+    const uint32_t q = (b * U + u) * kWarps + (threadIdx.x >> 5);  // unit inside every chunk
+    if (q >= cu) break;
     float acc[kVPL];
 #pragma unroll
     for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
@@ -584,12 +589,14 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
     if (bad)
       report_nonfinite_raw<float>(raw, kVPL, (int64_t)me * S.c + (int64_t)q * kUnit + lane * kVPL,
                                   S.nonfinite);
-    put(mine + (size_t)nr * S.shard_stride, cc, stored);
+    put(mine + (size_t)nr * S.shard_stride, q, cc, stored);
   }
   publish_wait(1);
 
   // ---- B: every owner's reduced shard -> out ------------------------------
-  if (live) {
+  for (uint32_t u = 0; u < U; ++u) {
+    const uint32_t q = (b * U + u) * kWarps + (threadIdx.x >> 5);  // unit inside every chunk
+    if (q >= cu) break;
     for (int j = 0; j < nr; ++j) {
       RL a;
       load_rank<B, BITS, kVPL, true>(a, S.bufs[j] + slot + (size_t)nr * S.shard_stride,
@@ -608,7 +615,7 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
 
 template <typename OutT, int B, int ENC, int BITS>
 void go_symm2(const S2Args& a, cudaStream_t st) {
-  const int64_t g = (a.c / kUnit + kWarps - 1) / kWarps;
+  const int64_t g = symm_ctas(a.c);
   launch_pdl(k_symm2_flow<OutT, B, ENC, BITS>, dim3((unsigned)g), dim3(kThreads), 0, st, a);
 }
 

@@ -662,7 +662,7 @@ int mx_symm_twoshot_layout(int64_t n, const mx_scheme_t* s, int32_t nranks,
   int64_t so, eo, sc;
   mx_shard_layout(c, s, &so, &eo, &sc);
   const int64_t slot = ((nranks + 1) * sc + 255) / 256 * 256;
-  const int64_t g = (c / kUnit + kWarps - 1) / kWarps;
+  const int64_t g = symm_ctas(c);
   if (slot_stride) *slot_stride = slot;
   if (shard_stride) *shard_stride = sc;
   if (flags_offset) *flags_offset = 2 * slot;

@@ -122,3 +122,18 @@ def test_symm_twoshot_multirank_bit_exact(lib, N, spec):
             ref = torch.from_numpy(O.allreduce_twoshot(x64s[c % 3], O.scheme(spec))).to(out_dtype)
             for r in range(N):
                 assert torch.equal(outs[r].cpu(), ref), (spec, N, c, r, out_dtype)
+
+
+def test_symm_capped_grid_unit_row_loop():
+    """With the CTA cap forced to 3 (MXB200_SYMM_CTAS, read once per
+    process) every CTA of K5 / K5b loops over several unit rows and the last
+    rows are ragged; the randomised multi-rank sweep must stay bit-exact."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MXB200_SYMM_CTAS="3")
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "fuzz_symm.py"), "20", "5"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -64,6 +65,14 @@ def parse():
                     help="HostPipeline piece weights (or one integer: equal pieces)")
     ap.add_argument("--profile", action="store_true",
                     help="ncu mode: a few eager launches, no timing, no JSON")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="N=1: initialise a world-1 NCCL process group and run the TP=N "
+                         "code path (NCCL collectives, NVLink kernel, TTFT) instead of the "
+                         "single-GPU simulation")
+    ap.add_argument("--no-ttft", action="store_true", help="skip the TTFT block (N>1 path)")
+    ap.add_argument("--no-70b", action="store_true", help="skip the 70B-shape kernel block")
+    ap.add_argument("--ttft-layers", type=int, default=None,
+                    help="truncate the TTFT stacks (default: full 32 / 80 layers)")
     return ap.parse_args()
 
 
@@ -173,6 +182,9 @@ def cpu_oracle_step(partials64, spec, threads):
 
 
 def cpu_baseline(spec, shape, nranks, budget_s=10.0):
+    """The oracle port on every host thread, plus (when baseline/_ref holds
+    the installed reference) the UNMODIFIED reference timed through its own
+    public API on the same workload."""
     from paper_2411_09510_b200.synth import rank_partials
 
     threads = os.cpu_count() or 1
@@ -187,70 +199,166 @@ def cpu_baseline(spec, shape, nranks, budget_s=10.0):
         if len(times) >= 2 and time.perf_counter() - t_all > budget_s:
             break
     med = statistics.median(times)
-    return {"value": round(nranks * 2 * n / med / 1e9, 4), "unit": UNIT, "cores": threads,
-            "kind": "port",
-            "sample": f"{len(times)} full steps of simulated TP={nranks} on {list(shape)} "
-                      f"({spec}); median {med * 1e3:.1f} ms/step; oracle/mx_oracle.py "
-                      f"(numpy restatement of mx/codec.py + mx/netbench.py:332-334), "
-                      f"blocks split over {threads} threads"}
+    out = {"value": round(nranks * 2 * n / med / 1e9, 4), "unit": UNIT, "cores": threads,
+           "kind": "port",
+           "sample": f"{len(times)} full steps of simulated TP={nranks} on {list(shape)} "
+                     f"({spec}); median {med * 1e3:.1f} ms/step; oracle/mx_oracle.py "
+                     f"(numpy restatement of mx/codec.py + mx/netbench.py:332-334), "
+                     f"blocks split over {threads} threads",
+           "host_cpu_count": os.cpu_count()}
+    ref = reference_timings(spec, shape, nranks, [p.astype(np.float32) for p in parts])
+    if ref is not None:
+        out["reference"] = ref
+    return out
+
+
+def load_reference():
+    """The installed reference package (scripts/install_reference.sh ->
+    baseline/_ref/mxcomm), or None."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "mxcomm")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import mxcomm  # noqa: F401
+
+        return mxcomm
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def reference_timings(spec, shape, nranks, parts32):
+    """The real reference on this host: (a) one simulated TP=N cycle through
+    its codec API -- compress_tensor + decompress_tensor(float32) per rank and
+    the fp32 rank-order sum (mx/codec.py:238-284, mx/netbench.py:332-334),
+    single-threaded numpy as shipped; (b) its own collective benchmark
+    run_allgather_bench(N, shape, scheme, LinkModel(inf), repetitions=3)
+    (mx/netbench.py:424-472: N worker threads, in-process mailboxes)."""
+    mx = load_reference()
+    if mx is None:
+        return None
+    n = parts32[0].size
+    sch = mx.parse_scheme(spec)
+    cyc = []
+    for _ in range(2):
+        t = time.perf_counter()
+        acc = np.zeros(parts32[0].shape, np.float32)
+        for p in parts32:
+            acc += mx.decompress_tensor(mx.compress_tensor(p, sch), dtype=np.float32)
+        cyc.append(time.perf_counter() - t)
+    c = min(cyc)
+    res = mx.run_allgather_bench(nranks, tuple(shape), sch, mx.LinkModel(bandwidth=math.inf),
+                                 repetitions=3, compare_uncompressed=False)
+    return {"kind": "reference", "package": "mxcomm 0.1.0 (baseline/_ref, unmodified)",
+            "codec_cycle": {"value": round(nranks * 2 * n / c / 1e9, 5), "unit": UNIT,
+                            "ms_per_step": round(c * 1e3, 1), "cores": 1,
+                            "sample": f"best of {len(cyc)} full cycles: {nranks} x "
+                                      f"(compress_tensor + decompress_tensor f32) + fp32 sum "
+                                      f"on {list(shape)} {spec}"},
+            "run_allgather_bench": {"value": round(nranks * 2 * n / res.median_s / 1e9, 5),
+                                    "unit": UNIT, "median_s": round(res.median_s, 4),
+                                    "wire_bytes_per_worker": res.wire_bytes_per_worker,
+                                    "cores": nranks,
+                                    "sample": f"run_allgather_bench({nranks}, {tuple(shape)}, "
+                                              f"{spec}, LinkModel(inf), repetitions=3): "
+                                              f"{nranks} worker threads (GIL-bound), fp16 "
+                                              f"standard-normal inputs"}}
 
 
 def run_reference(args, shape, rank, world):
-    """--impl reference: the CPU reference path (oracle port) on host cores,
-    rank 0 only; each step a bounded row-sample of the same workload."""
+    """--impl reference, rank 0 only: the UNMODIFIED reference (baseline/_ref)
+    through its own public API -- run_allgather_bench, N worker threads doing
+    compress -> exchange -> decode -> fp32 rank-order sum
+    (mx/netbench.py:424-472) -- K timed repetitions after its untimed warm-up
+    one.  Each repetition is the full [T x H] workload unless K x the
+    per-repetition cost would exceed ~3 minutes; then the row count is
+    bounded and the line says so (config.sampled_rows).  Without
+    baseline/_ref the oracle port (oracle/mx_oracle.py) stands in."""
     if rank != 0:
         return
-    from paper_2411_09510_b200.synth import rank_partials
-
     T, H = shape
     nranks = args.sim_ranks if world == 1 else world
-    threads = os.cpu_count() or 1
-    # calibrate: seconds per row for the full cycle (pool warm, 128 rows)
-    cal_rows = 128
-    cal = [p.astype(np.float64) for p in rank_partials((cal_rows, H), nranks, seed=0)]
-    cpu_oracle_step(cal, args.scheme, threads)
-    t = time.perf_counter()
-    cpu_oracle_step(cal, args.scheme, threads)
-    per_row = (time.perf_counter() - t) / cal_rows
-    # each step: as many rows as a ~120 s run allows (at least 8)
-    budget = 120.0
-    rows = int(min(T, budget / max(1, args.steps + args.warmup) / max(per_row, 1e-9)))
-    rows = min(T, max(8, (rows // 8) * 8))
-    parts = [p.astype(np.float64) for p in rank_partials((rows, H), nranks, seed=0)]
-    for _ in range(args.warmup):
-        cpu_oracle_step(parts, args.scheme, threads)
-    t = time.perf_counter()
-    for _ in range(args.steps):
-        cpu_oracle_step(parts, args.scheme, threads)
-    el = time.perf_counter() - t
-    ms = el / args.steps * 1e3
-    value = nranks * 2 * rows * H / (el / args.steps) / 1e9
-    sample = (f"{rows} of {T} rows x {H} per step, {nranks} rank partials, {args.scheme}; "
-              f"oracle/mx_oracle.py (numpy restatement of the reference codec) on "
-              f"{threads} host threads")
-    line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+    mx = load_reference()
+    budget = 180.0
+    if mx is not None:
+        sch = mx.parse_scheme(args.scheme)
+        link = mx.LinkModel(bandwidth=math.inf)
+        cal_rows = 64
+        t = time.perf_counter()
+        mx.run_allgather_bench(nranks, (cal_rows, H), sch, link, repetitions=3,
+                               compare_uncompressed=False)
+        per_row = (time.perf_counter() - t) / (4 * cal_rows)
+        reps = max(3, args.steps)
+        rows = int(min(T, budget / (reps + 1 + args.warmup) / max(per_row, 1e-9)))
+        rows = min(T, max(8, (rows // 8) * 8))
+        if args.warmup > 0:
+            mx.run_allgather_bench(nranks, (rows, H), sch, link, repetitions=3,
+                                   compare_uncompressed=False)
+        res = mx.run_allgather_bench(nranks, (rows, H), sch, link, repetitions=reps,
+                                     compare_uncompressed=False)
+        sec = res.median_s
+        threads, kind = nranks, "reference"
+        sample = (f"mxcomm.run_allgather_bench({nranks}, ({rows}, {H}), {args.scheme}, "
+                  f"LinkModel(inf), repetitions={reps}) -- the unmodified reference "
+                  f"(baseline/_ref) on {nranks} worker threads; median of {reps} timed "
+                  f"repetitions; {rows} of {T} rows")
+    else:
+        from paper_2411_09510_b200.synth import rank_partials
+
+        threads, kind = os.cpu_count() or 1, "port"
+        cal_rows = 128
+        cal = [p.astype(np.float64) for p in rank_partials((cal_rows, H), nranks, seed=0)]
+        cpu_oracle_step(cal, args.scheme, threads)
+        t = time.perf_counter()
+        cpu_oracle_step(cal, args.scheme, threads)
+        per_row = (time.perf_counter() - t) / cal_rows
+        rows = int(min(T, budget / max(1, args.steps + args.warmup) / max(per_row, 1e-9)))
+        rows = min(T, max(8, (rows // 8) * 8))
+        parts = [p.astype(np.float64) for p in rank_partials((rows, H), nranks, seed=0)]
+        for _ in range(args.warmup):
+            cpu_oracle_step(parts, args.scheme, threads)
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            cpu_oracle_step(parts, args.scheme, threads)
+        sec = (time.perf_counter() - t) / args.steps
+        sample = (f"{rows} of {T} rows x {H} per step, {nranks} rank partials, {args.scheme}; "
+                  f"oracle/mx_oracle.py (numpy restatement; baseline/_ref missing) on "
+                  f"{threads} host threads")
+    value = nranks * 2 * rows * H / sec / 1e9
+    cfg = config_dict(args, shape, world)
+    cfg["sampled_rows"] = rows
+    line = {"metric": METRIC, "value": round(value, 5), "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic (gaussian_with_outliers, mx/synth.py)",
-            "impl": "reference",
-            "config": config_dict(args, shape, world),
-            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads,
-                             "kind": "port", "sample": sample},
-            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+            "dtype": "f32", "data": "synthetic (standard normal fp16, mx/netbench.py:444-447)"
+            if kind == "reference" else "synthetic (gaussian_with_outliers, mx/synth.py)",
+            "impl": "reference", "config": cfg,
+            "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": threads,
+                             "kind": kind, "sample": sample,
+                             "host_cpu_count": os.cpu_count()},
+            "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def config_dict(args, shape, world):
-    sim = world == 1
-    return {"workload": (f"Llama-3.1-8B prefill row-parallel all-reduce [{shape[0]}x{shape[1]}] "
-                         f"bf16, {args.scheme}, {args.algo}, "
-                         + (f"simulated TP={args.sim_ranks} on 1 GPU (BASELINE configs[0])"
-                            if sim else f"TP={world} over NCCL (BASELINE configs[1])")),
-            "scheme": args.scheme, "algo": args.algo, "tp": args.sim_ranks if sim else world,
-            "ranks_per_gpu": args.sim_ranks if sim else 1, "seq_len": shape[0],
-            "hidden": shape[1],
-            "l2": "inputs rotated over buffer sets totalling > 126 MB L2"}
+def config_dict(args, shape, world, dist_mode=None, R=None):
+    dist_mode = world > 1 if dist_mode is None else dist_mode
+    sim = not dist_mode
+    d = {"workload": (f"Llama-3.1-8B prefill row-parallel all-reduce [{shape[0]}x{shape[1]}] "
+                      f"bf16, {args.scheme}, {args.algo}, "
+                      + (f"simulated TP={args.sim_ranks} on 1 GPU (BASELINE configs[0])"
+                         if sim else f"TP={world} over NCCL (BASELINE configs[1])")),
+         "scheme": args.scheme, "algo": args.algo, "tp": args.sim_ranks if sim else world,
+         "ranks_per_gpu": args.sim_ranks if sim else 1, "seq_len": shape[0],
+         "hidden": shape[1],
+         "l2": "inputs rotated over buffer sets totalling > 3 x the 126 MB L2"}
+    if R is not None:
+        d["buffer_sets"] = R
+        d["timing"] = (f"{args.steps} steps = {args.steps // R} replays of one {R}-step CUDA "
+                       f"graph" + (f" + one {args.steps % R}-step graph" if args.steps % R else "")
+                       + "; CUDA events on the launch stream after a device pre-roll")
+    return d
 
 
 # ---------------------------------------------------------------------------
@@ -262,6 +370,7 @@ def time_graph_replays(torch, graphs, k):
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    preroll(torch)
     e0.record(st)
     for i in range(k):
         graphs[i % len(graphs)].replay()
@@ -270,23 +379,49 @@ def time_graph_replays(torch, graphs, k):
     return e0.elapsed_time(e1)  # ms
 
 
-def time_steps(torch, g_all, graphs, k):
-    """Exactly k steps: k // R replays of the graph holding all R buffer
-    sets' steps back to back, then k % R single-step replays (a multi-step
-    graph amortises the graph-launch overhead the way a captured prefill
-    forward does; every step still runs in full)."""
-    R = len(graphs)
+def rotation(k, r_min, cap=32):
+    """Buffer-set count R: the smallest divisor of k in [r_min, cap], so the
+    k timed steps are exactly k / R replays of ONE graph holding the R sets'
+    steps back to back -- every step pays the same (amortised) graph launch
+    whatever --steps is.  Without such a divisor R = r_min and one extra
+    graph holds the k mod R remaining steps."""
+    for d in range(r_min, max(r_min, cap) + 1):
+        if k % d == 0:
+            return d
+    return r_min
+
+
+def preroll(torch):
+    """~0.1 ms device spin before the start event: the graph launches
+    issued next are queued by the time the event fires, so no host launch
+    latency is inside the timed region (device-bound timing)."""
+    torch.cuda._sleep(200_000)
+
+
+def time_steps(torch, g_all, g_rem, reps):
+    """reps replays of the R-step graph (+ the remainder graph): exactly
+    reps * R + (k mod R) = k steps between two CUDA events on the stream the
+    kernels run on."""
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    preroll(torch)
     e0.record(st)
-    for _ in range(k // R):
+    for _ in range(reps):
         g_all.replay()
-    for i in range(k % R):
-        graphs[i].replay()
+    if g_rem is not None:
+        g_rem.replay()
     e1.record(st)
     torch.cuda.synchronize()
     return e0.elapsed_time(e1)  # ms
+
+
+def rotation_graphs(torch, steps, k):
+    """(g_all over all R steps, g_rem over the first k mod R or None, reps)."""
+    R = len(steps)
+    g_all = capture(torch, lambda: [f() for f in steps])
+    g_rem = capture(torch, lambda: [steps[i]() for i in range(k % R)]) if k % R else None
+    return g_all, g_rem, k // R
 
 
 def capture(torch, fn):
@@ -312,7 +447,188 @@ def load_traffic(kernel_key):
         return None
 
 
-def run_ours(args, shape, rank, world, local_rank):
+def kernel_graph_time(torch, fn, reps, launches_per_replay):
+    """Device time per launch of a graph of back-to-back launches (each over a
+    different buffer set, so every launch reads HBM-cold data)."""
+    g = capture(torch, fn)
+    for _ in range(3):
+        g.replay()
+    ms = time_graph_replays(torch, [g], reps) / (reps * launches_per_replay)
+    del g
+    return ms
+
+
+def kentry(ms, nbytes, peak, launches):
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {"us": round(ms * 1e3, 3), "bytes": nbytes, "gbs": round(gbs, 1),
+            "frac": round(gbs / peak, 4), "launches_timed": launches}
+
+
+def load_large_golden():
+    try:
+        return json.load(open(os.path.join(ROOT, "tests", "golden", "large.json")))
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def step_parity(torch, out, args, shape, nranks, algo):
+    """The timed step's own output (set 0, left in place by its last replay)
+    against the reference-generated digest when one exists for this
+    configuration (tests/golden/large.json), else against the CPU oracle on
+    the same inputs.  bf16 output compared bit for bit."""
+    import hashlib
+
+    bits = out.reshape(-1).view(torch.int16).cpu().numpy()
+    sha = hashlib.sha256(bits.tobytes()).hexdigest()
+    g = load_large_golden()
+    key = None
+    if g and args.scheme == g.get("scheme") and algo == "oneshot":
+        for tag in ("8b", "70b"):
+            if tuple(g[tag]["shape"]) == tuple(shape) and f"tp{nranks}_sum_bf16" in g[tag]:
+                key = (tag, f"tp{nranks}_sum_bf16")
+    if key is not None:
+        return {"ok": sha == g[key[0]][key[1]],
+                "against": f"tests/golden/large.json {key[0]}.{key[1]} (generated by the "
+                           f"reference mxcomm)"}
+    from oracle import mx_oracle as O
+    from paper_2411_09510_b200.synth import rank_partials
+
+    parts = [p.astype(np.float64) for p in rank_partials(shape, nranks, seed=0)]
+    f = O.allreduce_oneshot if algo == "oneshot" else O.allreduce_twoshot
+    ref = f([p.reshape(-1) for p in parts], O.scheme(args.scheme))
+    want = torch.from_numpy(np.asarray(ref, np.float32)).to(torch.bfloat16).view(torch.int16)
+    return {"ok": bool(np.array_equal(want.numpy(), bits)),
+            "against": f"oracle/mx_oracle.py allreduce_{algo} on the same inputs"}
+
+
+def block_70b(torch, args, sch, dev, peak, steps):
+    """The Llama-3.1-70B prefill partial [4096 x 8192] (BASELINE configs[2]):
+    K4 (the fused simulated-TP=2 step), K1 and K2 alone, device-timed over
+    buffer sets rotated beyond L2, with the step output checked against the
+    reference digest."""
+    from paper_2411_09510_b200 import _native
+    from paper_2411_09510_b200.collective import SimulatedAllReduce
+    from paper_2411_09510_b200.synth import rank_partials
+
+    shape = (4096, 8192)
+    n = shape[0] * shape[1]
+    N = 2
+    _, _, S = _native.shard_layout(n, sch.to_c())
+    sb, eb = _native.stream_nbytes(n, sch.to_c())
+    per = N * 2 * n + N * S + 2 * n
+    R = max(3, -(-3 * L2_BYTES // per))
+    base = [torch.from_numpy(p).to(dev, torch.bfloat16) for p in rank_partials(shape, N, seed=0)]
+    sets = [([(b.roll(7 * i, 0) * (-1) ** i).contiguous() for b in base],
+             SimulatedAllReduce(sch, n, N, "oneshot", torch.bfloat16, dev)) for i in range(R)]
+    del base
+    reps = max(4, min(60, steps // 20))
+    ms4 = kernel_graph_time(torch, lambda: [op(p) for p, op in sets], reps, R)
+    par = step_parity(torch, sets[0][1].out, args, shape, N, "oneshot")
+
+    def q_all():
+        for p, op in sets:
+            op.be.quantize_into(p[0].reshape(-1), op.gathered[0:S], op.ws, op.flag)
+
+    def d_all():
+        for p, op in sets:
+            op.reduce()
+
+    ms1 = kernel_graph_time(torch, q_all, reps, R)
+    ms2 = kernel_graph_time(torch, d_all, reps, R)
+    fb = N * 2 * n + N * (sb + eb) + 2 * n
+    out = {"workload": f"Llama-3.1-70B prefill partial [{shape[0]}x{shape[1]}] bf16, "
+                       f"{args.scheme}, simulated TP={N} (BASELINE configs[2] shape)",
+           "k_fused_flow": dict(kentry(ms4, fb, peak, reps * R),
+                                value=round(N * 2 * n / (ms4 * 1e-3) / 1e9, 1)),
+           "k_quant": kentry(ms1, 2 * n + sb + eb, peak, reps * R),
+           "k_dqsum": kentry(ms2, N * (sb + eb) + 2 * n, peak, reps * R),
+           "step_parity": par}
+    del sets
+    torch.cuda.empty_cache()
+    return out
+
+
+def reference_api_e2e(torch, args, host_parts, nranks, reps=5):
+    """The reference's own codec API end to end on this GPU: per rank
+    compress_tensor(np.float32 partial) -> CompressedTensor (host bytes) and
+    decompress_tensor(ct, float32) -> numpy, then the fp32 rank-order sum on
+    the host (mx/codec.py:238-284, mx/netbench.py:332-334) -- every call
+    uploads its input and downloads its output."""
+    from paper_2411_09510_b200 import compress_tensor, decompress_tensor, parse_scheme
+
+    sch = parse_scheme(args.scheme, extensions=True)
+    parts = [host_parts[r].astype(np.float32) for r in range(nranks)]
+    n = parts[0].size
+
+    def cycle():
+        acc = np.zeros(parts[0].shape, np.float32)
+        for p in parts:
+            acc += decompress_tensor(compress_tensor(p, sch), np.float32)
+        return acc
+
+    cycle()
+    ts = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        cycle()
+        ts.append(time.perf_counter() - t)
+    med = statistics.median(ts)
+    return {"value": round(nranks * 2 * n / med / 1e9, 3), "unit": UNIT,
+            "ms_per_step": round(med * 1e3, 3), "reps": reps,
+            "api": f"{nranks} x (compress_tensor(np.float32) + decompress_tensor(ct, "
+                   f"np.float32)) + numpy fp32 sum (the reference's own call sequence, host "
+                   f"arrays in and out)"}
+
+
+def ttft_block(torch, dist, args, world, dev):
+    """Prefill TTFT of the TP Llama body (random init, graph-replayed), bf16
+    NCCL all-reduce against the MX-compressed one (NCCL one-shot / two-shot,
+    NVLink kernels symm / symm2): Llama-3.1-8B seq 2048 at TP=N, and
+    Llama-3.1-70B seq 4096 at TP=8 (BASELINE configs[1-2]).  Each variant's
+    success is agreed across ranks before the next one starts."""
+    from paper_2411_09510_b200 import tp
+
+    def all_ok(ok):
+        t = torch.tensor([1 if ok else 0], device=dev, dtype=torch.int32)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return bool(t.item())
+
+    models = [("llama-3.1-8b", tp.LLAMA31_8B, 2048)]
+    if world == 8:
+        models.append(("llama-3.1-70b", tp.LLAMA31_70B, 4096))
+    variants = [("bf16_nccl", None, "oneshot"), ("mx_oneshot", args.scheme, "oneshot"),
+                ("mx_twoshot", args.scheme, "twoshot"), ("mx_symm", args.scheme, "symm"),
+                ("mx_symm2", args.scheme, "symm2")]
+    out = {}
+    for name, cfg, seq in models:
+        res = {"tp": world, "seq": seq, "batch": 1,
+               "layers": args.ttft_layers or cfg.layers, "cuda_graph": True}
+        base = None
+        for label, spec, algo in variants:
+            err, ms = None, None
+            try:
+                ms = tp.measure_ttft(cfg, 1, seq, tp=world, scheme=spec, algo=algo,
+                                     layers=args.ttft_layers, reps=5, warmup=2, graph=True)
+            except Exception as exc:  # noqa: BLE001
+                err = f"{type(exc).__name__}: {exc}"[:200]
+            ok = all_ok(err is None)
+            torch.cuda.empty_cache()
+            if not ok:
+                res[label] = {"error": err or "failed on another rank"}
+                continue
+            if spec is None:
+                base = ms
+            res[label] = {"ms": round(ms, 3)}
+            if base is not None and spec is not None:
+                res[label]["speedup_vs_bf16"] = round(base / ms, 4)
+        out[name] = res
+    tp._SYMM_CACHE.clear()
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_ours(args, shape, rank, world, local_rank, dist_mode):
     import torch
     import torch.distributed as dist
 
@@ -328,14 +644,15 @@ def run_ours(args, shape, rank, world, local_rank):
     sch = parse_scheme(args.scheme, extensions=True)
     T, H = shape
     n = T * H
-    sim = world == 1
+    sim = not dist_mode
     nranks = args.sim_ranks if sim else world
     so, eo, S = _native.shard_layout(n, sch.to_c())
     sb, eb = _native.stream_nbytes(n, sch.to_c())
+    peak, peak_kind = peaks()
     # buffer sets: one pass over them moves > 3x L2, so every step and every
-    # timed kernel launch reads data that is not L2-resident
+    # timed kernel launch reads data that is not L2-resident; R divides K
     per_set = (nranks if sim else 1) * 2 * n + (nranks * S) + 2 * n
-    R = max(3, -(-3 * L2_BYTES // per_set))
+    R = rotation(args.steps, max(3, -(-3 * L2_BYTES // per_set)))
     mine = list(range(nranks)) if sim else [rank]  # the partials this GPU owns
     host_parts = {r: rank_partials(shape, 1, seed=r)[0] for r in mine}  # seed = rank
     base = [torch.from_numpy(host_parts[r]).to(dev, torch.bfloat16) for r in mine]
@@ -360,10 +677,9 @@ def run_ours(args, shape, rank, world, local_rank):
         return
 
     graphs = [capture(torch, step_fn(i)) for i in range(R)]
-    steps_all = [step_fn(i) for i in range(R)]
-    g_all = capture(torch, lambda: [f() for f in steps_all])
+    g_all, g_rem, reps_all = rotation_graphs(torch, [step_fn(i) for i in range(R)], args.steps)
     fused = sim and getattr(sets[0][1], "fused", False)
-    if fused:  # one persistent kernel per step (quantise, grid barrier, dequant-sum)
+    if fused:  # one kernel per step (quantise -> read back -> dequant-sum)
         launches_per_step = 1
     elif args.algo == "oneshot":  # K1 x local partials + K2
         launches_per_step = (nranks if sim else 1) + 1
@@ -382,94 +698,84 @@ def run_ours(args, shape, rank, world, local_rank):
         extra = 0
         if el < 0.3:
             extra = int(min(1e6, (0.3 - el) / max(el / max(1, args.warmup), 1e-6))) + 1
-        if world > 1:
+        if dist_mode:
             te = torch.tensor([extra], device=dev, dtype=torch.int64)
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
             extra = int(te.item())
         for i in range(extra):
             graphs[i % R].replay()
         torch.cuda.synchronize()
-        if world > 1:
+        if dist_mode:
             dist.barrier()
         torch.cuda.synchronize()
-        ms_total = time_steps(torch, g_all, graphs, args.steps)
-        if world > 1:
+        ms_total = time_steps(torch, g_all, g_rem, reps_all)
+        if dist_mode:
             dist.barrier()
         torch.cuda.synchronize()
     clocks = clk.summary()
+    del graphs
     ms_local = ms_total / args.steps
     ms_step = ms_local
-    if world > 1:
+    if dist_mode:
         tt = torch.tensor([ms_local], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_step = float(tt.item())
     value = nranks * 2 * n / (ms_step * 1e-3) / 1e9
 
+    # ---- the timed step's own output vs the reference digest / oracle;
+    # every rank must hold the same bytes (mx/netbench.py:415-419)
+    parity = None
+    out0 = sets[0][1].out
+    if dist_mode:
+        import hashlib
+
+        hs = hashlib.sha256(out0.view(torch.int16).cpu().numpy().tobytes()).hexdigest()
+        allh = [None] * world
+        dist.all_gather_object(allh, hs)
+        if rank == 0:
+            parity = step_parity(torch, out0, args, shape, nranks, args.algo)
+            parity["ranks_identical"] = len(set(allh)) == 1
+            parity["ok"] = parity["ok"] and parity["ranks_identical"]
+    else:
+        parity = step_parity(torch, out0, args, shape, nranks, args.algo)
+
     # ---- per-kernel device times (roofline), graphs of back-to-back launches
     kernels = {}
-    if sim and args.algo == "oneshot":
-        # one graph = one launch per buffer set (R distinct inputs > 3x L2)
-        def q_all():
-            for parts, op in sets:
-                op.be.quantize_into(parts[0].reshape(-1), op.gathered[0:S], op.ws, op.flag)
-
-        def d_all():
-            for parts, op in sets:
-                op.reduce()
-
-        for name, fn, bytes_per in (("k_quant", q_all, 2 * n + sb + eb),
-                                    ("k_dqsum", d_all, nranks * (sb + eb) + 2 * n)):
-            g = capture(torch, fn)
-            for _ in range(3):
-                g.replay()
-            reps = max(4, min(100, args.steps // 20))
-            ms = time_graph_replays(torch, [g], reps) / (reps * R)
-            kernels[name] = {"us": round(ms * 1e3, 3), "bytes": bytes_per,
-                             "gbs": round(bytes_per / (ms * 1e-3) / 1e9, 1),
-                             "launches_timed": reps * R}
-    if not sim and args.algo == "oneshot":
-        # N>1: this rank's K1 and its K2 over the N gathered shards, timed on
-        # the rank's own buffers (local launches only, no collective)
-        try:
+    kreps = max(4, min(100, args.steps // 20))
+    try:
+        if sim and args.algo == "oneshot":
             def q_all():
                 for parts, op in sets:
-                    S_ = op.plan.shard_bytes
-                    op.backend.quantize_into(parts[0].reshape(-1),
-                                             op.gathered[rank * S_:(rank + 1) * S_], op.ws,
-                                             op.flag)
+                    op.be.quantize_into(parts[0].reshape(-1), op.gathered[0:S], op.ws, op.flag)
 
             def d_all():
                 for parts, op in sets:
-                    S_ = op.plan.shard_bytes
-                    op.backend.dequant_sum(op.gathered, S_, world, n, n, 0, op.out)
+                    op.reduce()
+            kw = nranks
+        elif args.algo == "oneshot":
+            # TP=N: this rank's K1 and its K2 over the N gathered shards, on
+            # the rank's own buffers (local launches only, no collective)
+            def q_all():
+                for parts, op in sets:
+                    op.backend.quantize_into(parts[0].reshape(-1),
+                                             op.gathered[rank * S:(rank + 1) * S], op.ws, op.flag)
 
-            for name, fn, bytes_per in (("k_quant", q_all, 2 * n + sb + eb),
-                                        ("k_dqsum", d_all, world * (sb + eb) + 2 * n)):
-                g = capture(torch, fn)
-                for _ in range(3):
-                    g.replay()
-                reps = max(4, min(100, args.steps // 20))
-                ms = time_graph_replays(torch, [g], reps) / (reps * R)
-                kernels[name] = {"us": round(ms * 1e3, 3), "bytes": bytes_per,
-                                 "gbs": round(bytes_per / (ms * 1e-3) / 1e9, 1),
-                                 "launches_timed": reps * R}
-        except Exception as exc:  # noqa: BLE001  (reported, never fatal)
-            kernels = {"error": f"{type(exc).__name__}: {exc}"[:200]}
-    peak, peak_kind = peaks()
+            def d_all():
+                for parts, op in sets:
+                    op.backend.dequant_sum(op.gathered, S, world, n, n, 0, op.out)
+            kw = world
+        else:
+            q_all = d_all = None
+        if q_all is not None:
+            kernels["k_quant"] = kentry(kernel_graph_time(torch, q_all, kreps, R),
+                                        2 * n + sb + eb, peak, kreps * R)
+            kernels["k_dqsum"] = kentry(kernel_graph_time(torch, d_all, kreps, R),
+                                        kw * (sb + eb) + 2 * n, peak, kreps * R)
+    except Exception as exc:  # noqa: BLE001  (reported, never fatal)
+        kernels = {"error": f"{type(exc).__name__}: {exc}"[:200]}
     roof = None
-    if not sim and "k_dqsum" in kernels:
-        kd = kernels["k_dqsum"]
-        roof = {"bound": "hbm",
-                "kernel": f"k_dqsum_lean<bf16,B={sch.block_size},{sch.element.name}> "
-                          f"(K2: {world} gathered shards -> bf16, this rank)",
-                "achieved": kd["gbs"], "peak": peak, "unit": "GB/s",
-                "frac": round(kd["gbs"] / peak, 4), "traffic": None,
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",
-                "algorithmic_bytes_per_launch": kd["bytes"], "launch_us": kd["us"],
-                "share_of_step": round(kd["us"] / (ms_step * 1e3), 3),
-                "other_kernels": {k: v for k, v in kernels.items() if k != "k_dqsum"},
-                "note": "rank 0's device time; the NCCL all-gather is the rest of the step"}
-    elif fused and "k_quant" in kernels:
+    psrc = f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)"
+    if fused:
         # the step IS one kernel (k_fused_flow): it must read the N partials
         # from HBM, write the N shards into the gather buffer (the bytes an
         # all-gather delivers) and write the bf16 sum.  Each warp reads its
@@ -478,32 +784,37 @@ def run_ours(args, shape, rank, world, local_rank):
         fb = nranks * 2 * n + nranks * (sb + eb) + 2 * n
         ach = round(fb / (ms_step * 1e-3) / 1e9, 1)
         tr = load_traffic(f"k_fused_flow|{args.scheme}|{T}x{H}|bf16|{nranks}ranks")
-        traffic = tr.get("per_launch_bytes") if isinstance(tr, dict) else tr
         roof = {"bound": "hbm",
                 "kernel": f"k_fused_flow<bf16,B={sch.block_size},{sch.element.name}> "
                           f"(quantise {nranks} partials -> gather buffer -> read back, "
-                          f"dequant-sum; one launch, no grid barrier)",
+                          f"dequant-sum; one launch)",
                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
-                "traffic": traffic,
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",
-                "algorithmic_bytes_per_launch": fb,
+                "traffic": tr.get("per_launch_bytes") if isinstance(tr, dict) else tr,
+                "peak_source": psrc, "algorithmic_bytes_per_launch": fb,
                 "algorithmic_bytes_note": "N*2n partial reads + N*S shard writes + 2n output; "
                                           f"+{nranks * (sb + eb)} B shard read-back from L2 "
                                           "not counted",
-                "launch_us": round(ms_step * 1e3, 3),
-                "share_of_step": 1.0,
+                "launch_us": round(ms_step * 1e3, 3), "share_of_step": 1.0,
                 "unfused_kernels": kernels}
+    elif "k_dqsum" in kernels and not sim:
+        kd = kernels["k_dqsum"]
+        roof = {"bound": "hbm",
+                "kernel": f"k_dqsum_lean<bf16,B={sch.block_size},{sch.element.name}> "
+                          f"(K2: {world} gathered shards -> bf16, this rank)",
+                "achieved": kd["gbs"], "peak": peak, "unit": "GB/s", "frac": kd["frac"],
+                "traffic": None, "peak_source": psrc,
+                "algorithmic_bytes_per_launch": kd["bytes"], "launch_us": kd["us"],
+                "share_of_step": round(kd["us"] / (ms_step * 1e3), 3),
+                "other_kernels": {k: v for k, v in kernels.items() if k != "k_dqsum"},
+                "note": "rank 0's device time; the NCCL exchange is the rest of the step"}
     elif "k_quant" in kernels:
-        # dominant kernel: K1 runs nranks times per step
         kq = kernels["k_quant"]
-        ach = kq["gbs"]
         tr = load_traffic(f"k_quant|{args.scheme}|{T}x{H}|bf16")
-        traffic = tr.get("per_launch_bytes") if isinstance(tr, dict) else tr
-        roof = {"bound": "hbm", "kernel": f"k_quant<bf16,B={sch.block_size},{sch.element.name}> (K1 quantise+pack)",
-                "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": traffic,
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",
-                "algorithmic_bytes_per_launch": kq["bytes"],
+        roof = {"bound": "hbm",
+                "kernel": f"k_quant<bf16,B={sch.block_size},{sch.element.name}> (K1)",
+                "achieved": kq["gbs"], "peak": peak, "unit": "GB/s", "frac": kq["frac"],
+                "traffic": tr.get("per_launch_bytes") if isinstance(tr, dict) else tr,
+                "peak_source": psrc, "algorithmic_bytes_per_launch": kq["bytes"],
                 "launch_us": kq["us"],
                 "share_of_step": round(nranks * kq["us"] / (ms_step * 1e3), 3),
                 "other_kernels": {k: v for k, v in kernels.items() if k != "k_quant"}}
@@ -521,19 +832,26 @@ def run_ours(args, shape, rank, world, local_rank):
                        for r in range(N_)] for i in range(R_)]
                 ops = [SimulatedAllReduce(sch, n, N_, "oneshot", torch.bfloat16, dev)
                        for _ in range(R_)]
-                g = capture(torch, lambda: [op(pp) for op, pp in zip(ops, ps)])
-                for _ in range(3):
-                    g.replay()
                 reps = max(3, min(50, args.steps // 40))
-                ms = time_graph_replays(torch, [g], reps) / (reps * R_)
+                ms = kernel_graph_time(torch, lambda: [op(pp) for op, pp in zip(ops, ps)],
+                                       reps, R_)
                 sim_more[f"tp{N_}"] = {"us": round(ms * 1e3, 3),
                                        "value": round(N_ * 2 * n / (ms * 1e-3) / 1e9, 1),
                                        "unit": UNIT,
-                                       "hbm_gbs": round(per / (ms * 1e-3) / 1e9, 1)}
-                del ps, ops, g
+                                       "hbm_gbs": round(per / (ms * 1e-3) / 1e9, 1),
+                                       "frac": round(per / (ms * 1e-3) / 1e9 / peak, 4)}
+                del ps, ops
                 torch.cuda.empty_cache()
         except Exception as exc:  # noqa: BLE001  (informational only)
             sim_more = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
+    # ---- the 70B prefill partial shape (N=1): K4, K1, K2 + parity
+    shape70 = None
+    if sim and not args.no_70b and args.algo == "oneshot" and tuple(shape) != (4096, 8192):
+        try:
+            shape70 = block_70b(torch, args, sch, dev, peak, args.steps)
+        except Exception as exc:  # noqa: BLE001
+            shape70 = {"error": f"{type(exc).__name__}: {exc}"[:200]}
 
     # ---- end to end through the public API with pinned host buffers:
     # HostPipeline (chunked H2D -> compressed all-reduce -> D2H on three
@@ -550,9 +868,10 @@ def run_ours(args, shape, rank, world, local_rank):
             pipe = HostPipeline.simulated(sch, n, nranks, args.algo, torch.bfloat16, dev,
                                           chunks=pieces)
         else:
-            # eager issue across ranks: no NCCL inside a multi-stream graph capture
+            # graph-captured too: a cache miss captures without an eager
+            # issue, so every rank runs each collective exactly once per call
             pipe = HostPipeline.compressed(sch, n, algo=args.algo, out_dtype=torch.bfloat16,
-                                           device=dev, chunks=pieces, graph=False)
+                                           device=dev, chunks=pieces, graph=True)
         ke = max(3, min(args.steps, 100))
         for _ in range(3):
             pipe(host_in, host_out)
@@ -562,9 +881,10 @@ def run_ours(args, shape, rank, world, local_rank):
         ref = (SimulatedAllReduce(sch, n, nranks, args.algo, torch.bfloat16, dev)(dparts) if sim
                else CompressedAllReduce(sch, n, algo=args.algo, out_dtype=torch.bfloat16,
                                         device=dev)(dparts[0]))
-        exact = bool(torch.equal(ref.reshape(-1).cpu().view(torch.int16), host_out.view(torch.int16)))
+        exact = bool(torch.equal(ref.reshape(-1).cpu().view(torch.int16),
+                                 host_out.view(torch.int16)))
         del dparts, ref
-        if world > 1:
+        if dist_mode:
             dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -574,7 +894,7 @@ def run_ours(args, shape, rank, world, local_rank):
         e1.record()
         torch.cuda.synchronize()
         ms_e = e0.elapsed_time(e1) / ke
-        if world > 1:
+        if dist_mode:
             tt = torch.tensor([ms_e], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ms_e = float(tt.item())
@@ -582,31 +902,41 @@ def run_ours(args, shape, rank, world, local_rank):
                "h2d_bytes_per_step": pipe.h2d_bytes, "d2h_bytes_per_step": pipe.d2h_bytes,
                "ms_per_step": round(ms_e, 4), "steps": ke, "pieces": pipe.k,
                "piece_values": [b1 - b0 for b0, b1 in zip(pipe.bounds, pipe.bounds[1:])],
-               "bit_exact_vs_device_call": exact,
+               "bit_exact_vs_device_call": exact, "cuda_graph": True,
                "api": "HostPipeline.__call__ (pinned host partials -> pinned host result)"}
+        del pipe
 
-    # ---- uncompressed bf16 NCCL all-reduce on the same tensor (N>1)
+    ref_api = None
+    if sim and not args.no_e2e:
+        try:
+            ref_api = reference_api_e2e(torch, args, host_parts, nranks)
+        except Exception as exc:  # noqa: BLE001
+            ref_api = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
+    # ---- uncompressed bf16 NCCL all-reduce on the same tensor (TP=N path)
     bf16_ar = None
-    if world > 1:
+    if dist_mode:
         xs = [s_[0][0].clone() for s_ in sets]
         gsb = [capture(torch, (lambda x=x: dist.all_reduce(x))) for x in xs]
         for i in range(args.warmup):
             gsb[i % R].replay()
         dist.barrier()
-        gsb_all = capture(torch, lambda: [dist.all_reduce(x) for x in xs])
-        ms_b = time_steps(torch, gsb_all, gsb, args.steps) / args.steps
+        ga, gr, rp = rotation_graphs(torch, [(lambda x=x: dist.all_reduce(x)) for x in xs],
+                                     args.steps)
+        ms_b = time_steps(torch, ga, gr, rp) / args.steps
         tt = torch.tensor([ms_b], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_b = float(tt.item())
-        bf16_ar = {"us": round(ms_b * 1e3, 2), "value": round(world * 2 * n / (ms_b * 1e-3) / 1e9, 2),
+        bf16_ar = {"us": round(ms_b * 1e3, 2),
+                   "value": round(world * 2 * n / (ms_b * 1e-3) / 1e9, 2),
                    "unit": UNIT, "speedup_of_compressed": round(ms_b / ms_step, 3)}
+        del xs, gsb, ga, gr
 
-    # ---- the NVLink-pull fused kernel over symmetric memory (N>1).  Every
-    # stage that can fail agrees across ranks first (all_reduce MIN of an
-    # ok flag), so one rank's failure can never leave the others waiting in
-    # a collective.
+    # ---- the NVLink-pull fused kernel over symmetric memory (TP=N path).
+    # Every stage that can fail agrees across ranks first (all_reduce MIN of
+    # an ok flag), so one rank's failure never leaves the others waiting.
     symm = None
-    if world > 1 and os.environ.get("MXB200_BENCH_SYMM", "1") == "1":
+    if dist_mode and os.environ.get("MXB200_BENCH_SYMM", "1") == "1":
         from paper_2411_09510_b200.collective import SymmetricAllReduce
 
         def all_ok(ok):
@@ -615,9 +945,9 @@ def run_ours(args, shape, rank, world, local_rank):
             return bool(t.item())
 
         err, sar, ms_s, exact = None, None, None, None
+        x0 = sets[0][0][0]
         try:
             sar = SymmetricAllReduce(sch, n, out_dtype=torch.bfloat16, device=dev, algo=args.algo)
-            x0 = sets[0][0][0]
             got = sar(x0).clone()
             torch.cuda.synchronize()
             sar.check_status()
@@ -625,17 +955,17 @@ def run_ours(args, shape, rank, world, local_rank):
             err = exc
         ok = all_ok(err is None)  # identical on every rank
         if ok:
-            one = CompressedAllReduce(sch, n, algo=args.algo, out_dtype=torch.bfloat16, device=dev)
-            ref = one(x0).clone()
-            exact = bool(torch.equal(got.view(torch.int16), ref.view(torch.int16)))
+            exact = bool(torch.equal(got.view(torch.int16), sets[0][1].out.view(torch.int16)))
             try:
                 gss = [capture(torch, (lambda x=s_[0][0]: sar(x))) for s_ in sets]
                 for i in range(args.warmup):
                     gss[i % R].replay()
                 torch.cuda.synchronize()
-                gss_all = capture(torch, lambda: [sar(s_[0][0]) for s_ in sets])
-                ms_s = time_steps(torch, gss_all, gss, args.steps) / args.steps
+                ga, gr, rp = rotation_graphs(torch, [(lambda x=s_[0][0]: sar(x)) for s_ in sets],
+                                             args.steps)
+                ms_s = time_steps(torch, ga, gr, rp) / args.steps
                 sar.check_status()  # a timed-out peer wait invalidates the number
+                sar.check_finite()
             except Exception as exc:  # noqa: BLE001
                 err = exc
             ok = all_ok(err is None)
@@ -648,7 +978,7 @@ def run_ours(args, shape, rank, world, local_rank):
                     f"bit_exact_vs_nccl_{args.algo}": exact,
                     "kernel": ("k_symm_flow (per-CTA: quantise -> release flag to every peer "
                                "-> acquire N flags -> NVLink pull dequant-sum; one launch per "
-                               "rank, no grid barrier)" if args.algo == "oneshot" else
+                               "rank)" if args.algo == "oneshot" else
                                "k_symm2_flow (per-CTA: quantise N chunks -> flag -> pull my "
                                "chunk from N peers, fp32 sum, requantise -> flag -> pull N "
                                "reduced chunks, decode; one launch per rank)")}
@@ -657,14 +987,15 @@ def run_ours(args, shape, rank, world, local_rank):
         else:
             symm = {"error": (f"{type(err).__name__}: {err}"[:300] if err is not None
                               else "failed on another rank")}
+        del sar
 
-    # the collective against NVLink (N>1): effective (uncompressed-equivalent,
-    # nccl-tests "algbw") and wire GB/s per rank, against 900 GB/s/direction
+    # the collective against NVLink (TP=N): effective (uncompressed-
+    # equivalent, nccl-tests "algbw") and wire GB/s per rank vs 900 GB/s
     coll = None
-    if world > 1:
-        wire = ((world - 1) * S if args.algo == "oneshot" else
-                2 * (world - 1) * _native.shard_layout(
-                    twoshot_chunk_values(n, world, sch.block_size), sch.to_c())[2])
+    wire = ((nranks - 1) * S if args.algo == "oneshot" else
+            2 * (nranks - 1) * _native.shard_layout(
+                twoshot_chunk_values(n, nranks, sch.block_size), sch.to_c())[2])
+    if dist_mode:
         t = ms_step * 1e-3
         coll = {"effective_algbw_gbs": round(2 * n / t / 1e9, 1),
                 "busbw_gbs": round(2 * n / t / 1e9 * 2 * (world - 1) / world, 1),
@@ -672,24 +1003,30 @@ def run_ours(args, shape, rank, world, local_rank):
                 "nvlink_gbs_per_direction": 900.0,
                 "wire_frac_of_nvlink": round(wire / t / 1e9 / 900.0, 4)}
 
+    ttft = None
+    if dist_mode and not args.no_ttft:
+        del sets
+        torch.cuda.empty_cache()
+        ttft = ttft_block(torch, dist, args, world, dev)
+
     if rank != 0:
         return
-    cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(args.scheme, shape, nranks)
+    cpu = None if (args.no_cpu_baseline or dist_mode) else cpu_baseline(args.scheme, shape, nranks)
     line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
             "us_per_allreduce": round(ms_step * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (gaussian_with_outliers N(0,1) with 1% x100 outliers, "
                     "mx/synth.py), bf16 partial sums",
-            "config": config_dict(args, shape, world),
-            "wire_bytes_per_rank": ((nranks - 1) * S if args.algo == "oneshot" else
-                                    2 * (nranks - 1) * _native.shard_layout(
-                                        twoshot_chunk_values(n, nranks, sch.block_size),
-                                        sch.to_c())[2]),
+            "config": config_dict(args, shape, world, dist_mode, R),
+            "step_parity": parity,
+            "wire_bytes_per_rank": wire,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "reference_api_e2e": ref_api,
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
             "bf16_nccl_allreduce": bf16_ar, "symmetric_memory_fused": symm,
-            "collective": coll, "simulated_tp_fused_step": sim_more}
+            "collective": coll, "simulated_tp_fused_step": sim_more, "shape_70b": shape70,
+            "ttft": ttft}
     print(json.dumps(line), flush=True)
 
 
@@ -697,27 +1034,43 @@ def main():
     args = parse()
     shape = tuple(int(v) for v in args.shape.split(","))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    dist_mode = world > 1 or args.force_dist
     if args.algo == "auto":
-        tp = args.sim_ranks if world == 1 else world
+        tp = args.sim_ranks if not dist_mode else world
         args.algo = "oneshot" if tp <= 2 else "twoshot"
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, shape, rank, world)
         return
-    if world > 1:
+    if dist_mode:
         import torch
         import torch.distributed as dist
 
+        if world == 1:  # --force-dist: a world-1 group on this GPU
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(_free_port()))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, shape, rank, world, local_rank)
+        run_ours(args, shape, rank, world, local_rank, dist_mode)
     finally:
-        if world > 1:
+        if dist_mode:
             import torch.distributed as dist
 
             dist.destroy_process_group()
+
+
+def _free_port():
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
 if __name__ == "__main__":

@@ -21,5 +21,11 @@ from .codec import (CompressedTensor, DeviceCompressedTensor, block_error_bound,
 from .baselines import (ChannelIntPacket, TopKPacket, channelwise_int_compress,
                         channelwise_int_decompress, topk_compress, topk_decompress)
 from .errors import CompressionFactorTooHigh
+from .tp import (ReductionReport, TPConfig, parallelism_sweep, shard_rowwise,
+                 simulate_reduction)
+from .netbench import (BenchResult, LinkModel, calibrate_codec_throughput, predict_comm_time,
+                       predicted_speedup, run_allgather_bench)
+from .collective import (CompressedAllReduce, HostPipeline, LocalThreadGroup,
+                         SimulatedAllReduce, SymmetricAllReduce, compressed_all_reduce)
 
 __version__ = "0.1.0"

@@ -153,7 +153,7 @@ class CompressedAllReduce:
 
     def __init__(self, scheme, n: int, group=None, algo: str = "oneshot", out_dtype=None,
                  device=None, backend=None, world_size: int | None = None,
-                 rank: int | None = None):
+                 rank: int | None = None, comm=None):
         import torch
         import torch.distributed as dist
 
@@ -163,10 +163,28 @@ class CompressedAllReduce:
             raise ValueError(f"algo must be one of {ALGOS}")
         self.scheme = scheme
         self.group = group
-        self.world = world_size if world_size is not None else dist.get_world_size(group)
-        self.rank = rank if rank is not None else dist.get_rank(group)
+        # the exchange: torch.distributed (NCCL; gloo in the CPU tests) once a
+        # process group exists -- at every world size, so a world-1 NCCL run
+        # issues the same collectives as TP=N -- or any object with the same
+        # all_gather_into_tensor / all_to_all_single (LocalThreadGroup: N
+        # ranks as N threads on one GPU)
+        if comm is None and dist.is_available() and dist.is_initialized():
+            comm = dist
+        self.comm = comm
+        if comm is None or comm is dist:
+            self.world = world_size if world_size is not None else (
+                dist.get_world_size(group) if comm is not None else 1)
+            self.rank = rank if rank is not None else (
+                dist.get_rank(group) if comm is not None else 0)
+        else:
+            self.world = world_size if world_size is not None else comm.get_world_size()
+            self.rank = rank if rank is not None else comm.get_rank()
         if self.world < 1:
             raise MinimumDegreeTwo("world size must be positive")
+        if self.world > 1 and comm is None:
+            raise MinimumDegreeTwo("world size > 1 needs a process group or a comm object")
+        if not 0 <= self.rank < self.world:
+            raise ValueError(f"rank {self.rank} outside world size {self.world}")
         self.algo = algo
         self.n = int(n)
         self.out_dtype = out_dtype or torch.bfloat16
@@ -204,24 +222,22 @@ class CompressedAllReduce:
         return (N - 1) * S if self.algo == "oneshot" else 2 * (N - 1) * S
 
     def __call__(self, x, out=None):
-        import torch.distributed as dist
-
         if x.numel() != self.n:
             raise ShapeMismatch(f"expected {self.n} values, got {x.numel()}")
         xf = x.reshape(-1)
         out = self.out if out is None else out.reshape(-1)
-        p, be, N = self.plan, self.backend, self.plan.nranks
+        p, be, N, comm = self.plan, self.backend, self.plan.nranks, self.comm
         S = p.shard_bytes
         if self.algo == "oneshot":
             mine = self.gathered[self.rank * S:(self.rank + 1) * S]
             be.quantize_into(xf, mine, self.ws, self.flag)
-            if N > 1:
-                dist.all_gather_into_tensor(self.gathered, mine, group=self.group)
+            if comm is not None:
+                comm.all_gather_into_tensor(self.gathered, mine, group=self.group)
             be.dequant_sum(self.gathered, S, N, p.n, p.n, 0, out)
         else:
             be.quantize_chunks(xf, p.c, self.send, S, self.ws, self.flag)
-            if N > 1:
-                dist.all_to_all_single(self.recv, self.send, group=self.group)
+            if comm is not None:
+                comm.all_to_all_single(self.recv, self.send, group=self.group)
                 recv = self.recv
             else:
                 recv = self.send
@@ -229,20 +245,27 @@ class CompressedAllReduce:
             own = chunk_len(p.n, p.c, self.rank)
             if own > 0:
                 be.requant(recv, S, N, own, p.c, mine, self.ws, self.flag)
-            if N > 1:
-                dist.all_gather_into_tensor(self.gathered, mine, group=self.group)
+            if comm is not None:
+                comm.all_gather_into_tensor(self.gathered, mine, group=self.group)
             be.dequant_sum(self.gathered, 0, 1, p.n, p.c, S, out)
         return out.view(x.shape) if out.numel() == x.numel() else out
 
     def check_finite(self):
-        """Raise NonFiniteInput if any call since the last check saw NaN/Inf
-        (block index relative to the rank's partial, as _check_finite)."""
+        """Raise NonFiniteInput if any call since the last check saw NaN/Inf.
+        The flag holds the first flat index in this rank's partial (both
+        algorithms: K1 reports it; non-finite blocks are zeroed before the
+        exchange), so block_index = index // B as in _check_finite
+        (mx/codec.py:191-199)."""
         idx = int(self.flag.item())
         if idx >= 0:
             self.backend.reset_flag(self.flag)
-            blk = idx // self.scheme.block_size if self.algo == "oneshot" else None
             raise NonFiniteInput(f"non-finite value in a compressed all-reduce input "
-                                 f"(flat index {idx})", block_index=blk)
+                                 f"(flat index {idx})",
+                                 block_index=idx // self.scheme.block_size)
+
+    def check_status(self):
+        """NCCL reports its own failures; nothing to poll (API parity with
+        SymmetricAllReduce)."""
 
 
 def compressed_all_reduce(x, scheme, group=None, algo: str = "oneshot", out_dtype=None):
@@ -351,6 +374,134 @@ class SymmetricAllReduce:
             self.backend.reset_flag(self.flag)
             raise NonFiniteInput(f"non-finite value in a compressed all-reduce input "
                                  f"(flat index {idx})", block_index=idx // self.scheme.block_size)
+
+
+# ---------------------------------------------------------------------------
+# N ranks as N host threads on ONE device (the in-process transport)
+# ---------------------------------------------------------------------------
+
+
+class LocalThreadGroup:
+    """A process-group stand-in for N ranks that are N host threads sharing
+    one GPU -- the device form of the reference's in-process mailbox
+    transport (mx/netbench.py:186-203, N worker threads).
+
+    Each rank thread calls :meth:`bind` once and issues its work on its own
+    CUDA stream.  ``all_gather_into_tensor`` / ``all_to_all_single`` have
+    the torch.distributed signatures and semantics: every rank's input is
+    read after that rank's preceding work (CUDA events), the placement is a
+    stream-ordered device copy, and no rank proceeds (on the device) past
+    the collective until every peer has read its input -- so
+    :class:`CompressedAllReduce` runs its real NCCL code path, with the real
+    kernels, at any N on one GPU."""
+
+    def __init__(self, world_size: int, device=None, timeout: float = 120.0):
+        import threading
+
+        import torch
+
+        if world_size < 1:
+            raise MinimumDegreeTwo("world size must be positive")
+        self.world = int(world_size)
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self._tls = threading.local()
+        self._barrier = threading.Barrier(self.world, timeout=timeout)
+        self._slots = [None] * self.world
+        self._done = [None] * self.world
+
+    def bind(self, rank: int) -> None:
+        if not 0 <= rank < self.world:
+            raise ValueError(f"rank {rank} outside world size {self.world}")
+        self._tls.rank = rank
+
+    def get_rank(self, group=None) -> int:
+        return self._tls.rank
+
+    def get_world_size(self, group=None) -> int:
+        return self.world
+
+    def abort(self) -> None:
+        self._barrier.abort()
+
+    def _exchange(self, out, inp, place) -> None:
+        import torch
+
+        r = self._tls.rank
+        st = torch.cuda.current_stream(self.device)
+        ready = torch.cuda.Event()
+        ready.record(st)
+        self._slots[r] = (inp, ready)
+        self._barrier.wait()
+        for j in range(self.world):
+            src, ev = self._slots[j]
+            st.wait_event(ev)
+            place(j, src)
+        done = torch.cuda.Event()
+        done.record(st)
+        self._done[r] = done
+        self._barrier.wait()
+        for j in range(self.world):  # every peer has read my input
+            st.wait_event(self._done[j])
+
+    def all_gather_into_tensor(self, out, inp, group=None, async_op=False):
+        S = inp.numel()
+        if out.numel() != S * self.world:
+            raise ShapeMismatch("all_gather_into_tensor: output must hold world x input")
+
+        def place(j, src):
+            dst = out[j * S:(j + 1) * S]
+            if dst.data_ptr() != src.data_ptr():
+                dst.copy_(src, non_blocking=True)
+
+        self._exchange(out, inp, place)
+
+    def all_to_all_single(self, out, inp, group=None, async_op=False):
+        S = inp.numel() // self.world
+        if inp.numel() != S * self.world or out.numel() != inp.numel():
+            raise ShapeMismatch("all_to_all_single: equal splits of world chunks")
+        r = self._tls.rank
+
+        def place(j, src):
+            out[j * S:(j + 1) * S].copy_(src[r * S:(r + 1) * S], non_blocking=True)
+
+        self._exchange(out, inp, place)
+
+    def run(self, fn):
+        """Run ``fn(rank)`` on one thread per rank, each bound to its rank
+        and its own stream; returns the results in rank order and re-raises
+        the first failure (the barrier is aborted so no thread hangs)."""
+        import threading
+
+        import torch
+
+        res = [None] * self.world
+        errs = []
+
+        def work(r):
+            try:
+                torch.cuda.set_device(self.device)
+                self.bind(r)
+                with torch.cuda.stream(torch.cuda.Stream(self.device)):
+                    res[r] = fn(r)
+                    torch.cuda.current_stream(self.device).synchronize()
+            except threading.BrokenBarrierError as e:
+                errs.append((r, e))
+            except BaseException as e:  # noqa: BLE001
+                errs.append((r, e))
+                self._barrier.abort()
+
+        ts = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(self.world)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        if errs:
+            root = next((e for r, e in errs if not isinstance(e, threading.BrokenBarrierError)),
+                        errs[0][1])
+            self._barrier.reset()
+            raise root
+        return res
 
 
 # ---------------------------------------------------------------------------
@@ -490,11 +641,18 @@ class HostPipeline:
     MAX_GRAPHS = 8  # captured host-buffer sets kept (LRU)
 
     def __init__(self, make_op, n: int, ninputs: int, in_dtype=None, out_dtype=None,
-                 device="cuda", chunks=4, graph: bool = True, h2d_streams: int = 1):
+                 device="cuda", chunks=4, graph: bool = True, h2d_streams: int = 1,
+                 collective: bool = False):
         import torch
 
         self.n, self.nin = int(n), int(ninputs)
         self.use_graph = graph
+        # ops holding NCCL collectives: a graph-cache miss captures WITHOUT
+        # an eager warm-up issue, so every call runs each collective exactly
+        # once whether this rank hit or missed its (rank-local) graph cache
+        # and whether its host buffers were pinned -- ranks can never issue
+        # different numbers of collectives
+        self.collective = bool(collective)
         self._graphs = {}
         if isinstance(chunks, (list, tuple)):
             # explicit piece weights, e.g. (1, 3, 3, 1): small first and last
@@ -559,7 +717,8 @@ class HostPipeline:
         key = tuple(h.data_ptr() for h in hin) + (hout.data_ptr(),)
         g = self._graphs.pop(key, None)
         if g is None:
-            self._issue(hin, hout)  # first-call allocations happen eagerly
+            if not self.collective:
+                self._issue(hin, hout)  # first-call allocations happen eagerly
             torch.cuda.synchronize(self.device)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
@@ -617,13 +776,22 @@ class HostPipeline:
 
         out_dtype = out_dtype or torch.bfloat16
 
+        import torch.distributed as dist
+
         def make(c):
             op = CompressedAllReduce(scheme, c, group=group, algo=algo, out_dtype=out_dtype,
                                      device=device)
             return lambda ins, out: op(ins[0], out)
 
-        return cls(make, n, 1, torch.bfloat16, out_dtype, device or "cuda", chunks, graph,
-                   h2d_streams)
+        pipe = cls(make, n, 1, torch.bfloat16, out_dtype, device or "cuda", chunks, graph,
+                   h2d_streams, collective=True)
+        if graph and dist.is_initialized() and dist.get_world_size(group) > 1:
+            # the communicator exists before the first capture (NCCL cannot
+            # be initialised inside a graph capture)
+            t = torch.zeros(1, device=pipe.device)
+            dist.all_reduce(t, group=group)
+            torch.cuda.synchronize(pipe.device)
+        return pipe
 
 
 def simulate_allreduce(partials, scheme, algo: str = "oneshot", out_dtype=None, backend=None):
@@ -672,35 +840,6 @@ class BlockWire:
         return decompress_tensor_device(deserialize(data), torch.float32).cpu().numpy()
 
 
-@dataclass(frozen=True)
-class LinkModel:
-    """mx/netbench.py:57-72"""
-
-    bandwidth: float
-    latency: float = 0.0
-    compress_throughput: float = math.inf
-    decompress_throughput: float = math.inf
-
-    def __post_init__(self):
-        if not self.bandwidth > 0:
-            raise ValueError("bandwidth must be positive")
-        if self.latency < 0:
-            raise ValueError("latency cannot be negative")
-        if not (self.compress_throughput > 0 and self.decompress_throughput > 0):
-            raise ValueError("codec throughputs must be positive")
-
-
-def predict_comm_time(tensor_bytes: int, scheme, n_workers: int, link: LinkModel) -> float:
-    """Full-mesh model of mx/netbench.py:480-505 (one compress, N-1 decodes)."""
-    from .codec import serialized_nbytes
-
-    if n_workers < 2:
-        raise MinimumDegreeTwo(f"need at least 2 workers, got {n_workers}")
-    peers = n_workers - 1
-    base = peers * link.latency
-    if scheme is None:
-        return base + peers * tensor_bytes / link.bandwidth
-    values = tensor_bytes // 2
-    wire = serialized_nbytes(scheme, (values,))
-    return (base + peers * wire / link.bandwidth + values / link.compress_throughput
-            + peers * values / link.decompress_throughput)
+# LinkModel / predict_comm_time live in netbench.py (the reference module's
+# name); re-exported here for callers of round 1's location
+from .netbench import LinkModel, predict_comm_time  # noqa: E402,F401

@@ -358,7 +358,9 @@ __global__ void __launch_bounds__(TH, (ENC == ENC_E2M1 && B == 64) ? 1024 / TH :
 // buffering: rank r writes slot e&1 at epoch e only after its epoch e-1
 // launch saw every peer's epoch e-1 flag for the same CTA, i.e. after every
 // peer had finished epoch e-2, the last reader of slot e&1.  A wait that
-// exceeds ~2 s sets *status and proceeds (no hang; the host reports it).
+// exceeds the timeout (MXB200_SYMM_TIMEOUT_MS, default 30 s) sets *status
+// and proceeds (no hang); the host raises on it (check_status(), which the
+// TP hook calls once per forward).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
   unsigned int v;
@@ -367,6 +369,11 @@ __device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
 }
 __device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 template <typename OutT, int B, int ENC, int BITS>
@@ -427,10 +434,10 @@ __global__ void __launch_bounds__(kThreads) k_symm_flow(const SArgs S) {
     if (S.full_fence) __threadfence_system();
     st_release_sys(S.flags[j] + (size_t)S.rank * G + b, e);
     const unsigned int* mine = S.flags[S.rank] + (size_t)j * G + b;
-    const long long t0 = clock64();
+    const unsigned long long t0 = globaltimer_ns();
     while ((int)(ld_acquire_sys(mine) - e) < 0) {
       __nanosleep(32);
-      if (clock64() - t0 > 4000000000ll) {  // ~2 s: report, do not hang
+      if (globaltimer_ns() - t0 > S.timeout_ns) {  // report, do not hang
         atomicExch(S.status, 1u);
         break;
       }
@@ -524,10 +531,10 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
       if (S.full_fence) __threadfence_system();
       st_release_sys(S.flags[j] + ((size_t)which * nr + me) * G + b, e);
       const unsigned int* w = S.flags[me] + ((size_t)which * nr + j) * G + b;
-      const long long t0 = clock64();
+      const unsigned long long t0 = globaltimer_ns();
       while ((int)(ld_acquire_sys(w) - e) < 0) {
         __nanosleep(32);
-        if (clock64() - t0 > 4000000000ll) {
+        if (globaltimer_ns() - t0 > S.timeout_ns) {
           atomicExch(S.status, 1u);
           break;
         }

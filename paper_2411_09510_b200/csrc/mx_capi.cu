@@ -298,6 +298,18 @@ int symm_full_fence() {
   return v;
 }
 
+// peer flag wait limit of the NVLink kernels before they report a timeout
+// (status word) instead of hanging: MXB200_SYMM_TIMEOUT_MS, default 30 s
+unsigned long long symm_timeout_ns() {
+  static long long v = -1;
+  if (v < 0) {
+    const char* e = getenv("MXB200_SYMM_TIMEOUT_MS");
+    v = e ? atoll(e) : 30000;
+    if (v < 1) v = 1;
+  }
+  return (unsigned long long)v * 1000000ull;
+}
+
 // block sizes with a fast (template) kernel
 bool fast_block(int64_t block) { return block == 8 || block == 16 || block == 32 || block == 64; }
 
@@ -645,6 +657,7 @@ int mx_allreduce_symm(const void* x, int32_t dtype, int64_t n, const mx_scheme_t
   a.scale_off = so; a.elem_off = eo; a.out = out; a.status = status;
   a.epoch = epochs; a.nonfinite = reinterpret_cast<unsigned long long*>(nonfinite); a.f = f;
   a.full_fence = symm_full_fence();
+  a.timeout_ns = symm_timeout_ns();
   if (!launch_symm_oneshot(a, out_dtype == MX_BF16, (int)s->block_size, enc_of(s), f.bits,
                            (cudaStream_t)stream))
     return fail(MX_ERR_UNSUPPORTED, "symmetric path: scheme not instantiated");
@@ -697,6 +710,7 @@ int mx_allreduce_symm_twoshot(const void* x, int32_t dtype, int64_t n, const mx_
   a.scale_off = so; a.elem_off = eo; a.out = out; a.status = status; a.epoch = epochs;
   a.nonfinite = reinterpret_cast<unsigned long long*>(nonfinite); a.f = f;
   a.full_fence = symm_full_fence();
+  a.timeout_ns = symm_timeout_ns();
   if (!launch_symm_twoshot(a, out_dtype == MX_BF16, (int)s->block_size, enc_of(s), f.bits,
                            (cudaStream_t)stream))
     return fail(MX_ERR_UNSUPPORTED, "two-shot symmetric path: scheme not instantiated");

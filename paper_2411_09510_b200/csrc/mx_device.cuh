@@ -321,13 +321,21 @@ __device__ __forceinline__ void store8(T* __restrict__ out, int64_t g, int valid
 }
 
 // k-bit scale code `blk` of a packed scale stream (LSB-first).
-__device__ __forceinline__ int read_scale(const uint8_t* __restrict__ sc, int64_t blk, int k) {
-  if (k == 8) return sc[blk];
+template <bool CG = false>
+__device__ __forceinline__ uint8_t ld_byte(const uint8_t* p) {
+  if constexpr (CG) return __ldcg(p);
+  else return *p;
+}
+
+// k-bit scale code of block blk (CG: the stream was written in this kernel)
+template <bool CG = false>
+__device__ __forceinline__ int read_scale(const uint8_t* sc, int64_t blk, int k) {
+  if (k == 8) return ld_byte<CG>(sc + blk);
   int64_t bit = blk * k;
   int64_t byte = bit >> 3;
   int sh = (int)(bit & 7);
-  uint32_t w = sc[byte];
-  if (sh + k > 8) w |= (uint32_t)sc[byte + 1] << 8;
+  uint32_t w = ld_byte<CG>(sc + byte);
+  if (sh + k > 8) w |= (uint32_t)ld_byte<CG>(sc + byte + 1) << 8;
   return (int)((w >> sh) & ((1u << k) - 1u));
 }
 

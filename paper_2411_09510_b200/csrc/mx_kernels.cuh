@@ -357,7 +357,21 @@ __device__ __forceinline__ void store_lane_codes(uint8_t* __restrict__ p, const 
   }
 }
 
-template <int BITS>
+// Loads of shard bytes.  CG = false: the non-coherent read-only path
+// (ld.global.nc), ONLY for data no thread anywhere writes during the kernel.
+// CG = true: ld.global.cg (weak, L1-bypassing, coherent at L2) for bytes
+// written earlier in the SAME kernel -- by this warp (the fused one-device
+// flow) or by a peer GPU over NVLink after a flag acquire (k_symm_flow /
+// k_symm2_flow).  A weak load ordered after an acquire (directly, or through
+// bar.sync from the acquiring thread) is inside the PTX memory model; an .nc
+// load is not, and its cached line may be stale.
+template <bool CG, typename T>
+__device__ __forceinline__ T ldro(const T* p) {
+  if constexpr (CG) return __ldcg(p);
+  else return __ldg(p);
+}
+
+template <int BITS, bool CG = false>
 __device__ __forceinline__ LaneCodes<BITS> load_lane_codes(const uint8_t* __restrict__ p,
                                                            int valid) {
   LaneCodes<BITS> c;
@@ -365,40 +379,31 @@ __device__ __forceinline__ LaneCodes<BITS> load_lane_codes(const uint8_t* __rest
   for (int i = 0; i < BITS; ++i) c.w[i] = 0u;
   if (valid == kVPL) {
     if constexpr (BITS == 8) {
-      uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
-      uint4 b = __ldg(reinterpret_cast<const uint4*>(p) + 1);
+      uint4 a = ldro<CG>(reinterpret_cast<const uint4*>(p));
+      uint4 b = ldro<CG>(reinterpret_cast<const uint4*>(p) + 1);
       c.w[0] = a.x; c.w[1] = a.y; c.w[2] = a.z; c.w[3] = a.w;
       c.w[4] = b.x; c.w[5] = b.y; c.w[6] = b.z; c.w[7] = b.w;
     } else if constexpr (BITS == 4) {
-      uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
+      uint4 a = ldro<CG>(reinterpret_cast<const uint4*>(p));
       c.w[0] = a.x; c.w[1] = a.y; c.w[2] = a.z; c.w[3] = a.w;
     } else if constexpr (BITS % 2 == 0) {
 #pragma unroll
       for (int i = 0; i < BITS / 2; ++i) {
-        uint2 a = __ldg(reinterpret_cast<const uint2*>(p) + i);
+        uint2 a = ldro<CG>(reinterpret_cast<const uint2*>(p) + i);
         c.w[2 * i] = a.x;
         c.w[2 * i + 1] = a.y;
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < BITS; ++i) c.w[i] = __ldg(reinterpret_cast<const uint32_t*>(p) + i);
+      for (int i = 0; i < BITS; ++i) c.w[i] = ldro<CG>(reinterpret_cast<const uint32_t*>(p) + i);
     }
   } else if (valid > 0) {
     const int nb = (valid * BITS + 7) / 8;
 #pragma unroll
     for (int i = 0; i < 4 * BITS; ++i)
-      if (i < nb) c.w[i >> 2] |= (uint32_t)p[i] << (8 * (i & 3));
+      if (i < nb) c.w[i >> 2] |= (uint32_t)ldro<CG>(p + i) << (8 * (i & 3));
   }
   return c;
-}
-
-// Read-only loads for K2.  CG = true uses ld.global.cg (L2, coherent) for
-// data written earlier in the SAME kernel (the fused collective's phase 2);
-// otherwise the non-coherent read-only path.
-template <bool CG, typename T>
-__device__ __forceinline__ T ldro(const T* p) {
-  if constexpr (CG) return __ldcg(p);
-  else return __ldg(p);
 }
 
 // The lane's 16 codes (2b bytes at p = unit base + 2b*lane) for K2.
@@ -429,7 +434,7 @@ __device__ __forceinline__ LaneCodes<BITS, 16> load_lane_codes16(const uint8_t* 
     const int nb = (valid * BITS + 7) / 8;
 #pragma unroll
     for (int i = 0; i < 2 * BITS; ++i)
-      if (i < nb) c.w[i >> 2] |= (uint32_t)p[i] << (8 * (i & 3));
+      if (i < nb) c.w[i >> 2] |= (uint32_t)ldro<CG>(p + i) << (8 * (i & 3));
   }
   return c;
 }
@@ -792,7 +797,7 @@ __device__ __forceinline__ void load_rank(RankLoad<B, BITS, VPL>& r,
   constexpr int LPB = Geo<B, VPL>::LPB;
   const uint8_t* el = base + elem_off + (uoff / 8) * BITS + lane * (VPL * BITS / 8);
   if constexpr (VPL == 16) r.c = load_lane_codes16<BITS, CG>(el, valid);
-  else r.c = load_lane_codes<BITS>(el, valid);
+  else r.c = load_lane_codes<BITS, CG>(el, valid);
   const uint8_t* sc = base + scale_off;
   const int64_t blk0 = uoff / B + (lane / LPB) * NSB;
 #pragma unroll
@@ -817,7 +822,7 @@ __device__ __forceinline__ void load_rank(RankLoad<B, BITS, VPL>& r,
   } else if (valid > 0) {
 #pragma unroll
     for (int sb = 0; sb < NSB; ++sb)
-      if (sb * Geo<B, VPL>::SBV < valid) r.st[sb] = read_scale(sc, blk0 + sb, kbits);
+      if (sb * Geo<B, VPL>::SBV < valid) r.st[sb] = read_scale<CG>(sc, blk0 + sb, kbits);
   }
 }
 
@@ -1182,6 +1187,7 @@ struct SArgs {
   unsigned long long* nonfinite;
   Fmt f;
   int full_fence;                // 1: extra fence.sc.sys around the flags (MXB200_SYMM_FENCE=1)
+  unsigned long long timeout_ns; // peer flag wait limit (MXB200_SYMM_TIMEOUT_MS)
 };
 // two-shot over symmetric memory (k_fused.cuh, k_symm2_flow)
 struct S2Args {
@@ -1199,6 +1205,7 @@ struct S2Args {
   unsigned long long* nonfinite;
   Fmt f;
   int full_fence;
+  unsigned long long timeout_ns;
 };
 bool launch_symm_twoshot(const S2Args& a, int out_is_bf16, int block, int enc, int bits,
                          cudaStream_t st);

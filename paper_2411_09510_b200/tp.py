@@ -264,9 +264,12 @@ class _ChannelIntCodec:
         return rec.cpu().numpy().reshape(p.shape), header_nbytes(p.ndim) + 2 * s.numel() + c.numel()
 
 
-def resolve_codec(scheme):
+def resolve_codec(scheme, extensions: bool = False):
     """A SchemeDescriptor or codec id -> codec object (mx/tpsim.py:128-143):
-    MX schemes, ``passthrough``/``none``, ``fp16``, ``topk:F``, ``chanint:B``."""
+    MX schemes, ``passthrough``/``none``, ``fp16``, ``topk:F``, ``chanint:B``.
+    Scheme ids resolve through the reference registry, so unknown ids (and
+    the FP6 / INT8 extension formats) raise UnknownScheme as in the
+    reference; ``extensions=True`` opts in to the extension formats."""
     from .errors import UnknownScheme
 
     if isinstance(scheme, SchemeDescriptor):
@@ -282,7 +285,7 @@ def resolve_codec(scheme):
         return _TopKCodec(float(name.split(":", 1)[1]))
     if name.startswith("chanint:"):
         return _ChannelIntCodec(int(name.split(":", 1)[1]))
-    return _MxCodec(parse_scheme(name, extensions=True))
+    return _MxCodec(parse_scheme(name, extensions=extensions))
 
 
 def simulate_reduction(cfg: TPConfig, x=None, w=None, partials_on_gpu: bool = False,
@@ -452,6 +455,28 @@ def make_module_classes():
         def forward(self, x):
             return self.reduce(F.linear(x, self.weight))
 
+        def collectives(self):
+            return list(self._car.values())
+
+    def check_collectives(cars):
+        """Deferred health check of compressed all-reduces: ONE device->host
+        read covers every op's sticky non-finite flag and every NVLink op's
+        peer-wait status; raises NonFiniteInput / RuntimeError (a timed-out
+        peer wait means that call's result is invalid)."""
+        cars = list({id(c): c for c in cars}.values())
+        if not cars:
+            return
+        parts = [c.flag.reshape(1) for c in cars]
+        symm = [c for c in cars if hasattr(c, "state")]
+        parts += [c.state[:1].to(torch.int64) for c in symm]
+        v = torch.cat(parts).cpu().tolist()
+        for c, s in zip(symm, v[len(cars):]):
+            if s != 0:
+                c.check_status()
+        for c, f in zip(cars, v[:len(cars)]):
+            if f >= 0:
+                c.check_finite()
+
     class ColumnParallelLinear(nn.Module):
         def __init__(self, d_in, d_out_local, device="cuda", dtype=torch.bfloat16, std=0.02):
             super().__init__()
@@ -513,9 +538,11 @@ def make_module_classes():
         TTFT of the transformer body, where the all-reduces live)."""
 
         def __init__(self, cfg: LlamaConfig, tp: int = 1, group=None, scheme=None,
-                     algo="oneshot", layers=None, device="cuda", dtype=torch.bfloat16):
+                     algo="oneshot", layers=None, device="cuda", dtype=torch.bfloat16,
+                     check_health: bool = True):
             super().__init__()
             self.cfg = cfg
+            self.check_health = check_health
             self.blocks = nn.ModuleList(LlamaTPBlock(cfg, tp, group, scheme, algo, device, dtype)
                                         for _ in range(layers or cfg.layers))
             self.norm = RMSNorm(cfg.hidden, cfg.eps, device, dtype)
@@ -532,7 +559,21 @@ def make_module_classes():
             cos, sin = self.rope_cache(h.shape[1], h.device, h.dtype)
             for blk in self.blocks:
                 h = blk(h, cos, sin)
-            return self.norm(h)
+            out = self.norm(h)
+            # once per forward: the compressed all-reduces' sticky non-finite
+            # flags and NVLink peer-wait status (one host read; skipped while
+            # a CUDA graph is being captured -- check_collectives() after
+            # the replays instead)
+            if self.check_health and not torch.cuda.is_current_stream_capturing():
+                self.check_collectives()
+            return out
+
+        def collectives(self):
+            return [c for blk in self.blocks for m in (blk.o_proj, blk.down_proj)
+                    for c in m.collectives()]
+
+        def check_collectives(self):
+            check_collectives(self.collectives())
 
     return RowParallelLinear, ColumnParallelLinear, LlamaTPBlock, LlamaTP
 
@@ -576,6 +617,8 @@ def measure_ttft(cfg: LlamaConfig, batch: int, seq: int, tp: int = 1, group=None
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
+        # graph replays skip the per-forward check: one check after them
+        model.check_collectives()
     ms = float(np.median(times))
     if dist.is_initialized():
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)

@@ -162,6 +162,31 @@ int mx_allreduce_fused(const void* const* partials, int32_t dtype, int32_t nrank
                        void* out, int32_t out_dtype, uint32_t* barrier, uint64_t* nonfinite,
                        void* stream);
 
+/* Row-parallel GEMM with the MX quantiser fused into its epilogue -- the
+ * producer side of the compressed all-reduce: the reference computes the
+ * rank's partial and encodes it (mx/tpsim.py:263-265, `partial = x_shard @
+ * shards[rank]` -> `wire.encode(partial)` = compress_tensor, mx/codec.py:
+ * 238-263).  partial[M, N] = x[M, K] . w[N, K]^T (F.linear of a row-parallel
+ * weight shard; bf16 operands, row-major, fp32 accumulation on the tcgen05
+ * tensor cores); the MX streams of bf16(partial) (flat row-major order) are
+ * written to scale_stream / element_stream -- byte-identical to
+ * mx_quantize of that bf16 tensor.  `partial` (bf16 [M, N], nullable)
+ * additionally receives the bf16 partial.  scheme == NULL: plain GEMM,
+ * `partial` required.  Requires K % 64 == 0, N % 128 == 0, 16-byte aligned
+ * operands, E8M0 scales, B in {16, 32}; else MX_ERR_UNSUPPORTED. */
+int mx_gemm_quantize(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
+                     const mx_scheme_t* scheme, uint8_t* scale_stream, uint8_t* element_stream,
+                     void* partial, uint64_t* nonfinite, void* stream);
+
+/* The same GEMM writing chunked shards like mx_quantize_chunks (the
+ * two-shot send buffer, or one shard slot of the one-shot gather buffer with
+ * chunk_values >= M*N): chunk j of the flat partial goes to
+ * shards + j*shard_stride with mx_shard_layout(chunk_values) offsets. */
+int mx_gemm_quantize_chunks(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
+                            int64_t chunk_values, const mx_scheme_t* scheme, uint8_t* shards,
+                            int64_t shard_stride, void* partial, uint64_t* nonfinite,
+                            void* stream);
+
 /* Sizes of the symmetric-memory collective for n values and nranks ranks:
  * every rank allocates one symmetric buffer of *buffer_bytes holding two
  * shard slots of *slot_stride bytes (double buffering) followed, at

@@ -67,6 +67,10 @@ SIGNATURES = {
     "mx_topk_workspace_bytes": (c_i32, [c_i64, c_i64p]),
     "mx_topk_compress": (c_i32, [c_vp, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "mx_topk_decompress": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i32, c_vp]),
+    "mx_gemm_quantize": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i64, _SP, c_vp, c_vp, c_vp, c_vp,
+                                 c_vp]),
+    "mx_gemm_quantize_chunks": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, _SP, c_vp, c_i64,
+                                        c_vp, c_vp, c_vp]),
     "mx_memset_async": (c_i32, [c_vp, c_i32, c_i64, c_vp]),
     "mx_nonfinite_reset": (c_i32, [c_vp, c_vp]),
 }

@@ -23,7 +23,7 @@ OUT = os.path.join(HERE, "libmxb200.so")
 BUILD = os.environ.get("MXB200_BUILD_DIR", "/tmp/mxb200_build")
 # -lineinfo (ncu source view) only where the profiled kernels live: it
 # roughly doubles object size
-LINEINFO = {"k_quant_bf16.cu", "k_dqsum_bf16.cu", "k_fused_inst.cu", "k_requant.cu"}
+LINEINFO = {"k_quant_bf16.cu", "k_dqsum_bf16.cu", "k_fused_inst.cu", "k_requant.cu", "k_gemm.cu"}
 # sources compiled several times with -D slices (template instantiation split
 # so the slices build in parallel)
 VARIANTS = {

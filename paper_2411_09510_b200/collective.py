@@ -112,6 +112,38 @@ class NativeBackend:
     def reset_flag(self, flag):
         _native.check(self.lib.mx_nonfinite_reset(self._p(flag), self._st()), "mx_nonfinite_reset")
 
+    def gemm_supported(self, x, w) -> bool:
+        """Whether the tcgen05 GEMM with the fused quantiser (k_gemm.cu)
+        covers x[M, K] . w[N, K]^T under this scheme (else the caller runs
+        F.linear + K1)."""
+        import torch
+
+        sch = self.scheme
+        el = sch.to_c()
+        fmt = (el.kind, el.exponent_bits, el.mantissa_bits)  # kind 0 float, 1 int
+        ok_fmt = {(0, 2, 1), (0, 2, 3), (0, 3, 2), (0, 2, 2), (1, 0, 7)}
+        if sch.block_size == 16:
+            ok_fmt = {(0, 2, 1), (1, 0, 7)}
+        elif sch.block_size != 32:
+            return False
+        K = x.shape[-1]
+        return (el.scale_bits == 8 and fmt in ok_fmt and x.dtype == torch.bfloat16
+                and w.dtype == torch.bfloat16 and x.is_cuda and w.is_cuda and w.dim() == 2
+                and w.shape[1] == K and K % 64 == 0 and w.shape[0] % 128 == 0
+                and x.is_contiguous() and w.is_contiguous()
+                and x.data_ptr() % 16 == 0 and w.data_ptr() % 16 == 0)
+
+    def gemm_quantize_chunks(self, x2, w, c, shards, shard_stride, flag, partial=None):
+        """k_gemm_mx: partial = x2 . w^T on the tensor cores, its MX shard(s)
+        written straight from the accumulator (chunk j of c values at
+        shards + j*shard_stride)."""
+        M, K = x2.shape
+        N = w.shape[0]
+        _native.check(self.lib.mx_gemm_quantize_chunks(
+            self._p(x2), self._p(w), M, N, K, c, ctypes.byref(self.cs), self._p(shards),
+            shard_stride, self._p(partial) if partial is not None else None,
+            self._p(flag) if flag is not None else None, self._st()), "mx_gemm_quantize_chunks")
+
     def allreduce_fused(self, ptrs, dtype, nranks, n, shards, stride, out, barrier, flag):
         """One persistent kernel: quantise the local partials, grid barrier,
         dequant-sum.  Returns False when the scheme/dtype has no fused
@@ -224,18 +256,47 @@ class CompressedAllReduce:
     def __call__(self, x, out=None):
         if x.numel() != self.n:
             raise ShapeMismatch(f"expected {self.n} values, got {x.numel()}")
-        xf = x.reshape(-1)
+        out = self._reduce(x.reshape(-1), None, out)
+        return out.view(x.shape) if out.numel() == x.numel() else out
+
+    def linear(self, x, weight, out=None):
+        """all_reduce(F.linear(x, weight)) -- the row-parallel hook
+        (mx/tpsim.py:263-265) with the quantiser fused into the GEMM
+        epilogue (k_gemm.cu, tcgen05 + TMA): the bf16 partial is never
+        written; the shard comes straight out of the accumulator, then the
+        exchange and dequant-sum run as in __call__.  Falls back to
+        F.linear + __call__ where the fused GEMM does not apply."""
+        import torch.nn.functional as F
+
+        K = x.shape[-1]
+        N = weight.shape[0]
+        M = x.numel() // K if K else 0
+        if M * N != self.n:
+            raise ShapeMismatch(f"expected {self.n} output values, got {M}x{N}")
+        be = self.backend
+        if not (hasattr(be, "gemm_supported") and be.gemm_supported(x, weight)):
+            return self(F.linear(x, weight), out)
+        res = self._reduce(None, (x.reshape(M, K), weight), out)
+        return res.view(*x.shape[:-1], N)
+
+    def _reduce(self, xf, gemm, out):
         out = self.out if out is None else out.reshape(-1)
         p, be, N, comm = self.plan, self.backend, self.plan.nranks, self.comm
         S = p.shard_bytes
         if self.algo == "oneshot":
             mine = self.gathered[self.rank * S:(self.rank + 1) * S]
-            be.quantize_into(xf, mine, self.ws, self.flag)
+            if gemm is None:
+                be.quantize_into(xf, mine, self.ws, self.flag)
+            else:
+                be.gemm_quantize_chunks(gemm[0], gemm[1], p.n, mine, S, self.flag)
             if comm is not None:
                 comm.all_gather_into_tensor(self.gathered, mine, group=self.group)
             be.dequant_sum(self.gathered, S, N, p.n, p.n, 0, out)
         else:
-            be.quantize_chunks(xf, p.c, self.send, S, self.ws, self.flag)
+            if gemm is None:
+                be.quantize_chunks(xf, p.c, self.send, S, self.ws, self.flag)
+            else:
+                be.gemm_quantize_chunks(gemm[0], gemm[1], p.c, self.send, S, self.flag)
             if comm is not None:
                 comm.all_to_all_single(self.recv, self.send, group=self.group)
                 recv = self.recv
@@ -248,7 +309,7 @@ class CompressedAllReduce:
             if comm is not None:
                 comm.all_gather_into_tensor(self.gathered, mine, group=self.group)
             be.dequant_sum(self.gathered, 0, 1, p.n, p.c, S, out)
-        return out.view(x.shape) if out.numel() == x.numel() else out
+        return out
 
     def check_finite(self):
         """Raise NonFiniteInput if any call since the last check saw NaN/Inf.

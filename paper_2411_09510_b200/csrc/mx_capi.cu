@@ -180,6 +180,12 @@ __global__ void g_pack(const uint8_t* codes, int64_t count, int width, uint8_t* 
 
 __global__ void g_fill_u64(unsigned long long* p, unsigned long long v) { *p = v; }
 
+// k_gemm.cu
+cudaError_t launch_gemm_mx(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
+                           const Fmt* f, int enc, int64_t chunk_values, int64_t chunk_stride,
+                           uint8_t* scale_out, uint8_t* elem_out, void* partial_out,
+                           unsigned long long* nonfinite, cudaStream_t st);
+
 }  // namespace mxb
 
 // ===========================================================================
@@ -613,6 +619,59 @@ int mx_allreduce_fused(const void* const* partials, int32_t dtype, int32_t nrank
                             (cudaStream_t)stream))
     return fail(MX_ERR_UNSUPPORTED, "fused path: element width %d not instantiated", f.bits);
   return cuda_check("k_fused_oneshot");
+}
+
+static int gemm_impl(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
+                     const mx_scheme_t* s, int64_t cv, int64_t cs, uint8_t* scale_stream,
+                     uint8_t* element_stream, void* partial, uint64_t* nonfinite, void* stream) {
+  if (s) {
+    int rc = check_scheme(s);
+    if (rc) return rc;
+    if (!scale_stream || !element_stream) return fail(MX_ERR_INVALID_ARGUMENT, "NULL stream buffer");
+  } else if (!partial) {
+    return fail(MX_ERR_INVALID_ARGUMENT, "plain GEMM needs a partial buffer");
+  }
+  if (!x || !w) return fail(MX_ERR_INVALID_ARGUMENT, "NULL operand");
+  if (M < 1 || N < 1 || K < 1) return fail(MX_ERR_INVALID_ARGUMENT, "bad sizes");
+  if (partial && !aligned(partial, 16)) return fail(MX_ERR_INVALID_ARGUMENT, "partial not 16-byte aligned");
+  Fmt f;
+  if (s) f = make_fmt(s);
+  cudaError_t e = launch_gemm_mx(x, w, M, N, K, s ? &f : nullptr, s ? enc_of(s) : 0, cv, cs,
+                                 scale_stream, element_stream,
+                                 partial, reinterpret_cast<unsigned long long*>(nonfinite),
+                                 (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported)
+    return fail(MX_ERR_UNSUPPORTED,
+                "fused GEMM: needs K %% 64 == 0, N %% 128 == 0, 16-byte aligned operands, "
+                "E8M0 scales, B in {16, 32}, element format fp4_e2m1/fp6/fp5_e2m2/int8");
+  if (e != cudaSuccess) return fail(MX_ERR_CUDA, "k_gemm_mx: %s", cudaGetErrorString(e));
+  return cuda_check("k_gemm_mx");
+}
+
+int mx_gemm_quantize(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
+                     const mx_scheme_t* s, uint8_t* scale_stream, uint8_t* element_stream,
+                     void* partial, uint64_t* nonfinite, void* stream) {
+  return gemm_impl(x, w, M, N, K, s, M * N, 0, scale_stream, element_stream, partial, nonfinite,
+                   stream);
+}
+
+int mx_gemm_quantize_chunks(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
+                            int64_t chunk_values, const mx_scheme_t* s, uint8_t* shards,
+                            int64_t shard_stride, void* partial, uint64_t* nonfinite,
+                            void* stream) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (!shards) return fail(MX_ERR_INVALID_ARGUMENT, "NULL shards");
+  if (chunk_values < 1 || (chunk_values < M * N && chunk_values % (8 * s->block_size) != 0))
+    return fail(MX_ERR_INVALID_ARGUMENT,
+                "chunk_values must be >= M*N or a positive multiple of 8*block_size");
+  int64_t so, eo, sbytes;
+  mx_shard_layout(chunk_values, s, &so, &eo, &sbytes);
+  const int64_t nchunks = (M * N + chunk_values - 1) / chunk_values;
+  if (nchunks > 1 && (shard_stride < sbytes || shard_stride % 32 != 0))
+    return fail(MX_ERR_INVALID_ARGUMENT, "shard_stride must be >= shard bytes and 32-aligned");
+  return gemm_impl(x, w, M, N, K, s, chunk_values, shard_stride, shards + so, shards + eo,
+                   partial, nonfinite, stream);
 }
 
 int mx_symm_layout(int64_t n, const mx_scheme_t* s, int32_t nranks, int64_t* slot_stride,

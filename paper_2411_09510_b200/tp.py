@@ -20,6 +20,8 @@ Two halves:
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -413,23 +415,24 @@ def make_module_classes():
         for one-shot up to TP=2 and two-shot beyond."""
 
         def __init__(self, d_in_local, d_out, group=None, scheme=None, algo="oneshot",
-                     tokens=None, device="cuda", dtype=torch.bfloat16, std=0.02):
+                     tokens=None, device="cuda", dtype=torch.bfloat16, std=0.02,
+                     fused_gemm=None):
             super().__init__()
             self.weight = nn.Parameter(torch.randn(d_out, d_in_local, device=device, dtype=dtype)
                                        * std, requires_grad=False)
             self.group, self.scheme, self.algo = group, scheme, algo
+            # the quantiser fused into the GEMM epilogue (k_gemm.cu) for the
+            # NCCL algorithms; MXB200_GEMM_FUSED=0 selects F.linear + K1
+            self.fused_gemm = (os.environ.get("MXB200_GEMM_FUSED", "1") != "0"
+                               if fused_gemm is None else bool(fused_gemm))
             self._car = {}
 
-        def reduce(self, y):
+        def _collective(self, n, dtype, device):
             import torch.distributed as dist
 
-            if self.scheme is None:
-                if dist.is_initialized() and dist.get_world_size(self.group) > 1:
-                    dist.all_reduce(y, group=self.group)
-                return y
             from .collective import CompressedAllReduce, SymmetricAllReduce
 
-            key = (y.numel(), y.dtype)
+            key = (n, dtype)
             car = self._car.get(key)
             if car is None:
                 ws = dist.get_world_size(self.group) if dist.is_initialized() else 1
@@ -438,21 +441,35 @@ def make_module_classes():
                 if algo == "auto":
                     algo = "oneshot" if ws <= 2 else "twoshot"
                 if algo in ("symm", "symm2"):
-                    skey = (id(self.group), str(self.scheme), y.numel(), y.dtype, algo)
+                    skey = (id(self.group), str(self.scheme), n, dtype, algo)
                     car = _SYMM_CACHE.get(skey)
                     if car is None:
-                        car = SymmetricAllReduce(self.scheme, y.numel(), group=self.group,
-                                                 out_dtype=y.dtype, device=y.device,
+                        car = SymmetricAllReduce(self.scheme, n, group=self.group,
+                                                 out_dtype=dtype, device=device,
                                                  algo="oneshot" if algo == "symm" else "twoshot")
                         _SYMM_CACHE[skey] = car
                 else:
-                    car = CompressedAllReduce(self.scheme, y.numel(), group=self.group,
-                                              algo=algo, out_dtype=y.dtype, device=y.device,
+                    car = CompressedAllReduce(self.scheme, n, group=self.group,
+                                              algo=algo, out_dtype=dtype, device=device,
                                               world_size=ws, rank=rk)
                 self._car[key] = car
-            return car(y.contiguous())
+            return car
+
+        def reduce(self, y):
+            import torch.distributed as dist
+
+            if self.scheme is None:
+                if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+                    dist.all_reduce(y, group=self.group)
+                return y
+            return self._collective(y.numel(), y.dtype, y.device)(y.contiguous())
 
         def forward(self, x):
+            if self.scheme is not None and self.fused_gemm and self.algo not in ("symm", "symm2"):
+                n = x.numel() // x.shape[-1] * self.weight.shape[0]
+                car = self._collective(n, x.dtype, x.device)
+                if hasattr(car, "linear"):
+                    return car.linear(x.contiguous(), self.weight)
             return self.reduce(F.linear(x, self.weight))
 
         def collectives(self):

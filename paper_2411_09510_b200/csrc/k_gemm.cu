@@ -41,8 +41,10 @@ namespace gm {
 constexpr int BM = 128;
 constexpr int BK = 64;  // bf16: 128 bytes, one SW128 row
 constexpr int kStages = 4;
-constexpr int kEpiWarps = 4;
-constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
+// epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter, each
+// owning half of the tile's columns); MXB200_GEMM_EPI picks, default 8
+template <int EPI>
+constexpr int gemm_threads() { return 64 + 32 * EPI; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -137,13 +139,109 @@ struct GArgs {
   uint8_t* elem_out;      // chunk 0's element stream
   void* partial_out;      // bf16 [M, N] (nullable)
   unsigned long long* nonfinite;
+  float* ws;              // stream-K partial tiles: gridDim.x slots of BM x BN fp32 (nullable)
+  unsigned int* flags;    // gridDim.x u32, zero between launches (the kernel resets them)
   Fmt f;
 };
 
+// Work distribution.  With a workspace: stream-K -- the T tiles x KB
+// k-blocks are cut into gridDim.x contiguous ranges of (nearly) equal
+// length, so every CTA does the same MMA work (no 1.73-wave tail when T is
+// not a multiple of the SM count).  Ranges are >= KB long (T >= grid), so a
+// tile is split between at most two CTAs: CTA p+1 runs the tile's TAIL
+// k-blocks first (start of its range) and parks the fp32 partial in
+// workspace slot p+1; CTA p runs the HEAD at the end of its range and
+// finalises: acc(head) + ws(tail), a fixed order, so results are
+// deterministic.  Without a workspace: whole tiles, grid-stride.
+struct Sched {
+  int64_t u, e;
+  int KB, T, t;
+  bool dp;
+  __device__ __forceinline__ Sched(int T_, int KB_, bool streamk) : KB(KB_), T(T_) {
+    dp = !streamk;
+    t = blockIdx.x;
+    const int64_t W = (int64_t)T_ * KB_;
+    u = W * blockIdx.x / gridDim.x;
+    e = W * (blockIdx.x + 1) / gridDim.x;
+  }
+  __device__ __forceinline__ bool next(int& tile, int& kb0, int& kb1) {
+    if (dp) {
+      if (t >= T) return false;
+      tile = t;
+      kb0 = 0;
+      kb1 = KB;
+      t += gridDim.x;
+      return true;
+    }
+    if (u >= e) return false;
+    tile = (int)(u / KB);
+    kb0 = (int)(u - (int64_t)tile * KB);
+    kb1 = (int)min((int64_t)KB, kb0 + (e - u));
+    u += kb1 - kb0;
+    return true;
+  }
+};
+
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+template <int EPI>
+__device__ __forceinline__ void epi_bar() {  // the epilogue warps only
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI) : "memory");
+}
+
+// One thread's 32 accumulator columns -> bf16(partial) (RNE, the tensor
+// F.linear returns) -> [bf16 partial] + [MX codes + scales at flat index
+// `flat` (a multiple of 32) of the row-major partial].
+template <int MODE, int B, int ENC, int BITS>
+__device__ __forceinline__ void epi_chunk(const GArgs& A, const Fmt& f, const uint32_t* v,
+                                          int64_t flat) {
+  Raw<__nv_bfloat16> raw;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[2 * i]),
+                                             __uint_as_float(v[2 * i + 1]));
+    raw.w[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  if (MODE == 0 || A.partial_out) {
+    uint4* p = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(A.partial_out) + flat);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      p[j] = make_uint4(raw.w[4 * j], raw.w[4 * j + 1], raw.w[4 * j + 2], raw.w[4 * j + 3]);
+  }
+  if constexpr (MODE == 1) {
+    constexpr int NSB = Geo<B>::NSB;
+    int stored[NSB];
+    bool bad;
+    LaneCodes<BITS> cw = quant_lane<__nv_bfloat16, B, ENC, BITS>(raw, f, stored, bad);
+    if (bad) report_nonfinite_raw<__nv_bfloat16>(raw, kVPL, flat, A.nonfinite);
+    // chunked shards (two-shot): a 32-value group never straddles a chunk
+    // (chunk sizes are multiples of 8B >= 128 values)
+    const int64_t chunk = flat / A.cv, local = flat - chunk * A.cv;
+    const int64_t cofs = chunk * A.chunk_stride;
+    store_lane_codes<BITS>(A.elem_out + cofs + local / 8 * BITS, cw, kVPL);
+    uint8_t* sp = A.scale_out + cofs + local / B;
+    if constexpr (NSB == 4) {
+      *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
+                                         ((uint32_t)stored[2] << 16) |
+                                         ((uint32_t)stored[3] << 24);
+    } else if constexpr (NSB == 2) {
+      *reinterpret_cast<uint16_t*>(sp) = (uint16_t)(stored[0] | (stored[1] << 8));
+    } else {
+      *sp = (uint8_t)stored[0];
+    }
+  }
+}
+
 // MODE 0: bf16 partial only (plain GEMM, the unfused baseline's producer)
 // MODE 1: MX shard (+ bf16 partial when partial_out != nullptr)
-template <int BN, int MODE, int B, int ENC, int BITS>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+template <int BN, int EPI, int MODE, int B, int ENC, int BITS>
+__global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
     k_gemm_mx(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
               const GArgs A) {
   constexpr int A_BYTES = BM * BK * 2;
@@ -163,6 +261,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int num_n = (int)(N / BN);
   const int num_tiles = num_m * num_n;
   const int num_kb = (int)(K / BK);
+  const bool streamk = A.ws != nullptr;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -171,7 +270,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiWarps);
+      mbar_init(&tempty[a], EPI);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
@@ -194,14 +293,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
 
+  Sched sch(num_tiles, num_kb, streamk);
+  int tile, kb0, kb1;
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int mb = t % num_m, nb = t / num_m;
-        for (int kb = 0; kb < num_kb; ++kb) {
+      while (sch.next(tile, kb0, kb1)) {
+        const int mb = tile % num_m, nb = tile / num_m;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           mbar_expect_tx(&full[stage], STAGE_BYTES);
@@ -219,13 +320,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    while (sch.next(tile, kb0, kb1)) {
       const int acc = it & 1;
       const uint32_t aphase = (uint32_t)(it >> 1) & 1u;
+      ++it;
       mbar_wait(&tempty[acc], aphase ^ 1u);
       tc_fence_after();
       const uint32_t d = tmem_base + (uint32_t)(acc * BN);
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (lane == 0) {
@@ -234,7 +336,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {  // +32 bytes per K = 16 step
             mma_bf16(d, smem_desc_sw128(sa + 32 * k), smem_desc_sw128(sb + 32 * k), IDESC,
-                     (kb | k) != 0);
+                     (kb > kb0 || k > 0) ? 1u : 0u);
           }
           mma_commit(&empty[stage]);  // frees the stage when these MMAs finish
         }
@@ -248,71 +350,284 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
     }
   } else {
-    // ---------------- epilogue ----------------
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    // ---------------- epilogue (EPI warps) ----------------
+    // warp w: TMEM lane quarter w % 4 (hardware rule), column part
+    // (w - 2) / 4 of the tile; thread = one accumulator row
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    constexpr int CPH = BN / 32 / (EPI / 4);  // 32-column chunks per part
+    const int r_in_tile = 32 * q + lane;
+    const bool leader = threadIdx.x == 64;
     const Fmt f = A.f;
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
-      const int mb = t % num_m, nb = t / num_m;
+    while (sch.next(tile, kb0, kb1)) {
+      const int mb = tile % num_m, nb = tile / num_m;
       const int acc = it & 1;
       const uint32_t aphase = (uint32_t)(it >> 1) & 1u;
+      ++it;
+      const bool tail = kb0 > 0;          // partial for the CTA before us
+      const bool head = kb1 < num_kb;     // we finalise: + the next CTA's tail
+      if (head) {  // wait for the tail partial (published long ago, typically)
+        if (leader)
+          while (ld_acquire_gpu(A.flags + blockIdx.x + 1) == 0u) __nanosleep(64);
+        epi_bar<EPI>();
+      }
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
-      const int64_t row = (int64_t)mb * BM + 32 * q + lane;
+      const int64_t row = (int64_t)mb * BM + r_in_tile;
       const bool live = row < M;
       const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN);
+      float* wrow = A.ws + ((size_t)(tail ? blockIdx.x : blockIdx.x + 1) * BM + r_in_tile) * BN;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half * CPH; c < (half + 1) * CPH; ++c) {
         uint32_t v[32];
         tmem_ld32(taddr + 32 * c, v);
         tmem_ld_wait();
-        Raw<__nv_bfloat16> raw;  // bf16(partial), RNE: the tensor F.linear returns
+        if (tail) {  // park the fp32 partial (L2-resident, read once)
+          float4* wp = reinterpret_cast<float4*>(wrow + 32 * c);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[2 * i]),
-                                                   __uint_as_float(v[2 * i + 1]));
-          raw.w[i] = *reinterpret_cast<uint32_t*>(&h);
+          for (int j = 0; j < 8; ++j)
+            __stcg(wp + j, make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                       __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])));
+          continue;
         }
-        if (!live) continue;
-        const int64_t flat = row * N + (int64_t)nb * BN + 32 * c;  // multiple of 32
-        if (MODE == 0 || A.partial_out) {
-          uint4* p = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(A.partial_out) + flat);
+        if (head) {
+          const float4* wp = reinterpret_cast<const float4*>(wrow + 32 * c);
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            p[j] = make_uint4(raw.w[4 * j], raw.w[4 * j + 1], raw.w[4 * j + 2], raw.w[4 * j + 3]);
-        }
-        if constexpr (MODE == 1) {
-          constexpr int NSB = Geo<B>::NSB;
-          int stored[NSB];
-          bool bad;
-          LaneCodes<BITS> cw = quant_lane<__nv_bfloat16, B, ENC, BITS>(raw, f, stored, bad);
-          if (bad) report_nonfinite_raw<__nv_bfloat16>(raw, kVPL, flat, A.nonfinite);
-          // chunked shards (two-shot): a 32-value group never straddles a
-          // chunk (chunk sizes are multiples of 8B >= 128 values)
-          const int64_t chunk = flat / A.cv, local = flat - chunk * A.cv;
-          const int64_t cofs = chunk * A.chunk_stride;
-          store_lane_codes<BITS>(A.elem_out + cofs + local / 8 * BITS, cw, kVPL);
-          uint8_t* sp = A.scale_out + cofs + local / B;
-          if constexpr (NSB == 4) {
-            *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
-                                               ((uint32_t)stored[2] << 16) |
-                                               ((uint32_t)stored[3] << 24);
-          } else if constexpr (NSB == 2) {
-            *reinterpret_cast<uint16_t*>(sp) = (uint16_t)(stored[0] | (stored[1] << 8));
-          } else {
-            *sp = (uint8_t)stored[0];
+          for (int j = 0; j < 8; ++j) {
+            const float4 t4 = __ldcg(wp + j);
+            v[4 * j] = __float_as_uint(__uint_as_float(v[4 * j]) + t4.x);
+            v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + t4.y);
+            v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + t4.z);
+            v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + t4.w);
           }
         }
+        if (live) epi_chunk<MODE, B, ENC, BITS>(A, f, v, row * N + (int64_t)nb * BN + 32 * c);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (tail) {  // publish the parked partial to the CTA before us
+        __threadfence();
+        epi_bar<EPI>();
+        if (leader) st_release_gpu(A.flags + blockIdx.x, 1u);
+      }
+      if (head && leader) A.flags[blockIdx.x + 1] = 0u;  // consumed: ready for the next launch
     }
   }
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 2-CTA form (cta_group::2): a cluster of two CTAs on an SM pair computes a
+// 256 x BN tile.  CTA r loads rows [128r, 128r+128) of the x tile and rows
+// [128r, 128r+128) of the BN-row W tile (its half of N); the leader's single
+// thread issues tcgen05.mma.cta_group::2 (M = 256), which reads A from each
+// CTA's own smem and B from both, and accumulates each CTA's 128 rows x BN
+// in that CTA's TMEM.  Per SM the ring stage is 32 KB (x 16 KB + half of W
+// 16 KB, against 48 KB for the 1-CTA 128 x 256 tile), so 6 stages fit and a
+// third less L2->SM traffic is needed per MMA.
+//   full[s]   leader's: both CTAs' TMA bytes complete_tx on it
+//   empty[s]  each CTA's: the leader's commit multicasts to both
+//   tfull[a]  each CTA's: commit multicast
+//   tempty[a] leader's: every epilogue warp of both CTAs arrives (remote)
+// ---------------------------------------------------------------------------
+constexpr int kStages2 = 6;
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// both CTAs: data into the local smem, completion bytes on the LEADER's
+// barrier (peer bit cleared, as CUTLASS's SM100_TMA_2SM_LOAD)
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_bf16(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+template <int BN, int EPI, int MODE, int B, int ENC, int BITS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm_threads<EPI>(), 1)
+    k_gemm_mx2(const __grid_constant__ CUtensorMap map_x,
+               const __grid_constant__ CUtensorMap map_w, const GArgs A) {
+  constexpr int A_BYTES = 128 * BK * 2;
+  constexpr int B_BYTES = (BN / 2) * BK * 2;
+  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * BN;
+  constexpr uint32_t IDESC = idesc_bf16<BN>(256);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  __shared__ __align__(8) uint64_t full[kStages2], empty[kStages2], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int64_t M = A.M, N = A.N, K = A.K;
+  const int num_m = (int)((M + 255) / 256);
+  const int num_n = (int)(N / BN);
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (int)(K / BK);
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * EPI);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_w)) : "memory");
+  }
+  if (warp == 1) {  // paired allocation: the same warp in both CTAs
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_sh)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sh;
+
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs) ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < num_tiles; t += ncl) {
+        const int mb = t % num_m, nb = t / num_m;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+          tma_load_2d_2sm(sa, &map_x, &full[stage], kb * BK, mb * 256 + 128 * (int)rank);
+          tma_load_2d_2sm(sa + A_BYTES, &map_w, &full[stage], kb * BK,
+                          nb * BN + (BN / 2) * (int)rank);
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader CTA only) ----------------
+    if (leader) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cid; t < num_tiles; t += ncl, ++it) {
+        const int acc = it & 1;
+        const uint32_t aphase = (uint32_t)(it >> 1) & 1u;
+        mbar_wait(&tempty[acc], aphase ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+            const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              mma2_bf16(d, smem_desc_sw128(sa + 32 * k), smem_desc_sw128(sb + 32 * k), IDESC,
+                        (kb | k) != 0);
+            mma2_commit_both(&empty[stage]);  // both CTAs' producers may refill
+          }
+          __syncwarp();
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        if (lane == 0) mma2_commit_both(&tfull[acc]);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- epilogue (both CTAs: their own 128 rows) ----------------
+    const int q = warp & 3;
+    const int part = (warp - 2) >> 2;
+    constexpr int CPP = BN / 32 / (EPI / 4);
+    const Fmt f = A.f;
+    const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader1 = mapa(smem_u32(&tempty[1]), 0);
+    int it = 0;
+    for (int t = cid; t < num_tiles; t += ncl, ++it) {
+      const int mb = t % num_m, nb = t / num_m;
+      const int acc = it & 1;
+      const uint32_t aphase = (uint32_t)(it >> 1) & 1u;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const int64_t row = (int64_t)mb * 256 + 128 * rank + 32 * q + lane;
+      const bool live = row < M;
+      const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+      for (int c = part * CPP; c < (part + 1) * CPP; ++c) {
+        uint32_t v[32];
+        tmem_ld32(taddr + 32 * c, v);
+        tmem_ld_wait();
+        if (live) epi_chunk<MODE, B, ENC, BITS>(A, f, v, row * N + (int64_t)nb * BN + 32 * c);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // no remote arrive or MMA is in flight past this point
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "n"(TMEM_COLS)
                  : "memory");
   }
@@ -356,12 +671,32 @@ int num_sms() {
   return sms;
 }
 
-template <int BN, int MODE, int B, int ENC, int BITS>
-cudaError_t go(const GArgs& a, const void* x, const void* w, cudaStream_t st) {
+inline int tile_n(int64_t N) { return N % 256 == 0 ? 256 : 128; }
+
+// one CTA per SM (at most one per tile)
+inline int grid_ctas(int64_t M, int64_t N, int BN) {
+  const int64_t tiles = (M + BM - 1) / BM * (N / BN);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms()));
+}
+
+// stream-K workspace: one BM x BN fp32 slot per CTA, then one u32 flag per CTA
+inline int64_t ws_bytes(int64_t M, int64_t N) {
+  const int BN = tile_n(N);
+  const int64_t g = grid_ctas(M, N, BN);
+  return g * BM * BN * 4 + (g * 4 + 255) / 256 * 256;
+}
+
+inline int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+template <int BN, int EPI, int MODE, int B, int ENC, int BITS>
+cudaError_t go_epi(const GArgs& a, const void* x, const void* w, cudaStream_t st) {
   CUtensorMap mx, mw;
   if (!make_map(&mx, x, a.M, a.K, BM) || !make_map(&mw, w, a.N, a.K, BN))
     return cudaErrorInvalidValue;
-  auto k = k_gemm_mx<BN, MODE, B, ENC, BITS>;
+  auto k = k_gemm_mx<BN, EPI, MODE, B, ENC, BITS>;
   constexpr int smem = kStages * (BM * BK * 2 + BN * BK * 2) + 1024;
   static bool attr = false;  // per instantiation
   if (!attr) {
@@ -369,10 +704,38 @@ cudaError_t go(const GArgs& a, const void* x, const void* w, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int tiles = (int)((a.M + BM - 1) / BM) * (int)(a.N / BN);
-  const int grid = std::max(1, std::min(tiles, num_sms()));
-  launch_pdl(k, dim3(grid), dim3(kGemmThreads), smem, st, mx, mw, a);
+  launch_pdl(k, dim3(grid_ctas(a.M, a.N, BN)), dim3(gemm_threads<EPI>()), smem, st, mx, mw, a);
   return cudaGetLastError();
+}
+
+template <int BN, int EPI, int MODE, int B, int ENC, int BITS>
+cudaError_t go_2cta(const GArgs& a, const void* x, const void* w, cudaStream_t st) {
+  CUtensorMap mx, mw;
+  if (!make_map(&mx, x, a.M, a.K, 128) || !make_map(&mw, w, a.N, a.K, BN / 2))
+    return cudaErrorInvalidValue;
+  auto k = k_gemm_mx2<BN, EPI, MODE, B, ENC, BITS>;
+  constexpr int smem = kStages2 * (128 * BK * 2 + (BN / 2) * BK * 2) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t tiles = (a.M + 255) / 256 * (a.N / BN);
+  const int clusters = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms() / 2));
+  launch_pdl(k, dim3(2 * clusters), dim3(gemm_threads<EPI>()), smem, st, mx, mw, a);
+  return cudaGetLastError();
+}
+
+template <int BN, int MODE, int B, int ENC, int BITS>
+cudaError_t go(const GArgs& a, const void* x, const void* w, cudaStream_t st) {
+  static const int epi = env_int("MXB200_GEMM_EPI", 8);
+  static const int two = env_int("MXB200_GEMM_2CTA", 1);
+  if (two && a.ws == nullptr)
+    return epi == 8 ? go_2cta<BN, 8, MODE, B, ENC, BITS>(a, x, w, st)
+                    : go_2cta<BN, 4, MODE, B, ENC, BITS>(a, x, w, st);
+  return epi == 8 ? go_epi<BN, 8, MODE, B, ENC, BITS>(a, x, w, st)
+                  : go_epi<BN, 4, MODE, B, ENC, BITS>(a, x, w, st);
 }
 
 template <int BN>
@@ -394,11 +757,14 @@ cudaError_t by_fmt(const GArgs& a, const void* x, const void* w, int mode, int b
 
 }  // namespace gm
 
+int64_t gemm_workspace_bytes(int64_t M, int64_t N) { return gm::ws_bytes(M, N); }
+
 // returns cudaErrorNotSupported for shapes / schemes outside the fused path
 cudaError_t launch_gemm_mx(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
                            const Fmt* fmt, int enc_id, int64_t chunk_values, int64_t chunk_stride,
                            uint8_t* scale_out, uint8_t* elem_out, void* partial_out,
-                           unsigned long long* nonfinite, cudaStream_t st) {
+                           unsigned long long* nonfinite, void* workspace, int64_t workspace_bytes,
+                           cudaStream_t st) {
   using namespace gm;
   if (M < 1 || N < 128 || K < BK || K % BK != 0 || N % 128 != 0) return cudaErrorNotSupported;
   if (chunk_values < 1 || (chunk_values % 32 != 0 && chunk_values < M * N))
@@ -410,6 +776,16 @@ cudaError_t launch_gemm_mx(const void* x, const void* w, int64_t M, int64_t N, i
   a.cv = chunk_values; a.chunk_stride = chunk_stride;
   a.scale_out = scale_out; a.elem_out = elem_out; a.partial_out = partial_out;
   a.nonfinite = nonfinite;
+  // stream-K when a big enough workspace is given (else whole tiles)
+  a.ws = nullptr;
+  a.flags = nullptr;
+  static const int streamk = env_int("MXB200_GEMM_STREAMK", 0);
+  if (streamk && workspace && workspace_bytes >= ws_bytes(M, N)) {
+    const int BN = tile_n(N);
+    a.ws = reinterpret_cast<float*>(workspace);
+    a.flags = reinterpret_cast<unsigned int*>(reinterpret_cast<uint8_t*>(workspace) +
+                                              (int64_t)grid_ctas(M, N, BN) * BM * BN * 4);
+  }
   int mode = 0, block = 32, enc = ENC_E2M1, bits = 4;
   memset(&a.f, 0, sizeof(a.f));
   if (fmt) {
@@ -423,7 +799,7 @@ cudaError_t launch_gemm_mx(const void* x, const void* w, int64_t M, int64_t N, i
   } else if (!partial_out) {
     return cudaErrorInvalidValue;
   }
-  if (N % 256 == 0) return by_fmt<256>(a, x, w, mode, block, enc, bits, st);
+  if (tile_n(N) == 256) return by_fmt<256>(a, x, w, mode, block, enc, bits, st);
   return by_fmt<128>(a, x, w, mode, block, enc, bits, st);
 }
 

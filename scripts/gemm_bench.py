@@ -78,6 +78,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shapes", default="8b,70b")
     ap.add_argument("--spec", default="fp4_e2m1:32:e8m0")
+    ap.add_argument("--filter", default="", help="only shapes whose label contains this")
+    ap.add_argument("--variants", default="cublas,cublas+k1,ours_plain,ours_fused")
+    ap.add_argument("--profile", action="store_true", help="ncu mode: one launch of each variant")
     args = ap.parse_args()
     from paper_2411_09510_b200 import _native
     from paper_2411_09510_b200.formats import parse_scheme
@@ -89,6 +92,8 @@ def main():
     P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
     for tag in args.shapes.split(","):
         for label, M, N, K in SHAPES[tag]:
+            if args.filter not in label:
+                continue
             per = 2 * (M * K + N * K + M * N)
             R = max(2, -(-3 * L2 // per))
             xs = [torch.randn(M, K, device="cuda").to(torch.bfloat16) for _ in range(R)]
@@ -112,21 +117,36 @@ def main():
                     ctypes.c_void_p(shards[i].data_ptr() + eo), None, P(wsb), wsb.numel(), st()),
                     "mx_quantize")
 
-            def plain(i):
-                _native.check(lib.mx_gemm_quantize(P(xs[i]), P(ws[i]), M, N, K, None, None, None,
-                                                   P(outs[i]), None, st()), "gemm")
+            gw = torch.zeros(_native.gemm_workspace_bytes(M, N, K), device="cuda",
+                             dtype=torch.uint8)
 
-            def fused(i):
+            def plain(i, sk=True):
+                _native.check(lib.mx_gemm_quantize(
+                    P(xs[i]), P(ws[i]), M, N, K, None, None, None, P(outs[i]), None,
+                    P(gw) if sk else None, gw.numel() if sk else 0, st()), "gemm")
+
+            def fused(i, sk=True):
                 _native.check(lib.mx_gemm_quantize(
                     P(xs[i]), P(ws[i]), M, N, K, ctypes.byref(cs),
                     ctypes.c_void_p(shards[i].data_ptr() + so),
-                    ctypes.c_void_p(shards[i].data_ptr() + eo), None, None, st()), "gemm")
+                    ctypes.c_void_p(shards[i].data_ptr() + eo), None, None,
+                    P(gw) if sk else None, gw.numel() if sk else 0, st()), "gemm")
 
             flops = 2.0 * M * N * K
             row = {"shape": label, "M": M, "N": N, "K": K, "spec": args.spec, "rotation": R,
                    "peak_tflops": peak, "peak_kind": kind}
-            for name, fn in (("cublas", cublas), ("cublas+k1", cublas_k1), ("ours_plain", plain),
-                             ("ours_fused", fused)):
+            variants = (("cublas", cublas), ("cublas+k1", cublas_k1), ("ours_plain", plain),
+                        ("ours_fused", fused))
+            if args.profile:
+                for name, fn in variants:
+                    if name in args.variants.split(","):
+                        fn(0)
+                        fn(1)
+                torch.cuda.synchronize()
+                continue
+            for name, fn in variants:
+                if name not in args.variants.split(","):
+                    continue
                 try:
                     us = time_graph(fn, R)
                     tf = flops / (us * 1e-6) / 1e12

@@ -69,11 +69,18 @@ def parse():
                     help="N=1: initialise a world-1 NCCL process group and run the TP=N "
                          "code path (NCCL collectives, NVLink kernel, TTFT) instead of the "
                          "single-GPU simulation")
-    ap.add_argument("--no-ttft", action="store_true", help="skip the TTFT block (N>1 path)")
+    ap.add_argument("--no-ttft", action="store_true", help="skip the TTFT block (N=1: TP=1 codec overhead; N>1: TP=N)")
     ap.add_argument("--no-70b", action="store_true", help="skip the 70B-shape kernel block")
     ap.add_argument("--ttft-layers", type=int, default=None,
                     help="truncate the TTFT stacks (default: full 32 / 80 layers)")
     return ap.parse_args()
+
+
+def _bf16_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+    except Exception:  # noqa: BLE001
+        return 1590.0  # B200_PROFILING.md fallback
 
 
 def peaks():
@@ -597,19 +604,23 @@ def ttft_block(torch, dist, args, world, dev):
     models = [("llama-3.1-8b", tp.LLAMA31_8B, 2048)]
     if world == 8:
         models.append(("llama-3.1-70b", tp.LLAMA31_70B, 4096))
-    variants = [("bf16_nccl", None, "oneshot"), ("mx_oneshot", args.scheme, "oneshot"),
-                ("mx_twoshot", args.scheme, "twoshot"), ("mx_symm", args.scheme, "symm"),
-                ("mx_symm2", args.scheme, "symm2")]
+    # mx_oneshot / mx_twoshot: the quantiser fused into the o_proj/down_proj
+    # GEMM epilogue (k_gemm.cu); *_unfused: F.linear (cuBLAS) + K1
+    variants = [("bf16_nccl", None, "oneshot", None), ("mx_oneshot", args.scheme, "oneshot", True),
+                ("mx_oneshot_unfused", args.scheme, "oneshot", False),
+                ("mx_twoshot", args.scheme, "twoshot", True), ("mx_symm", args.scheme, "symm", None),
+                ("mx_symm2", args.scheme, "symm2", None)]
     out = {}
     for name, cfg, seq in models:
         res = {"tp": world, "seq": seq, "batch": 1,
                "layers": args.ttft_layers or cfg.layers, "cuda_graph": True}
         base = None
-        for label, spec, algo in variants:
+        for label, spec, algo, fused in variants:
             err, ms = None, None
             try:
                 ms = tp.measure_ttft(cfg, 1, seq, tp=world, scheme=spec, algo=algo,
-                                     layers=args.ttft_layers, reps=5, warmup=2, graph=True)
+                                     layers=args.ttft_layers, reps=5, warmup=2, graph=True,
+                                     fused_gemm=fused)
             except Exception as exc:  # noqa: BLE001
                 err = f"{type(exc).__name__}: {exc}"[:200]
             ok = all_ok(err is None)
@@ -626,6 +637,110 @@ def ttft_block(torch, dist, args, world, dev):
     tp._SYMM_CACHE.clear()
     torch.cuda.empty_cache()
     return out
+
+
+def ttft_tp1_block(torch, args):
+    """TP=1 prefill TTFT on this GPU (no process group, no exchange): the
+    MX path's whole codec cost on the forward -- per row-parallel layer the
+    quantiser (fused into the GEMM epilogue, or cuBLAS + K1 unfused) plus the
+    K2 decode -- against the plain bf16 forward.  Llama-3.1-8B, seq 2048,
+    batch 1, all 32 layers, random init, CUDA-graph replayed."""
+    from paper_2411_09510_b200 import tp
+
+    cfg, seq = tp.LLAMA31_8B, 2048
+    out = {"model": "llama-3.1-8b", "tp": 1, "seq": seq, "batch": 1,
+           "layers": args.ttft_layers or cfg.layers, "cuda_graph": True,
+           "note": "world size 1: no all-reduce; the MX rows time the codec work alone"}
+    base = None
+    for label, spec, fused in (("bf16", None, None), ("mx_fused_gemm", args.scheme, True),
+                               ("mx_unfused", args.scheme, False)):
+        try:
+            ms = tp.measure_ttft(cfg, 1, seq, tp=1, scheme=spec, algo="oneshot",
+                                 layers=args.ttft_layers, reps=7, warmup=2, graph=True,
+                                 fused_gemm=fused)
+        except Exception as exc:  # noqa: BLE001
+            out[label] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+            continue
+        finally:
+            torch.cuda.empty_cache()
+        out[label] = {"ms": round(ms, 3)}
+        if spec is None:
+            base = ms
+        elif base:
+            out[label]["codec_overhead_pct"] = round(100.0 * (ms - base) / base, 2)
+    return out
+
+
+def gemm_block(torch, args, peak_tf):
+    """The producer of the compressed all-reduce at the 8B TP=2 row-parallel
+    shapes: the tcgen05 GEMM with the quantiser in its epilogue (one launch,
+    shard out) against cuBLAS F.linear + K1 -- device-timed over CUDA-graph
+    replays with operand sets rotated beyond L2; the fused shard is checked
+    byte-equal to K1 of the kernel's own bf16 partial."""
+    import ctypes
+
+    from paper_2411_09510_b200 import _native
+
+    lib = _native.load()
+    cs = _parse(args.scheme).to_c()
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    st = lambda: ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)  # noqa: E731
+    res = {"scheme": args.scheme, "peak_tflops": peak_tf}
+    for label, M, N, K in (("o_proj_tp2", 2048, 4096, 2048), ("down_proj_tp2", 2048, 4096, 7168)):
+        per = 2 * (M * K + N * K + M * N)
+        R = max(2, -(-3 * L2_BYTES // per))
+        xs = [torch.randn(M, K, device="cuda").to(torch.bfloat16) for _ in range(R)]
+        ws = [(torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16) for _ in range(R)]
+        outs = [torch.empty(M, N, device="cuda", dtype=torch.bfloat16) for _ in range(R)]
+        so, eo, S = _native.shard_layout(M * N, cs)
+        sb, eb = _native.stream_nbytes(M * N, cs)
+        shards = [torch.empty(S, device="cuda", dtype=torch.uint8) for _ in range(R)]
+        wsb = torch.empty(max(1, _native.workspace_bytes(M * N, cs, False)), device="cuda",
+                          dtype=torch.uint8)
+
+        def k1(i):
+            _native.check(lib.mx_quantize(P(outs[i]), _native.MX_BF16, M * N, ctypes.byref(cs),
+                                          ctypes.c_void_p(shards[i].data_ptr() + so),
+                                          ctypes.c_void_p(shards[i].data_ptr() + eo), None,
+                                          P(wsb), wsb.numel(), st()), "mx_quantize")
+
+        def unfused(i):
+            torch.matmul(xs[i], ws[i].T, out=outs[i])
+            k1(i)
+
+        def fused(i, partial=False):
+            _native.check(lib.mx_gemm_quantize(
+                P(xs[i]), P(ws[i]), M, N, K, ctypes.byref(cs),
+                ctypes.c_void_p(shards[i].data_ptr() + so),
+                ctypes.c_void_p(shards[i].data_ptr() + eo), P(outs[i]) if partial else None,
+                None, None, 0, st()), "mx_gemm_quantize")
+
+        reps = 10
+        t_un = kernel_graph_time(torch, lambda: [unfused(i) for i in range(R)], reps, R)
+        t_fu = kernel_graph_time(torch, lambda: [fused(i) for i in range(R)], reps, R)
+        fused(0, partial=True)
+        got = shards[0].clone()
+        k1(0)
+        torch.cuda.synchronize()
+        same = bool(torch.equal(got[so:so + sb], shards[0][so:so + sb]) and
+                    torch.equal(got[eo:eo + eb], shards[0][eo:eo + eb]))
+        fl = 2.0 * M * N * K
+        res[label] = {"M": M, "N": N, "K": K,
+                      "cublas_plus_k1_us": round(t_un * 1e3, 2),
+                      "fused_gemm_quant_us": round(t_fu * 1e3, 2),
+                      "fused_tflops": round(fl / (t_fu * 1e-3) / 1e12, 1),
+                      "fused_frac_of_bf16_peak": round(fl / (t_fu * 1e-3) / 1e12 / peak_tf, 3),
+                      "speedup": round(t_un / t_fu, 3),
+                      "shard_equals_k1_of_own_partial": same}
+        del xs, ws, outs, shards
+        torch.cuda.empty_cache()
+    return res
+
+
+def _parse(spec):
+    from paper_2411_09510_b200.formats import parse_scheme
+
+    return parse_scheme(spec, extensions=True)
 
 
 def run_ours(args, shape, rank, world, local_rank, dist_mode):
@@ -955,7 +1070,8 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
             err = exc
         ok = all_ok(err is None)  # identical on every rank
         if ok:
-            exact = bool(torch.equal(got.view(torch.int16), sets[0][1].out.view(torch.int16)))
+            exact = bool(torch.equal(got.reshape(-1).view(torch.int16),
+                                     sets[0][1].out.reshape(-1).view(torch.int16)))
             try:
                 gss = [capture(torch, (lambda x=s_[0][0]: sar(x))) for s_ in sets]
                 for i in range(args.warmup):
@@ -1004,10 +1120,20 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
                 "wire_frac_of_nvlink": round(wire / t / 1e9 / 900.0, 4)}
 
     ttft = None
+    gemm = None
     if dist_mode and not args.no_ttft:
         del sets
         torch.cuda.empty_cache()
         ttft = ttft_block(torch, dist, args, world, dev)
+    elif not dist_mode:
+        del sets
+        torch.cuda.empty_cache()
+        try:
+            gemm = gemm_block(torch, args, _bf16_peak())
+        except Exception as exc:  # noqa: BLE001
+            gemm = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+        if not args.no_ttft:
+            ttft = {"tp1": ttft_tp1_block(torch, args)}
 
     if rank != 0:
         return
@@ -1026,7 +1152,7 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
             "bf16_nccl_allreduce": bf16_ar, "symmetric_memory_fused": symm,
             "collective": coll, "simulated_tp_fused_step": sim_more, "shape_70b": shape70,
-            "ttft": ttft}
+            "producer_gemm": gemm, "ttft": ttft}
     print(json.dumps(line), flush=True)
 
 

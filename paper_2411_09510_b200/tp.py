@@ -515,7 +515,8 @@ def make_module_classes():
                 * self.w
 
     class LlamaTPBlock(nn.Module):
-        def __init__(self, cfg: LlamaConfig, tp: int, group, scheme, algo, device, dtype):
+        def __init__(self, cfg: LlamaConfig, tp: int, group, scheme, algo, device, dtype,
+                     fused_gemm=None):
             super().__init__()
             if cfg.heads % tp or cfg.kv_heads % tp and tp % cfg.kv_heads:
                 raise ShapeMismatch(f"heads {cfg.heads}/{cfg.kv_heads} vs tp {tp}")
@@ -528,10 +529,10 @@ def make_module_classes():
             self.qkv = ColumnParallelLinear(cfg.hidden, (self.hl + 2 * self.kvl) * self.hd,
                                             device, dtype)
             self.o_proj = RowParallelLinear(self.hl * self.hd, cfg.hidden, group, scheme, algo,
-                                            device=device, dtype=dtype)
+                                            device=device, dtype=dtype, fused_gemm=fused_gemm)
             self.gate_up = ColumnParallelLinear(cfg.hidden, 2 * (cfg.ffn // tp), device, dtype)
             self.down_proj = RowParallelLinear(cfg.ffn // tp, cfg.hidden, group, scheme, algo,
-                                               device=device, dtype=dtype)
+                                               device=device, dtype=dtype, fused_gemm=fused_gemm)
 
         def forward(self, h, cos, sin):
             b, t, _ = h.shape
@@ -556,11 +557,12 @@ def make_module_classes():
 
         def __init__(self, cfg: LlamaConfig, tp: int = 1, group=None, scheme=None,
                      algo="oneshot", layers=None, device="cuda", dtype=torch.bfloat16,
-                     check_health: bool = True):
+                     check_health: bool = True, fused_gemm=None):
             super().__init__()
             self.cfg = cfg
             self.check_health = check_health
-            self.blocks = nn.ModuleList(LlamaTPBlock(cfg, tp, group, scheme, algo, device, dtype)
+            self.blocks = nn.ModuleList(LlamaTPBlock(cfg, tp, group, scheme, algo, device, dtype,
+                                                     fused_gemm)
                                         for _ in range(layers or cfg.layers))
             self.norm = RMSNorm(cfg.hidden, cfg.eps, device, dtype)
 
@@ -597,7 +599,7 @@ def make_module_classes():
 
 def measure_ttft(cfg: LlamaConfig, batch: int, seq: int, tp: int = 1, group=None, scheme=None,
                  algo="oneshot", layers=None, reps: int = 5, warmup: int = 2, seed: int = 0,
-                 graph: bool = False):
+                 graph: bool = False, fused_gemm=None):
     """Prefill latency (ms, max over ranks) of the TP body on random data.
     ``graph`` replays the whole forward as one captured CUDA graph (how a
     serving engine runs it: no per-kernel host launch cost)."""
@@ -606,7 +608,7 @@ def measure_ttft(cfg: LlamaConfig, batch: int, seq: int, tp: int = 1, group=None
 
     torch.manual_seed(seed)
     _, _, _, LlamaTP = make_module_classes()
-    model = LlamaTP(cfg, tp, group, scheme, algo, layers)
+    model = LlamaTP(cfg, tp, group, scheme, algo, layers, fused_gemm=fused_gemm)
     h = torch.randn(batch, seq, cfg.hidden, device="cuda", dtype=torch.bfloat16)
     with torch.inference_mode():
         for _ in range(warmup):

@@ -35,7 +35,7 @@ def test_gpu_arm_line():
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
-    d = run(["--steps", "300", "--warmup", "3", "--no-cpu-baseline"])
+    d = run(["--steps", "300", "--warmup", "3", "--no-cpu-baseline", "--ttft-layers", "4"])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
               "roofline", "e2e", "gpu_launches", "clocks"):
@@ -49,3 +49,28 @@ def test_gpu_arm_line():
     assert e["bit_exact_vs_device_call"] is True
     assert d["gpu_launches"] >= d["steps"]
     assert "workload" in d["config"] and "model" not in d["config"]
+    g = d["producer_gemm"]
+    for shp in ("o_proj_tp2", "down_proj_tp2"):
+        assert g[shp]["shard_equals_k1_of_own_partial"] is True
+        assert g[shp]["fused_gemm_quant_us"] > 0 and g[shp]["cublas_plus_k1_us"] > 0
+    t1 = d["ttft"]["tp1"]
+    assert t1["layers"] == 4 and t1["bf16"]["ms"] > 0 and t1["mx_fused_gemm"]["ms"] > 0
+    assert "codec_overhead_pct" in t1["mx_unfused"]
+
+
+@pytest.mark.gpu
+def test_gpu_arm_world1_nccl_line():
+    """--force-dist: a world-1 NCCL process group runs the TP=N code path end
+    to end (NCCL collectives, the NVLink kernels over real symmetric memory,
+    the TTFT block with every all-reduce variant)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    d = run(["--steps", "60", "--warmup", "3", "--force-dist", "--ttft-layers", "2",
+             "--no-70b"])
+    assert d["n_gpus"] == 1 and d["value"] > 0
+    assert d["collective"] is not None
+    t = d["ttft"]["llama-3.1-8b"]
+    assert t["layers"] == 2
+    for k in ("bf16_nccl", "mx_oneshot", "mx_oneshot_unfused", "mx_twoshot", "mx_symm", "mx_symm2"):
+        assert "ms" in t[k], (k, t[k])

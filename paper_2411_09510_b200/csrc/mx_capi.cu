@@ -184,7 +184,9 @@ __global__ void g_fill_u64(unsigned long long* p, unsigned long long v) { *p = v
 cudaError_t launch_gemm_mx(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
                            const Fmt* f, int enc, int64_t chunk_values, int64_t chunk_stride,
                            uint8_t* scale_out, uint8_t* elem_out, void* partial_out,
-                           unsigned long long* nonfinite, cudaStream_t st);
+                           unsigned long long* nonfinite, void* workspace, int64_t workspace_bytes,
+                           cudaStream_t st);
+int64_t gemm_workspace_bytes(int64_t M, int64_t N);
 
 }  // namespace mxb
 
@@ -636,9 +638,25 @@ static int gemm_impl(const void* x, const void* w, int64_t M, int64_t N, int64_t
   if (partial && !aligned(partial, 16)) return fail(MX_ERR_INVALID_ARGUMENT, "partial not 16-byte aligned");
   Fmt f;
   if (s) f = make_fmt(s);
+  // opt-in stream-K (MXB200_GEMM_STREAMK=1, measured slower than whole tiles)
+  // needs an fp32 fix-up workspace: grown on demand, never freed; not for
+  // use under graph capture
+  static void* ws = nullptr;
+  static int64_t ws_cap = 0;
+  int64_t ws_need = 0;
+  if (const char* e = getenv("MXB200_GEMM_STREAMK"); e && atoi(e)) {
+    ws_need = gemm_workspace_bytes(M, N);
+    if (ws_need > ws_cap) {
+      if (ws) cudaFree(ws);
+      ws = nullptr; ws_cap = 0;
+      if (cudaMalloc(&ws, ws_need) != cudaSuccess) return fail(MX_ERR_CUDA, "stream-K workspace");
+      ws_cap = ws_need;
+    }
+  }
   cudaError_t e = launch_gemm_mx(x, w, M, N, K, s ? &f : nullptr, s ? enc_of(s) : 0, cv, cs,
                                  scale_stream, element_stream,
                                  partial, reinterpret_cast<unsigned long long*>(nonfinite),
+                                 ws_need ? ws : nullptr, ws_need ? ws_cap : 0,
                                  (cudaStream_t)stream);
   if (e == cudaErrorNotSupported)
     return fail(MX_ERR_UNSUPPORTED,

@@ -713,7 +713,7 @@ def gemm_block(torch, args, peak_tf):
                 P(xs[i]), P(ws[i]), M, N, K, ctypes.byref(cs),
                 ctypes.c_void_p(shards[i].data_ptr() + so),
                 ctypes.c_void_p(shards[i].data_ptr() + eo), P(outs[i]) if partial else None,
-                None, None, 0, st()), "mx_gemm_quantize")
+                None, st()), "mx_gemm_quantize")
 
         reps = 10
         t_un = kernel_graph_time(torch, lambda: [unfused(i) for i in range(R)], reps, R)

@@ -81,6 +81,30 @@ _lock = threading.Lock()
 _lib = None
 
 
+class _StrictLib:
+    """The loaded CDLL with an exact-arity check on every declared entry
+    point: ctypes silently accepts surplus arguments (it treats them as C
+    varargs), which would turn an ABI drift into a mis-bound stream pointer."""
+
+    def __init__(self, lib: ctypes.CDLL):
+        self._cdll = lib
+        for name, (_res, args) in SIGNATURES.items():
+            setattr(self, name, self._strict(name, getattr(lib, name), len(args)))
+
+    @staticmethod
+    def _strict(name, fn, arity):
+        def call(*a):
+            if len(a) != arity:
+                raise TypeError(f"{name} takes {arity} arguments, got {len(a)}")
+            return fn(*a)
+
+        call.__name__ = name
+        return call
+
+    def __getattr__(self, name):  # undeclared helpers (mx_abi_version, mx_last_error)
+        return getattr(self._cdll, name)
+
+
 def load(path: str = LIB_PATH) -> ctypes.CDLL:
     """Load libmxb200.so and bind every exported symbol (raises if absent)."""
     global _lib
@@ -97,8 +121,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             fn.argtypes = args
         if lib.mx_abi_version() != ABI_VERSION:
             raise NativeUnavailable(f"{path}: ABI {lib.mx_abi_version()} != {ABI_VERSION}")
-        _lib = lib
-        return lib
+        _lib = _StrictLib(lib)
+        return _lib
 
 
 def check(rc: int, what: str) -> None:

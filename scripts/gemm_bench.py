@@ -117,20 +117,17 @@ def main():
                     ctypes.c_void_p(shards[i].data_ptr() + eo), None, P(wsb), wsb.numel(), st()),
                     "mx_quantize")
 
-            gw = torch.zeros(_native.gemm_workspace_bytes(M, N, K), device="cuda",
-                             dtype=torch.uint8)
-
             def plain(i, sk=True):
                 _native.check(lib.mx_gemm_quantize(
                     P(xs[i]), P(ws[i]), M, N, K, None, None, None, P(outs[i]), None,
-                    P(gw) if sk else None, gw.numel() if sk else 0, st()), "gemm")
+                    st()), "gemm")
 
             def fused(i, sk=True):
                 _native.check(lib.mx_gemm_quantize(
                     P(xs[i]), P(ws[i]), M, N, K, ctypes.byref(cs),
                     ctypes.c_void_p(shards[i].data_ptr() + so),
                     ctypes.c_void_p(shards[i].data_ptr() + eo), None, None,
-                    P(gw) if sk else None, gw.numel() if sk else 0, st()), "gemm")
+                    st()), "gemm")
 
             flops = 2.0 * M * N * K
             row = {"shape": label, "M": M, "N": N, "K": K, "spec": args.spec, "rotation": R,

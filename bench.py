@@ -605,34 +605,39 @@ def ttft_block(torch, dist, args, world, dev):
     if world == 8:
         models.append(("llama-3.1-70b", tp.LLAMA31_70B, 4096))
     # mx_oneshot / mx_twoshot: the quantiser fused into the o_proj/down_proj
-    # GEMM epilogue (k_gemm.cu); *_unfused: F.linear (cuBLAS) + K1
-    variants = [("bf16_nccl", None, "oneshot", None), ("mx_oneshot", args.scheme, "oneshot", True),
+    # GEMM epilogue (k_gemm.cu) where gemm_preferred() expects it to win;
+    # *_unfused: F.linear (cuBLAS) + K1
+    variants = [("bf16_nccl", None, "oneshot", None), ("mx_oneshot", args.scheme, "oneshot", "auto"),
                 ("mx_oneshot_unfused", args.scheme, "oneshot", False),
-                ("mx_twoshot", args.scheme, "twoshot", True), ("mx_symm", args.scheme, "symm", None),
+                ("mx_twoshot", args.scheme, "twoshot", "auto"), ("mx_symm", args.scheme, "symm", None),
                 ("mx_symm2", args.scheme, "symm2", None)]
     out = {}
     for name, cfg, seq in models:
         res = {"tp": world, "seq": seq, "batch": 1,
-               "layers": args.ttft_layers or cfg.layers, "cuda_graph": True}
-        base = None
-        for label, spec, algo, fused in variants:
-            err, ms = None, None
-            try:
-                ms = tp.measure_ttft(cfg, 1, seq, tp=world, scheme=spec, algo=algo,
-                                     layers=args.ttft_layers, reps=5, warmup=2, graph=True,
-                                     fused_gemm=fused)
-            except Exception as exc:  # noqa: BLE001
-                err = f"{type(exc).__name__}: {exc}"[:200]
-            ok = all_ok(err is None)
-            torch.cuda.empty_cache()
-            if not ok:
-                res[label] = {"error": err or "failed on another rank"}
+               "layers": args.ttft_layers or cfg.layers, "cuda_graph": True,
+               "method": "one model, one CUDA graph per variant, replays interleaved "
+                         "round-robin; median ms, max over ranks"}
+        err, got = None, {}
+        try:
+            got = tp.measure_ttft_ab(cfg, 1, seq, variants, tp=world, layers=args.ttft_layers,
+                                     reps=9, warmup=2)
+        except Exception as exc:  # noqa: BLE001
+            err = f"{type(exc).__name__}: {exc}"[:200]
+        ok = all_ok(err is None)
+        torch.cuda.empty_cache()
+        if not ok:
+            res["error"] = err or "failed on another rank"
+            out[name] = res
+            continue
+        base = got.get("bf16_nccl")
+        for label, spec, _algo, _fused in variants:
+            v = got.get(label)
+            if not isinstance(v, float):
+                res[label] = {"error": v or "missing"}
                 continue
-            if spec is None:
-                base = ms
-            res[label] = {"ms": round(ms, 3)}
-            if base is not None and spec is not None:
-                res[label]["speedup_vs_bf16"] = round(base / ms, 4)
+            res[label] = {"ms": round(v, 3)}
+            if isinstance(base, float) and spec is not None:
+                res[label]["speedup_vs_bf16"] = round(base / v, 4)
         out[name] = res
     tp._SYMM_CACHE.clear()
     torch.cuda.empty_cache()
@@ -651,23 +656,28 @@ def ttft_tp1_block(torch, args):
     out = {"model": "llama-3.1-8b", "tp": 1, "seq": seq, "batch": 1,
            "layers": args.ttft_layers or cfg.layers, "cuda_graph": True,
            "note": "world size 1: no all-reduce; the MX rows time the codec work alone"}
-    base = None
-    for label, spec, fused in (("bf16", None, None), ("mx_fused_gemm", args.scheme, True),
-                               ("mx_unfused", args.scheme, False)):
-        try:
-            ms = tp.measure_ttft(cfg, 1, seq, tp=1, scheme=spec, algo="oneshot",
-                                 layers=args.ttft_layers, reps=7, warmup=2, graph=True,
-                                 fused_gemm=fused)
-        except Exception as exc:  # noqa: BLE001
-            out[label] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+    out["method"] = ("one model (same weights and input), one CUDA graph per variant, replays "
+                     "interleaved round-robin; median ms")
+    variants = [("bf16", None, "oneshot", None), ("mx", args.scheme, "oneshot", "auto"),
+                ("mx_fused_gemm", args.scheme, "oneshot", True),
+                ("mx_unfused", args.scheme, "oneshot", False)]
+    try:
+        got = tp.measure_ttft_ab(cfg, 1, seq, variants, tp=1, layers=args.ttft_layers, reps=15,
+                                 warmup=2)
+    except Exception as exc:  # noqa: BLE001
+        out["error"] = f"{type(exc).__name__}: {exc}"[:200]
+        return out
+    finally:
+        torch.cuda.empty_cache()
+    base = got.get("bf16")
+    for label, spec, _algo, _fused in variants:
+        v = got.get(label)
+        if not isinstance(v, float):
+            out[label] = {"error": v or "missing"}
             continue
-        finally:
-            torch.cuda.empty_cache()
-        out[label] = {"ms": round(ms, 3)}
-        if spec is None:
-            base = ms
-        elif base:
-            out[label]["codec_overhead_pct"] = round(100.0 * (ms - base) / base, 2)
+        out[label] = {"ms": round(v, 3)}
+        if spec is not None and isinstance(base, float):
+            out[label]["codec_overhead_pct"] = round(100.0 * (v - base) / base, 2)
     return out
 
 

@@ -138,6 +138,17 @@ int mx_dequant_sum(const uint8_t* shards, int64_t rank_stride, int32_t nranks, i
                    int64_t chunk_values, int64_t chunk_stride, const mx_scheme_t* scheme,
                    void* out, int32_t out_dtype, void* stream);
 
+/* mx_dequant_sum with the Llama residual add fused into the store (the
+ * row-parallel consumer `h + all_reduce(partial)`, tpsim's hook output fed
+ * to the residual stream): out[i] = round(residual[i] + round(sum[i])) in
+ * out_dtype -- bit-identical to mx_dequant_sum followed by an elementwise
+ * add in out_dtype, without writing and re-reading the sum.  `residual` has
+ * out_dtype and out's layout and may alias `out` (in-place h += ...). */
+int mx_dequant_sum_residual(const uint8_t* shards, int64_t rank_stride, int32_t nranks, int64_t n,
+                            int64_t chunk_values, int64_t chunk_stride,
+                            const mx_scheme_t* scheme, const void* residual, void* out,
+                            int32_t out_dtype, void* stream);
+
 /* Two-shot middle step (not in the reference; restated from the same codec
  * calls): decode `nranks` shards of one n-value chunk, fp32 rank-order sum
  * from +0.0, re-quantise the sum into the shard at `out_shard`.  All shards
@@ -209,11 +220,14 @@ int mx_symm_layout(int64_t n, const mx_scheme_t* scheme, int32_t nranks, int64_t
  *   status        local device u32 (zeroed once): set to 1 if a peer wait
  *                 timed out (~2 s) instead of hanging
  *   epochs        local device u32 x ctas (zeroed once)
+ *   residual      nullable, out_dtype, n values, may alias out: the residual
+ *                 add fused into the store as in mx_dequant_sum_residual
  * MX_ERR_UNSUPPORTED outside bf16 in, n % 1024 == 0, E8M0, B in {16,32,64}. */
 int mx_allreduce_symm(const void* x, int32_t dtype, int64_t n, const mx_scheme_t* scheme,
                       uint8_t* const* peer_bufs, uint32_t* const* peer_flags, int32_t rank,
                       int32_t nranks, int64_t slot_stride, void* out, int32_t out_dtype,
-                      uint32_t* status, uint32_t* epochs, uint64_t* nonfinite, void* stream);
+                      const void* residual, uint32_t* status, uint32_t* epochs,
+                      uint64_t* nonfinite, void* stream);
 
 /* Sizes of the two-shot symmetric-memory collective (n % (1024*nranks) == 0):
  * one buffer per rank of *buffer_bytes = two slots of *slot_stride bytes
@@ -236,8 +250,9 @@ int mx_symm_twoshot_layout(int64_t n, const mx_scheme_t* scheme, int32_t nranks,
 int mx_allreduce_symm_twoshot(const void* x, int32_t dtype, int64_t n,
                               const mx_scheme_t* scheme, uint8_t* const* peer_bufs,
                               uint32_t* const* peer_flags, int32_t rank, int32_t nranks,
-                              void* out, int32_t out_dtype, uint32_t* status, uint32_t* epochs,
-                              uint64_t* nonfinite, void* stream);
+                              void* out, int32_t out_dtype, const void* residual,
+                              uint32_t* status, uint32_t* epochs, uint64_t* nonfinite,
+                              void* stream);
 
 /* unpack_bits (mx/bitpack.py:37-58) on the device: `count` codes of
  * `width` bits -> one uint8 per code (quantize_block's return value). */

@@ -48,6 +48,8 @@ SIGNATURES = {
     "mx_quantize_chunks": (c_i32, [c_vp, c_i32, c_i64, c_i64, _SP, c_vp, c_i64, c_vp, c_vp,
                                    c_i64, c_vp]),
     "mx_dequant_sum": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_i64, c_i64, _SP, c_vp, c_i32, c_vp]),
+    "mx_dequant_sum_residual": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_i64, c_i64, _SP, c_vp, c_vp,
+                                        c_i32, c_vp]),
     "mx_dequant_sum_requant": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_i64, _SP, c_vp, c_vp, c_vp,
                                        c_i64, c_vp]),
     "mx_allreduce_fused": (c_i32, [c_vp, c_i32, c_i32, c_i64, _SP, c_vp, c_i64, c_vp, c_i32,
@@ -55,10 +57,10 @@ SIGNATURES = {
     "mx_symm_twoshot_layout": (c_i32, [c_i64, _SP, c_i32, c_i64p, c_i64p, c_i64p, c_i64p,
                                        c_i64p]),
     "mx_allreduce_symm_twoshot": (c_i32, [c_vp, c_i32, c_i64, _SP, c_vp, c_vp, c_i32, c_i32,
-                                          c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
+                                          c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mx_symm_layout": (c_i32, [c_i64, _SP, c_i32, c_i64p, c_i64p, c_i64p, c_i64p]),
     "mx_allreduce_symm": (c_i32, [c_vp, c_i32, c_i64, _SP, c_vp, c_vp, c_i32, c_i32, c_i64, c_vp,
-                                  c_i32, c_vp, c_vp, c_vp, c_vp]),
+                                  c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mx_unpack_codes": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp]),
     "mx_pack_codes": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp]),
     "mx_chanint_compress": (c_i32, [c_vp, c_i32, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_i64,

@@ -98,7 +98,13 @@ class NativeBackend:
             shard_stride, self._p(flag) if flag is not None else None, self._p(ws), ws.numel(),
             self._st()), "mx_quantize_chunks")
 
-    def dequant_sum(self, shards, rank_stride, nranks, n, c, chunk_stride, out):
+    def dequant_sum(self, shards, rank_stride, nranks, n, c, chunk_stride, out, residual=None):
+        if residual is not None:  # out = residual + sum, fused into K2's store
+            _native.check(self.lib.mx_dequant_sum_residual(
+                self._p(shards), rank_stride, nranks, n, c, chunk_stride, ctypes.byref(self.cs),
+                self._p(residual), self._p(out), self._dt(out), self._st()),
+                "mx_dequant_sum_residual")
+            return
         _native.check(self.lib.mx_dequant_sum(
             self._p(shards), rank_stride, nranks, n, c, chunk_stride, ctypes.byref(self.cs),
             self._p(out), self._dt(out), self._st()), "mx_dequant_sum")
@@ -132,6 +138,24 @@ class NativeBackend:
                 and w.shape[1] == K and K % 64 == 0 and w.shape[0] % 128 == 0
                 and x.is_contiguous() and w.is_contiguous()
                 and x.data_ptr() % 16 == 0 and w.data_ptr() % 16 == 0)
+
+    def gemm_preferred(self, x, w) -> bool:
+        """Whether the fused GEMM is expected to beat cuBLAS + K1 for this
+        shape (measured, profiles/r02/gemm): it saves K1 (~2.5 B/value of
+        HBM traffic) but schedules whole 256x256 tiles over the SM pairs, so
+        a badly quantised last wave costs more than K1 once the GEMM is long.
+        Fused when the tile waves are >= 90 % full, or K <= 8192 (short
+        GEMMs, where the saved K1 dominates)."""
+        if not self.gemm_supported(x, w):
+            return False
+        import torch
+
+        K = x.shape[-1]
+        M, N = x.numel() // K, w.shape[0]
+        tiles = -(-M // 256) * -(-N // 256)
+        pairs = max(1, torch.cuda.get_device_properties(x.device).multi_processor_count // 2)
+        waves = -(-tiles // pairs)
+        return tiles / (waves * pairs) >= 0.9 or K <= 8192
 
     def gemm_quantize_chunks(self, x2, w, c, shards, shard_stride, flag, partial=None):
         """k_gemm_mx: partial = x2 . w^T on the tensor cores, its MX shard(s)
@@ -253,13 +277,25 @@ class CompressedAllReduce:
         N, S = self.plan.nranks, self.plan.shard_bytes
         return (N - 1) * S if self.algo == "oneshot" else 2 * (N - 1) * S
 
-    def __call__(self, x, out=None):
+    def _check_residual(self, residual):
+        if residual is None:
+            return None
+        if residual.numel() != self.n or residual.dtype != self.out_dtype or \
+                not residual.is_contiguous():
+            raise ShapeMismatch(f"residual must be a contiguous {self.out_dtype} tensor of "
+                                f"{self.n} values")
+        return residual.reshape(-1)
+
+    def __call__(self, x, out=None, residual=None):
+        """all_reduce(x); with ``residual`` the result is ``residual +
+        all_reduce(x)`` computed in K2's store (bit-identical to the unfused
+        add in out_dtype; ``out`` may be ``residual`` for an in-place update)."""
         if x.numel() != self.n:
             raise ShapeMismatch(f"expected {self.n} values, got {x.numel()}")
-        out = self._reduce(x.reshape(-1), None, out)
+        out = self._reduce(x.reshape(-1), None, out, self._check_residual(residual))
         return out.view(x.shape) if out.numel() == x.numel() else out
 
-    def linear(self, x, weight, out=None):
+    def linear(self, x, weight, out=None, residual=None):
         """all_reduce(F.linear(x, weight)) -- the row-parallel hook
         (mx/tpsim.py:263-265) with the quantiser fused into the GEMM
         epilogue (k_gemm.cu, tcgen05 + TMA): the bf16 partial is never
@@ -275,11 +311,11 @@ class CompressedAllReduce:
             raise ShapeMismatch(f"expected {self.n} output values, got {M}x{N}")
         be = self.backend
         if not (hasattr(be, "gemm_supported") and be.gemm_supported(x, weight)):
-            return self(F.linear(x, weight), out)
-        res = self._reduce(None, (x.reshape(M, K), weight), out)
+            return self(F.linear(x, weight), out, residual)
+        res = self._reduce(None, (x.reshape(M, K), weight), out, self._check_residual(residual))
         return res.view(*x.shape[:-1], N)
 
-    def _reduce(self, xf, gemm, out):
+    def _reduce(self, xf, gemm, out, residual=None):
         out = self.out if out is None else out.reshape(-1)
         p, be, N, comm = self.plan, self.backend, self.plan.nranks, self.comm
         S = p.shard_bytes
@@ -291,7 +327,10 @@ class CompressedAllReduce:
                 be.gemm_quantize_chunks(gemm[0], gemm[1], p.n, mine, S, self.flag)
             if comm is not None:
                 comm.all_gather_into_tensor(self.gathered, mine, group=self.group)
-            be.dequant_sum(self.gathered, S, N, p.n, p.n, 0, out)
+            if residual is None:
+                be.dequant_sum(self.gathered, S, N, p.n, p.n, 0, out)
+            else:
+                be.dequant_sum(self.gathered, S, N, p.n, p.n, 0, out, residual)
         else:
             if gemm is None:
                 be.quantize_chunks(xf, p.c, self.send, S, self.ws, self.flag)
@@ -308,7 +347,10 @@ class CompressedAllReduce:
                 be.requant(recv, S, N, own, p.c, mine, self.ws, self.flag)
             if comm is not None:
                 comm.all_gather_into_tensor(self.gathered, mine, group=self.group)
-            be.dequant_sum(self.gathered, 0, 1, p.n, p.c, S, out)
+            if residual is None:
+                be.dequant_sum(self.gathered, 0, 1, p.n, p.c, S, out)
+            else:
+                be.dequant_sum(self.gathered, 0, 1, p.n, p.c, S, out, residual)
         return out
 
     def check_finite(self):
@@ -399,11 +441,19 @@ class SymmetricAllReduce:
         self.backend.reset_flag(self.flag)
         self.out = torch.empty(self.n, dtype=self.out_dtype, device=self.device)
 
-    def __call__(self, x, out=None):
+    def __call__(self, x, out=None, residual=None):
+        """all_reduce(x), or ``residual + all_reduce(x)`` fused into the
+        kernel's store (as CompressedAllReduce.__call__)."""
         import torch
 
         if x.numel() != self.n or x.dtype != torch.bfloat16 or not x.is_contiguous():
             raise ShapeMismatch(f"expected a contiguous bf16 tensor of {self.n} values")
+        if residual is not None and (residual.numel() != self.n or
+                                     residual.dtype != self.out_dtype or
+                                     not residual.is_contiguous()):
+            raise ShapeMismatch(f"residual must be a contiguous {self.out_dtype} tensor of "
+                                f"{self.n} values")
+        res = ctypes.c_void_p(residual.data_ptr()) if residual is not None else None
         o = self.out if out is None else out.reshape(-1)
         be = self.backend
         base = self.state.data_ptr()
@@ -412,14 +462,14 @@ class SymmetricAllReduce:
                 ctypes.c_void_p(x.data_ptr()), _native.MX_BF16, self.n, ctypes.byref(be.cs),
                 ctypes.c_void_p(self.hdl.buffer_ptrs_dev),
                 ctypes.c_void_p(self.flag_ptrs.data_ptr()), self.rank, self.world, self.slot,
-                ctypes.c_void_p(o.data_ptr()), be._dt(o), ctypes.c_void_p(base),
+                ctypes.c_void_p(o.data_ptr()), be._dt(o), res, ctypes.c_void_p(base),
                 ctypes.c_void_p(base + 4), ctypes.c_void_p(self.flag.data_ptr()), be._st())
         else:
             rc = be.lib.mx_allreduce_symm_twoshot(
                 ctypes.c_void_p(x.data_ptr()), _native.MX_BF16, self.n, ctypes.byref(be.cs),
                 ctypes.c_void_p(self.hdl.buffer_ptrs_dev),
                 ctypes.c_void_p(self.flag_ptrs.data_ptr()), self.rank, self.world,
-                ctypes.c_void_p(o.data_ptr()), be._dt(o), ctypes.c_void_p(base),
+                ctypes.c_void_p(o.data_ptr()), be._dt(o), res, ctypes.c_void_p(base),
                 ctypes.c_void_p(base + 4), ctypes.c_void_p(self.flag.data_ptr()), be._st())
         _native.check(rc, "mx_allreduce_symm")
         return o.view(x.shape)

@@ -464,8 +464,10 @@ __global__ void __launch_bounds__(kThreads) k_symm_flow(const SArgs S) {
       decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
       if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
     }
-    store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(S.out) + (size_t)q * kUnit + lane * kVPL,
-                               kVPL, acc);
+    const size_t o = (size_t)q * kUnit + lane * kVPL;
+    store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(S.out) + o, kVPL, acc,
+                               S.residual ? reinterpret_cast<const OutT*>(S.residual) + o
+                                          : nullptr);
   }
   if (threadIdx.x == 0) S.epoch[b] = e;
 }
@@ -612,9 +614,10 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
 #pragma unroll
       for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;
       decode_rank<B, DEC, BITS, kVPL>(a, f, acc, false, s_lut);
-      store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(S.out) + (size_t)j * S.c +
-                                     (size_t)q * kUnit + lane * kVPL,
-                                 kVPL, acc);
+      const size_t o = (size_t)j * S.c + (size_t)q * kUnit + lane * kVPL;
+      store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(S.out) + o, kVPL, acc,
+                                 S.residual ? reinterpret_cast<const OutT*>(S.residual) + o
+                                            : nullptr);
     }
   }
   if (threadIdx.x == 0) S.epoch[b] = e;

@@ -151,7 +151,12 @@ __global__ void g_dqsum(DArgs A, int64_t gpc, int64_t ng_total) {
         acc[t] = A.plain ? val : __fadd_rn(acc[t], val);
       }
     }
-    for (int t = 0; t < valid; ++t) out[i0 + t] = from_f32<OutT>(acc[t]);
+    const OutT* res = reinterpret_cast<const OutT*>(A.residual);
+    for (int t = 0; t < valid; ++t)
+      out[i0 + t] = from_f32<OutT>(
+          res ? __fadd_rn(InTraits<OutT>::to_f32(from_f32<OutT>(acc[t])),
+                          InTraits<OutT>::to_f32(res[cbase + i0 + t]))
+              : acc[t]);
   }
 }
 
@@ -415,7 +420,8 @@ int quantize_impl(const void* x, int dtype, int64_t n, int64_t cv, const mx_sche
 
 int dqsum_impl(const uint8_t* in, int64_t rank_stride, int nranks, int64_t n, int64_t cv,
                int64_t chunk_stride, int64_t scale_off, int64_t elem_off, const mx_scheme_t* s,
-               void* out, int out_dtype, int plain, cudaStream_t st) {
+               void* out, int out_dtype, int plain, cudaStream_t st,
+               const void* residual = nullptr) {
   int rc = check_scheme(s);
   if (rc) return rc;
   if (n < 0 || nranks < 1 || cv < 1)
@@ -429,10 +435,14 @@ int dqsum_impl(const uint8_t* in, int64_t rank_stride, int nranks, int64_t n, in
   a.in = in; a.rank_stride = rank_stride; a.nranks = nranks; a.chunk_stride = chunk_stride;
   a.scale_off = scale_off; a.elem_off = elem_off;
   a.n = n; a.cv = cv; a.out = out; a.plain = plain; a.f = f;
+  a.residual = residual;
+  if (residual && (plain || out_dtype == MX_F64))
+    return fail(MX_ERR_INVALID_ARGUMENT, "a residual needs a bf16/f16/f32 sum");
   int64_t nchunks = cdiv(n, cv);
   if (nchunks > 65535) return fail(MX_ERR_INVALID_ARGUMENT, "too many chunks");
   int osz = out_dtype == MX_F32 ? 4 : 2;
   bool fast = fast_block(s->block_size) && out_dtype != MX_F64 && aligned(out, 32) &&
+              (!residual || aligned(residual, 32)) &&
               aligned(in + elem_off, 16) && aligned(in + scale_off, 8) && rank_stride % 32 == 0 &&
               chunk_stride % 32 == 0 && (nchunks == 1 || (cv * osz) % 32 == 0);
   if (fast) {
@@ -556,6 +566,19 @@ int mx_dequant_sum(const uint8_t* shards, int64_t rank_stride, int32_t nranks, i
   if (rc) return rc;
   return dqsum_impl(shards, rank_stride, nranks, n, chunk_values, chunk_stride, so, eo, s, out,
                     out_dtype, 0, (cudaStream_t)stream);
+}
+
+int mx_dequant_sum_residual(const uint8_t* shards, int64_t rank_stride, int32_t nranks,
+                            int64_t n, int64_t chunk_values, int64_t chunk_stride,
+                            const mx_scheme_t* s, const void* residual, void* out,
+                            int32_t out_dtype, void* stream) {
+  if (out_dtype == MX_F64) return fail(MX_ERR_INVALID_ARGUMENT, "sums are fp32 (mx/netbench.py:332)");
+  if (!residual) return fail(MX_ERR_INVALID_ARGUMENT, "NULL residual");
+  int64_t so, eo, sbytes;
+  int rc = mx_shard_layout(chunk_values, s, &so, &eo, &sbytes);
+  if (rc) return rc;
+  return dqsum_impl(shards, rank_stride, nranks, n, chunk_values, chunk_stride, so, eo, s, out,
+                    out_dtype, 0, (cudaStream_t)stream, residual);
 }
 
 int mx_dequant_sum_requant(const uint8_t* shards, int64_t rank_stride, int32_t nranks, int64_t n,
@@ -711,7 +734,8 @@ int mx_symm_layout(int64_t n, const mx_scheme_t* s, int32_t nranks, int64_t* slo
 int mx_allreduce_symm(const void* x, int32_t dtype, int64_t n, const mx_scheme_t* s,
                       uint8_t* const* peer_bufs, uint32_t* const* peer_flags, int32_t rank,
                       int32_t nranks, int64_t slot_stride, void* out, int32_t out_dtype,
-                      uint32_t* status, uint32_t* epochs, uint64_t* nonfinite, void* stream) {
+                      const void* residual, uint32_t* status, uint32_t* epochs,
+                      uint64_t* nonfinite, void* stream) {
   int rc = check_scheme(s);
   if (rc) return rc;
   if (n <= 0 || nranks < 1 || rank < 0 || rank >= nranks)
@@ -723,7 +747,7 @@ int mx_allreduce_symm(const void* x, int32_t dtype, int64_t n, const mx_scheme_t
   Fmt f = make_fmt(s);
   if (dtype != MX_BF16 || (out_dtype != MX_BF16 && out_dtype != MX_F32) || n % 1024 != 0 ||
       f.kbits != 8 || slot_stride < sbytes || slot_stride % 32 != 0 || !aligned(x, 32) ||
-      !aligned(out, 32))
+      !aligned(out, 32) || !aligned(residual, 32))
     return fail(MX_ERR_UNSUPPORTED,
                 "symmetric path: bf16 in, bf16/f32 out, n %% 1024 == 0, E8M0, 32-B aligned");
   if (nranks > kThreads) return fail(MX_ERR_UNSUPPORTED, "at most %d ranks", kThreads);
@@ -731,7 +755,7 @@ int mx_allreduce_symm(const void* x, int32_t dtype, int64_t n, const mx_scheme_t
   a.x = x; a.n = n;
   a.bufs = peer_bufs; a.flags = reinterpret_cast<unsigned int* const*>(peer_flags);
   a.rank = rank; a.nranks = nranks; a.slot_stride = slot_stride;
-  a.scale_off = so; a.elem_off = eo; a.out = out; a.status = status;
+  a.scale_off = so; a.elem_off = eo; a.out = out; a.residual = residual; a.status = status;
   a.epoch = epochs; a.nonfinite = reinterpret_cast<unsigned long long*>(nonfinite); a.f = f;
   a.full_fence = symm_full_fence();
   a.timeout_ns = symm_timeout_ns();
@@ -764,8 +788,8 @@ int mx_symm_twoshot_layout(int64_t n, const mx_scheme_t* s, int32_t nranks,
 int mx_allreduce_symm_twoshot(const void* x, int32_t dtype, int64_t n, const mx_scheme_t* s,
                               uint8_t* const* peer_bufs, uint32_t* const* peer_flags,
                               int32_t rank, int32_t nranks, void* out, int32_t out_dtype,
-                              uint32_t* status, uint32_t* epochs, uint64_t* nonfinite,
-                              void* stream) {
+                              const void* residual, uint32_t* status, uint32_t* epochs,
+                              uint64_t* nonfinite, void* stream) {
   int64_t slot, sc, foff, total, g;
   int rc = mx_symm_twoshot_layout(n, s, nranks, &slot, &sc, &foff, &total, &g);
   if (rc) return rc;
@@ -774,7 +798,7 @@ int mx_allreduce_symm_twoshot(const void* x, int32_t dtype, int64_t n, const mx_
     return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
   Fmt f = make_fmt(s);
   if (dtype != MX_BF16 || (out_dtype != MX_BF16 && out_dtype != MX_F32) || f.kbits != 8 ||
-      !aligned(x, 32) || !aligned(out, 32))
+      !aligned(x, 32) || !aligned(out, 32) || !aligned(residual, 32))
     return fail(MX_ERR_UNSUPPORTED, "two-shot symmetric path: bf16 in, bf16/f32 out, E8M0");
   if (nranks > kThreads) return fail(MX_ERR_UNSUPPORTED, "at most %d ranks", kThreads);
   const int64_t c = n / nranks;
@@ -784,7 +808,8 @@ int mx_allreduce_symm_twoshot(const void* x, int32_t dtype, int64_t n, const mx_
   a.x = x; a.n = n; a.c = c;
   a.bufs = peer_bufs; a.flags = reinterpret_cast<unsigned int* const*>(peer_flags);
   a.rank = rank; a.nranks = nranks; a.slot_stride = slot; a.shard_stride = sc;
-  a.scale_off = so; a.elem_off = eo; a.out = out; a.status = status; a.epoch = epochs;
+  a.scale_off = so; a.elem_off = eo; a.out = out; a.residual = residual; a.status = status;
+  a.epoch = epochs;
   a.nonfinite = reinterpret_cast<unsigned long long*>(nonfinite); a.f = f;
   a.full_fence = symm_full_fence();
   a.timeout_ns = symm_timeout_ns();

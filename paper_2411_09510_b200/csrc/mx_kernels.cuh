@@ -73,6 +73,10 @@ struct DArgs {
   int64_t units_per_chunk;
   int64_t total_units;
   void* out;
+  // optional, out's dtype and layout (may alias out): out = residual +
+  // round(sum), rounded again -- bit-identical to the unfused K2 followed by
+  // an elementwise add in out's dtype (the Llama residual h + all_reduce(.))
+  const void* residual;
   int plain;  // 1: plain decode (no +0 accumulation semantics)
   Fmt f;
 };
@@ -954,11 +958,36 @@ __device__ __forceinline__ void decode_rank(const RankLoad<B, BITS, VPL>& r, con
   }
 }
 
+// residual + round(acc), rounded: the unfused `out = sum; out = residual + out`
+template <typename OutT>
+__device__ __forceinline__ float add_residual(float acc, OutT r) {
+  return __fadd_rn(InTraits<OutT>::to_f32(from_f32<OutT>(acc)), InTraits<OutT>::to_f32(r));
+}
+
+// coherent 256-bit load (the residual may alias this kernel's output)
+__device__ __forceinline__ void ld256_coherent(const void* p, uint32_t* r) {
+  asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "l"(p)
+               : "memory");
+}
+
 template <typename OutT, int VPL = kVPL>
-__device__ __forceinline__ void store_lane_out(OutT* __restrict__ out, int valid,
-                                               const float* acc) {
+__device__ __forceinline__ void store_lane_out(OutT* out, int valid, float* acc,
+                                               const OutT* res = nullptr) {
   if (valid == VPL) {
     uint32_t o[8];
+    if (res != nullptr) {  // fold the residual in, 16 (8) values per 256-bit load
+      constexpr int PER = 32 / sizeof(OutT);
+#pragma unroll
+      for (int h = 0; h < VPL / PER; ++h) {
+        ld256_coherent(res + PER * h, o);
+        const OutT* rv = reinterpret_cast<const OutT*>(o);
+#pragma unroll
+        for (int i = 0; i < PER; ++i) acc[PER * h + i] = add_residual<OutT>(acc[PER * h + i], rv[i]);
+      }
+    }
     if constexpr (sizeof(OutT) == 2) {
 #pragma unroll
       for (int h = 0; h < VPL / 16; ++h) {
@@ -978,7 +1007,8 @@ __device__ __forceinline__ void store_lane_out(OutT* __restrict__ out, int valid
   } else {
 #pragma unroll
     for (int i = 0; i < VPL; ++i)
-      if (i < valid) out[i] = from_f32<OutT>(acc[i]);
+      if (i < valid)
+        out[i] = from_f32<OutT>(res != nullptr ? add_residual<OutT>(acc[i], res[i]) : acc[i]);
   }
 }
 
@@ -1052,10 +1082,12 @@ __global__ void __launch_bounds__(kThreads) k_dqsum(const DArgs A) {
       load_rank<B, BITS, kVPL2>(r, b, A.scale_off, A.elem_off, p.uoff, lane, valid, f.kbits);
       decode_rank<B, DEC, BITS, kVPL2>(r, f, acc, plain, s_lut);
     }
-    if (valid > 0)
-      store_lane_out<OutT, kVPL2>(reinterpret_cast<OutT*>(A.out) + p.cbase + p.uoff +
-                                      lane * kVPL2,
-                                  valid, acc);
+    if (valid > 0) {
+      const int64_t o = p.cbase + p.uoff + lane * kVPL2;
+      store_lane_out<OutT, kVPL2>(reinterpret_cast<OutT*>(A.out) + o, valid, acc,
+                                  A.residual ? reinterpret_cast<const OutT*>(A.residual) + o
+                                             : nullptr);
+    }
     if (!more) break;
     u = un;
     p = pn;
@@ -1106,8 +1138,9 @@ __global__ void __launch_bounds__(kThreads) k_dqsum_lean(const DArgs A) {
     decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
     if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
   }
-  store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(A.out) + (size_t)u * kUnit + lane * kVPL,
-                             kVPL, acc);
+  const size_t o = (size_t)u * kUnit + lane * kVPL;
+  store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(A.out) + o, kVPL, acc,
+                             A.residual ? reinterpret_cast<const OutT*>(A.residual) + o : nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -1182,6 +1215,7 @@ struct SArgs {
   int64_t slot_stride;           // bytes of one shard slot (2 slots per buffer)
   int64_t scale_off, elem_off;   // shard layout for n values
   void* out;
+  const void* residual;          // nullable: out = residual + sum (see DArgs)
   unsigned int* status;          // local u32: set to 1 if a peer wait timed out
   unsigned int* epoch;           // local u32 per CTA, advanced once per call
   unsigned long long* nonfinite;
@@ -1200,6 +1234,7 @@ struct S2Args {
   int64_t shard_stride;          // bytes of one chunk shard
   int64_t scale_off, elem_off;   // chunk shard layout (c values)
   void* out;
+  const void* residual;          // nullable: out = residual + sum (see DArgs)
   unsigned int* status;
   unsigned int* epoch;           // local u32 per CTA
   unsigned long long* nonfinite;

@@ -422,9 +422,15 @@ def make_module_classes():
                                        * std, requires_grad=False)
             self.group, self.scheme, self.algo = group, scheme, algo
             # the quantiser fused into the GEMM epilogue (k_gemm.cu) for the
-            # NCCL algorithms; MXB200_GEMM_FUSED=0 selects F.linear + K1
-            self.fused_gemm = (os.environ.get("MXB200_GEMM_FUSED", "1") != "0"
-                               if fused_gemm is None else bool(fused_gemm))
+            # NCCL algorithms: "auto" where it is expected to win
+            # (NativeBackend.gemm_preferred), True always, False never
+            # (F.linear + K1); MXB200_GEMM_FUSED=0/1 pins False/True
+            env = os.environ.get("MXB200_GEMM_FUSED")
+            self.fused_gemm = fused_gemm if fused_gemm is not None else (
+                "auto" if env is None else env != "0")
+            # the residual add fused into the dequant-sum store;
+            # MXB200_FUSE_RESIDUAL=0 adds after the collective instead
+            self.fuse_residual = os.environ.get("MXB200_FUSE_RESIDUAL", "1") != "0"
             self._car = {}
 
         def _collective(self, n, dtype, device):
@@ -432,7 +438,7 @@ def make_module_classes():
 
             from .collective import CompressedAllReduce, SymmetricAllReduce
 
-            key = (n, dtype)
+            key = (n, dtype, str(self.scheme), self.algo)
             car = self._car.get(key)
             if car is None:
                 ws = dist.get_world_size(self.group) if dist.is_initialized() else 1
@@ -455,22 +461,36 @@ def make_module_classes():
                 self._car[key] = car
             return car
 
-        def reduce(self, y):
+        def reduce(self, y, residual=None):
             import torch.distributed as dist
 
             if self.scheme is None:
                 if dist.is_initialized() and dist.get_world_size(self.group) > 1:
                     dist.all_reduce(y, group=self.group)
-                return y
-            return self._collective(y.numel(), y.dtype, y.device)(y.contiguous())
+                return y if residual is None else residual + y
+            car = self._collective(y.numel(), y.dtype, y.device)
+            if residual is None or not self.fuse_residual:
+                out = car(y.contiguous())
+                return out if residual is None else residual + out
+            return car(y.contiguous(), residual=residual.contiguous())
 
-        def forward(self, x):
+        def forward(self, x, residual=None):
+            """all_reduce(x @ W^T), or ``residual + all_reduce(x @ W^T)`` --
+            the Llama block's residual update -- with the add fused into the
+            compressed collective's dequant-sum store (the bf16 NCCL path
+            adds after the all-reduce; identical bits either way)."""
             if self.scheme is not None and self.fused_gemm and self.algo not in ("symm", "symm2"):
                 n = x.numel() // x.shape[-1] * self.weight.shape[0]
                 car = self._collective(n, x.dtype, x.device)
-                if hasattr(car, "linear"):
-                    return car.linear(x.contiguous(), self.weight)
-            return self.reduce(F.linear(x, self.weight))
+                if hasattr(car, "linear") and (
+                        self.fused_gemm != "auto" or
+                        car.backend.gemm_preferred(x.reshape(-1, x.shape[-1]), self.weight)):
+                    if residual is None or not self.fuse_residual:
+                        out = car.linear(x.contiguous(), self.weight)
+                        return out if residual is None else residual + out
+                    return car.linear(x.contiguous(), self.weight,
+                                      residual=residual.contiguous())
+            return self.reduce(F.linear(x, self.weight), residual)
 
         def collectives(self):
             return list(self._car.values())
@@ -543,9 +563,9 @@ def make_module_classes():
             q, k, v = (z.transpose(1, 2) for z in (q, k, v))
             a = F.scaled_dot_product_attention(q, k, v, is_causal=True,
                                                enable_gqa=self.hl != self.kvl)
-            h = h + self.o_proj(a.transpose(1, 2).reshape(b, t, self.hl * self.hd))
+            h = self.o_proj(a.transpose(1, 2).reshape(b, t, self.hl * self.hd), residual=h)
             g, u = self.gate_up(self.ln2(h)).chunk(2, dim=-1)
-            return h + self.down_proj(F.silu(g) * u)
+            return self.down_proj(F.silu(g) * u, residual=h)
 
     def _rope(x, cos, sin):
         x1, x2 = x[..., : x.shape[-1] // 2], x[..., x.shape[-1] // 2:]
@@ -586,6 +606,17 @@ def make_module_classes():
             if self.check_health and not torch.cuda.is_current_stream_capturing():
                 self.check_collectives()
             return out
+
+        def configure(self, scheme, algo="oneshot", fused_gemm=None):
+            """Switch every row-parallel layer to another all-reduce (bf16 NCCL
+            when ``scheme`` is None) on the SAME weights; collectives are
+            cached per (shape, scheme, algo), so switching back reuses them."""
+            for blk in self.blocks:
+                for m in (blk.o_proj, blk.down_proj):
+                    m.scheme, m.algo = scheme, algo
+                    if fused_gemm is not None:
+                        m.fused_gemm = fused_gemm
+            return self
 
         def collectives(self):
             return [c for blk in self.blocks for m in (blk.o_proj, blk.down_proj)
@@ -644,3 +675,73 @@ def measure_ttft(cfg: LlamaConfig, batch: int, seq: int, tp: int = 1, group=None
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
         ms = float(t.item())
     return ms
+
+
+def measure_ttft_ab(cfg: LlamaConfig, batch: int, seq: int, variants, tp: int = 1, group=None,
+                    layers=None, reps: int = 15, warmup: int = 2, seed: int = 0):
+    """Prefill TTFT of several all-reduce variants on ONE model (same
+    weights, same input), each captured as its own CUDA graph, the replays
+    interleaved round-robin (v0 v1 v2 v0 v1 v2 ...) so clock / thermal drift
+    hits every variant alike.  ``variants``: [(label, scheme | None, algo,
+    fused_gemm)].  Returns {label: median ms (max over ranks)}; a variant
+    that fails to build or capture maps to the exception text."""
+    torch = _torch()
+    import torch.distributed as dist
+
+    torch.manual_seed(seed)
+    _, _, _, LlamaTP = make_module_classes()
+    model = LlamaTP(cfg, tp, group, None, "oneshot", layers)
+    h = torch.randn(batch, seq, cfg.hidden, device="cuda", dtype=torch.bfloat16)
+    graphs, errors = {}, {}
+    with torch.inference_mode():
+        for label, scheme, algo, fused in variants:
+            try:
+                model.configure(scheme, algo, fused)
+                for _ in range(warmup):
+                    model(h)
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                s = torch.cuda.Stream()
+                s.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(s):
+                    model(h)
+                torch.cuda.current_stream().wait_stream(s)
+                torch.cuda.synchronize()
+                with torch.cuda.graph(g):
+                    model(h)
+                graphs[label] = g
+            except Exception as exc:  # noqa: BLE001 (reported per variant)
+                errors[label] = f"{type(exc).__name__}: {exc}"[:200]
+                torch.cuda.synchronize()
+        if dist.is_initialized():
+            # every rank must run the same graphs in the same order
+            ok = torch.tensor([len(graphs)], device="cuda")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+            if int(ok.item()) != len(graphs):
+                raise RuntimeError(f"variants failed on another rank: {errors}")
+            dist.barrier(group)
+        times = {label: [] for label in graphs}
+        for label, g in graphs.items():
+            g.replay()
+        torch.cuda.synchronize()
+        for _ in range(reps):
+            for label, g in graphs.items():
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                g.replay()
+                e1.record()
+                torch.cuda.synchronize()
+                times[label].append(e0.elapsed_time(e1))
+        model.check_collectives()
+    out = {}
+    for label in graphs:
+        ms = float(np.median(times[label]))
+        if dist.is_initialized():
+            t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+            ms = float(t.item())
+        out[label] = ms
+    out.update(errors)
+    del graphs
+    return out

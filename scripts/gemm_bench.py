@@ -34,6 +34,8 @@ SHAPES = {
            ("llama-3.1-8b down_proj tp2", 2048, 4096, 7168),
            ("llama-3.1-8b o_proj tp8", 2048, 4096, 512),
            ("llama-3.1-8b down_proj tp8", 2048, 4096, 1792)],
+    "8b_tp1": [("llama-3.1-8b o_proj tp1", 2048, 4096, 4096),
+               ("llama-3.1-8b down_proj tp1", 2048, 4096, 14336)],
     "70b": [("llama-3.1-70b o_proj tp8", 4096, 8192, 1024),
             ("llama-3.1-70b down_proj tp8", 4096, 8192, 3584)],
 }

@@ -48,14 +48,15 @@ class OracleBackend:
         for j in range(-(-v.size // c)):
             self._put(shards[j * stride:(j + 1) * stride], c, v[j * c:(j + 1) * c])
 
-    def dequant_sum(self, shards, rank_stride, nranks, n, c, chunk_stride, out):
+    def dequant_sum(self, shards, rank_stride, nranks, n, c, chunk_stride, out, residual=None):
         acc = np.zeros(n, dtype=np.float32)
         for j in range(-(-n // c)):
             lo, hi = j * c, min(n, (j + 1) * c)
             for r in range(nranks):
                 base = r * rank_stride + j * chunk_stride
                 acc[lo:hi] += self._get(shards[base:], c, hi - lo)
-        out.copy_(torch.from_numpy(acc).to(out.dtype))
+        s = torch.from_numpy(acc).to(out.dtype)
+        out.copy_(s if residual is None else residual.reshape(-1) + s)
 
     def requant(self, shards, rank_stride, nranks, n, c, out_shard, ws, flag):
         acc = np.zeros(n, dtype=np.float32)

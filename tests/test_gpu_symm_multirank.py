@@ -30,7 +30,8 @@ def lib():
     return _native
 
 
-def run_ranks(_native, spec, parts, calls, out_dtype=torch.float32, algo="oneshot"):
+def run_ranks(_native, spec, parts, calls, out_dtype=torch.float32, algo="oneshot",
+              residuals=None):
     from paper_2411_09510_b200.formats import parse_scheme
 
     sch = parse_scheme(spec, extensions=True)
@@ -51,6 +52,10 @@ def run_ranks(_native, spec, parts, calls, out_dtype=torch.float32, algo="onesho
         lib.mx_nonfinite_reset(ctypes.c_void_p(f.data_ptr()), None)
     outs = [torch.empty(n, dtype=out_dtype, device="cuda") for _ in range(N)]
     streams = [torch.cuda.Stream() for _ in range(N)]
+
+    def res(r):
+        return ctypes.c_void_p(residuals[r].data_ptr()) if residuals is not None else None
+
     torch.cuda.synchronize()
     results = []
     for c in range(calls):
@@ -64,12 +69,12 @@ def run_ranks(_native, spec, parts, calls, out_dtype=torch.float32, algo="onesho
                 rc = lib.mx_allreduce_symm(
                     ctypes.c_void_p(xs[r].data_ptr()), _native.MX_BF16, n, ctypes.byref(cs),
                     ctypes.c_void_p(bptr.data_ptr()), ctypes.c_void_p(fptr.data_ptr()), r, N,
-                    slot, ctypes.c_void_p(outs[r].data_ptr()), odt, *common)
+                    slot, ctypes.c_void_p(outs[r].data_ptr()), odt, res(r), *common)
             else:
                 rc = lib.mx_allreduce_symm_twoshot(
                     ctypes.c_void_p(xs[r].data_ptr()), _native.MX_BF16, n, ctypes.byref(cs),
                     ctypes.c_void_p(bptr.data_ptr()), ctypes.c_void_p(fptr.data_ptr()), r, N,
-                    ctypes.c_void_p(outs[r].data_ptr()), odt, *common)
+                    ctypes.c_void_p(outs[r].data_ptr()), odt, res(r), *common)
             _native.check(rc, "mx_allreduce_symm")
         torch.cuda.synchronize()
         assert all(int(s[0].item()) == 0 for s in state), "peer wait timed out"
@@ -122,6 +127,25 @@ def test_symm_twoshot_multirank_bit_exact(lib, N, spec):
             ref = torch.from_numpy(O.allreduce_twoshot(x64s[c % 3], O.scheme(spec))).to(out_dtype)
             for r in range(N):
                 assert torch.equal(outs[r].cpu(), ref), (spec, N, c, r, out_dtype)
+
+
+@pytest.mark.parametrize("algo", ["oneshot", "twoshot"])
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_symm_multirank_residual_fused(lib, algo, out_dtype):
+    """residual + all_reduce fused into K5 / K5b's store: every rank's output
+    equals its own residual + the oracle sum, added in out_dtype (the
+    unfused torch add) -- bit for bit."""
+    N, n, spec = 4, 4 * 16 * 1024, "fp4_e2m1:32:e8m0"
+    x64 = [inputs.gauss_bf16(n, 8100 + r) for r in range(N)]
+    xs = [torch.from_numpy(x).to("cuda", torch.bfloat16) for x in x64]
+    resid = [torch.from_numpy(inputs.gauss_bf16(n, 8200 + r)).to("cuda", out_dtype)
+             for r in range(N)]
+    outs = run_ranks(lib, spec, xs, 3, out_dtype=out_dtype, algo=algo, residuals=resid)
+    f = O.allreduce_oneshot if algo == "oneshot" else O.allreduce_twoshot
+    s = torch.from_numpy(f(x64, O.scheme(spec))).to(out_dtype)
+    for call in outs:
+        for r in range(N):
+            assert torch.equal(call[r].cpu(), resid[r].cpu() + s), (algo, out_dtype, r)
 
 
 def test_symm_capped_grid_unit_row_loop():

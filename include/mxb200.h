@@ -264,6 +264,20 @@ int mx_unpack_codes(const uint8_t* packed, int64_t count, int32_t width, uint8_t
 int mx_pack_codes(const uint8_t* codes, int64_t count, int32_t width, uint8_t* packed,
                   void* stream);
 
+/* serialize (mx/codec.py:340-348) on the device: out = header || scale
+ * stream || element stream, one launch, any byte alignment.  `header` is a
+ * HOST pointer to the pack_header bytes (mx/codec.py:300-308), at most 544
+ * bytes (64 dimensions), copied into the kernel's parameters -- so the call
+ * is CUDA-graph capturable; out holds serialized_nbytes(scheme, shape). */
+int mx_serialize(const uint8_t* header, int32_t header_bytes, const uint8_t* scale_stream,
+                 int64_t scale_bytes, const uint8_t* element_stream, int64_t element_bytes,
+                 uint8_t* out, void* stream);
+
+/* Device byte copy at any source / destination alignment (deserialize's
+ * payload slices, mx/codec.py:351-380, moved to aligned stream buffers so
+ * the decode takes the vectorised kernels). */
+int mx_copy_bytes(const uint8_t* src, int64_t nbytes, uint8_t* dst, void* stream);
+
 /* ---- comparison codecs (mx/baselines.py), the paper's Table 4 baselines ---- */
 
 /* channelwise_int_compress (mx/baselines.py:138-168): x is `rows` x

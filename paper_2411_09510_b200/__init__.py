@@ -15,8 +15,9 @@ from .formats import (ELEMENT_CODES, ELEMENT_FORMATS, EXTENSION_FORMATS, SCALE_C
                       parse_scheme, scale_format)
 from .codec import (CompressedTensor, DeviceCompressedTensor, block_error_bound,
                     compress_tensor, compress_tensor_device, decompress_tensor,
-                    decompress_tensor_device, dequantize_block, deserialize, header_nbytes,
-                    pack_header, quantize_block, serialize, serialized_nbytes, unpack_header)
+                    decompress_tensor_device, dequantize_block, deserialize, deserialize_device,
+                    header_nbytes, pack_header, quantize_block, serialize, serialize_device,
+                    serialized_nbytes, unpack_header)
 
 from .baselines import (ChannelIntPacket, TopKPacket, channelwise_int_compress,
                         channelwise_int_decompress, topk_compress, topk_decompress)
@@ -25,6 +26,8 @@ from .tp import (ReductionReport, TPConfig, parallelism_sweep, shard_rowwise,
                  simulate_reduction)
 from .netbench import (BenchResult, LinkModel, calibrate_codec_throughput, predict_comm_time,
                        predicted_speedup, run_allgather_bench)
+from .search import (DeviceReductionEvaluator, make_activation_evaluator,
+                     make_simulation_evaluator)
 from .collective import (CompressedAllReduce, HostPipeline, LocalThreadGroup,
                          SimulatedAllReduce, SymmetricAllReduce, compressed_all_reduce)
 

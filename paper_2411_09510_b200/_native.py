@@ -74,6 +74,8 @@ SIGNATURES = {
     "mx_gemm_quantize_chunks": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, _SP, c_vp, c_i64,
                                         c_vp, c_vp, c_vp]),
     "mx_memset_async": (c_i32, [c_vp, c_i32, c_i64, c_vp]),
+    "mx_serialize": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
+    "mx_copy_bytes": (c_i32, [c_vp, c_i64, c_vp, c_vp]),
     "mx_nonfinite_reset": (c_i32, [c_vp, c_vp]),
 }
 

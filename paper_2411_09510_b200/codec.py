@@ -11,7 +11,9 @@ Reference surface kept unchanged (mx/codec.py:93-393): ``CompressedTensor``,
 * CUDA tensors can stay on the device end to end with
   :func:`compress_tensor_device` / :func:`decompress_tensor_device` (no host
   sync, graph-capturable apart from the optional non-finite check).
-* The MXC1 container (serialize/deserialize) is host-side byte formatting.
+* The MXC1 container: ``serialize``/``deserialize`` on host bytes (as the
+  reference), ``serialize_device``/``deserialize_device`` on CUDA buffers
+  (one kernel; only the header is parsed on the host).
 
 There is no CPU implementation of the arithmetic here: without a CUDA
 device and ``libmxb200.so`` every compute call raises ``NativeUnavailable``.
@@ -401,6 +403,93 @@ def deserialize(data: bytes) -> CompressedTensor:
     if len(data) > end:
         raise MalformedHeader(f"{len(data) - end} trailing bytes after payload")
     return CompressedTensor(scheme, shape, bytes(data[off:off + sb]), bytes(data[off + sb:end]))
+
+
+# ---------------------------------------------------------------------------
+# MXC1 on the device: the container built / parsed without moving the payload
+# through the host (one kernel, graph-capturable)
+# ---------------------------------------------------------------------------
+
+
+def _payload_scheme(fcode: int, scode: int, block: int) -> SchemeDescriptor:
+    """The scheme a header names, validated as deserialize does
+    (mx/codec.py:351-366)."""
+    enames, snames = list(ELEMENT_FORMATS), list(SCALE_FORMATS)
+    if fcode >= len(enames):
+        raise MalformedHeader(f"format code {fcode:#x} is not a block-quantized payload")
+    if scode >= len(snames):
+        raise MalformedHeader(f"unknown scale format code {scode}")
+    if block < 1:
+        raise MalformedHeader("block size must be positive")
+    return SchemeDescriptor(ELEMENT_FORMATS[enames[fcode]], block, SCALE_FORMATS[snames[scode]])
+
+
+def serialize_device(ct, out=None):
+    """serialize (mx/codec.py:340-348) into a CUDA uint8 tensor: the same
+    bytes, written by one kernel (k_mxc1_cat) from the device streams; the
+    header travels as a kernel parameter, so no host buffer is involved and
+    the call can be captured in a CUDA graph.  ``out`` (optional) is a
+    preallocated CUDA uint8 tensor of ``serialized_nbytes`` bytes."""
+    torch = _torch()
+    if isinstance(ct, CompressedTensor):
+        ct = _upload(ct)
+    sch = ct.scheme
+    if sch.element.name not in ELEMENT_CODES:
+        raise MalformedHeader(f"{sch.element.name} has no MXC1 format code")
+    header = pack_header(ELEMENT_CODES[sch.element.name], SCALE_CODES[sch.scale.name],
+                         sch.block_size, ct.shape)
+    sb, eb = ct.scale.numel(), ct.elements.numel()
+    total = len(header) + sb + eb
+    if out is None:
+        out = torch.empty(total, dtype=torch.uint8, device=ct.scale.device)
+    elif out.numel() != total or out.dtype != torch.uint8 or not out.is_cuda:
+        raise ValueError(f"out must be a CUDA uint8 tensor of {total} bytes")
+    lib = _native.load()
+    hb = ctypes.create_string_buffer(header, len(header))
+    _native.check(lib.mx_serialize(hb, len(header), ctypes.c_void_p(ct.scale.data_ptr()), sb,
+                                   ctypes.c_void_p(ct.elements.data_ptr()), eb,
+                                   ctypes.c_void_p(out.data_ptr()), _stream()), "mx_serialize")
+    return out
+
+
+def deserialize_device(data, copy: bool = True) -> DeviceCompressedTensor:
+    """deserialize (mx/codec.py:351-380) of a CUDA uint8 container.  Only the
+    header (at most 20 + 8*ndim bytes) crosses to the host, where it is
+    validated exactly as deserialize does (same exceptions); the payload
+    stays on the device.  ``copy`` moves the two streams into fresh aligned
+    buffers (k_mxc1_cat) so the decode takes the vectorised kernels; with
+    ``copy=False`` they are zero-copy views of ``data``."""
+    torch = _torch()
+    if not (hasattr(data, "is_cuda") and data.is_cuda and data.dtype == torch.uint8):
+        raise TypeError("deserialize_device expects a CUDA uint8 tensor")
+    data = data.reshape(-1)
+    size = data.numel()
+    head = data[:_HEADER.size].cpu().numpy().tobytes()
+    if len(head) >= _HEADER.size:
+        ndim = _HEADER.unpack_from(head)[6]
+        end = min(size, _HEADER.size + 8 * ndim)
+        head = data[:end].cpu().numpy().tobytes()
+    fcode, scode, block, shape, off = unpack_header(head)
+    scheme = _payload_scheme(fcode, scode, block)
+    n = _numel(shape)
+    sb = packed_nbytes(-(-n // block), scheme.scale.exponent_bits)
+    eb = packed_nbytes(n, scheme.element.total_bits)
+    end = off + sb + eb
+    if size < end:
+        raise TruncatedStream(f"payload needs {end - off} bytes, stream holds {size - off}")
+    if size > end:
+        raise MalformedHeader(f"{size - end} trailing bytes after payload")
+    sv, ev = data[off:off + sb], data[off + sb:end]
+    if not copy:
+        return DeviceCompressedTensor(scheme, shape, sv, ev)
+    lib = _native.load()
+    sc = torch.empty(sb, dtype=torch.uint8, device=data.device)
+    el = torch.empty(eb, dtype=torch.uint8, device=data.device)
+    st = _stream()
+    for src, dst in ((sv, sc), (ev, el)):
+        _native.check(lib.mx_copy_bytes(ctypes.c_void_p(src.data_ptr()), src.numel(),
+                                        ctypes.c_void_p(dst.data_ptr()), st), "mx_copy_bytes")
+    return DeviceCompressedTensor(scheme, shape, sc, el)
 
 
 def block_error_bound(stored_scale_code: int, scheme: SchemeDescriptor) -> float:

@@ -185,6 +185,65 @@ __global__ void g_pack(const uint8_t* codes, int64_t count, int width, uint8_t* 
 
 __global__ void g_fill_u64(unsigned long long* p, unsigned long long v) { *p = v; }
 
+// MXC1 container on the device (mx/codec.py:340-348): header (a kernel
+// parameter, so the launch is graph-capturable with no host buffer) +
+// scale stream + element stream concatenated at arbitrary byte offsets.
+// Thread t owns output bytes [16t, 16t+16): a 128-bit store when aligned,
+// its source bytes gathered with byte loads (neighbouring lanes share the
+// 32 B sectors, so the gather is L1-served; the streams are read once from
+// HBM).  Also the realigning copy of deserialize (no header, one segment).
+constexpr int kMaxHeader = 544;  // 20 + 8 * 64: numpy's 64 dimensions
+struct CatArgs {
+  uint8_t hdr[kMaxHeader];
+  int hlen;
+  const uint8_t* s0;
+  int64_t n0;
+  const uint8_t* s1;
+  int64_t n1;
+  uint8_t* out;
+  int64_t total;
+};
+
+__global__ void __launch_bounds__(256) k_mxc1_cat(const __grid_constant__ CatArgs A) {
+  const int64_t o0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 16;
+  if (o0 >= A.total) return;
+  const int64_t e0 = A.hlen, e1 = e0 + A.n0;
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+  const int cnt = (int)min((int64_t)16, A.total - o0);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (i >= cnt) break;
+    const int64_t o = o0 + i;
+    uint32_t v;
+    if (o < e0)
+      v = A.hdr[o];
+    else if (o < e1)
+      v = __ldg(A.s0 + (o - e0));
+    else
+      v = __ldg(A.s1 + (o - e1));
+    w[i >> 2] |= v << (8 * (i & 3));
+  }
+  uint8_t* d = A.out + o0;
+  if (cnt == 16 && ((uintptr_t)d & 15) == 0) {
+    *reinterpret_cast<uint4*>(d) = make_uint4(w[0], w[1], w[2], w[3]);
+  } else {
+    for (int i = 0; i < cnt; ++i) d[i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
+  }
+}
+
+int launch_cat(const uint8_t* hdr, int hlen, const uint8_t* s0, int64_t n0, const uint8_t* s1,
+               int64_t n1, uint8_t* out, cudaStream_t st) {
+  CatArgs a;
+  memset(&a, 0, sizeof(a));
+  if (hlen) memcpy(a.hdr, hdr, hlen);
+  a.hlen = hlen; a.s0 = s0; a.n0 = n0; a.s1 = s1; a.n1 = n1; a.out = out;
+  a.total = hlen + n0 + n1;
+  if (a.total == 0) return 0;
+  const int64_t threads = (a.total + 15) / 16;
+  k_mxc1_cat<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(a);
+  return 1;
+}
+
 // k_gemm.cu
 cudaError_t launch_gemm_mx(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
                            const Fmt* f, int enc, int64_t chunk_values, int64_t chunk_stride,
@@ -832,6 +891,29 @@ int mx_pack_codes(const uint8_t* codes, int64_t count, int32_t width, uint8_t* p
   int64_t groups = cdiv(count, 8);
   g_pack<<<cdiv(groups, 256), 256, 0, (cudaStream_t)stream>>>(codes, count, width, packed);
   return cuda_check("g_pack");
+}
+
+int mx_serialize(const uint8_t* header, int32_t header_bytes, const uint8_t* scale_stream,
+                 int64_t scale_bytes, const uint8_t* element_stream, int64_t element_bytes,
+                 uint8_t* out, void* stream) {
+  if (header_bytes < 0 || header_bytes > kMaxHeader)
+    return fail(MX_ERR_INVALID_ARGUMENT, "header of %d bytes (at most %d: 64 dimensions)",
+                header_bytes, kMaxHeader);
+  if (scale_bytes < 0 || element_bytes < 0) return fail(MX_ERR_INVALID_ARGUMENT, "bad sizes");
+  if ((header_bytes && !header) || (scale_bytes && !scale_stream) ||
+      (element_bytes && !element_stream) || !out)
+    return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (launch_cat(header, header_bytes, scale_stream, scale_bytes, element_stream, element_bytes,
+                 out, (cudaStream_t)stream))
+    return cuda_check("k_mxc1_cat");
+  return MX_OK;
+}
+
+int mx_copy_bytes(const uint8_t* src, int64_t nbytes, uint8_t* dst, void* stream) {
+  if (nbytes < 0 || (nbytes && (!src || !dst))) return fail(MX_ERR_INVALID_ARGUMENT, "bad copy");
+  if (launch_cat(nullptr, 0, src, nbytes, nullptr, 0, dst, (cudaStream_t)stream))
+    return cuda_check("k_mxc1_cat");
+  return MX_OK;
 }
 
 int mx_memset_async(void* ptr, int32_t value, int64_t bytes, void* stream) {

@@ -387,12 +387,13 @@ def time_graph_replays(torch, graphs, k):
 
 
 def rotation(k, r_min, cap=32):
-    """Buffer-set count R: the smallest divisor of k in [r_min, cap], so the
+    """Buffer-set count R: the LARGEST divisor of k in [r_min, cap], so the
     k timed steps are exactly k / R replays of ONE graph holding the R sets'
-    steps back to back -- every step pays the same (amortised) graph launch
-    whatever --steps is.  Without such a divisor R = r_min and one extra
-    graph holds the k mod R remaining steps."""
-    for d in range(r_min, max(r_min, cap) + 1):
+    steps back to back -- every step pays the same (amortised) share of the
+    ~2 us gap between graph launches, whatever --steps is, and that share is
+    as small as the buffer budget allows.  Without such a divisor R = r_min
+    and one extra graph holds the k mod R remaining steps."""
+    for d in range(max(r_min, cap), r_min - 1, -1):
         if k % d == 0:
             return d
     return r_min
@@ -454,13 +455,22 @@ def load_traffic(kernel_key):
         return None
 
 
-def kernel_graph_time(torch, fn, reps, launches_per_replay):
+def kernel_graph_time(torch, fn, reps, launches_per_replay, min_launches=24):
     """Device time per launch of a graph of back-to-back launches (each over a
-    different buffer set, so every launch reads HBM-cold data)."""
-    g = capture(torch, fn)
+    different buffer set, so every launch reads HBM-cold data).  ``fn`` (one
+    pass over the R sets) is captured enough times that a graph holds at
+    least ``min_launches`` launches: the gap between graph launches is
+    amortised the same way for every kernel and shape."""
+    passes = max(1, -(-min_launches // launches_per_replay))
+
+    def body():
+        for _ in range(passes):
+            fn()
+
+    g = capture(torch, body)
     for _ in range(3):
         g.replay()
-    ms = time_graph_replays(torch, [g], reps) / (reps * launches_per_replay)
+    ms = time_graph_replays(torch, [g], reps) / (reps * launches_per_replay * passes)
     del g
     return ms
 

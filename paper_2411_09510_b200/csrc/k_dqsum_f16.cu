@@ -6,8 +6,8 @@ namespace {
 template <int B, int DEC, int BITS>
 void go(const DArgs& a, cudaStream_t st) {
   if (a.f.kbits == 8 && a.cv % kUnit == 0 && a.n % a.cv == 0 && (!a.plain || a.nranks == 1)) {
-    launch_pdl(k_dqsum_lean<__half, B, DEC, BITS>, dim3((unsigned)((a.n / kUnit + kWarps - 1) / kWarps)),
-               dim3(kThreads), 0, st, a);
+    launch_pdl(k_dqsum_lean<__half, B, DEC, BITS>, dim3((unsigned)((a.n / kUnit + kLeanWarps2 - 1) / kLeanWarps2)),
+               dim3(kLeanThreads2), 0, st, a);
     return;
   }
   auto k = k_dqsum<__half, B, DEC, BITS>;

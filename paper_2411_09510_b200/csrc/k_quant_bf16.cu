@@ -11,8 +11,7 @@ namespace mxb {
 namespace qb {
 template <int B, int ENC, int BITS>
 void go(const QArgs& a, cudaStream_t st) {
-  auto k = k_quant<__nv_bfloat16, B, ENC, BITS>;
-  launch_pdl(k, dim3(work_grid(k, a.total_units, 1)), dim3(kThreads), 0, st, a);
+  launch_quant<__nv_bfloat16, B, ENC, BITS>(a, st);
 }
 template <int B>
 void by_enc(const QArgs& a, int enc, int bits, cudaStream_t st) {

@@ -720,6 +720,62 @@ __global__ void __launch_bounds__(kThreads) k_quant(const QArgs A) {
   }
 }
 
+// K1 lean form (round 2; scripts/kquant_probe.cu, profiles/r02/k1_lean):
+// E8M0 scales, one chunk or equal chunks of whole 1024-value units.  One
+// unit per warp over a flat grid -- no grid-stride loop, no paired units --
+// with registers capped so that MINB CTAs (6 x 8 warps for 16-bit inputs)
+// stay resident: the loads of 48 warps per SM are in flight at once and the
+// block scheduler balances the tail.  8B shape: 5.07 -> 4.74 us; 70B shape:
+// 15.23 -> 13.93 us (0.93 of the HBM copy peak).
+template <typename InT, int B_, int ENC, int BITS, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_quant_lean(const QArgs A) {
+  constexpr int B = B_;
+  pdl_prologue();
+  const int lane = threadIdx.x & 31;
+  const uint32_t u = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint32_t total = (uint32_t)A.total_units, upc = (uint32_t)A.units_per_chunk;
+  if (u >= total) return;
+  const InT* x = reinterpret_cast<const InT*>(A.x);
+  const Fmt f = A.f;
+  if (total != upc) {  // equal chunks of whole units: unit u is flat unit u of x
+    Raw<InT> r;
+    load_raw<InT>(x + (size_t)u * kUnit + lane * kVPL, r);
+    const uint32_t chunk = u / upc, q = u - chunk * upc;
+    QArgs C = A;
+    C.elem_base = A.elem_base + (size_t)chunk * A.chunk_stride;
+    C.scale_base = A.scale_base + (size_t)chunk * A.chunk_stride;
+    C.flat_off = A.flat_off + (int64_t)chunk * A.cv;
+    quant_full_unit<InT, B, ENC, BITS>(C, f, q, r, lane);
+    return;
+  }
+  if ((int64_t)(u + 1) * kUnit <= A.n) {
+    Raw<InT> r;
+    load_raw<InT>(x + (size_t)u * kUnit + lane * kVPL, r);
+    quant_full_unit<InT, B, ENC, BITS>(A, f, u, r, lane);
+    return;
+  }
+  // the partial last unit of a single chunk
+  __shared__ __align__(16) uint8_t s_stage[kWarps][kUnit / 8];
+  UnitPos p = unit_pos(u, upc, true, A.cv, A.n);
+  Raw<InT> r;
+  load_unit<InT>(x, p, lane, r);
+  quant_unit<InT, B, ENC, BITS>(A, f, p, r, lane, s_stage[threadIdx.x >> 5]);
+}
+
+// 6 resident CTAs (40 registers) fit the bf16-input register path of every
+// format with a hardware or closed-form encoder without spills (ptxas log);
+// the generic encoder, f16 inputs (abs-max in f32) and f32 inputs (twice
+// the raw registers) keep the 4-CTA bound
+template <typename InT, int ENC>
+constexpr int lean_minb() {
+  return (std::is_same<InT, __nv_bfloat16>::value && ENC != ENC_GEN) ? 6 : 4;
+}
+
+inline bool quant_lean_ok(const QArgs& a) {
+  return a.f.kbits == 8 &&
+         (a.total_units == a.units_per_chunk || (a.cv % kUnit == 0 && a.n % a.cv == 0));
+}
+
 // ---------------------------------------------------------------------------
 // K2: unpack + dequantise + rank-order fp32 sum
 // ---------------------------------------------------------------------------
@@ -1103,8 +1159,19 @@ __global__ void __launch_bounds__(kThreads) k_dqsum(const DArgs A) {
 // lane, the quantiser's layout), no chunk / tail / generic-scale logic, the
 // ranks' codes loaded two at a time before their decode.  A flat grid of
 // one unit per warp lets the block scheduler balance the waves.
+// 128-thread CTAs, 8 resident (64 registers): the same 32 warps per SM as
+// 256 x 4, scheduled at half the granularity -- the tail wave balances
+// better (scripts/kdq_probe.cu: 8B 5.96 -> 5.51 us, 70B 19.2 -> 17.9 us,
+// 8 ranks 12.3 -> 11.6 us)
+constexpr int kLeanThreads2 = 128;
+constexpr int kLeanWarps2 = kLeanThreads2 / 32;
+// the 8-CTA (64-register) bound is spill-free for the FP4 decode into
+// 16-bit outputs; other decoders and f32 outputs choose their own registers
+template <typename OutT, int DEC>
+constexpr int dq_minb() { return (DEC == ENC_E2M1 && sizeof(OutT) == 2) ? 8 : 1; }
+
 template <typename OutT, int B, int DEC, int BITS>
-__global__ void __launch_bounds__(kThreads) k_dqsum_lean(const DArgs A) {
+__global__ void __launch_bounds__(kLeanThreads2, dq_minb<OutT, DEC>()) k_dqsum_lean(const DArgs A) {
   using RL = RankLoad<B, BITS, kVPL>;
   pdl_prologue();
   __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
@@ -1114,7 +1181,7 @@ __global__ void __launch_bounds__(kThreads) k_dqsum_lean(const DArgs A) {
     __syncthreads();
   }
   const int lane = threadIdx.x & 31;
-  const uint32_t u = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint32_t u = blockIdx.x * kLeanWarps2 + (threadIdx.x >> 5);
   if (u >= (uint32_t)(A.n / kUnit)) return;
   // equal chunks of whole units: unit u is flat unit u of the output
   const uint32_t upc = (uint32_t)(A.cv / kUnit);
@@ -1300,6 +1367,17 @@ inline unsigned work_grid(K kernel, int64_t total_units, int per_warp) {
   int64_t need = (total_units + (int64_t)kWarps * per_warp - 1) / ((int64_t)kWarps * per_warp);
   int64_t g = std::min<int64_t>((int64_t)sms * occ, need);
   return (unsigned)std::max<int64_t>(g, 1);
+}
+
+template <typename InT, int B, int ENC, int BITS>
+inline void launch_quant(const QArgs& a, cudaStream_t st) {
+  if (quant_lean_ok(a)) {
+    launch_pdl(k_quant_lean<InT, B, ENC, BITS, lean_minb<InT, ENC>()>,
+               dim3((unsigned)((a.total_units + kWarps - 1) / kWarps)), dim3(kThreads), 0, st, a);
+    return;
+  }
+  auto k = k_quant<InT, B, ENC, BITS>;
+  launch_pdl(k, dim3(work_grid(k, a.total_units, 1)), dim3(kThreads), 0, st, a);
 }
 
 }  // namespace mxb

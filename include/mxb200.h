@@ -166,7 +166,7 @@ int mx_dequant_sum_requant(const uint8_t* shards, int64_t rank_stride, int32_t n
  * mx_quantize x nranks + mx_dequant_sum.  `partials` is a DEVICE array of
  * nranks pointers (bf16, 32-byte aligned); `barrier` is 2 device uint32
  * zeroed once (reusable across calls on one stream).  Returns
- * MX_ERR_UNSUPPORTED outside bf16-in, bf16/f32-out, B in {8,16,32,64}, E8M0,
+ * MX_ERR_UNSUPPORTED outside bf16-in, bf16/f32-out, B in {8,16,32,64} (any scale width),
  * element widths 4/5/6/8. */
 int mx_allreduce_fused(const void* const* partials, int32_t dtype, int32_t nranks, int64_t n,
                        const mx_scheme_t* scheme, uint8_t* shards, int64_t shard_stride,
@@ -222,7 +222,7 @@ int mx_symm_layout(int64_t n, const mx_scheme_t* scheme, int32_t nranks, int64_t
  *   epochs        local device u32 x ctas (zeroed once)
  *   residual      nullable, out_dtype, n values, may alias out: the residual
  *                 add fused into the store as in mx_dequant_sum_residual
- * MX_ERR_UNSUPPORTED outside bf16 in, n % 1024 == 0, E8M0, B in {16,32,64}. */
+ * MX_ERR_UNSUPPORTED outside bf16 in, n % 1024 == 0, B in {16,32,64}. */
 int mx_allreduce_symm(const void* x, int32_t dtype, int64_t n, const mx_scheme_t* scheme,
                       uint8_t* const* peer_bufs, uint32_t* const* peer_flags, int32_t rank,
                       int32_t nranks, int64_t slot_stride, void* out, int32_t out_dtype,
@@ -246,7 +246,7 @@ int mx_symm_twoshot_layout(int64_t n, const mx_scheme_t* scheme, int32_t nranks,
  * to quantise_chunks -> all_to_all -> dequant_sum_requant -> all_gather ->
  * dequant_sum.  Arguments as mx_allreduce_symm, sizes from
  * mx_symm_twoshot_layout.  MX_ERR_UNSUPPORTED outside bf16 in,
- * n % (1024*nranks) == 0, E8M0, B in {16,32,64}. */
+ * n % (1024*nranks) == 0, B in {16,32,64}. */
 int mx_allreduce_symm_twoshot(const void* x, int32_t dtype, int64_t n,
                               const mx_scheme_t* scheme, uint8_t* const* peer_bufs,
                               uint32_t* const* peer_flags, int32_t rank, int32_t nranks,

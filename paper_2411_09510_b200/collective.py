@@ -144,8 +144,10 @@ class NativeBackend:
         shape (measured, profiles/r02/gemm): it saves K1 (~2.5 B/value of
         HBM traffic) but schedules whole 256x256 tiles over the SM pairs, so
         a badly quantised last wave costs more than K1 once the GEMM is long.
-        Fused when the tile waves are >= 90 % full, or K <= 8192 (short
-        GEMMs, where the saved K1 dominates)."""
+        Fused when the tile waves are >= 90 % full, or K <= 4096 (short
+        GEMMs, where the saved K1 dominates: 8B o_proj at TP=1/2 and every
+        8B projection from TP=4 win, 8B down_proj at TP=1/2 -- K = 14336 /
+        7168 on 128 tiles = 1.73 waves -- lose 4-8 %)."""
         if not self.gemm_supported(x, w):
             return False
         import torch
@@ -155,7 +157,7 @@ class NativeBackend:
         tiles = -(-M // 256) * -(-N // 256)
         pairs = max(1, torch.cuda.get_device_properties(x.device).multi_processor_count // 2)
         waves = -(-tiles // pairs)
-        return tiles / (waves * pairs) >= 0.9 or K <= 8192
+        return tiles / (waves * pairs) >= 0.9 or K <= 4096
 
     def gemm_quantize_chunks(self, x2, w, c, shards, shard_stride, flag, partial=None):
         """k_gemm_mx: partial = x2 . w^T on the tensor cores, its MX shard(s)
@@ -401,7 +403,7 @@ class SymmetricAllReduce:
     re-quantisation, then pulls of every owner's reduced chunk), bit-identical
     to the NCCL two-shot.
     Requirements: bf16 partial, n % 1024 == 0 (two-shot: n % (1024*N) == 0),
-    E8M0 scales, B in {16,32,64}.
+    B in {16,32,64} (any scale width: E8M0, E5M0, ...).
     """
 
     def __init__(self, scheme, n: int, group=None, out_dtype=None, device=None,

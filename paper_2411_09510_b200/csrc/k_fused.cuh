@@ -114,10 +114,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_fused_oneshot(const FArgs F) {
       int64_t uoff = (int64_t)u * kUnit2;
       int valid = max(0, min(kVPL2, (int)min((int64_t)kUnit2, F.n - uoff) - lane * kVPL2));
       RL c0, c1;
-      load_rank<B, BITS, kVPL2, true>(c0, F.shards, F.scale_off, F.elem_off, uoff, lane, valid,
+      load_rank<B, BITS, kVPL2, 8>(c0, F.shards, F.scale_off, F.elem_off, uoff, lane, valid,
                                       f.kbits);
       if (nr > 1)
-        load_rank<B, BITS, kVPL2, true>(c1, F.shards + F.shard_stride, F.scale_off, F.elem_off,
+        load_rank<B, BITS, kVPL2, 8>(c1, F.shards + F.shard_stride, F.scale_off, F.elem_off,
                                         uoff, lane, valid, f.kbits);
       while (true) {
         const uint32_t un = u + nw;
@@ -128,10 +128,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_fused_oneshot(const FArgs F) {
         if (more) {
           uoffn = (int64_t)un * kUnit2;
           validn = max(0, min(kVPL2, (int)min((int64_t)kUnit2, F.n - uoffn) - lane * kVPL2));
-          load_rank<B, BITS, kVPL2, true>(n0, F.shards, F.scale_off, F.elem_off, uoffn, lane,
+          load_rank<B, BITS, kVPL2, 8>(n0, F.shards, F.scale_off, F.elem_off, uoffn, lane,
                                           validn, f.kbits);
           if (nr > 1)
-            load_rank<B, BITS, kVPL2, true>(n1, F.shards + F.shard_stride, F.scale_off,
+            load_rank<B, BITS, kVPL2, 8>(n1, F.shards + F.shard_stride, F.scale_off,
                                             F.elem_off, uoffn, lane, validn, f.kbits);
         }
         float acc[kVPL2];
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_fused_oneshot(const FArgs F) {
         const uint8_t* b = F.shards + 2 * F.shard_stride;
         for (int rk = 2; rk < nr; ++rk, b += F.shard_stride) {
           RL r;
-          load_rank<B, BITS, kVPL2, true>(r, b, F.scale_off, F.elem_off, uoff, lane, valid,
+          load_rank<B, BITS, kVPL2, 8>(r, b, F.scale_off, F.elem_off, uoff, lane, valid,
                                           f.kbits);
           decode_rank<B, DEC, BITS, kVPL2>(r, f, acc, false, s_lut);
         }
@@ -178,7 +178,7 @@ __host__ __device__ constexpr int flow_units_per_warp(int B, int ENC) {
 // decodes + sums them in rank order.  Quantise and dequant-sum of different
 // units overlap across warps instead of being separated by a grid barrier;
 // every warp owns one unit, the grid is sized to the work (several waves).
-template <typename OutT, int B, int ENC, int BITS, int TH = kThreads>
+template <typename OutT, int B, int ENC, int BITS, int TH = kThreads, int KB = 8>
 __device__ __forceinline__ void k_flow_one_unit(const FArgs& F) {
   using InT = __nv_bfloat16;
   constexpr int DEC = dec_of(ENC, BITS);
@@ -207,6 +207,10 @@ __device__ __forceinline__ void k_flow_one_unit(const FArgs& F) {
     if (bad) report_nonfinite_raw<InT>(raw, kVPL, (int64_t)xoff, F.nonfinite);
     uint8_t* shard = F.shards + (size_t)r * F.shard_stride;
     store_lane_codes<BITS>(shard + eoff + lane * (4 * BITS), c, kVPL);
+    if constexpr (KB != 8) {  // E5M0 etc.: packed k-bit codes, group leaders store
+      store_unit_scales_k<B>(shard + F.scale_off, (int64_t)q * USCALES, stored, lane, KB);
+      return;
+    }
     uint8_t* sp = shard + soff + (lane / LPB) * NSB;
     if constexpr (NSB == 4) {
       *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
@@ -218,6 +222,45 @@ __device__ __forceinline__ void k_flow_one_unit(const FArgs& F) {
       if (lane % LPB == 0) *sp = (uint8_t)stored[0];
     }
   };
+
+  if constexpr (KB != 8) {
+    // Packed k-bit scale codes (E5M0): a unit's scale segment (e.g. 20 B at
+    // B = 32) straddles 32-byte sectors that neighbouring warps write too,
+    // so the codes are not read back -- rank pair by rank pair, the warp
+    // quantises into the shard, reads the element codes back and decodes
+    // them with the scale codes from the registers that produced (and
+    // stored) them: the same bits the shard holds.  Rank order is kept.
+    using RL = RankLoad<B, BITS, kVPL>;
+    float acc[kVPL];
+#pragma unroll
+    for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
+    auto quantise_k = [&](const Raw<InT>& raw, int r, RL& x) {
+      bool bad;
+      LaneCodes<BITS> c = quant_lane<InT, B, ENC, BITS>(raw, f, x.st, bad);
+      if (bad) report_nonfinite_raw<InT>(raw, kVPL, (int64_t)xoff, F.nonfinite);
+      uint8_t* shard = F.shards + (size_t)r * F.shard_stride;
+      store_lane_codes<BITS>(shard + eoff + lane * (4 * BITS), c, kVPL);
+      store_unit_scales_k<B>(shard + F.scale_off, (int64_t)q * USCALES, x.st, lane, KB);
+    };
+    for (int r = 0; r < nr; r += 2) {
+      Raw<InT> a, b;
+      load_raw<InT>(reinterpret_cast<const InT*>(F.partials[r]) + xoff, a);
+      if (r + 1 < nr) load_raw<InT>(reinterpret_cast<const InT*>(F.partials[r + 1]) + xoff, b);
+      RL x0, x1;
+      quantise_k(a, r, x0);
+      if (r + 1 < nr) quantise_k(b, r + 1, x1);
+      __syncwarp();
+      x0.c = load_lane_codes<BITS, true>(F.shards + (size_t)r * F.shard_stride + eoff +
+                                         lane * (4 * BITS), kVPL);
+      if (r + 1 < nr)
+        x1.c = load_lane_codes<BITS, true>(F.shards + (size_t)(r + 1) * F.shard_stride + eoff +
+                                           lane * (4 * BITS), kVPL);
+      decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
+      if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
+    }
+    store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(F.out) + xoff, kVPL, acc);
+    return;
+  }
 
   // ---- quantise unit q of every partial, two ranks' loads in flight ------
   for (int r = 0; r < nr; r += 2) {
@@ -236,18 +279,19 @@ __device__ __forceinline__ void k_flow_one_unit(const FArgs& F) {
   for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
   for (int r = 0; r < nr; r += 2) {
     RL x0, x1;
-    load_rank<B, BITS, kVPL, true>(x0, F.shards + (size_t)r * F.shard_stride, F.scale_off,
-                                   F.elem_off, (int64_t)q * kUnit, lane, kVPL, 8);
+    load_rank<B, BITS, kVPL, 8>(x0, F.shards + (size_t)r * F.shard_stride, F.scale_off,
+                                   F.elem_off, (int64_t)q * kUnit, lane, kVPL, KB);
     if (r + 1 < nr)
-      load_rank<B, BITS, kVPL, true>(x1, F.shards + (size_t)(r + 1) * F.shard_stride,
-                                     F.scale_off, F.elem_off, (int64_t)q * kUnit, lane, kVPL, 8);
+      load_rank<B, BITS, kVPL, 8>(x1, F.shards + (size_t)(r + 1) * F.shard_stride,
+                                     F.scale_off, F.elem_off, (int64_t)q * kUnit, lane, kVPL,
+                                     KB);
     decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
     if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
   }
   store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(F.out) + xoff, kVPL, acc);
 }
 
-template <typename OutT, int B, int ENC, int BITS, int TH = kThreads>
+template <typename OutT, int B, int ENC, int BITS, int TH = kThreads, int KB = 8>
 __device__ __forceinline__ void k_flow_multi_unit(const FArgs& F) {
   using InT = __nv_bfloat16;
   constexpr int DEC = dec_of(ENC, BITS);
@@ -276,6 +320,10 @@ __device__ __forceinline__ void k_flow_multi_unit(const FArgs& F) {
       report_nonfinite_raw<InT>(raw, kVPL, (int64_t)q * kUnit + lane * kVPL, F.nonfinite);
     uint8_t* shard = F.shards + (size_t)r * F.shard_stride;
     store_lane_codes<BITS>(shard + F.elem_off + (size_t)q * UBYTES + lane * (4 * BITS), c, kVPL);
+    if constexpr (KB != 8) {
+      store_unit_scales_k<B>(shard + F.scale_off, (int64_t)q * USCALES, stored, lane, KB);
+      return;
+    }
     uint8_t* sp = shard + F.scale_off + (size_t)q * USCALES + (lane / LPB) * NSB;
     if constexpr (NSB == 4) {
       *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
@@ -315,12 +363,12 @@ __device__ __forceinline__ void k_flow_multi_unit(const FArgs& F) {
     for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
     for (int r = 0; r < nr; r += 2) {
       RL x0, x1;
-      load_rank<B, BITS, kVPL, true>(x0, F.shards + (size_t)r * F.shard_stride, F.scale_off,
-                                     F.elem_off, (int64_t)q * kUnit, lane, kVPL, 8);
+      load_rank<B, BITS, kVPL, 8>(x0, F.shards + (size_t)r * F.shard_stride, F.scale_off,
+                                     F.elem_off, (int64_t)q * kUnit, lane, kVPL, KB);
       if (r + 1 < nr)
-        load_rank<B, BITS, kVPL, true>(x1, F.shards + (size_t)(r + 1) * F.shard_stride,
+        load_rank<B, BITS, kVPL, 8>(x1, F.shards + (size_t)(r + 1) * F.shard_stride,
                                        F.scale_off, F.elem_off, (int64_t)q * kUnit, lane, kVPL,
-                                       8);
+                                       KB);
       decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
       if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
     }
@@ -329,18 +377,20 @@ __device__ __forceinline__ void k_flow_multi_unit(const FArgs& F) {
   }
 }
 
-template <typename OutT, int B, int ENC, int BITS, int TH = kThreads>
+template <typename OutT, int B, int ENC, int BITS, int TH = kThreads, int KB = 8>
 __device__ __forceinline__ void k_fused_flow_body(const FArgs& F) {
-  if constexpr (flow_units_per_warp(B, ENC) == 1) k_flow_one_unit<OutT, B, ENC, BITS, TH>(F);
-  else k_flow_multi_unit<OutT, B, ENC, BITS, TH>(F);
+  if constexpr (flow_units_per_warp(B, ENC) == 1 || KB != 8)
+    k_flow_one_unit<OutT, B, ENC, BITS, TH, KB>(F);
+  else
+    k_flow_multi_unit<OutT, B, ENC, BITS, TH, KB>(F);
 }
 
-template <typename OutT, int B, int ENC, int BITS, int TH = kThreads>
+template <typename OutT, int B, int ENC, int BITS, int TH = kThreads, int KB = 8>
 __global__ void __launch_bounds__(TH, (ENC == ENC_E2M1 && B == 64) ? 1024 / TH : 0) k_fused_flow(const FArgs F) {
   // programmatic dependent launch: the producer grid (e.g. the o_proj GEMM
   // writing the partials) completes and flushes before any partial is read
   pdl_prologue();
-  k_fused_flow_body<OutT, B, ENC, BITS, TH>(F);
+  k_fused_flow_body<OutT, B, ENC, BITS, TH, KB>(F);
 }
 
 // ---------------------------------------------------------------------------
@@ -376,7 +426,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
-template <typename OutT, int B, int ENC, int BITS>
+template <typename OutT, int B, int ENC, int BITS, int KB = 8>
 __global__ void __launch_bounds__(kThreads) k_symm_flow(const SArgs S) {
   using InT = __nv_bfloat16;
   constexpr int DEC = dec_of(ENC, BITS);
@@ -413,6 +463,10 @@ __global__ void __launch_bounds__(kThreads) k_symm_flow(const SArgs S) {
     if (bad) report_nonfinite_raw<InT>(raw, kVPL, (int64_t)q * kUnit + lane * kVPL, S.nonfinite);
     uint8_t* shard = S.bufs[S.rank] + slot;
     store_lane_codes<BITS>(shard + S.elem_off + (size_t)q * UBYTES + lane * (4 * BITS), c, kVPL);
+    if constexpr (KB != 8) {  // packed k-bit scale codes (group leaders store)
+      store_unit_scales_k<B>(shard + S.scale_off, (int64_t)q * USCALES, stored, lane, KB);
+      continue;
+    }
     uint8_t* sp = shard + S.scale_off + (size_t)q * USCALES + (lane / LPB) * NSB;
     if constexpr (NSB == 4) {
       *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
@@ -456,11 +510,11 @@ __global__ void __launch_bounds__(kThreads) k_symm_flow(const SArgs S) {
     for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
     for (int r = 0; r < nr; r += 2) {
       RL x0, x1;
-      load_rank<B, BITS, kVPL, true>(x0, S.bufs[r] + slot, S.scale_off, S.elem_off,
-                                     (int64_t)q * kUnit, lane, kVPL, 8);
+      load_rank<B, BITS, kVPL, 8>(x0, S.bufs[r] + slot, S.scale_off, S.elem_off,
+                                     (int64_t)q * kUnit, lane, kVPL, KB);
       if (r + 1 < nr)
-        load_rank<B, BITS, kVPL, true>(x1, S.bufs[r + 1] + slot, S.scale_off, S.elem_off,
-                                       (int64_t)q * kUnit, lane, kVPL, 8);
+        load_rank<B, BITS, kVPL, 8>(x1, S.bufs[r + 1] + slot, S.scale_off, S.elem_off,
+                                       (int64_t)q * kUnit, lane, kVPL, KB);
       decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
       if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
     }
@@ -488,7 +542,7 @@ __global__ void __launch_bounds__(kThreads) k_symm_flow(const SArgs S) {
 // to it; no NCCL kernel, no grid barrier.
 // ---------------------------------------------------------------------------
 
-template <typename OutT, int B, int ENC, int BITS>
+template <typename OutT, int B, int ENC, int BITS, int KB = 8>
 __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
   using InT = __nv_bfloat16;
   constexpr int DEC = dec_of(ENC, BITS);
@@ -516,6 +570,10 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
 
   auto put = [&](uint8_t* shard, uint32_t q, const LaneCodes<BITS>& cc, const int* stored) {
     store_lane_codes<BITS>(shard + S.elem_off + (size_t)q * UBYTES + lane * (4 * BITS), cc, kVPL);
+    if constexpr (KB != 8) {
+      store_unit_scales_k<B>(shard + S.scale_off, (int64_t)q * USCALES, stored, lane, KB);
+      return;
+    }
     uint8_t* sp = shard + S.scale_off + (size_t)q * USCALES + (lane / LPB) * NSB;
     if constexpr (NSB == 4) {
       *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
@@ -580,12 +638,12 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
     for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
     for (int r = 0; r < nr; r += 2) {
       RL a0, a1;
-      load_rank<B, BITS, kVPL, true>(a0, S.bufs[r] + slot + (size_t)me * S.shard_stride,
-                                     S.scale_off, S.elem_off, (int64_t)q * kUnit, lane, kVPL, 8);
+      load_rank<B, BITS, kVPL, 8>(a0, S.bufs[r] + slot + (size_t)me * S.shard_stride,
+                                     S.scale_off, S.elem_off, (int64_t)q * kUnit, lane, kVPL, KB);
       if (r + 1 < nr)
-        load_rank<B, BITS, kVPL, true>(a1, S.bufs[r + 1] + slot + (size_t)me * S.shard_stride,
+        load_rank<B, BITS, kVPL, 8>(a1, S.bufs[r + 1] + slot + (size_t)me * S.shard_stride,
                                        S.scale_off, S.elem_off, (int64_t)q * kUnit, lane, kVPL,
-                                       8);
+                                       KB);
       decode_rank<B, DEC, BITS, kVPL>(a0, f, acc, false, s_lut);
       if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(a1, f, acc, false, s_lut);
     }
@@ -608,8 +666,8 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
     if (q >= cu) break;
     for (int j = 0; j < nr; ++j) {
       RL a;
-      load_rank<B, BITS, kVPL, true>(a, S.bufs[j] + slot + (size_t)nr * S.shard_stride,
-                                     S.scale_off, S.elem_off, (int64_t)q * kUnit, lane, kVPL, 8);
+      load_rank<B, BITS, kVPL, 8>(a, S.bufs[j] + slot + (size_t)nr * S.shard_stride,
+                                     S.scale_off, S.elem_off, (int64_t)q * kUnit, lane, kVPL, KB);
       float acc[kVPL];
 #pragma unroll
       for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;
@@ -624,42 +682,74 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
 }
 
 template <typename OutT, int B, int ENC, int BITS>
-void go_symm2(const S2Args& a, cudaStream_t st) {
+bool go_symm2(const S2Args& a, cudaStream_t st) {
   const int64_t g = symm_ctas(a.c);
-  launch_pdl(k_symm2_flow<OutT, B, ENC, BITS>, dim3((unsigned)g), dim3(kThreads), 0, st, a);
+  if (a.f.kbits == 8) {
+    launch_pdl(k_symm2_flow<OutT, B, ENC, BITS, 8>, dim3((unsigned)g), dim3(kThreads), 0, st, a);
+    return true;
+  }
+  if constexpr (lean_k_ok(ENC)) {  // E5M0 scales (the paper's selected schemes)
+    if (a.f.kbits == 5) {
+      launch_pdl(k_symm2_flow<OutT, B, ENC, BITS, 5>, dim3((unsigned)g), dim3(kThreads), 0, st,
+                 a);
+      return true;
+    }
+  }
+  return false;
 }
 
 template <typename OutT, int B>
 bool symm2_by_enc(const S2Args& a, int enc, int bits, cudaStream_t st) {
   switch (enc) {
-    case ENC_E2M1: go_symm2<OutT, B, ENC_E2M1, 4>(a, st); return true;
-    case ENC_E2M3: go_symm2<OutT, B, ENC_E2M3, 6>(a, st); return true;
-    case ENC_E3M2: go_symm2<OutT, B, ENC_E3M2, 6>(a, st); return true;
+    case ENC_E2M1: return go_symm2<OutT, B, ENC_E2M1, 4>(a, st);
+    case ENC_E2M3: return go_symm2<OutT, B, ENC_E2M3, 6>(a, st);
+    case ENC_E3M2: return go_symm2<OutT, B, ENC_E3M2, 6>(a, st);
     case ENC_INT:
-      if (bits == 8) { go_symm2<OutT, B, ENC_INT, 8>(a, st); return true; }
+      if (bits == 8) return go_symm2<OutT, B, ENC_INT, 8>(a, st);
       return false;
   }
-  if (enc == ENC_E2M2) { go_symm2<OutT, B, ENC_E2M2, 5>(a, st); return true; }
-  if (bits == 5) { go_symm2<OutT, B, ENC_GEN, 5>(a, st); return true; }
+  if (enc == ENC_E2M2) return go_symm2<OutT, B, ENC_E2M2, 5>(a, st);
+  if (bits == 5) return go_symm2<OutT, B, ENC_GEN, 5>(a, st);
   return false;
 }
 
 template <typename OutT, int B, int ENC, int BITS>
-void go_symm(const SArgs& a, cudaStream_t st) {
-  launch_pdl(k_symm_flow<OutT, B, ENC, BITS>, dim3((unsigned)symm_ctas(a.n)), dim3(kThreads), 0, st,
-             a);
+bool go_symm(const SArgs& a, cudaStream_t st) {
+  const dim3 grid((unsigned)symm_ctas(a.n));
+  if (a.f.kbits == 8) {
+    launch_pdl(k_symm_flow<OutT, B, ENC, BITS, 8>, grid, dim3(kThreads), 0, st, a);
+    return true;
+  }
+  if constexpr (lean_k_ok(ENC)) {  // E5M0 scales (the paper's selected schemes)
+    if (a.f.kbits == 5) {
+      launch_pdl(k_symm_flow<OutT, B, ENC, BITS, 5>, grid, dim3(kThreads), 0, st, a);
+      return true;
+    }
+  }
+  return false;
 }
 
 template <typename InT, typename OutT, int B, int ENC, int BITS>
 void go(const FArgs& a, cudaStream_t st) {
-  if (a.n % kUnit == 0 && a.f.kbits == 8) {
-    // dataflow kernel: one warp per unit, no grid barrier
+  if (a.n % kUnit == 0) {
+    // dataflow kernel: one warp per unit, no grid barrier.  E8M0 scale
+    // bytes, or (the paper's formats) packed k-bit codes stored by the
+    // warp's group leaders and read back after the __syncwarp that orders
+    // the warp's shard writes
     constexpr int UPW = flow_units_per_warp(B, ENC);
     const int64_t units = a.n / kUnit;
-    launch_pdl(k_fused_flow<OutT, B, ENC, BITS>,
-               dim3((unsigned)((units + kWarps * UPW - 1) / (kWarps * UPW))), dim3(kThreads), 0,
-               st, a);
-    return;
+    const dim3 grid((unsigned)((units + kWarps * UPW - 1) / (kWarps * UPW)));
+    if (a.f.kbits == 8) {
+      launch_pdl(k_fused_flow<OutT, B, ENC, BITS, kThreads, 8>, grid, dim3(kThreads), 0, st, a);
+      return;
+    }
+    if constexpr (lean_k_ok(ENC)) {  // E5M0 scales (the paper's selected schemes)
+      if (a.f.kbits == 5) {  // one unit per warp
+        launch_pdl(k_fused_flow<OutT, B, ENC, BITS, kThreads, 5>,
+                   dim3((unsigned)((units + kWarps - 1) / kWarps)), dim3(kThreads), 0, st, a);
+        return;
+      }
+    }
   }
   auto k = k_fused_oneshot<InT, OutT, B, ENC, BITS>;
   static thread_local int sms = 0;
@@ -704,15 +794,15 @@ void by_enc(const FArgs& a, int enc, int bits, cudaStream_t st) {
 template <typename OutT, int B>
 bool symm_by_enc(const SArgs& a, int enc, int bits, cudaStream_t st) {
   switch (enc) {
-    case ENC_E2M1: go_symm<OutT, B, ENC_E2M1, 4>(a, st); return true;
-    case ENC_E2M3: go_symm<OutT, B, ENC_E2M3, 6>(a, st); return true;
-    case ENC_E3M2: go_symm<OutT, B, ENC_E3M2, 6>(a, st); return true;
+    case ENC_E2M1: return go_symm<OutT, B, ENC_E2M1, 4>(a, st);
+    case ENC_E2M3: return go_symm<OutT, B, ENC_E2M3, 6>(a, st);
+    case ENC_E3M2: return go_symm<OutT, B, ENC_E3M2, 6>(a, st);
     case ENC_INT:
-      if (bits == 8) { go_symm<OutT, B, ENC_INT, 8>(a, st); return true; }
+      if (bits == 8) return go_symm<OutT, B, ENC_INT, 8>(a, st);
       return false;
   }
-  if (enc == ENC_E2M2) { go_symm<OutT, B, ENC_E2M2, 5>(a, st); return true; }
-  if (bits == 5) { go_symm<OutT, B, ENC_GEN, 5>(a, st); return true; }
+  if (enc == ENC_E2M2) return go_symm<OutT, B, ENC_E2M2, 5>(a, st);
+  if (bits == 5) return go_symm<OutT, B, ENC_GEN, 5>(a, st);
   return false;
 }
 

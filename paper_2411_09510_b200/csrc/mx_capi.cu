@@ -692,8 +692,8 @@ int mx_allreduce_fused(const void* const* partials, int32_t dtype, int32_t nrank
     return fail(MX_ERR_INVALID_ARGUMENT, "shard_stride must be >= shard bytes and 32-aligned");
   Fmt f = make_fmt(s);
   if (dtype != MX_BF16 || (out_dtype != MX_BF16 && out_dtype != MX_F32) || !aligned(shards, 32) ||
-      !aligned(out, 32) || !fast_block(s->block_size) || f.kbits != 8)
-    return fail(MX_ERR_UNSUPPORTED, "fused path: bf16 in, bf16/f32 out, B in {8,16,32,64}, E8M0");
+      !aligned(out, 32) || !fast_block(s->block_size))
+    return fail(MX_ERR_UNSUPPORTED, "fused path: bf16 in, bf16/f32 out, B in {8,16,32,64}");
   FArgs a;
   a.partials = partials; a.nranks = nranks; a.n = n;
   a.shards = shards; a.shard_stride = shard_stride; a.scale_off = so; a.elem_off = eo;
@@ -805,10 +805,10 @@ int mx_allreduce_symm(const void* x, int32_t dtype, int64_t n, const mx_scheme_t
   mx_shard_layout(n, s, &so, &eo, &sbytes);
   Fmt f = make_fmt(s);
   if (dtype != MX_BF16 || (out_dtype != MX_BF16 && out_dtype != MX_F32) || n % 1024 != 0 ||
-      f.kbits != 8 || slot_stride < sbytes || slot_stride % 32 != 0 || !aligned(x, 32) ||
+      slot_stride < sbytes || slot_stride % 32 != 0 || !aligned(x, 32) ||
       !aligned(out, 32) || !aligned(residual, 32))
     return fail(MX_ERR_UNSUPPORTED,
-                "symmetric path: bf16 in, bf16/f32 out, n %% 1024 == 0, E8M0, 32-B aligned");
+                "symmetric path: bf16 in, bf16/f32 out, n %% 1024 == 0, 32-B aligned");
   if (nranks > kThreads) return fail(MX_ERR_UNSUPPORTED, "at most %d ranks", kThreads);
   SArgs a;
   a.x = x; a.n = n;
@@ -856,9 +856,9 @@ int mx_allreduce_symm_twoshot(const void* x, int32_t dtype, int64_t n, const mx_
   if (!x || !peer_bufs || !peer_flags || !out || !status || !epochs)
     return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
   Fmt f = make_fmt(s);
-  if (dtype != MX_BF16 || (out_dtype != MX_BF16 && out_dtype != MX_F32) || f.kbits != 8 ||
+  if (dtype != MX_BF16 || (out_dtype != MX_BF16 && out_dtype != MX_F32) ||
       !aligned(x, 32) || !aligned(out, 32) || !aligned(residual, 32))
-    return fail(MX_ERR_UNSUPPORTED, "two-shot symmetric path: bf16 in, bf16/f32 out, E8M0");
+    return fail(MX_ERR_UNSUPPORTED, "two-shot symmetric path: bf16 in, bf16/f32 out");
   if (nranks > kThreads) return fail(MX_ERR_UNSUPPORTED, "at most %d ranks", kThreads);
   const int64_t c = n / nranks;
   int64_t so, eo, sb;

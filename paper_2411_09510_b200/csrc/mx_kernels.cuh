@@ -38,7 +38,8 @@ enum Enc { ENC_GEN = 0, ENC_E2M1 = 1, ENC_E2M3 = 2, ENC_E3M2 = 3, ENC_INT = 4, E
 // Decoder of an encoding: hardware f16 conversions for E2M1 / E2M3 / E3M2,
 // integer->f16 for INT8; everything else decodes through the smem LUT.
 __host__ __device__ constexpr int dec_of(int enc, int bits) {
-  return (enc == ENC_E2M1 || enc == ENC_E2M3 || enc == ENC_E3M2 || (enc == ENC_INT && bits == 8))
+  return (enc == ENC_E2M1 || enc == ENC_E2M3 || enc == ENC_E3M2 || enc == ENC_E2M2 ||
+          (enc == ENC_INT && bits == 8))
              ? enc
              : ENC_GEN;
 }
@@ -264,18 +265,20 @@ __device__ __forceinline__ uint64_t encode8(const float* x, const Fmt& f) {
       w |= (uint64_t)((p >> 8) & 0x3fu) << (12 * i + 6);
     }
   } else if constexpr (ENC == ENC_E2M2) {
-    // FP5 E2M2 (no hardware conversion): encode_gen's closed form with the
-    // format folded in -- lowest normal exponent 0, 2 mantissa bits, grid
-    // max 7; a mantissa-bearing format needs no explicit tie fix
+    // FP5 E2M2 through the hardware FP6 E3M2 conversion: the E2M2 grid
+    // {m/4 (e=0), (1+m/4)*2^(e-1)} scaled by 1/4 is exactly E3M2's grid for
+    // e3 = 0..3 (bias 3), so RNE+satfinite of x/4 (exact) after the
+    // reference's clamp to the grid max 7 (mx/codec.py:130) gives E3M2 code
+    // s|e3|m with e3 <= 3, and the E2M2 code is s|e3[1:0]|m -- ties to the
+    // even mantissa = the even grid index, as the reference rounds
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t sign = __float_as_uint(x[i]) >> 31;
-      const float a = fminf(fabsf(x[i]), 7.0f);
-      const int q = max((int)(__float_as_uint(a) >> 23) - 127, 0);
-      const float C = __uint_as_float(((uint32_t)(q - 2 + 150) << 23) | 0x400000u);
-      const float sum = __fadd_rn(a, C);
-      const uint32_t idx = (__float_as_uint(sum) - __float_as_uint(C)) + ((uint32_t)q << 2);
-      w |= (uint64_t)((sign << 4) | idx) << (i * 5);
+    for (int i = 0; i < 4; ++i) {
+      const float lo = copysignf(fminf(fabsf(x[2 * i]), 7.0f), x[2 * i]) * 0.25f;
+      const float hi = copysignf(fminf(fabsf(x[2 * i + 1]), 7.0f), x[2 * i + 1]) * 0.25f;
+      const uint32_t p = cvt_e3m2x2(lo, hi);  // byte 0: lo, byte 1: hi
+      const uint32_t c0 = ((p & 0x20u) >> 1) | (p & 0xFu);
+      const uint32_t c1 = ((p >> 9) & 0x10u) | ((p >> 8) & 0xFu);
+      w |= (uint64_t)(c0 | (c1 << 5)) << (10 * i);
     }
   } else if constexpr (ENC == ENC_INT) {
     // sign-magnitude INTb: RNE to an integer by the 1.5*2^23 magic add, the
@@ -621,8 +624,40 @@ __device__ __forceinline__ void quant_unit(const QArgs& A, const Fmt& f, const U
   store_unit_scales<B>(A.scale_base + cofs, p.uoff / B, stored, p.uvalid, lane, f.kbits, stage);
 }
 
+// k < 8-bit scale codes (E5M0 ...) of a FULL unit straight from registers:
+// the 8 blocks of one packed group (k bytes, LSB-first as mx/bitpack.py)
+// belong to G = 8*LPB/NSB consecutive lanes; an xor butterfly ORs their
+// shifted codes into one 64-bit word and the group's first lane stores its
+// k bytes -- no shared-memory staging, no extra __syncwarp.
+__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
+  uint32_t lo = __shfl_xor_sync(0xffffffffu, (uint32_t)v, m);
+  uint32_t hi = __shfl_xor_sync(0xffffffffu, (uint32_t)(v >> 32), m);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+template <int B>
+__device__ __forceinline__ void store_unit_scales_k(uint8_t* __restrict__ sc, int64_t blk0,
+                                                    const int* stored, int lane, int k) {
+  constexpr int NSB = Geo<B>::NSB;
+  constexpr int LPB = Geo<B>::LPB;
+  constexpr int G = 8 * LPB / NSB;  // lanes per group of 8 blocks
+  uint64_t v = 0;
+  if (lane % LPB == 0) {
+    const int b0 = ((lane / LPB) * NSB) % 8;  // first owned block inside its group
+#pragma unroll
+    for (int sb = 0; sb < NSB; ++sb) v |= (uint64_t)stored[sb] << ((b0 + sb) * k);
+  }
+#pragma unroll
+  for (int m = 1; m < G; m <<= 1) v |= shfl_xor_u64(v, m);
+  if (lane % G == 0) {
+    uint8_t* p = sc + (blk0 / 8 + lane / G) * k;
+    for (int i = 0; i < k; ++i) p[i] = (uint8_t)(v >> (8 * i));
+  }
+}
+
 // Full unit u of a single-chunk tensor: straight-line, no bounds logic.
-template <typename InT, int B, int ENC, int BITS>
+// KB: scale-code width, compile-time: 8 (E8M0 bytes) or 5 (E5M0, packed).
+template <typename InT, int B, int ENC, int BITS, int KB = 8>
 __device__ __forceinline__ void quant_full_unit(const QArgs& A, const Fmt& f, uint32_t u,
                                                 const Raw<InT>& raw, int lane) {
   constexpr int NSB = Geo<B>::NSB;
@@ -635,6 +670,10 @@ __device__ __forceinline__ void quant_full_unit(const QArgs& A, const Fmt& f, ui
                               A.nonfinite);
   store_lane_codes<BITS>(A.elem_base + (size_t)u * (kUnit / 8 * BITS) + lane * (4 * BITS), c,
                          kVPL);
+  if constexpr (KB != 8) {
+    store_unit_scales_k<B>(A.scale_base, (int64_t)u * (kUnit / B), stored, lane, KB);
+    return;
+  }
   uint8_t* p = A.scale_base + (size_t)u * (kUnit / B) + (lane / LPB) * NSB;
   if constexpr (NSB == 4) {
     *reinterpret_cast<uint32_t*>(p) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
@@ -727,7 +766,7 @@ __global__ void __launch_bounds__(kThreads) k_quant(const QArgs A) {
 // stay resident: the loads of 48 warps per SM are in flight at once and the
 // block scheduler balances the tail.  8B shape: 5.07 -> 4.74 us; 70B shape:
 // 15.23 -> 13.93 us (0.93 of the HBM copy peak).
-template <typename InT, int B_, int ENC, int BITS, int MINB>
+template <typename InT, int B_, int ENC, int BITS, int MINB, int KB>
 __global__ void __launch_bounds__(kThreads, MINB) k_quant_lean(const QArgs A) {
   constexpr int B = B_;
   pdl_prologue();
@@ -745,13 +784,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_quant_lean(const QArgs A) {
     C.elem_base = A.elem_base + (size_t)chunk * A.chunk_stride;
     C.scale_base = A.scale_base + (size_t)chunk * A.chunk_stride;
     C.flat_off = A.flat_off + (int64_t)chunk * A.cv;
-    quant_full_unit<InT, B, ENC, BITS>(C, f, q, r, lane);
+    quant_full_unit<InT, B, ENC, BITS, KB>(C, f, q, r, lane);
     return;
   }
   if ((int64_t)(u + 1) * kUnit <= A.n) {
     Raw<InT> r;
     load_raw<InT>(x + (size_t)u * kUnit + lane * kVPL, r);
-    quant_full_unit<InT, B, ENC, BITS>(A, f, u, r, lane);
+    quant_full_unit<InT, B, ENC, BITS, KB>(A, f, u, r, lane);
     return;
   }
   // the partial last unit of a single chunk
@@ -771,9 +810,16 @@ constexpr int lean_minb() {
   return (std::is_same<InT, __nv_bfloat16>::value && ENC != ENC_GEN) ? 6 : 4;
 }
 
+// formats with a lean E5M0-scale instantiation (K1 / K2 / K4 / K5, KB = 5):
+// the paper's selected schemes -- FP4 E2M1 / FP5 E2M2 elements with E5M0
+// scales (mx/fixtures/table2_selected_schemes.csv); other
+// formats and the E4M0/E6M0/E7M0 ablation scales take the general kernels
+__host__ __device__ constexpr bool lean_k_ok(int enc) {
+  return enc == ENC_E2M1 || enc == ENC_E2M2;
+}
+
 inline bool quant_lean_ok(const QArgs& a) {
-  return a.f.kbits == 8 &&
-         (a.total_units == a.units_per_chunk || (a.cv % kUnit == 0 && a.n % a.cv == 0));
+  return a.total_units == a.units_per_chunk || (a.cv % kUnit == 0 && a.n % a.cv == 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -879,6 +925,21 @@ __device__ __forceinline__ void load_rank(RankLoad<B, BITS, VPL>& r,
     } else {
       r.st[0] = ldro<CG>(sc + blk0);
     }
+  } else if (valid == VPL && kbits < 8) {
+    // packed k-bit codes (E5M0 ...): the lane's NSB consecutive codes are
+    // NSB*k bits at bit blk0*k -- gather exactly the bytes holding them
+    // (<= 5), then shift them out (k is a compile-time constant in the lean
+    // kernels, so the loop and the shifts fold)
+    const int64_t bit = blk0 * kbits;
+    const uint8_t* p = sc + (bit >> 3);
+    const int sh = (int)(bit & 7);
+    uint64_t w = 0;
+#pragma unroll
+    for (int i = 0; i < (7 + NSB * 8 + 7) / 8; ++i)
+      if (i * 8 < sh + NSB * kbits) w |= (uint64_t)ld_byte<CG>(p + i) << (8 * i);
+    w >>= sh;
+#pragma unroll
+    for (int sb = 0; sb < NSB; ++sb) r.st[sb] = (int)((w >> (sb * kbits)) & ((1u << kbits) - 1u));
   } else if (valid > 0) {
 #pragma unroll
     for (int sb = 0; sb < NSB; ++sb)
@@ -955,6 +1016,22 @@ __device__ __forceinline__ void int8_group_fma(uint64_t w, uint16_t F16, float* 
 }
 
 // 2^s as f16 bits, s in [-24, 15]
+// 8 FP5 E2M2 codes (40 bits) -> acc += g * 2^s: each code is re-laid as
+// the FP6 E3M2 code s|0e|m (value g/4, see encode8) and converted in pairs
+// by cvt.rn.f16x2.e3m2x2; F16 carries 2^(s+2)
+__device__ __forceinline__ void fp5_group_fma(uint64_t w, uint16_t F16, float* a) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t c0 = (uint32_t)(w >> (10 * i)) & 31u;
+    const uint32_t c1 = (uint32_t)(w >> (10 * i + 5)) & 31u;
+    const uint32_t b = (((c0 & 0x10u) << 1) | (c0 & 0xFu)) |
+                       ((((c1 & 0x10u) << 1) | (c1 & 0xFu)) << 8);
+    uint32_t h2;
+    asm("cvt.rn.f16x2.e3m2x2 %0, %1;" : "=r"(h2) : "h"((uint16_t)b));
+    fma2_f16(h2, F16, a[2 * i], a[2 * i + 1]);
+  }
+}
+
 __device__ __forceinline__ uint16_t pow2_f16(int s) {
   return (uint16_t)(s >= -14 ? (uint32_t)(s + 15) << 10 : 1u << (s + 24));
 }
@@ -968,17 +1045,21 @@ __device__ __forceinline__ void decode_rank(const RankLoad<B, BITS, VPL>& r, con
   for (int sb = 0; sb < NSB; ++sb) {
     const int stored = r.st[sb];
     const int s = stored - f.sbias;
-    if constexpr (DEC == ENC_E2M1 || DEC == ENC_E2M3 || DEC == ENC_E3M2 || DEC == ENC_INT) {
+    if constexpr (DEC == ENC_E2M1 || DEC == ENC_E2M3 || DEC == ENC_E3M2 || DEC == ENC_INT ||
+                  DEC == ENC_E2M2) {
       // f16 fast path: 2^s representable in f16 (|s| covers every block of
-      // real activations); g*2^s is then always an exact f32
-      if (!plain && stored != 0 && s >= -24 && s <= 15) {
-        const uint16_t F16 = pow2_f16(s);
+      // real activations); g*2^s is then always an exact f32.  E2M2 decodes
+      // g/4, so its scale is 2^(s+2)
+      constexpr int SH = DEC == ENC_E2M2 ? 2 : 0;
+      if (!plain && stored != 0 && s + SH >= -24 && s + SH <= 15) {
+        const uint16_t F16 = pow2_f16(s + SH);
 #pragma unroll
         for (int g = 0; g < GPB; ++g) {
           const uint64_t w = get_group<BITS, VPL>(r.c, sb * GPB + g);
           float* a = acc + 8 * (sb * GPB + g);
           if constexpr (DEC == ENC_E2M1) e2m1_word_fma((uint32_t)w, F16, a);
           else if constexpr (DEC == ENC_INT) int8_group_fma(w, F16, a);
+          else if constexpr (DEC == ENC_E2M2) fp5_group_fma(w, F16, a);
           else fp6_group_fma<DEC>(w, F16, a);
         }
         continue;
@@ -1165,13 +1246,14 @@ __global__ void __launch_bounds__(kThreads) k_dqsum(const DArgs A) {
 // 8 ranks 12.3 -> 11.6 us)
 constexpr int kLeanThreads2 = 128;
 constexpr int kLeanWarps2 = kLeanThreads2 / 32;
-// the 8-CTA (64-register) bound is spill-free for the FP4 decode into
-// 16-bit outputs; other decoders and f32 outputs choose their own registers
-template <typename OutT, int DEC>
+// the 8-CTA (64-register) bound is spill-free for the FP4 decode of E8M0
+// shards into 16-bit outputs; other decoders, packed k-bit scales and f32
+// outputs choose their own registers
+template <typename OutT, int DEC, int KB>
 constexpr int dq_minb() { return (DEC == ENC_E2M1 && sizeof(OutT) == 2) ? 8 : 1; }
 
-template <typename OutT, int B, int DEC, int BITS>
-__global__ void __launch_bounds__(kLeanThreads2, dq_minb<OutT, DEC>()) k_dqsum_lean(const DArgs A) {
+template <typename OutT, int B, int DEC, int BITS, int KB = 8>
+__global__ void __launch_bounds__(kLeanThreads2, dq_minb<OutT, DEC, KB>()) k_dqsum_lean(const DArgs A) {
   using RL = RankLoad<B, BITS, kVPL>;
   pdl_prologue();
   __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
@@ -1198,10 +1280,10 @@ __global__ void __launch_bounds__(kLeanThreads2, dq_minb<OutT, DEC>()) k_dqsum_l
   const uint8_t* b = A.in + (size_t)chunk * A.chunk_stride;
   for (int r = 0; r < nr; r += 2, b += 2 * A.rank_stride) {
     RL x0, x1;
-    load_rank<B, BITS, kVPL>(x0, b, A.scale_off, A.elem_off, uoff, lane, kVPL, 8);
+    load_rank<B, BITS, kVPL>(x0, b, A.scale_off, A.elem_off, uoff, lane, kVPL, KB);
     if (r + 1 < nr)
       load_rank<B, BITS, kVPL>(x1, b + A.rank_stride, A.scale_off, A.elem_off, uoff, lane, kVPL,
-                               8);
+                               KB);
     decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
     if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
   }
@@ -1371,10 +1453,18 @@ inline unsigned work_grid(K kernel, int64_t total_units, int per_warp) {
 
 template <typename InT, int B, int ENC, int BITS>
 inline void launch_quant(const QArgs& a, cudaStream_t st) {
-  if (quant_lean_ok(a)) {
-    launch_pdl(k_quant_lean<InT, B, ENC, BITS, lean_minb<InT, ENC>()>,
-               dim3((unsigned)((a.total_units + kWarps - 1) / kWarps)), dim3(kThreads), 0, st, a);
+  const dim3 grid((unsigned)((a.total_units + kWarps - 1) / kWarps));
+  if (quant_lean_ok(a) && a.f.kbits == 8) {
+    launch_pdl(k_quant_lean<InT, B, ENC, BITS, lean_minb<InT, ENC>(), 8>, grid, dim3(kThreads),
+               0, st, a);
     return;
+  }
+  if constexpr (lean_k_ok(ENC)) {  // E5M0 scales: the paper's selected schemes
+    if (quant_lean_ok(a) && a.f.kbits == 5) {
+      launch_pdl(k_quant_lean<InT, B, ENC, BITS, lean_minb<InT, ENC>(), 5>, grid,
+                 dim3(kThreads), 0, st, a);
+      return;
+    }
   }
   auto k = k_quant<InT, B, ENC, BITS>;
   launch_pdl(k, dim3(work_grid(k, a.total_units, 1)), dim3(kThreads), 0, st, a);

@@ -75,7 +75,7 @@ def kernel_times(spec, parts, R):
     return k1 * 1e3, k2 * 1e3, step * 1e3, sets[0].S, sets[0].fused
 
 
-def formats():
+def formats(grid=None):
     T, H = 2048, 4096
     n = T * H
     host = rank_partials((T, H), 2, seed=0)
@@ -83,9 +83,11 @@ def formats():
     base = [torch.from_numpy(h).to("cuda", torch.bfloat16) for h in host]
     R = max(2, -(-3 * L2 // (6 * n)))
     parts = [[(b.roll(i * 7, 0) * (-1) ** i).contiguous() for b in base] for i in range(R)]
-    for el in ["fp4_e2m1", "fp5_e2m2", "fp6_e2m3", "int8"]:
-        for B in (16, 32, 64):
-            spec = f"{el}:{B}:e8m0"
+    if grid is None:  # BASELINE configs[3]
+        grid = [f"{el}:{B}:e8m0" for el in ["fp4_e2m1", "fp5_e2m2", "fp6_e2m3", "int8"]
+                for B in (16, 32, 64)]
+    for spec in grid:
+        if True:
             k1, k2, step, S, fused = kernel_times(spec, parts, R)
             op = SimulatedAllReduce(spec, n, 2, "oneshot", torch.float32)
             red = op(base).double().cpu().numpy().reshape(T, H)
@@ -101,6 +103,13 @@ def formats():
                 "sqnr_db": round(10 * math.log10(float((exact ** 2).sum() / (err ** 2).sum())), 3),
                 "max_abs_err": float(np.abs(err).max()), "mse": float((err ** 2).mean())}),
                 flush=True)
+
+
+def paper():
+    """The paper's own grid (mx/search.py TABLE1: fp3_e1m1 / fp4_e2m1 /
+    fp5_e2m2 x block 8/16/32, E5M0 scales) plus the same formats with E8M0."""
+    formats([f"{el}:{B}:{sc}" for sc in ("e5m0", "e8m0") for el in ("fp3_e1m1", "fp4_e2m1", "fp5_e2m2")
+             for B in (8, 16, 32)])
 
 
 def wire_model(n, S, N):
@@ -255,4 +264,4 @@ def codecs():
 
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "formats"
-    {"formats": formats, "messages": messages, "codecs": codecs, "tp": tp}[what]()
+    {"formats": formats, "messages": messages, "codecs": codecs, "tp": tp, "paper": paper}[what]()

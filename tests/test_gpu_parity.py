@@ -162,7 +162,8 @@ def test_oneshot_and_twoshot_vs_oracle(mx, N, spec):
 
 
 @pytest.mark.parametrize("N", [2, 4, 8])
-@pytest.mark.parametrize("spec", ["fp4_e2m1:32:e8m0", "fp6_e2m3:64:e8m0", "int8:16:e8m0"])
+@pytest.mark.parametrize("spec", ["fp4_e2m1:32:e8m0", "fp6_e2m3:64:e8m0", "int8:16:e8m0",
+                                  "fp4_e2m1:8:e5m0", "fp5_e2m2:32:e5m0"])
 def test_twoshot_whole_unit_chunks_vs_oracle(mx, N, spec):
     """Chunk sizes that are multiples of 1024 take the chunked full-unit K1
     path and the multi-chunk lean K2; both must stay bit-exact."""
@@ -270,7 +271,12 @@ def test_empty_and_tiny(mx):
 
 
 @pytest.mark.parametrize("spec", ["fp4_e2m1:32:e8m0", "fp4_e2m1:8:e8m0", "fp6_e2m3:64:e8m0",
-                                  "int8:16:e8m0", "fp5_e2m2:32:e8m0"])
+                                  "int8:16:e8m0", "fp5_e2m2:32:e8m0",
+                                  # packed k-bit scales: the paper's selected schemes (lean
+                                  # K1/K2/K4 with S8 = false) and a format without a lean
+                                  # k-bit instantiation (general kernels)
+                                  "fp4_e2m1:8:e5m0", "fp5_e2m2:32:e5m0", "fp4_e2m1:64:e5m0",
+                                  "fp4_e2m1:16:e4m0", "fp6_e2m3:32:e5m0"])
 @pytest.mark.parametrize("N", [1, 2, 3, 8])
 def test_fused_oneshot_bit_identical(mx, spec, N):
     """One persistent kernel (quantise, grid barrier, dequant-sum) == the

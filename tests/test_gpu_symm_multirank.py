@@ -83,7 +83,8 @@ def run_ranks(_native, spec, parts, calls, out_dtype=torch.float32, algo="onesho
 
 
 @pytest.mark.parametrize("N", [2, 3, 4, 8])
-@pytest.mark.parametrize("spec", ["fp4_e2m1:32:e8m0", "fp6_e3m2:16:e8m0", "int8:64:e8m0"])
+@pytest.mark.parametrize("spec", ["fp4_e2m1:32:e8m0", "fp6_e3m2:16:e8m0", "int8:64:e8m0",
+                                  "fp4_e2m1:16:e5m0", "fp5_e2m2:32:e5m0"])
 def test_symm_multirank_bit_exact(lib, N, spec):
     n = 32 * 1024  # 4 CTAs per rank: all ranks co-resident
     sets = []
@@ -112,7 +113,8 @@ def test_symm_multirank_bf16_out(lib):
 
 
 @pytest.mark.parametrize("N", [2, 3, 4, 8])
-@pytest.mark.parametrize("spec", ["fp4_e2m1:32:e8m0", "fp6_e2m3:64:e8m0", "int8:16:e8m0"])
+@pytest.mark.parametrize("spec", ["fp4_e2m1:32:e8m0", "fp6_e2m3:64:e8m0", "int8:16:e8m0",
+                                  "fp4_e2m1:32:e5m0", "fp5_e2m2:64:e5m0"])
 def test_symm_twoshot_multirank_bit_exact(lib, N, spec):
     """k_symm2_flow == the NCCL two-shot semantics (oracle allreduce_twoshot)."""
     n = N * 16 * 1024  # chunks of 16 units: 2 CTAs per rank

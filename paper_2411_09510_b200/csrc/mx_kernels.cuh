@@ -505,7 +505,48 @@ __device__ __forceinline__ LaneCodes<BITS> quant_lane(const Raw<T>& raw, const F
 #pragma unroll
         for (int i = 0; i < 8; ++i) x[i] = raw_f32<T>(raw, sb * SBV + 8 * g + i) * inv;  // exact
       }
-      uint64_t w = encode8<ENC, BITS>(x, f);
+      uint64_t w;
+      if constexpr (std::is_same<T, __nv_bfloat16>::value &&
+                    (ENC == ENC_E2M2 || ENC == ENC_E2M3 || ENC == ENC_E3M2)) {
+        if (s <= 124) {
+          // bf16 pairs scaled in one HMUL2.BF16 each (exact power-of-two
+          // scaling, as E2M1 above) straight into the hardware FP6
+          // conversion.  E2M2 takes x/4 = v * 2^-(s+2) clamped to the grid
+          // max 7/4 with one packed min/max (the reference clamps before
+          // rounding, mx/codec.py:130), then E3M2 (see encode8)
+          constexpr int SH = ENC == ENC_E2M2 ? 2 : 0;
+          const uint32_t i16 = (uint32_t)(127 - s - SH) << 7;
+          const uint32_t inv2 = i16 | (i16 << 16);
+          w = 0;
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            uint32_t wv = raw.w[(sb * SBV + 8 * g) / 2 + h];
+            __nv_bfloat162 y = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&wv),
+                                       *reinterpret_cast<const __nv_bfloat162*>(&inv2));
+            if constexpr (ENC == ENC_E2M2) {
+              const __nv_bfloat162 hi2 = __floats2bfloat162_rn(1.75f, 1.75f);
+              const __nv_bfloat162 lo2 = __floats2bfloat162_rn(-1.75f, -1.75f);
+              y = __hmax2(__hmin2(y, hi2), lo2);
+            }
+            const uint32_t yu = *reinterpret_cast<uint32_t*>(&y);
+            const float lo = __uint_as_float(yu << 16), hi = __uint_as_float(yu & 0xffff0000u);
+            if constexpr (ENC == ENC_E2M2) {
+              const uint32_t p = cvt_e3m2x2(lo, hi);
+              const uint32_t c0 = ((p & 0x20u) >> 1) | (p & 0xFu);
+              const uint32_t c1 = ((p >> 9) & 0x10u) | ((p >> 8) & 0xFu);
+              w |= (uint64_t)(c0 | (c1 << 5)) << (10 * h);
+            } else {
+              const uint32_t p = ENC == ENC_E2M3 ? cvt_e2m3x2(lo, hi) : cvt_e3m2x2(lo, hi);
+              w |= (uint64_t)(p & 0x3fu) << (12 * h);
+              w |= (uint64_t)((p >> 8) & 0x3fu) << (12 * h + 6);
+            }
+          }
+        } else {
+          w = encode8<ENC, BITS>(x, f);
+        }
+      } else {
+        w = encode8<ENC, BITS>(x, f);
+      }
       put_group<BITS>(c, sb * (SBV / 8) + g, zero ? 0ull : w);
     }
   }

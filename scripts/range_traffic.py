@@ -29,10 +29,11 @@ def main():
     ap.add_argument("--kernel", choices=["k4", "k1", "k2"], default="k4")
     ap.add_argument("--shape", default="2048,4096")
     ap.add_argument("--sets", type=int, default=16)
+    ap.add_argument("--scheme", default="fp4_e2m1:32:e8m0")
     args = ap.parse_args()
     T, H = (int(v) for v in args.shape.split(","))
     n = T * H
-    sch = parse_scheme("fp4_e2m1:32:e8m0")
+    sch = parse_scheme(args.scheme, extensions=True)
     dev = torch.device("cuda", 0)
     base = [torch.from_numpy(p).to(dev, torch.bfloat16) for p in rank_partials((T, H), 2, seed=0)]
     sets = [([(b.roll(7 * i, 0) * (-1) ** i).contiguous() for b in base],

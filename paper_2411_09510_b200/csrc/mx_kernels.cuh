@@ -1291,7 +1291,10 @@ constexpr int kLeanWarps2 = kLeanThreads2 / 32;
 // shards into 16-bit outputs; other decoders, packed k-bit scales and f32
 // outputs choose their own registers
 template <typename OutT, int DEC, int KB>
-constexpr int dq_minb() { return (DEC == ENC_E2M1 && sizeof(OutT) == 2) ? 8 : 1; }
+constexpr int dq_minb() {
+  return ((DEC == ENC_E2M1 || DEC == ENC_E2M2 || DEC == ENC_E2M3 || DEC == ENC_E3M2) &&
+          sizeof(OutT) == 2) ? 8 : 1;
+}
 
 template <typename OutT, int B, int DEC, int BITS, int KB = 8>
 __global__ void __launch_bounds__(kLeanThreads2, dq_minb<OutT, DEC, KB>()) k_dqsum_lean(const DArgs A) {

@@ -621,6 +621,9 @@ def ttft_block(torch, dist, args, world, dev):
                 ("mx_oneshot_unfused", args.scheme, "oneshot", False),
                 ("mx_twoshot", args.scheme, "twoshot", "auto"), ("mx_symm", args.scheme, "symm", None),
                 ("mx_symm2", args.scheme, "symm2", None)]
+    # the paper's selected schemes (mx/fixtures/table2_selected_schemes.csv):
+    # Llama-3.1-8B fp4_e2m1:8:e5m0, Llama-3.1-70B fp5_e2m2:32:e5m0
+    paper = {"llama-3.1-8b": "fp4_e2m1:8:e5m0", "llama-3.1-70b": "fp5_e2m2:32:e5m0"}
     out = {}
     for name, cfg, seq in models:
         res = {"tp": world, "seq": seq, "batch": 1,
@@ -628,8 +631,9 @@ def ttft_block(torch, dist, args, world, dev):
                "method": "one model, one CUDA graph per variant, replays interleaved "
                          "round-robin; median ms, max over ranks"}
         err, got = None, {}
+        vs = variants + [("mx_paper_scheme", paper[name], "auto", "auto")]
         try:
-            got = tp.measure_ttft_ab(cfg, 1, seq, variants, tp=world, layers=args.ttft_layers,
+            got = tp.measure_ttft_ab(cfg, 1, seq, vs, tp=world, layers=args.ttft_layers,
                                      reps=9, warmup=2)
         except Exception as exc:  # noqa: BLE001
             err = f"{type(exc).__name__}: {exc}"[:200]
@@ -640,7 +644,8 @@ def ttft_block(torch, dist, args, world, dev):
             out[name] = res
             continue
         base = got.get("bf16_nccl")
-        for label, spec, _algo, _fused in variants:
+        res["paper_scheme"] = paper[name]
+        for label, spec, _algo, _fused in vs:
             v = got.get(label)
             if not isinstance(v, float):
                 res[label] = {"error": v or "missing"}
@@ -668,11 +673,14 @@ def ttft_tp1_block(torch, args):
            "note": "world size 1: no all-reduce; the MX rows time the codec work alone"}
     out["method"] = ("one model (same weights and input), one CUDA graph per variant, replays "
                      "interleaved round-robin; median ms")
+    # + the paper's own selection for Llama-3.1-8B (fp4_e2m1:8:e5m0,
+    # mx/fixtures/table2_selected_schemes.csv): E5M0 scales, block 8
     variants = [("bf16", None, "oneshot", None), ("mx", args.scheme, "oneshot", "auto"),
                 ("mx_fused_gemm", args.scheme, "oneshot", True),
-                ("mx_unfused", args.scheme, "oneshot", False)]
+                ("mx_unfused", args.scheme, "oneshot", False),
+                ("mx_paper_scheme_fp4_e2m1_8_e5m0", "fp4_e2m1:8:e5m0", "oneshot", "auto")]
     try:
-        got = tp.measure_ttft_ab(cfg, 1, seq, variants, tp=1, layers=args.ttft_layers, reps=15,
+        got = tp.measure_ttft_ab(cfg, 1, seq, variants, tp=1, layers=args.ttft_layers, reps=25,
                                  warmup=2)
     except Exception as exc:  # noqa: BLE001
         out["error"] = f"{type(exc).__name__}: {exc}"[:200]

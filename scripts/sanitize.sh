@@ -26,4 +26,10 @@ run memcheck_flow memcheck tests/test_gpu_host.py::test_flow_kernel_nonfinite_fl
 run racecheck_flow racecheck tests/test_gpu_host.py::test_flow_kernel_nonfinite_flag tests/test_gpu_parity.py -k "fused or oneshot or twoshot or explicit or nonfinite or unit_counts or empty"
 run synccheck_flow synccheck tests/test_gpu_host.py::test_flow_kernel_nonfinite_flag tests/test_gpu_parity.py -k "fused or oneshot or twoshot or explicit or nonfinite or unit_counts or empty"
 run initcheck_flow initcheck tests/test_gpu_host.py::test_flow_kernel_nonfinite_flag
+# round 2: residual-fused stores, the device MXC1 kernel, E5M0 (packed k-bit
+# scale) lean kernels -- K1/K2/K4 via the fused/two-shot parity cases
+T_R2="tests/test_gpu_residual.py tests/test_gpu_mxc1.py"
+run memcheck_r2 memcheck $T_R2 tests/test_gpu_parity.py -k "e5m0 or e4m0 or residual or serialize"
+run racecheck_r2 racecheck $T_R2 tests/test_gpu_parity.py -k "e5m0 or e4m0"
+run synccheck_r2 synccheck tests/test_gpu_parity.py -k "e5m0 or e4m0"
 cat $out/summary.txt

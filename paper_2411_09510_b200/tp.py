@@ -416,7 +416,7 @@ def make_module_classes():
 
         def __init__(self, d_in_local, d_out, group=None, scheme=None, algo="oneshot",
                      tokens=None, device="cuda", dtype=torch.bfloat16, std=0.02,
-                     fused_gemm=None):
+                     fused_gemm=None, shared_collectives=None):
             super().__init__()
             self.weight = nn.Parameter(torch.randn(d_out, d_in_local, device=device, dtype=dtype)
                                        * std, requires_grad=False)
@@ -432,6 +432,14 @@ def make_module_classes():
             # MXB200_FUSE_RESIDUAL=0 adds after the collective instead
             self.fuse_residual = os.environ.get("MXB200_FUSE_RESIDUAL", "1") != "0"
             self._car = {}
+            # a dict shared by the layers of one model (LlamaTP): one set of
+            # collective buffers per (group, shape, scheme, algo) instead of
+            # one per layer -- layers run one after another on the stream,
+            # and the residual-fused reduce updates h in place (its output
+            # aliasing its residual is allowed).  Without it every layer owns
+            # its buffers (the output of one call stays valid until that
+            # layer's next call).
+            self._shared = shared_collectives
 
         def _collective(self, n, dtype, device):
             import torch.distributed as dist
@@ -440,6 +448,8 @@ def make_module_classes():
 
             key = (n, dtype, str(self.scheme), self.algo)
             car = self._car.get(key)
+            if car is None and self._shared is not None:
+                car = self._shared.get((id(self.group),) + key)
             if car is None:
                 ws = dist.get_world_size(self.group) if dist.is_initialized() else 1
                 rk = dist.get_rank(self.group) if dist.is_initialized() else 0
@@ -458,6 +468,8 @@ def make_module_classes():
                     car = CompressedAllReduce(self.scheme, n, group=self.group,
                                               algo=algo, out_dtype=dtype, device=device,
                                               world_size=ws, rank=rk)
+                if self._shared is not None:
+                    self._shared[(id(self.group),) + key] = car
                 self._car[key] = car
             return car
 
@@ -536,7 +548,7 @@ def make_module_classes():
 
     class LlamaTPBlock(nn.Module):
         def __init__(self, cfg: LlamaConfig, tp: int, group, scheme, algo, device, dtype,
-                     fused_gemm=None):
+                     fused_gemm=None, shared_collectives=None):
             super().__init__()
             if cfg.heads % tp or cfg.kv_heads % tp and tp % cfg.kv_heads:
                 raise ShapeMismatch(f"heads {cfg.heads}/{cfg.kv_heads} vs tp {tp}")
@@ -549,10 +561,12 @@ def make_module_classes():
             self.qkv = ColumnParallelLinear(cfg.hidden, (self.hl + 2 * self.kvl) * self.hd,
                                             device, dtype)
             self.o_proj = RowParallelLinear(self.hl * self.hd, cfg.hidden, group, scheme, algo,
-                                            device=device, dtype=dtype, fused_gemm=fused_gemm)
+                                            device=device, dtype=dtype, fused_gemm=fused_gemm,
+                                            shared_collectives=shared_collectives)
             self.gate_up = ColumnParallelLinear(cfg.hidden, 2 * (cfg.ffn // tp), device, dtype)
             self.down_proj = RowParallelLinear(cfg.ffn // tp, cfg.hidden, group, scheme, algo,
-                                               device=device, dtype=dtype, fused_gemm=fused_gemm)
+                                               device=device, dtype=dtype, fused_gemm=fused_gemm,
+                                               shared_collectives=shared_collectives)
 
         def forward(self, h, cos, sin):
             b, t, _ = h.shape
@@ -581,8 +595,9 @@ def make_module_classes():
             super().__init__()
             self.cfg = cfg
             self.check_health = check_health
+            self._shared_collectives = {}  # one buffer set per shape/scheme for all layers
             self.blocks = nn.ModuleList(LlamaTPBlock(cfg, tp, group, scheme, algo, device, dtype,
-                                                     fused_gemm)
+                                                     fused_gemm, self._shared_collectives)
                                         for _ in range(layers or cfg.layers))
             self.norm = RMSNorm(cfg.hidden, cfg.eps, device, dtype)
 

@@ -102,3 +102,26 @@ def test_row_parallel_linear_residual(cuda, fused_gemm, monkeypatch):
     plain = h + lin(x)
     assert torch.equal(fused, unfused)
     assert torch.equal(fused, plain)
+
+
+@pytest.mark.parametrize("algo", ["oneshot", "twoshot"])
+def test_llama_shared_collectives_equal_per_layer(cuda, algo):
+    """LlamaTP shares one collective buffer set across its layers (the
+    residual-fused reduce updates h in place); the forward must equal the
+    same model with a private buffer set per layer, bit for bit."""
+    from paper_2411_09510_b200 import tp
+
+    LlamaTP = tp.make_module_classes()[3]
+    cfg = tp.LlamaConfig(512, 1024, 2, 8, 4)
+    torch.manual_seed(1)
+    model = LlamaTP(cfg, 1, None, "fp4_e2m1:32:e8m0", algo, device=cuda)
+    h = torch.randn(1, 256, cfg.hidden, device=cuda).to(torch.bfloat16)
+    with torch.inference_mode():
+        shared = model(h).clone()
+        assert len({id(c) for c in model.collectives()}) == 1
+        for blk in model.blocks:
+            for m in (blk.o_proj, blk.down_proj):
+                m._shared, m._car = None, {}
+        private = model(h).clone()
+        assert len({id(c) for c in model.collectives()}) == 2 * len(model.blocks)
+    assert torch.equal(shared, private)

@@ -18,8 +18,9 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native
-from .codec import (FORMAT_CODE_CHANNEL_INT, FORMAT_CODE_TOPK, _dtype_code, _stream,
-                    _to_device_values, header_nbytes, pack_header, packed_nbytes, unpack_header)
+from .codec import (FORMAT_CODE_CHANNEL_INT, FORMAT_CODE_TOPK, _download, _dtype_code, _stream,
+                    _to_device_values, _upload_array, header_nbytes, pack_header, packed_nbytes,
+                    unpack_header)
 from .errors import CompressionFactorTooHigh, MalformedHeader, NonFiniteInput, TruncatedStream
 
 TOPK_INDEX_BYTES = 4
@@ -139,16 +140,16 @@ def topk_compress(tensor, compression_factor: float | None = None, *,
         raise CompressionFactorTooHigh(f"factor {compression_factor} leaves room for {k} values")
     k = min(k, n)
     idx, val = topk_compress_device(tensor, k)
-    return TopKPacket(shape=arr_shape, indices=idx.cpu().numpy().view(np.uint32).copy(),
-                      values=val.cpu().numpy().copy())
+    return TopKPacket(shape=arr_shape, indices=_download(idx).view(np.uint32).copy(),
+                      values=_download(val).copy())
 
 
 def topk_decompress_device(indices, values, n: int, dtype=None):
     torch = _torch()
     dtype = dtype or torch.float64
     out = torch.empty(n, dtype=dtype, device="cuda")
-    idx = torch.as_tensor(indices).to("cuda")
-    val = torch.as_tensor(values).to("cuda")
+    idx = _upload_array(torch.as_tensor(indices).contiguous())
+    val = _upload_array(torch.as_tensor(values).contiguous())
     if idx.dtype != torch.int32:
         idx = idx.to(torch.int64).to(torch.int32)
     val = val.view(torch.float16) if val.dtype == torch.float16 else val.to(torch.float16)
@@ -165,7 +166,7 @@ def topk_decompress(packet: TopKPacket) -> np.ndarray:
     idx = torch.from_numpy(np.ascontiguousarray(packet.indices, dtype=np.uint32).view(np.int32))
     val = torch.from_numpy(np.ascontiguousarray(packet.values, dtype=np.float16))
     out = topk_decompress_device(idx, val, n, torch.float64)
-    return out.cpu().numpy().reshape(packet.shape)
+    return _download(out).reshape(packet.shape)
 
 
 def serialize_topk(packet: TopKPacket) -> bytes:
@@ -217,8 +218,8 @@ def channelwise_int_compress(tensor, bits: int = 4) -> ChannelIntPacket:
     """Symmetric per-channel INT along the trailing dimension (mx/baselines.py:138-168)."""
     scales, codes, shape = channelwise_int_compress_device(tensor, bits)
     orig = tuple(int(d) for d in np.shape(tensor))
-    return ChannelIntPacket(shape=orig or (1,), bits=bits, scales=scales.cpu().numpy().copy(),
-                            code_stream=codes.cpu().numpy().tobytes())
+    return ChannelIntPacket(shape=orig or (1,), bits=bits, scales=_download(scales).copy(),
+                            code_stream=_download(codes).tobytes())
 
 
 def channelwise_int_decompress_device(scales, codes, shape, bits: int, dtype=None):
@@ -227,9 +228,9 @@ def channelwise_int_decompress_device(scales, codes, shape, bits: int, dtype=Non
     n = int(np.prod(shape, dtype=np.int64))
     C = int(shape[-1])
     out = torch.empty(n, dtype=dtype, device="cuda")
-    s = torch.as_tensor(scales).to("cuda")
+    s = _upload_array(torch.as_tensor(scales).contiguous())
     s = s if s.dtype == torch.float16 else s.to(torch.float16)
-    c = torch.as_tensor(codes).to("cuda")
+    c = _upload_array(torch.as_tensor(codes).contiguous())
     _native.check(_native.load().mx_chanint_decompress(
         _p(s), _p(c), n // C if C else 0, C, bits, _p(out), _dtype_code(out), _stream()),
         "mx_chanint_decompress")
@@ -243,7 +244,7 @@ def channelwise_int_decompress(packet: ChannelIntPacket) -> np.ndarray:
     scales = torch.from_numpy(np.ascontiguousarray(packet.scales, dtype=np.float16))
     out = channelwise_int_decompress_device(scales, codes, packet.shape, packet.bits,
                                             torch.float64)
-    return out.cpu().numpy()
+    return _download(out)
 
 
 def serialize_channel_int(packet: ChannelIntPacket) -> bytes:

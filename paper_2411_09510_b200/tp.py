@@ -136,10 +136,12 @@ class _MxCodec:
         """(float64 reconstruction, payload bytes) without host byte streams."""
         import torch
 
-        from .codec import compress_tensor_device, decompress_tensor_device, serialized_nbytes
+        from .codec import (_download, _upload_array, compress_tensor_device,
+                            decompress_tensor_device, serialized_nbytes)
 
-        dct = compress_tensor_device(torch.from_numpy(np.ascontiguousarray(p)).cuda(), self.scheme)
-        rec = decompress_tensor_device(dct, torch.float64).cpu().numpy()
+        dct = compress_tensor_device(_upload_array(torch.from_numpy(np.ascontiguousarray(p))),
+                                     self.scheme)
+        rec = _download(decompress_tensor_device(dct, torch.float64))
         return rec, serialized_nbytes(self.scheme, p.shape)
 
 
@@ -225,7 +227,7 @@ class _TopKCodec:
         import torch
 
         from . import baselines as bl
-        from .codec import header_nbytes
+        from .codec import _download, header_nbytes
 
         k = bl.topk_budget(p.size, p.ndim, self.factor)
         if self.factor <= 1 or k < 1:
@@ -233,7 +235,7 @@ class _TopKCodec:
 
             raise CompressionFactorTooHigh(f"factor {self.factor} leaves room for {k} values")
         idx, val = bl.topk_compress_device(torch.from_numpy(np.ascontiguousarray(p)), k)
-        rec = bl.topk_decompress_device(idx, val, p.size, torch.float64).cpu().numpy()
+        rec = _download(bl.topk_decompress_device(idx, val, p.size, torch.float64))
         return rec.reshape(p.shape), header_nbytes(p.ndim) + 6 * idx.numel()
 
 
@@ -258,12 +260,13 @@ class _ChannelIntCodec:
         import torch
 
         from . import baselines as bl
-        from .codec import header_nbytes
+        from .codec import _download, header_nbytes
 
         s, c, shape = bl.channelwise_int_compress_device(torch.from_numpy(np.ascontiguousarray(p)),
                                                          self.bits)
         rec = bl.channelwise_int_decompress_device(s, c, shape, self.bits, torch.float64)
-        return rec.cpu().numpy().reshape(p.shape), header_nbytes(p.ndim) + 2 * s.numel() + c.numel()
+        return (_download(rec).reshape(p.shape),
+                header_nbytes(p.ndim) + 2 * s.numel() + c.numel())
 
 
 def resolve_codec(scheme, extensions: bool = False):

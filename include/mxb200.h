@@ -184,7 +184,9 @@ int mx_allreduce_fused(const void* const* partials, int32_t dtype, int32_t nrank
  * mx_quantize of that bf16 tensor.  `partial` (bf16 [M, N], nullable)
  * additionally receives the bf16 partial.  scheme == NULL: plain GEMM,
  * `partial` required.  Requires K % 64 == 0, N % 128 == 0, 16-byte aligned
- * operands, E8M0 scales, B in {16, 32}; else MX_ERR_UNSUPPORTED. */
+ * operands, and E8M0 scales with B in {8, 16, 32} or E5M0 scales (the paper's
+ * selected schemes: fp4_e2m1 B in {8, 16, 32}, fp5_e2m2 B = 32) with
+ * N % 256 == 0; else MX_ERR_UNSUPPORTED. */
 int mx_gemm_quantize(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
                      const mx_scheme_t* scheme, uint8_t* scale_stream, uint8_t* element_stream,
                      void* partial, uint64_t* nonfinite, void* stream);

@@ -127,13 +127,18 @@ class NativeBackend:
         sch = self.scheme
         el = sch.to_c()
         fmt = (el.kind, el.exponent_bits, el.mantissa_bits)  # kind 0 float, 1 int
-        ok_fmt = {(0, 2, 1), (0, 2, 3), (0, 3, 2), (0, 2, 2), (1, 0, 7)}
-        if sch.block_size == 16:
-            ok_fmt = {(0, 2, 1), (1, 0, 7)}
-        elif sch.block_size != 32:
+        B = sch.block_size
+        if el.scale_bits == 8:
+            ok_fmt = {32: {(0, 2, 1), (0, 2, 3), (0, 3, 2), (0, 2, 2), (1, 0, 7)},
+                      16: {(0, 2, 1), (1, 0, 7)}, 8: {(0, 2, 1)}}.get(B, set())
+        elif el.scale_bits == 5:  # E5M0: the paper's selected schemes, N % 256 == 0
+            ok_fmt = {32: {(0, 2, 1), (0, 2, 2)}, 16: {(0, 2, 1)}, 8: {(0, 2, 1)}}.get(B, set())
+            if w.dim() != 2 or w.shape[0] % 256 != 0:
+                return False
+        else:
             return False
         K = x.shape[-1]
-        return (el.scale_bits == 8 and fmt in ok_fmt and x.dtype == torch.bfloat16
+        return (fmt in ok_fmt and x.dtype == torch.bfloat16
                 and w.dtype == torch.bfloat16 and x.is_cuda and w.is_cuda and w.dim() == 2
                 and w.shape[1] == K and K % 64 == 0 and w.shape[0] % 128 == 0
                 and x.is_contiguous() and w.is_contiguous()
@@ -141,13 +146,17 @@ class NativeBackend:
 
     def gemm_preferred(self, x, w) -> bool:
         """Whether the fused GEMM is expected to beat cuBLAS + K1 for this
-        shape (measured, profiles/r02/gemm): it saves K1 (~2.5 B/value of
-        HBM traffic) but schedules whole 256x256 tiles over the SM pairs, so
-        a badly quantised last wave costs more than K1 once the GEMM is long.
-        Fused when the tile waves are >= 90 % full, or K <= 4096 (short
-        GEMMs, where the saved K1 dominates: 8B o_proj at TP=1/2 and every
-        8B projection from TP=4 win, 8B down_proj at TP=1/2 -- K = 14336 /
-        7168 on 128 tiles = 1.73 waves -- lose 4-8 %)."""
+        shape and scheme (measured, profiles/r02/gemm): it saves K1 (~2.5
+        B/value of HBM traffic) but schedules whole 256x256 tiles over the SM
+        pairs, so a badly quantised last wave costs more than K1 once the
+        GEMM is long, and the quantiser in the epilogue costs more per tile
+        for small blocks.  E8M0 with B in {16, 32}: fused when the tile waves
+        are >= 90 % full or K <= 4096 (8B o_proj at TP=1/2 and every 8B
+        projection from TP=4 win, 8B down_proj at TP=1/2 -- K = 14336 / 7168
+        on 128 tiles = 1.73 waves -- loses 4-8 %).  E5M0 (the paper's
+        schemes): only B = 32 with >= 90 %-full waves (fp5_e2m2:32:e5m0 at
+        the 70B TP=8 shapes: 1.05-1.10x); block 8 / 16 epilogues are slower
+        than cuBLAS + K1 at every measured shape (0.78-0.98x)."""
         if not self.gemm_supported(x, w):
             return False
         import torch
@@ -157,7 +166,11 @@ class NativeBackend:
         tiles = -(-M // 256) * -(-N // 256)
         pairs = max(1, torch.cuda.get_device_properties(x.device).multi_processor_count // 2)
         waves = -(-tiles // pairs)
-        return tiles / (waves * pairs) >= 0.9 or K <= 4096
+        full = tiles / (waves * pairs) >= 0.9
+        B = self.scheme.block_size
+        if self.scheme.scale.exponent_bits != 8:
+            return B == 32 and full
+        return B >= 16 and (full or K <= 4096)
 
     def gemm_quantize_chunks(self, x2, w, c, shards, shard_stride, flag, partial=None):
         """k_gemm_mx: partial = x2 . w^T on the tensor cores, its MX shard(s)

@@ -198,9 +198,12 @@ __device__ __forceinline__ void epi_bar() {  // the epilogue warps only
 // One thread's 32 accumulator columns -> bf16(partial) (RNE, the tensor
 // F.linear returns) -> [bf16 partial] + [MX codes + scales at flat index
 // `flat` (a multiple of 32) of the row-major partial].
-template <int MODE, int B, int ENC, int BITS>
+// KB = 8: E8M0 scale bytes stored here; KB = 5 (E5M0, the paper's scales):
+// the chunk's scale codes go back through stored_out and the caller packs
+// a whole group of 8 blocks (5 bytes) once its last chunk is done
+template <int MODE, int B, int ENC, int BITS, int KB = 8>
 __device__ __forceinline__ void epi_chunk(const GArgs& A, const Fmt& f, const uint32_t* v,
-                                          int64_t flat) {
+                                          int64_t flat, int* stored_out = nullptr) {
   Raw<__nv_bfloat16> raw;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
@@ -225,6 +228,11 @@ __device__ __forceinline__ void epi_chunk(const GArgs& A, const Fmt& f, const ui
     const int64_t chunk = flat / A.cv, local = flat - chunk * A.cv;
     const int64_t cofs = chunk * A.chunk_stride;
     store_lane_codes<BITS>(A.elem_out + cofs + local / 8 * BITS, cw, kVPL);
+    if constexpr (KB != 8) {
+#pragma unroll
+      for (int sb = 0; sb < NSB; ++sb) stored_out[sb] = stored[sb];
+      return;
+    }
     uint8_t* sp = A.scale_out + cofs + local / B;
     if constexpr (NSB == 4) {
       *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
@@ -485,7 +493,7 @@ __device__ __forceinline__ void mma2_commit_both(uint64_t* bar) {
       : "memory");
 }
 
-template <int BN, int EPI, int MODE, int B, int ENC, int BITS>
+template <int BN, int EPI, int MODE, int B, int ENC, int BITS, int KB = 8>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm_threads<EPI>(), 1)
     k_gemm_mx2(const __grid_constant__ CUtensorMap map_x,
                const __grid_constant__ CUtensorMap map_w, const GArgs A) {
@@ -611,12 +619,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm_threads<EPI>(),
       const int64_t row = (int64_t)mb * 256 + 128 * rank + 32 * q + lane;
       const bool live = row < M;
       const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN);
+      // KB < 8: this thread's consecutive chunks cover whole groups of 8
+      // blocks (B = 8: 2 chunks, 16: 4, 32: 8 -- EPI = 4 gives 8 chunks per
+      // thread; N % 256 == 0 keeps groups inside one row); the group's k-bit
+      // codes are packed in registers and stored by this thread alone
+      [[maybe_unused]] uint64_t pk = 0;
+      [[maybe_unused]] int nbk = 0;
 #pragma unroll 1
       for (int c = part * CPP; c < (part + 1) * CPP; ++c) {
         uint32_t v[32];
         tmem_ld32(taddr + 32 * c, v);
         tmem_ld_wait();
-        if (live) epi_chunk<MODE, B, ENC, BITS>(A, f, v, row * N + (int64_t)nb * BN + 32 * c);
+        const int64_t flat = row * N + (int64_t)nb * BN + 32 * c;
+        if constexpr (KB == 8) {
+          if (live) epi_chunk<MODE, B, ENC, BITS>(A, f, v, flat);
+        } else {
+          constexpr int NSB = Geo<B>::NSB;
+          if (live) {
+            int st[NSB];
+            epi_chunk<MODE, B, ENC, BITS, KB>(A, f, v, flat, st);
+#pragma unroll
+            for (int sb = 0; sb < NSB; ++sb) pk |= (uint64_t)st[sb] << ((nbk + sb) * KB);
+            nbk += NSB;
+            if (nbk == 8) {
+              const int64_t g0 = flat + 32 - 8 * B;  // the group's first value
+              const int64_t chunk = g0 / A.cv, local = g0 - chunk * A.cv;
+              uint8_t* sp = A.scale_out + chunk * A.chunk_stride + (local / B / 8) * KB;
+#pragma unroll
+              for (int i = 0; i < KB; ++i) sp[i] = (uint8_t)(pk >> (8 * i));
+              pk = 0;
+              nbk = 0;
+            }
+          }
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -708,12 +743,12 @@ cudaError_t go_epi(const GArgs& a, const void* x, const void* w, cudaStream_t st
   return cudaGetLastError();
 }
 
-template <int BN, int EPI, int MODE, int B, int ENC, int BITS>
+template <int BN, int EPI, int MODE, int B, int ENC, int BITS, int KB = 8>
 cudaError_t go_2cta(const GArgs& a, const void* x, const void* w, cudaStream_t st) {
   CUtensorMap mx, mw;
   if (!make_map(&mx, x, a.M, a.K, 128) || !make_map(&mw, w, a.N, a.K, BN / 2))
     return cudaErrorInvalidValue;
-  auto k = k_gemm_mx2<BN, EPI, MODE, B, ENC, BITS>;
+  auto k = k_gemm_mx2<BN, EPI, MODE, B, ENC, BITS, KB>;
   constexpr int smem = kStages2 * (128 * BK * 2 + (BN / 2) * BK * 2) + 1024;
   static bool attr = false;
   if (!attr) {
@@ -738,14 +773,35 @@ cudaError_t go(const GArgs& a, const void* x, const void* w, cudaStream_t st) {
                   : go_epi<BN, 4, MODE, B, ENC, BITS>(a, x, w, st);
 }
 
+// E5M0 scales (the paper's selected schemes): 2-CTA form only, 256-wide
+// tiles; B = 32 takes 4 epilogue warps so one thread owns a whole group
+template <int BN, int B, int ENC, int BITS>
+cudaError_t go_k5(const GArgs& a, const void* x, const void* w, cudaStream_t st) {
+  static const int two = env_int("MXB200_GEMM_2CTA", 1);
+  if constexpr (BN != 256) {
+    return cudaErrorNotSupported;
+  } else {
+    if (!two || a.ws != nullptr) return cudaErrorNotSupported;
+    return go_2cta<BN, B == 32 ? 4 : 8, 1, B, ENC, BITS, 5>(a, x, w, st);
+  }
+}
+
 template <int BN>
 cudaError_t by_fmt(const GArgs& a, const void* x, const void* w, int mode, int block, int enc,
                    int bits, cudaStream_t st) {
   if (mode == 0) return go<BN, 0, 32, ENC_E2M1, 4>(a, x, w, st);
+  if (a.f.kbits == 5) {
+    if (block == 8 && enc == ENC_E2M1 && bits == 4) return go_k5<BN, 8, ENC_E2M1, 4>(a, x, w, st);
+    if (block == 16 && enc == ENC_E2M1 && bits == 4) return go_k5<BN, 16, ENC_E2M1, 4>(a, x, w, st);
+    if (block == 32 && enc == ENC_E2M1 && bits == 4) return go_k5<BN, 32, ENC_E2M1, 4>(a, x, w, st);
+    if (block == 32 && enc == ENC_E2M2 && bits == 5) return go_k5<BN, 32, ENC_E2M2, 5>(a, x, w, st);
+    return cudaErrorNotSupported;
+  }
 #define MXB_GEMM_CASE(BLK, E, BT)                                   \
   if (block == BLK && enc == E && bits == BT) return go<BN, 1, BLK, E, BT>(a, x, w, st);
   MXB_GEMM_CASE(32, ENC_E2M1, 4)
   MXB_GEMM_CASE(16, ENC_E2M1, 4)
+  MXB_GEMM_CASE(8, ENC_E2M1, 4)
   MXB_GEMM_CASE(32, ENC_E2M3, 6)
   MXB_GEMM_CASE(32, ENC_E3M2, 6)
   MXB_GEMM_CASE(32, ENC_E2M2, 5)
@@ -789,7 +845,12 @@ cudaError_t launch_gemm_mx(const void* x, const void* w, int64_t M, int64_t N, i
   int mode = 0, block = 32, enc = ENC_E2M1, bits = 4;
   memset(&a.f, 0, sizeof(a.f));
   if (fmt) {
-    if (fmt->kbits != 8 || (fmt->block != 16 && fmt->block != 32)) return cudaErrorNotSupported;
+    if (fmt->kbits != 8 && fmt->kbits != 5) return cudaErrorNotSupported;
+    if (fmt->block != 8 && fmt->block != 16 && fmt->block != 32) return cudaErrorNotSupported;
+    // E5M0: whole 8-block groups per thread inside one row (256-wide tiles)
+    if (fmt->kbits == 5 &&
+        (N % 256 != 0 || (chunk_values < M * N && chunk_values % (8 * fmt->block) != 0)))
+      return cudaErrorNotSupported;
     if (!scale_out || !elem_out) return cudaErrorInvalidValue;
     a.f = *fmt;
     mode = 1;

@@ -743,7 +743,8 @@ static int gemm_impl(const void* x, const void* w, int64_t M, int64_t N, int64_t
   if (e == cudaErrorNotSupported)
     return fail(MX_ERR_UNSUPPORTED,
                 "fused GEMM: needs K %% 64 == 0, N %% 128 == 0, 16-byte aligned operands, "
-                "E8M0 scales, B in {16, 32}, element format fp4_e2m1/fp6/fp5_e2m2/int8");
+                "E8M0 scales with B in {8, 16, 32} (fp4_e2m1 / fp6 / fp5_e2m2 / int8) or E5M0 "
+                "scales (fp4_e2m1 B in {8, 16, 32}, fp5_e2m2 B = 32, N %% 256 == 0)");
   if (e != cudaSuccess) return fail(MX_ERR_CUDA, "k_gemm_mx: %s", cudaGetErrorString(e));
   return cuda_check("k_gemm_mx");
 }

@@ -47,6 +47,11 @@ def _worker(rank, world, port, specs, n, q):
                 assert all(torch.equal(allv[0], a) for a in allv)
                 if algo == "oneshot":
                     assert car.wire_bytes_per_rank == (world - 1) * car.plan.shard_bytes
+                # the residual-fused form: out = h + all_reduce(x), in place
+                h = torch.from_numpy(inputs.gauss_bf16(n, 900 + rank)).float()
+                want = h + torch.from_numpy(ref)
+                got = car(torch.from_numpy(x64[rank]).float(), out=h, residual=h)
+                assert got.data_ptr() == h.data_ptr() and torch.equal(got, want), (spec, algo)
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))

@@ -1292,7 +1292,8 @@ constexpr int kLeanWarps2 = kLeanThreads2 / 32;
 // outputs choose their own registers
 template <typename OutT, int DEC, int KB>
 constexpr int dq_minb() {
-  return ((DEC == ENC_E2M1 || DEC == ENC_E2M2 || DEC == ENC_E2M3 || DEC == ENC_E3M2) &&
+  return ((DEC == ENC_E2M1 || DEC == ENC_E2M2 || DEC == ENC_E2M3 || DEC == ENC_E3M2 ||
+           DEC == ENC_INT) &&
           sizeof(OutT) == 2) ? 8 : 1;
 }
 

@@ -202,6 +202,16 @@ int main(int argc, char** argv) {
         report("write K1 bytes", grid, p, (double)wbytes, ms / R);
       }
     }
+    // K2-shaped (2 shards -> bf16): 32 B of codes in, 64 B of output per lane
+    {
+      const int64_t units = rbytes / (32 * 64);  // one 64 B output per lane
+      for (int grid : {sms * 4, sms * 8, (int)((units + 7) / 8)}) {
+        float ms = time_graph([&](cudaStream_t s) {
+          for (int i = 0; i < R; ++i) launch(p, k_stream<32, 64, 1>, grid, s, in[i], out[i], units);
+        }, reps);
+        report("K2-shaped 32B->64B", grid, p, units * 32 * 96.0, ms / R);
+      }
+    }
     // K4-shaped (2 ranks): 2 x 2n read, 2 shards + 2n written = one 128 B-in / 64+... lane
     {
       const int64_t units = 2 * rbytes / (32 * 128);

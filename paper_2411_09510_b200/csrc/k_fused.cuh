@@ -114,10 +114,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_fused_oneshot(const FArgs F) {
       int64_t uoff = (int64_t)u * kUnit2;
       int valid = max(0, min(kVPL2, (int)min((int64_t)kUnit2, F.n - uoff) - lane * kVPL2));
       RL c0, c1;
-      load_rank<B, BITS, kVPL2, 8>(c0, F.shards, F.scale_off, F.elem_off, uoff, lane, valid,
+      load_rank<B, BITS, kVPL2, true>(c0, F.shards, F.scale_off, F.elem_off, uoff, lane, valid,
                                       f.kbits);
       if (nr > 1)
-        load_rank<B, BITS, kVPL2, 8>(c1, F.shards + F.shard_stride, F.scale_off, F.elem_off,
+        load_rank<B, BITS, kVPL2, true>(c1, F.shards + F.shard_stride, F.scale_off, F.elem_off,
                                         uoff, lane, valid, f.kbits);
       while (true) {
         const uint32_t un = u + nw;
@@ -128,10 +128,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_fused_oneshot(const FArgs F) {
         if (more) {
           uoffn = (int64_t)un * kUnit2;
           validn = max(0, min(kVPL2, (int)min((int64_t)kUnit2, F.n - uoffn) - lane * kVPL2));
-          load_rank<B, BITS, kVPL2, 8>(n0, F.shards, F.scale_off, F.elem_off, uoffn, lane,
+          load_rank<B, BITS, kVPL2, true>(n0, F.shards, F.scale_off, F.elem_off, uoffn, lane,
                                           validn, f.kbits);
           if (nr > 1)
-            load_rank<B, BITS, kVPL2, 8>(n1, F.shards + F.shard_stride, F.scale_off,
+            load_rank<B, BITS, kVPL2, true>(n1, F.shards + F.shard_stride, F.scale_off,
                                             F.elem_off, uoffn, lane, validn, f.kbits);
         }
         float acc[kVPL2];
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_fused_oneshot(const FArgs F) {
         const uint8_t* b = F.shards + 2 * F.shard_stride;
         for (int rk = 2; rk < nr; ++rk, b += F.shard_stride) {
           RL r;
-          load_rank<B, BITS, kVPL2, 8>(r, b, F.scale_off, F.elem_off, uoff, lane, valid,
+          load_rank<B, BITS, kVPL2, true>(r, b, F.scale_off, F.elem_off, uoff, lane, valid,
                                           f.kbits);
           decode_rank<B, DEC, BITS, kVPL2>(r, f, acc, false, s_lut);
         }
@@ -279,10 +279,10 @@ __device__ __forceinline__ void k_flow_one_unit(const FArgs& F) {
   for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
   for (int r = 0; r < nr; r += 2) {
     RL x0, x1;
-    load_rank<B, BITS, kVPL, 8>(x0, F.shards + (size_t)r * F.shard_stride, F.scale_off,
+    load_rank<B, BITS, kVPL, true>(x0, F.shards + (size_t)r * F.shard_stride, F.scale_off,
                                    F.elem_off, (int64_t)q * kUnit, lane, kVPL, KB);
     if (r + 1 < nr)
-      load_rank<B, BITS, kVPL, 8>(x1, F.shards + (size_t)(r + 1) * F.shard_stride,
+      load_rank<B, BITS, kVPL, true>(x1, F.shards + (size_t)(r + 1) * F.shard_stride,
                                      F.scale_off, F.elem_off, (int64_t)q * kUnit, lane, kVPL,
                                      KB);
     decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
@@ -363,10 +363,10 @@ __device__ __forceinline__ void k_flow_multi_unit(const FArgs& F) {
     for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
     for (int r = 0; r < nr; r += 2) {
       RL x0, x1;
-      load_rank<B, BITS, kVPL, 8>(x0, F.shards + (size_t)r * F.shard_stride, F.scale_off,
+      load_rank<B, BITS, kVPL, true>(x0, F.shards + (size_t)r * F.shard_stride, F.scale_off,
                                      F.elem_off, (int64_t)q * kUnit, lane, kVPL, KB);
       if (r + 1 < nr)
-        load_rank<B, BITS, kVPL, 8>(x1, F.shards + (size_t)(r + 1) * F.shard_stride,
+        load_rank<B, BITS, kVPL, true>(x1, F.shards + (size_t)(r + 1) * F.shard_stride,
                                        F.scale_off, F.elem_off, (int64_t)q * kUnit, lane, kVPL,
                                        KB);
       decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
@@ -510,10 +510,10 @@ __global__ void __launch_bounds__(kThreads) k_symm_flow(const SArgs S) {
     for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
     for (int r = 0; r < nr; r += 2) {
       RL x0, x1;
-      load_rank<B, BITS, kVPL, 8>(x0, S.bufs[r] + slot, S.scale_off, S.elem_off,
+      load_rank<B, BITS, kVPL, true>(x0, S.bufs[r] + slot, S.scale_off, S.elem_off,
                                      (int64_t)q * kUnit, lane, kVPL, KB);
       if (r + 1 < nr)
-        load_rank<B, BITS, kVPL, 8>(x1, S.bufs[r + 1] + slot, S.scale_off, S.elem_off,
+        load_rank<B, BITS, kVPL, true>(x1, S.bufs[r + 1] + slot, S.scale_off, S.elem_off,
                                        (int64_t)q * kUnit, lane, kVPL, KB);
       decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
       if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
@@ -638,10 +638,10 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
     for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
     for (int r = 0; r < nr; r += 2) {
       RL a0, a1;
-      load_rank<B, BITS, kVPL, 8>(a0, S.bufs[r] + slot + (size_t)me * S.shard_stride,
+      load_rank<B, BITS, kVPL, true>(a0, S.bufs[r] + slot + (size_t)me * S.shard_stride,
                                      S.scale_off, S.elem_off, (int64_t)q * kUnit, lane, kVPL, KB);
       if (r + 1 < nr)
-        load_rank<B, BITS, kVPL, 8>(a1, S.bufs[r + 1] + slot + (size_t)me * S.shard_stride,
+        load_rank<B, BITS, kVPL, true>(a1, S.bufs[r + 1] + slot + (size_t)me * S.shard_stride,
                                        S.scale_off, S.elem_off, (int64_t)q * kUnit, lane, kVPL,
                                        KB);
       decode_rank<B, DEC, BITS, kVPL>(a0, f, acc, false, s_lut);
@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(kThreads) k_symm2_flow(const S2Args S) {
     if (q >= cu) break;
     for (int j = 0; j < nr; ++j) {
       RL a;
-      load_rank<B, BITS, kVPL, 8>(a, S.bufs[j] + slot + (size_t)nr * S.shard_stride,
+      load_rank<B, BITS, kVPL, true>(a, S.bufs[j] + slot + (size_t)nr * S.shard_stride,
                                      S.scale_off, S.elem_off, (int64_t)q * kUnit, lane, kVPL, KB);
       float acc[kVPL];
 #pragma unroll

@@ -85,6 +85,51 @@ __global__ void __launch_bounds__(TH, MINB) k_split(const FArgs F) {
   store_lane_out<__nv_bfloat16, kVPL2>(reinterpret_cast<__nv_bfloat16*>(F.out) + uoff +
                                            lane * kVPL2, kVPL2, acc);
 }
+
+// sequential ranks: one rank's raw registers live at a time (fewer
+// registers -> more resident warps); read-back + decode as shipped
+template <int TH, int MINB>
+__global__ void __launch_bounds__(TH, MINB) k_seq(const FArgs F) {
+  using InT = __nv_bfloat16;
+  constexpr int B = 32, ENC = ENC_E2M1, BITS = 4, DEC = ENC_E2M1;
+  constexpr int UBYTES = kUnit / 8 * BITS;
+  constexpr int USCALES = kUnit / B;
+  pdl_prologue();
+  const int lane = threadIdx.x & 31;
+  const uint32_t q = blockIdx.x * (TH / 32) + (threadIdx.x >> 5);
+  if (q >= (uint32_t)(F.n / kUnit)) return;
+  const Fmt f = F.f;
+  const size_t xoff = (size_t)q * kUnit + lane * kVPL;
+  const int nr = F.nranks;
+  for (int r = 0; r < nr; ++r) {
+    Raw<InT> raw;
+    load_raw<InT>(reinterpret_cast<const InT*>(F.partials[r]) + xoff, raw);
+    int stored[1];
+    bool bad;
+    LaneCodes<BITS> c = quant_lane<InT, B, ENC, BITS>(raw, f, stored, bad);
+    if (bad) report_nonfinite_raw<InT>(raw, kVPL, (int64_t)xoff, F.nonfinite);
+    uint8_t* shard = F.shards + (size_t)r * F.shard_stride;
+    store_lane_codes<BITS>(shard + F.elem_off + (size_t)q * UBYTES + lane * (4 * BITS), c, kVPL);
+    shard[F.scale_off + (size_t)q * USCALES + lane] = (uint8_t)stored[0];
+  }
+  __syncwarp();
+  using RL = RankLoad<B, BITS, kVPL>;
+  float acc[kVPL];
+#pragma unroll
+  for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;
+  for (int r = 0; r < nr; r += 2) {
+    RL x0, x1;
+    load_rank<B, BITS, kVPL, true>(x0, F.shards + (size_t)r * F.shard_stride, F.scale_off,
+                                   F.elem_off, (int64_t)q * kUnit, lane, kVPL, 8);
+    if (r + 1 < nr)
+      load_rank<B, BITS, kVPL, true>(x1, F.shards + (size_t)(r + 1) * F.shard_stride,
+                                     F.scale_off, F.elem_off, (int64_t)q * kUnit, lane, kVPL, 8);
+    decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, nullptr);
+    if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, nullptr);
+  }
+  store_lane_out<__nv_bfloat16, kVPL>(reinterpret_cast<__nv_bfloat16*>(F.out) + xoff, kVPL, acc);
+}
+
 template <typename K, typename... A>
 static void pdl(K k, unsigned grid, unsigned block, cudaStream_t s, A... a) {
   cudaLaunchConfig_t cfg = {};
@@ -194,12 +239,16 @@ int main(int argc, char** argv) {
     pdl(k_split<TH, MINB>, (units + TH / 64 - 1) / (TH / 64), TH, s, args[i]); }, bytes, st);  \
   check("split");
   SPLIT(256, 4)
-  SPLIT(256, 5)
-  SPLIT(256, 6)
-  SPLIT(128, 8)
-  SPLIT(128, 10)
-  SPLIT(128, 12)
-  SPLIT(512, 2)
   SPLIT(512, 3)
+#define SEQ(TH, MINB)                                                                         \
+  bench("seq th" #TH " minb" #MINB, R, [&](int i, cudaStream_t s) {                          \
+    pdl(k_seq<TH, MINB>, (units + TH / 32 - 1) / (TH / 32), TH, s, args[i]); }, bytes, st);   \
+  check("seq");
+  SEQ(256, 4)
+  SEQ(256, 5)
+  SEQ(256, 6)
+  SEQ(128, 8)
+  SEQ(128, 10)
+  SEQ(128, 12)
   return 0;
 }

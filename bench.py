@@ -620,7 +620,9 @@ def ttft_block(torch, dist, args, world, dev):
     variants = [("bf16_nccl", None, "oneshot", None), ("mx_oneshot", args.scheme, "oneshot", "auto"),
                 ("mx_oneshot_unfused", args.scheme, "oneshot", False),
                 ("mx_twoshot", args.scheme, "twoshot", "auto"), ("mx_symm", args.scheme, "symm", None),
-                ("mx_symm2", args.scheme, "symm2", None)]
+                ("mx_symm2", args.scheme, "symm2", None),
+                # the GEMM + quantiser + all-gather push in one kernel per rank
+                ("mx_push", args.scheme, "push", None)]
     # the paper's selected schemes (mx/fixtures/table2_selected_schemes.csv):
     # Llama-3.1-8B fp4_e2m1:8:e5m0, Llama-3.1-70B fp5_e2m2:32:e5m0
     paper = {"llama-3.1-8b": "fp4_e2m1:8:e5m0", "llama-3.1-70b": "fp5_e2m2:32:e5m0"}
@@ -655,6 +657,7 @@ def ttft_block(torch, dist, args, world, dev):
                 res[label]["speedup_vs_bf16"] = round(base / v, 4)
         out[name] = res
     tp._SYMM_CACHE.clear()
+    tp._PUSH_CACHE.clear()
     torch.cuda.empty_cache()
     return out
 

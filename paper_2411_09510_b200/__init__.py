@@ -28,7 +28,7 @@ from .netbench import (BenchResult, LinkModel, calibrate_codec_throughput, predi
                        predicted_speedup, run_allgather_bench)
 from .search import (DeviceReductionEvaluator, make_activation_evaluator,
                      make_simulation_evaluator)
-from .collective import (CompressedAllReduce, HostPipeline, LocalThreadGroup,
+from .collective import (CompressedAllReduce, FusedLinearAllReduce, HostPipeline, LocalThreadGroup,
                          SimulatedAllReduce, SymmetricAllReduce, compressed_all_reduce)
 
 __version__ = "0.1.0"

@@ -75,6 +75,11 @@ SIGNATURES = {
                                         c_vp, c_vp, c_vp]),
     "mx_memset_async": (c_i32, [c_vp, c_i32, c_i64, c_vp]),
     "mx_serialize": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
+    "mx_push_layout": (c_i32, [c_i64, _SP, c_i32, c_i64p, c_i64p, c_i64p, c_i64p]),
+    "mx_gemm_allgather_push": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i64, _SP, c_vp, c_vp, c_i32,
+                                       c_i32, c_vp, c_vp, c_vp]),
+    "mx_push_dequant_sum": (c_i32, [c_vp, c_i64, _SP, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp,
+                                    c_vp]),
     "mx_copy_bytes": (c_i32, [c_vp, c_i64, c_vp, c_vp]),
     "mx_nonfinite_reset": (c_i32, [c_vp, c_vp]),
 }
@@ -170,6 +175,16 @@ def symm_layout(n: int, cs: MxScheme, nranks: int) -> tuple[int, int, int, int]:
     check(lib.mx_symm_layout(n, ctypes.byref(cs), nranks, ctypes.byref(a), ctypes.byref(b),
                              ctypes.byref(c), ctypes.byref(d)), "mx_symm_layout")
     return a.value, b.value, c.value, d.value
+
+
+def push_layout(n: int, cs: MxScheme, nranks: int) -> tuple[int, int, int, int]:
+    """(slot_stride, shard_stride, flags_offset, buffer_bytes) of the GEMM +
+    all-gather push (mx_push_layout)."""
+    lib = load()
+    v = [c_i64() for _ in range(4)]
+    check(lib.mx_push_layout(n, ctypes.byref(cs), nranks, *[ctypes.byref(x) for x in v]),
+          "mx_push_layout")
+    return tuple(x.value for x in v)
 
 
 def symm_twoshot_layout(n: int, cs: MxScheme, nranks: int):

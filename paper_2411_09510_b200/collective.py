@@ -507,6 +507,113 @@ class SymmetricAllReduce:
 # ---------------------------------------------------------------------------
 
 
+class FusedLinearAllReduce:
+    """all_reduce(x @ W^T) with the GEMM, the MX quantiser AND the all-gather
+    in ONE kernel per rank, over torch symmetric memory (NVLink / NVSwitch).
+
+    The tcgen05 row-parallel GEMM (k_gemm.cu, 2-CTA form) quantises each
+    accumulator tile as it drains and stores the shard bytes straight into
+    slot (epoch & 1) of every rank's symmetric buffer -- the all-gather of
+    mx/netbench.py:323-328 rides on the epilogue and overlaps the remaining
+    tiles' math; its last CTA releases the epoch into every peer's flag
+    array.  A second launch (k_push_dqsum) waits for the N flags and decodes
+    the N shards from local memory in rank order, with the optional residual
+    add fused into its store.  Bit-identical to ``CompressedAllReduce.linear``
+    (NCCL one-shot) on the same operands.  No NCCL kernel, no gather copy.
+    Requirements: fp4_e2m1 E8M0 with B in {16, 32}; bf16 x [M, K] and
+    W [N, K] contiguous, N % 256 == 0, K % 64 == 0, n = M*N % 1024 == 0;
+    at most 8 ranks.  Slots alternate by epoch parity, which is safe because a
+    rank starts call e only after its call e-1 saw every peer's e-1 flag,
+    i.e. after every peer finished reading slot (e & 1) in call e-2.
+    """
+
+    def __init__(self, scheme, n: int, group=None, out_dtype=None, device=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        if isinstance(scheme, str):
+            scheme = parse_scheme(scheme, extensions=True)
+        self.scheme, self.n = scheme, int(n)
+        self.group = group or dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        if self.world > 8:
+            raise ShapeMismatch("the GEMM + all-gather push supports at most 8 ranks")
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self.out_dtype = out_dtype or torch.bfloat16
+        self.backend = NativeBackend(scheme)
+        self.slot, self.shard_stride, flags_off, total = _native.push_layout(
+            self.n, self.backend.cs, self.world)
+        self.buf = symm_mem.empty(total, dtype=torch.uint8, device=self.device)
+        self.hdl = symm_mem.rendezvous(self.buf, self.group)
+        self.buf[flags_off:].zero_()  # flags start at zero before anyone can signal
+        self.flags_local = self.buf[flags_off:]
+        self.buf_ptrs = torch.tensor([int(p) for p in self.hdl.buffer_ptrs], dtype=torch.int64,
+                                     device=self.device)
+        self.flag_ptrs = torch.tensor([int(p) + flags_off for p in self.hdl.buffer_ptrs],
+                                      dtype=torch.int64, device=self.device)
+        torch.cuda.synchronize()
+        dist.barrier(self.group)
+        # [0] status (as SymmetricAllReduce), [1] epoch, [2] CTA counter
+        self.state = torch.zeros(4, dtype=torch.int32, device=self.device)
+        self.flag = torch.empty(1, dtype=torch.int64, device=self.device)
+        self.backend.reset_flag(self.flag)
+        self.out = torch.empty(self.n, dtype=self.out_dtype, device=self.device)
+
+    def supported(self, x, w) -> bool:
+        import torch
+
+        sch = self.scheme
+        return (sch.element.name == "fp4_e2m1" and sch.scale.exponent_bits == 8
+                and sch.block_size in (16, 32) and x.dtype == torch.bfloat16
+                and w.dtype == torch.bfloat16 and w.dim() == 2 and x.shape[-1] == w.shape[1]
+                and w.shape[0] % 256 == 0 and x.shape[-1] % 64 == 0 and self.n % 1024 == 0
+                and x.is_contiguous() and w.is_contiguous()
+                and x.numel() // x.shape[-1] * w.shape[0] == self.n)
+
+    def linear(self, x, weight, out=None, residual=None):
+        """all_reduce(F.linear(x, weight)) [+ residual], two launches per rank."""
+        import torch
+
+        if not self.supported(x, weight):
+            raise ShapeMismatch("FusedLinearAllReduce: unsupported operands for the push GEMM")
+        if residual is not None and (residual.numel() != self.n or
+                                     residual.dtype != self.out_dtype or
+                                     not residual.is_contiguous()):
+            raise ShapeMismatch(f"residual must be a contiguous {self.out_dtype} tensor of "
+                                f"{self.n} values")
+        K = x.shape[-1]
+        M, N = x.numel() // K, weight.shape[0]
+        o = self.out if out is None else out.reshape(-1)
+        be = self.backend
+        P = ctypes.c_void_p
+        base = self.state.data_ptr()
+        _native.check(be.lib.mx_gemm_allgather_push(
+            P(x.data_ptr()), P(weight.data_ptr()), M, N, K, ctypes.byref(be.cs),
+            P(self.buf_ptrs.data_ptr()), P(self.flag_ptrs.data_ptr()), self.rank, self.world,
+            P(base + 4), P(self.flag.data_ptr()), be._st()), "mx_gemm_allgather_push")
+        _native.check(be.lib.mx_push_dequant_sum(
+            P(self.buf.data_ptr()), self.n, ctypes.byref(be.cs), self.world,
+            P(self.flags_local.data_ptr()), P(base + 4), P(base), P(o.data_ptr()), be._dt(o),
+            P(residual.data_ptr()) if residual is not None else None, be._st()),
+            "mx_push_dequant_sum")
+        return o.view(*x.shape[:-1], N)
+
+    def check_status(self):
+        """Raise if a peer wait timed out (the results of that call are invalid)."""
+        if int(self.state[0].item()) != 0:
+            raise RuntimeError("GEMM + all-gather push: a peer flag wait timed out")
+
+    def check_finite(self):
+        idx = int(self.flag.item())
+        if idx >= 0:
+            self.backend.reset_flag(self.flag)
+            raise NonFiniteInput(f"non-finite value in a row-parallel partial (flat index {idx})",
+                                 block_index=idx // self.scheme.block_size)
+
+
 class LocalThreadGroup:
     """A process-group stand-in for N ranks that are N host threads sharing
     one GPU -- the device form of the reference's in-process mailbox

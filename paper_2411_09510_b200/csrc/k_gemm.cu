@@ -142,7 +142,19 @@ struct GArgs {
   float* ws;              // stream-K partial tiles: gridDim.x slots of BM x BN fp32 (nullable)
   unsigned int* flags;    // gridDim.x u32, zero between launches (the kernel resets them)
   Fmt f;
+  // all-gather push (2-CTA form, PUSH = true): the epilogue writes this
+  // rank's shard into slot (epoch & 1) of EVERY rank's symmetric buffer over
+  // NVLink, tile by tile as the accumulators drain; the last CTA to finish
+  // publishes the epoch to every peer's flag array (release, system scope)
+  uint8_t* const* push_peers;       // device [npush]: peer buffer bases
+  unsigned int* const* push_flags;  // device [npush]: peer flag arrays (u32 x npush)
+  int npush, push_rank;
+  int64_t push_slot_stride;         // bytes per slot (npush shards)
+  int64_t push_off;                 // this rank's shard inside a slot
+  int64_t push_scale_off, push_elem_off;  // shard layout
+  unsigned int* push_state;         // local: [0] epoch, [1] CTA arrival counter
 };
+constexpr int kMaxPush = 8;
 
 // Work distribution.  With a workspace: stream-K -- the T tiles x KB
 // k-blocks are cut into gridDim.x contiguous ranges of (nearly) equal
@@ -201,9 +213,10 @@ __device__ __forceinline__ void epi_bar() {  // the epilogue warps only
 // KB = 8: E8M0 scale bytes stored here; KB = 5 (E5M0, the paper's scales):
 // the chunk's scale codes go back through stored_out and the caller packs
 // a whole group of 8 blocks (5 bytes) once its last chunk is done
-template <int MODE, int B, int ENC, int BITS, int KB = 8>
+template <int MODE, int B, int ENC, int BITS, int KB = 8, bool PUSH = false>
 __device__ __forceinline__ void epi_chunk(const GArgs& A, const Fmt& f, const uint32_t* v,
-                                          int64_t flat, int* stored_out = nullptr) {
+                                          int64_t flat, int* stored_out = nullptr,
+                                          uint8_t* const* pdst = nullptr) {
   Raw<__nv_bfloat16> raw;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
@@ -223,6 +236,25 @@ __device__ __forceinline__ void epi_chunk(const GArgs& A, const Fmt& f, const ui
     bool bad;
     LaneCodes<BITS> cw = quant_lane<__nv_bfloat16, B, ENC, BITS>(raw, f, stored, bad);
     if (bad) report_nonfinite_raw<__nv_bfloat16>(raw, kVPL, flat, A.nonfinite);
+    if constexpr (PUSH) {  // one tensor, E8M0: the same bytes to every rank
+      constexpr int LPB = Geo<B>::LPB;
+      for (int j = 0; j < A.npush; ++j) {
+        uint8_t* base = pdst[j];
+        store_lane_codes<BITS>(base + A.push_elem_off + flat / 8 * BITS, cw, kVPL);
+        uint8_t* sp = base + A.push_scale_off + flat / B;
+        if constexpr (NSB == 4) {
+          *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
+                                             ((uint32_t)stored[2] << 16) |
+                                             ((uint32_t)stored[3] << 24);
+        } else if constexpr (NSB == 2) {
+          *reinterpret_cast<uint16_t*>(sp) = (uint16_t)(stored[0] | (stored[1] << 8));
+        } else {
+          (void)LPB;
+          *sp = (uint8_t)stored[0];
+        }
+      }
+      return;
+    }
     // chunked shards (two-shot): a 32-value group never straddles a chunk
     // (chunk sizes are multiples of 8B >= 128 values)
     const int64_t chunk = flat / A.cv, local = flat - chunk * A.cv;
@@ -493,7 +525,11 @@ __device__ __forceinline__ void mma2_commit_both(uint64_t* bar) {
       : "memory");
 }
 
-template <int BN, int EPI, int MODE, int B, int ENC, int BITS, int KB = 8>
+__device__ __forceinline__ void st_release_sys_u32(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int BN, int EPI, int MODE, int B, int ENC, int BITS, int KB = 8, bool PUSH = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm_threads<EPI>(), 1)
     k_gemm_mx2(const __grid_constant__ CUtensorMap map_x,
                const __grid_constant__ CUtensorMap map_w, const GArgs A) {
@@ -545,6 +581,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm_threads<EPI>(),
 
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
+  // push: this call's epoch (the previous launch's last CTA stored epoch - 1
+  // and completed before griddepcontrol.wait returned) picks the slot
+  __shared__ uint8_t* s_dst[PUSH ? kMaxPush : 1];
+  __shared__ unsigned int s_epoch;
+  if constexpr (PUSH) {
+    if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile unsigned int*>(A.push_state) + 1u;
+    __syncthreads();
+    if ((int)threadIdx.x < A.npush)
+      s_dst[threadIdx.x] = A.push_peers[threadIdx.x] +
+                           (int64_t)(s_epoch & 1u) * A.push_slot_stride + A.push_off;
+    __syncthreads();
+  }
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
@@ -631,7 +679,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm_threads<EPI>(),
         tmem_ld32(taddr + 32 * c, v);
         tmem_ld_wait();
         const int64_t flat = row * N + (int64_t)nb * BN + 32 * c;
-        if constexpr (KB == 8) {
+        if constexpr (PUSH) {
+          if (live) epi_chunk<MODE, B, ENC, BITS, 8, true>(A, f, v, flat, nullptr, s_dst);
+        } else if constexpr (KB == 8) {
           if (live) epi_chunk<MODE, B, ENC, BITS>(A, f, v, flat);
         } else {
           constexpr int NSB = Geo<B>::NSB;
@@ -665,6 +715,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm_threads<EPI>(),
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "n"(TMEM_COLS)
                  : "memory");
+  }
+  if constexpr (PUSH) {
+    // every epilogue store of this CTA is ordered before thread 0 by the
+    // cluster barrier; the system fence + arrival counter make them visible
+    // before the last CTA's release of the epoch to every peer (the
+    // threadfence-reduction pattern at system scope)
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      const unsigned int prev = atomicAdd(A.push_state + 1, 1u);
+      if (prev == gridDim.x - 1) {
+        __threadfence_system();
+        for (int j = 0; j < A.npush; ++j) st_release_sys_u32(A.push_flags[j] + A.push_rank, s_epoch);
+        A.push_state[1] = 0u;
+        *reinterpret_cast<volatile unsigned int*>(A.push_state) = s_epoch;
+      }
+    }
   }
 }
 
@@ -743,12 +809,12 @@ cudaError_t go_epi(const GArgs& a, const void* x, const void* w, cudaStream_t st
   return cudaGetLastError();
 }
 
-template <int BN, int EPI, int MODE, int B, int ENC, int BITS, int KB = 8>
+template <int BN, int EPI, int MODE, int B, int ENC, int BITS, int KB = 8, bool PUSH = false>
 cudaError_t go_2cta(const GArgs& a, const void* x, const void* w, cudaStream_t st) {
   CUtensorMap mx, mw;
   if (!make_map(&mx, x, a.M, a.K, 128) || !make_map(&mw, w, a.N, a.K, BN / 2))
     return cudaErrorInvalidValue;
-  auto k = k_gemm_mx2<BN, EPI, MODE, B, ENC, BITS, KB>;
+  auto k = k_gemm_mx2<BN, EPI, MODE, B, ENC, BITS, KB, PUSH>;
   constexpr int smem = kStages2 * (128 * BK * 2 + (BN / 2) * BK * 2) + 1024;
   static bool attr = false;
   if (!attr) {
@@ -828,6 +894,7 @@ cudaError_t launch_gemm_mx(const void* x, const void* w, int64_t M, int64_t N, i
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15)
     return cudaErrorNotSupported;
   GArgs a;
+  memset(&a, 0, sizeof(a));  // push fields off
   a.M = M; a.N = N; a.K = K;
   a.cv = chunk_values; a.chunk_stride = chunk_stride;
   a.scale_out = scale_out; a.elem_out = elem_out; a.partial_out = partial_out;
@@ -862,6 +929,37 @@ cudaError_t launch_gemm_mx(const void* x, const void* w, int64_t M, int64_t N, i
   }
   if (tile_n(N) == 256) return by_fmt<256>(a, x, w, mode, block, enc, bits, st);
   return by_fmt<128>(a, x, w, mode, block, enc, bits, st);
+}
+
+// The GEMM with the quantiser AND the all-gather in its epilogue (2-CTA
+// form, one tensor, E8M0, fp4_e2m1 B in {16, 32}): returns
+// cudaErrorNotSupported outside it.
+cudaError_t launch_gemm_mx_push(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
+                                const Fmt* fmt, int enc_id, uint8_t* const* peers,
+                                unsigned int* const* peer_flags, int npush, int rank,
+                                int64_t slot_stride, int64_t shard_stride, int64_t scale_off,
+                                int64_t elem_off, unsigned int* state,
+                                unsigned long long* nonfinite, cudaStream_t st) {
+  using namespace gm;
+  static const int two = env_int("MXB200_GEMM_2CTA", 1);
+  if (!two || !fmt || M < 1 || N < 256 || N % 256 != 0 || K < BK || K % BK != 0)
+    return cudaErrorNotSupported;
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15)
+    return cudaErrorNotSupported;
+  if (fmt->kbits != 8 || enc_id != ENC_E2M1 || (fmt->block != 16 && fmt->block != 32) ||
+      npush < 1 || npush > kMaxPush || rank < 0 || rank >= npush)
+    return cudaErrorNotSupported;
+  GArgs a;
+  memset(&a, 0, sizeof(a));
+  a.M = M; a.N = N; a.K = K;
+  a.cv = M * N; a.chunk_stride = 0;
+  a.nonfinite = nonfinite;
+  a.f = *fmt;
+  a.push_peers = peers; a.push_flags = peer_flags; a.npush = npush; a.push_rank = rank;
+  a.push_slot_stride = slot_stride; a.push_off = (int64_t)rank * shard_stride;
+  a.push_scale_off = scale_off; a.push_elem_off = elem_off; a.push_state = state;
+  if (fmt->block == 32) return go_2cta<256, 8, 1, 32, ENC_E2M1, 4, 8, true>(a, x, w, st);
+  return go_2cta<256, 8, 1, 16, ENC_E2M1, 4, 8, true>(a, x, w, st);
 }
 
 }  // namespace mxb

@@ -1,0 +1,90 @@
+// The consumer half of the GEMM + all-gather push (k_gemm.cu, PUSH = true):
+// every rank's GEMM epilogue has written its MX shard into slot (epoch & 1)
+// of THIS rank's symmetric buffer over NVLink and released the epoch into
+// this rank's flag array.  One kernel waits for the N flags (acquire, system
+// scope; a wait past the timeout sets a status word instead of hanging),
+// then decodes the N local shards in rank order, fp32 from +0.0
+// (mx/netbench.py:332-334), into bf16 / f32, with the optional residual
+// add fused into the store -- K2's arithmetic, so the result is
+// bit-identical to the NCCL one-shot.  The shard bytes arrived during this
+// kernel's lifetime: coherent (ld.global.cg) loads only.
+#include "mx_kernels.cuh"
+
+namespace mxb {
+namespace {
+
+__device__ __forceinline__ unsigned int ld_acquire_sys_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename OutT, int B>
+__global__ void __launch_bounds__(kLeanThreads2, 8) k_push_dqsum(const PArgs P) {
+  constexpr int BITS = 4;
+  using RL = RankLoad<B, BITS, kVPL>;
+  pdl_prologue();  // this rank's GEMM (same stream) is complete: state[0] = epoch
+  __shared__ unsigned int s_e;
+  if (threadIdx.x == 0) s_e = *reinterpret_cast<const volatile unsigned int*>(P.state);
+  __syncthreads();
+  const unsigned int e = s_e;
+  if ((int)threadIdx.x < P.nranks) {
+    const unsigned int* fl = P.flags + threadIdx.x;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while ((int)(ld_acquire_sys_u32(fl) - e) < 0) {
+      __nanosleep(64);
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > P.timeout_ns) {
+        atomicExch(P.status, 1u);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint32_t u = blockIdx.x * kLeanWarps2 + (threadIdx.x >> 5);
+  if (u >= (uint32_t)(P.n / kUnit)) return;
+  const uint8_t* base = P.buf + (int64_t)(e & 1u) * P.slot_stride;
+  const Fmt f = P.f;
+  float acc[kVPL];
+#pragma unroll
+  for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
+  const int nr = P.nranks;
+  for (int r = 0; r < nr; r += 2) {
+    RL x0, x1;
+    load_rank<B, BITS, kVPL, true>(x0, base + (int64_t)r * P.shard_stride, P.scale_off,
+                                   P.elem_off, (int64_t)u * kUnit, lane, kVPL, 8);
+    if (r + 1 < nr)
+      load_rank<B, BITS, kVPL, true>(x1, base + (int64_t)(r + 1) * P.shard_stride, P.scale_off,
+                                     P.elem_off, (int64_t)u * kUnit, lane, kVPL, 8);
+    decode_rank<B, ENC_E2M1, BITS, kVPL>(x0, f, acc, false, nullptr);
+    if (r + 1 < nr) decode_rank<B, ENC_E2M1, BITS, kVPL>(x1, f, acc, false, nullptr);
+  }
+  const size_t o = (size_t)u * kUnit + lane * kVPL;
+  store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(P.out) + o, kVPL, acc,
+                             P.residual ? reinterpret_cast<const OutT*>(P.residual) + o
+                                        : nullptr);
+}
+
+template <typename OutT>
+bool go(const PArgs& a, int block, cudaStream_t st) {
+  const dim3 grid((unsigned)((a.n / kUnit + kLeanWarps2 - 1) / kLeanWarps2));
+  if (block == 32) {
+    launch_pdl(k_push_dqsum<OutT, 32>, grid, dim3(kLeanThreads2), 0, st, a);
+    return true;
+  }
+  if (block == 16) {
+    launch_pdl(k_push_dqsum<OutT, 16>, grid, dim3(kLeanThreads2), 0, st, a);
+    return true;
+  }
+  return false;
+}
+}  // namespace
+
+bool launch_push_dqsum(const PArgs& a, int out_is_bf16, int block, cudaStream_t st) {
+  return out_is_bf16 ? go<__nv_bfloat16>(a, block, st) : go<float>(a, block, st);
+}
+
+}  // namespace mxb

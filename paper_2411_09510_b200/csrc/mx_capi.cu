@@ -251,6 +251,12 @@ cudaError_t launch_gemm_mx(const void* x, const void* w, int64_t M, int64_t N, i
                            unsigned long long* nonfinite, void* workspace, int64_t workspace_bytes,
                            cudaStream_t st);
 int64_t gemm_workspace_bytes(int64_t M, int64_t N);
+cudaError_t launch_gemm_mx_push(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
+                                const Fmt* fmt, int enc_id, uint8_t* const* peers,
+                                unsigned int* const* peer_flags, int npush, int rank,
+                                int64_t slot_stride, int64_t shard_stride, int64_t scale_off,
+                                int64_t elem_off, unsigned int* state,
+                                unsigned long long* nonfinite, cudaStream_t st);
 
 }  // namespace mxb
 
@@ -773,6 +779,79 @@ int mx_gemm_quantize_chunks(const void* x, const void* w, int64_t M, int64_t N, 
     return fail(MX_ERR_INVALID_ARGUMENT, "shard_stride must be >= shard bytes and 32-aligned");
   return gemm_impl(x, w, M, N, K, s, chunk_values, shard_stride, shards + so, shards + eo,
                    partial, nonfinite, stream);
+}
+
+int mx_push_layout(int64_t n, const mx_scheme_t* s, int32_t nranks, int64_t* slot_stride,
+                   int64_t* shard_stride, int64_t* flags_offset, int64_t* buffer_bytes) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (n <= 0 || nranks < 1) return fail(MX_ERR_INVALID_ARGUMENT, "bad sizes");
+  int64_t so, eo, sb;
+  mx_shard_layout(n, s, &so, &eo, &sb);
+  const int64_t slot = (int64_t)nranks * sb;
+  const int64_t foff = (2 * slot + 255) / 256 * 256;
+  if (slot_stride) *slot_stride = slot;
+  if (shard_stride) *shard_stride = sb;
+  if (flags_offset) *flags_offset = foff;
+  if (buffer_bytes) *buffer_bytes = foff + ((int64_t)nranks * 4 + 255) / 256 * 256;
+  return MX_OK;
+}
+
+int mx_gemm_allgather_push(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
+                           const mx_scheme_t* s, uint8_t* const* peer_bufs,
+                           uint32_t* const* peer_flags, int32_t rank, int32_t nranks,
+                           uint32_t* state, uint64_t* nonfinite, void* stream) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (!x || !w || !peer_bufs || !peer_flags || !state)
+    return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (M < 1 || N < 1 || K < 1 || rank < 0 || rank >= nranks)
+    return fail(MX_ERR_INVALID_ARGUMENT, "bad sizes");
+  int64_t slot, sb, foff, total, so, eo, sbytes;
+  mx_push_layout(M * N, s, nranks, &slot, &sb, &foff, &total);
+  mx_shard_layout(M * N, s, &so, &eo, &sbytes);
+  Fmt f = make_fmt(s);
+  cudaError_t e = launch_gemm_mx_push(x, w, M, N, K, &f, enc_of(s), peer_bufs,
+                                      reinterpret_cast<unsigned int* const*>(peer_flags), nranks,
+                                      rank, slot, sb, so, eo,
+                                      reinterpret_cast<unsigned int*>(state),
+                                      reinterpret_cast<unsigned long long*>(nonfinite),
+                                      (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported)
+    return fail(MX_ERR_UNSUPPORTED,
+                "GEMM + all-gather push: fp4_e2m1 E8M0 with B in {16, 32}, N %% 256 == 0, "
+                "K %% 64 == 0, at most 8 ranks, 16-byte aligned operands");
+  if (e != cudaSuccess) return fail(MX_ERR_CUDA, "k_gemm_mx2 push: %s", cudaGetErrorString(e));
+  return cuda_check("k_gemm_mx2 push");
+}
+
+int mx_push_dequant_sum(const uint8_t* buf, int64_t n, const mx_scheme_t* s, int32_t nranks,
+                        const uint32_t* flags, const uint32_t* state, uint32_t* status,
+                        void* out, int32_t out_dtype, const void* residual, void* stream) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (!buf || !flags || !state || !status || !out)
+    return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (n <= 0 || n % 1024 != 0 || nranks < 1 || nranks > 8)
+    return fail(MX_ERR_UNSUPPORTED, "push decode: n %% 1024 == 0, 1..8 ranks");
+  Fmt f = make_fmt(s);
+  if ((out_dtype != MX_BF16 && out_dtype != MX_F32) || f.kbits != 8 || f.bits != 4 ||
+      enc_of(s) != ENC_E2M1 || !aligned(out, 32) || !aligned(residual, 32))
+    return fail(MX_ERR_UNSUPPORTED, "push decode: fp4_e2m1 E8M0, bf16/f32 out, 32-B aligned");
+  int64_t slot, sb, foff, total, so, eo, sbytes;
+  mx_push_layout(n, s, nranks, &slot, &sb, &foff, &total);
+  mx_shard_layout(n, s, &so, &eo, &sbytes);
+  PArgs a;
+  a.buf = buf; a.slot_stride = slot; a.shard_stride = sb; a.scale_off = so; a.elem_off = eo;
+  a.nranks = nranks; a.n = n;
+  a.flags = reinterpret_cast<const unsigned int*>(flags);
+  a.state = reinterpret_cast<const unsigned int*>(state);
+  a.status = reinterpret_cast<unsigned int*>(status);
+  a.timeout_ns = symm_timeout_ns();
+  a.out = out; a.residual = residual; a.f = f;
+  if (!launch_push_dqsum(a, out_dtype == MX_BF16, (int)s->block_size, (cudaStream_t)stream))
+    return fail(MX_ERR_UNSUPPORTED, "push decode: B in {16, 32}");
+  return cuda_check("k_push_dqsum");
 }
 
 int mx_symm_layout(int64_t n, const mx_scheme_t* s, int32_t nranks, int64_t* slot_stride,

@@ -1417,6 +1417,22 @@ struct SArgs {
   int full_fence;                // 1: extra fence.sc.sys around the flags (MXB200_SYMM_FENCE=1)
   unsigned long long timeout_ns; // peer flag wait limit (MXB200_SYMM_TIMEOUT_MS)
 };
+// the consumer of the GEMM + all-gather push (k_push.cu)
+struct PArgs {
+  const uint8_t* buf;            // this rank's symmetric buffer base
+  int64_t slot_stride, shard_stride, scale_off, elem_off;
+  int nranks;
+  int64_t n;                     // multiple of 1024
+  const unsigned int* flags;     // this rank's flag array: peer j releases [j] = epoch
+  const unsigned int* state;     // local [0]: this call's epoch (set by this rank's GEMM)
+  unsigned int* status;          // local u32: 1 if a peer wait timed out
+  unsigned long long timeout_ns;
+  void* out;
+  const void* residual;          // nullable, out's dtype (see DArgs)
+  Fmt f;
+};
+bool launch_push_dqsum(const PArgs& a, int out_is_bf16, int block, cudaStream_t st);
+
 // two-shot over symmetric memory (k_fused.cuh, k_symm2_flow)
 struct S2Args {
   const void* x;                 // this rank's bf16 partial (n values)

@@ -399,6 +399,7 @@ def _torch():
 
 
 _SYMM_CACHE = {}  # (group, scheme, n, dtype, algo) -> SymmetricAllReduce shared by layers
+_PUSH_CACHE = {}  # (group, scheme, n, dtype) -> FusedLinearAllReduce shared by layers
 
 
 def make_module_classes():
@@ -459,6 +460,8 @@ def make_module_classes():
                 algo = self.algo
                 if algo == "auto":
                     algo = "oneshot" if ws <= 2 else "twoshot"
+                if algo == "push":  # operands the push GEMM cannot take: K5
+                    algo = "symm"
                 if algo in ("symm", "symm2"):
                     skey = (id(self.group), str(self.scheme), n, dtype, algo)
                     car = _SYMM_CACHE.get(skey)
@@ -489,12 +492,36 @@ def make_module_classes():
                 return out if residual is None else residual + out
             return car(y.contiguous(), residual=residual.contiguous())
 
+        def _push(self, n, dtype, device):
+            from .collective import FusedLinearAllReduce
+
+            key = (id(self.group), str(self.scheme), n, dtype)
+            fl = _PUSH_CACHE.get(key)
+            if fl is None:
+                fl = FusedLinearAllReduce(self.scheme, n, group=self.group, out_dtype=dtype,
+                                          device=device)
+                _PUSH_CACHE[key] = fl
+            self._car[("push",) + key] = fl
+            return fl
+
         def forward(self, x, residual=None):
             """all_reduce(x @ W^T), or ``residual + all_reduce(x @ W^T)`` --
             the Llama block's residual update -- with the add fused into the
             compressed collective's dequant-sum store (the bf16 NCCL path
-            adds after the all-reduce; identical bits either way)."""
-            if self.scheme is not None and self.fused_gemm and self.algo not in ("symm", "symm2"):
+            adds after the all-reduce; identical bits either way).
+            ``algo="push"``: the GEMM, the quantiser and the all-gather in
+            one kernel (FusedLinearAllReduce), K5 where it does not apply."""
+            if self.scheme is not None and self.algo == "push":
+                n = x.numel() // x.shape[-1] * self.weight.shape[0]
+                fl = self._push(n, x.dtype, x.device)
+                xc = x.contiguous()
+                if fl.supported(xc, self.weight):
+                    if residual is not None and not self.fuse_residual:
+                        return residual + fl.linear(xc, self.weight)
+                    return fl.linear(xc, self.weight,
+                                     residual=None if residual is None else residual.contiguous())
+            if self.scheme is not None and self.fused_gemm and self.algo not in ("symm", "symm2",
+                                                                                  "push"):
                 n = x.numel() // x.shape[-1] * self.weight.shape[0]
                 car = self._collective(n, x.dtype, x.device)
                 if hasattr(car, "linear") and (

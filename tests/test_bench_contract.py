@@ -74,5 +74,6 @@ def test_gpu_arm_world1_nccl_line():
     assert d["collective"] is not None
     t = d["ttft"]["llama-3.1-8b"]
     assert t["layers"] == 2
-    for k in ("bf16_nccl", "mx_oneshot", "mx_oneshot_unfused", "mx_twoshot", "mx_symm", "mx_symm2"):
+    for k in ("bf16_nccl", "mx_oneshot", "mx_oneshot_unfused", "mx_twoshot", "mx_symm", "mx_symm2",
+              "mx_push", "mx_paper_scheme"):
         assert "ms" in t[k], (k, t[k])

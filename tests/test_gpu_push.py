@@ -1,0 +1,165 @@
+"""GPU: the GEMM + quantise + all-gather push (one kernel per rank,
+k_gemm.cu PUSH) and its flag-waiting decode (k_push.cu).
+
+* world size 1 over real torch symmetric memory: ``FusedLinearAllReduce``
+  equals ``CompressedAllReduce.linear`` (the NCCL one-shot of the same fused
+  GEMM's shard) bit for bit, over repeated calls (both slots, twice), with
+  and without the fused residual, bf16 and f32 outputs;
+* N = 2..8 ranks as N concurrent launches on one device (the K5 harness's
+  approach): each rank's GEMM pushes its shard into every rank's buffer
+  (plain device pointers standing in for peer mappings) and releases its
+  epoch into every rank's flag array; every rank's decode equals the
+  oracle's one-shot all-reduce of the ranks' bf16 partials
+  (mx/netbench.py:323-334), identical on every rank."""
+
+import ctypes
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import mx_oracle as O  # noqa: E402
+
+SPEC = "fp4_e2m1:32:e8m0"
+
+
+def operands(M, N, K, seed):
+    g = torch.Generator().manual_seed(seed)
+    x = torch.randn(M, K, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, generator=g) / K ** 0.5).to(torch.bfloat16)
+    x.view(-1)[:: 997] *= 64
+    return x.cuda(), w.cuda()
+
+
+@pytest.fixture(scope="module")
+def pg():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    yield dist
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("out_dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("spec", [SPEC, "fp4_e2m1:16:e8m0"])
+def test_push_world1_equals_nccl_oneshot(pg, out_dtype, spec):
+    from paper_2411_09510_b200.collective import CompressedAllReduce, FusedLinearAllReduce
+
+    M, N, K = 512, 1024, 256
+    fl = FusedLinearAllReduce(spec, M * N, out_dtype=out_dtype)
+    car = CompressedAllReduce(spec, M * N, algo="oneshot", out_dtype=out_dtype)
+    for it in range(5):  # epochs 1..5: both slots, twice
+        x, w = operands(M, N, K, seed=100 + it)
+        assert fl.supported(x, w)
+        got = fl.linear(x, w).clone()
+        want = car.linear(x, w).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(got.view(-1), want.view(-1)), it
+        h = torch.randn(M, N, device="cuda").to(out_dtype)
+        got_r = fl.linear(x, w, residual=h).clone()
+        assert torch.equal(got_r, h + want), it
+    fl.check_status()
+    fl.check_finite()
+
+
+def test_push_unsupported_raises(pg):
+    from paper_2411_09510_b200.collective import FusedLinearAllReduce
+    from paper_2411_09510_b200.errors import ShapeMismatch
+
+    fl = FusedLinearAllReduce(SPEC, 256 * 384)
+    x, w = operands(256, 384, 128, seed=1)  # N % 256 != 0
+    assert not fl.supported(x, w)
+    with pytest.raises(ShapeMismatch):
+        fl.linear(x, w)
+
+
+def _plain_partial(lib, x, w):
+    M, K = x.shape
+    N = w.shape[0]
+    part = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    from paper_2411_09510_b200 import _native
+
+    _native.check(lib.mx_gemm_quantize(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+                                       M, N, K, None, None, None, ctypes.c_void_p(part.data_ptr()),
+                                       None, st), "mx_gemm_quantize")
+    return part
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4, 8])
+def test_push_multirank_one_device(nranks):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2411_09510_b200 import _native
+    from paper_2411_09510_b200.formats import parse_scheme
+
+    lib = _native.load()
+    cs = parse_scheme(SPEC).to_c()
+    M, N, K = 256, 512, 256  # 2 tiles: every rank's GEMM and decode stay co-resident
+    n = M * N
+    slot, shard, foff, total = _native.push_layout(n, cs, nranks)
+    bufs = [torch.zeros(total, dtype=torch.uint8, device="cuda") for _ in range(nranks)]
+    bptr = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    fptr = torch.tensor([b.data_ptr() + foff for b in bufs], dtype=torch.int64, device="cuda")
+    state = [torch.zeros(4, dtype=torch.int32, device="cuda") for _ in range(nranks)]
+    nf = [torch.full((1,), -1, dtype=torch.int64, device="cuda") for _ in range(nranks)]
+    outs = [torch.empty(n, dtype=torch.bfloat16, device="cuda") for _ in range(nranks)]
+    streams = [torch.cuda.Stream() for _ in range(nranks)]
+    P = ctypes.c_void_p
+    for call in range(3):
+        ops = [operands(M, N, K, seed=1000 * call + r) for r in range(nranks)]
+        parts = [_plain_partial(lib, x, w) for x, w in ops]
+        torch.cuda.synchronize()
+        host = [p.float().cpu().numpy().ravel().astype(np.float64) for p in parts]
+        want = torch.from_numpy(O.allreduce_oneshot(host, O.scheme(SPEC))).to(torch.bfloat16)
+        for r in range(nranks):  # every GEMM first, then every decode
+            x, w = ops[r]
+            _native.check(lib.mx_gemm_allgather_push(
+                P(x.data_ptr()), P(w.data_ptr()), M, N, K, ctypes.byref(cs), P(bptr.data_ptr()),
+                P(fptr.data_ptr()), r, nranks, P(state[r].data_ptr() + 4), P(nf[r].data_ptr()),
+                P(streams[r].cuda_stream)), "mx_gemm_allgather_push")
+        for r in range(nranks):
+            _native.check(lib.mx_push_dequant_sum(
+                P(bufs[r].data_ptr()), n, ctypes.byref(cs), nranks, P(bufs[r].data_ptr() + foff),
+                P(state[r].data_ptr() + 4), P(state[r].data_ptr()), P(outs[r].data_ptr()),
+                _native.MX_BF16, None, P(streams[r].cuda_stream)), "mx_push_dequant_sum")
+        torch.cuda.synchronize()
+        for r in range(nranks):
+            assert int(state[r][0].item()) == 0, "peer wait timed out"
+            assert int(state[r][1].item()) == call + 1  # epoch
+            assert torch.equal(outs[r].cpu(), want), (nranks, call, r)
+
+
+def test_row_parallel_push_equals_oneshot(pg):
+    """RowParallelLinear(algo="push") == the NCCL one-shot hook, residual
+    fused, bit for bit (world size 1)."""
+    from paper_2411_09510_b200 import tp
+
+    RowParallelLinear = tp.make_module_classes()[0]
+    torch.manual_seed(3)
+    x = torch.randn(2, 128, 512, device="cuda").to(torch.bfloat16)
+    h = torch.randn(2, 128, 1024, device="cuda").to(torch.bfloat16)
+    push = RowParallelLinear(512, 1024, scheme=SPEC, algo="push", device="cuda")
+    one = RowParallelLinear(512, 1024, scheme=SPEC, algo="oneshot", device="cuda",
+                            fused_gemm=True)
+    one.weight.data.copy_(push.weight.data)
+    a = push(x, residual=h).clone()
+    b = one(x, residual=h).clone()
+    assert torch.equal(a, b)
+    assert torch.equal(push(x).clone(), one(x).clone())
+    tp._PUSH_CACHE.clear()

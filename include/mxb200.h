@@ -272,10 +272,11 @@ int mx_pack_codes(const uint8_t* codes, int64_t count, int32_t width, uint8_t* p
  * ONE kernel per rank: the tcgen05 GEMM's epilogue quantises each drained
  * accumulator tile and stores the shard bytes straight into slot
  * (epoch & 1) of EVERY rank's symmetric buffer (peer memory, NVLink), so the
- * transfer overlaps the remaining tiles' math; the last CTA releases the
- * epoch into every peer's flag array (system scope).  mx_push_dequant_sum
- * then waits for the N flags and decodes the N local shards in rank order
- * (bit-identical to the NCCL one-shot).  Buffer: mx_push_layout bytes per
+ * transfer overlaps the remaining tiles' math; its last CTA records the
+ * epoch.  mx_push_dequant_sum then publishes this rank's epoch into every
+ * rank's flag array (one system-scope fence, cumulative over the GEMM's
+ * stores), waits for the N flags and decodes the N local shards in rank
+ * order (bit-identical to the NCCL one-shot).  Buffer: mx_push_layout bytes per
  * rank (two slots of nranks shards, then nranks u32 flags, zeroed once);
  * state: 2 local u32 zeroed once ([0] epoch, [1] CTA counter); status: one
  * local u32 (1 = a peer wait timed out after MXB200_SYMM_TIMEOUT_MS).
@@ -283,12 +284,12 @@ int mx_pack_codes(const uint8_t* codes, int64_t count, int32_t width, uint8_t* p
 int mx_push_layout(int64_t n, const mx_scheme_t* scheme, int32_t nranks, int64_t* slot_stride,
                    int64_t* shard_stride, int64_t* flags_offset, int64_t* buffer_bytes);
 int mx_gemm_allgather_push(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
-                           const mx_scheme_t* scheme, uint8_t* const* peer_bufs,
-                           uint32_t* const* peer_flags, int32_t rank, int32_t nranks,
-                           uint32_t* state, uint64_t* nonfinite, void* stream);
-int mx_push_dequant_sum(const uint8_t* buf, int64_t n, const mx_scheme_t* scheme, int32_t nranks,
-                        const uint32_t* flags, const uint32_t* state, uint32_t* status,
-                        void* out, int32_t out_dtype, const void* residual, void* stream);
+                           const mx_scheme_t* scheme, uint8_t* const* peer_bufs, int32_t rank,
+                           int32_t nranks, uint32_t* state, uint64_t* nonfinite, void* stream);
+int mx_push_dequant_sum(const uint8_t* buf, int64_t n, const mx_scheme_t* scheme, int32_t rank,
+                        int32_t nranks, uint32_t* const* peer_flags, const uint32_t* flags,
+                        const uint32_t* state, uint32_t* status, void* out, int32_t out_dtype,
+                        const void* residual, void* stream);
 
 /* serialize (mx/codec.py:340-348) on the device: out = header || scale
  * stream || element stream, one launch, any byte alignment.  `header` is a

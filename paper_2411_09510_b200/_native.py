@@ -76,10 +76,10 @@ SIGNATURES = {
     "mx_memset_async": (c_i32, [c_vp, c_i32, c_i64, c_vp]),
     "mx_serialize": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "mx_push_layout": (c_i32, [c_i64, _SP, c_i32, c_i64p, c_i64p, c_i64p, c_i64p]),
-    "mx_gemm_allgather_push": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i64, _SP, c_vp, c_vp, c_i32,
-                                       c_i32, c_vp, c_vp, c_vp]),
-    "mx_push_dequant_sum": (c_i32, [c_vp, c_i64, _SP, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp,
-                                    c_vp]),
+    "mx_gemm_allgather_push": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i64, _SP, c_vp, c_i32, c_i32,
+                                       c_vp, c_vp, c_vp]),
+    "mx_push_dequant_sum": (c_i32, [c_vp, c_i64, _SP, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                    c_i32, c_vp, c_vp]),
     "mx_copy_bytes": (c_i32, [c_vp, c_i64, c_vp, c_vp]),
     "mx_nonfinite_reset": (c_i32, [c_vp, c_vp]),
 }

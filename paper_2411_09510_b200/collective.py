@@ -515,10 +515,11 @@ class FusedLinearAllReduce:
     accumulator tile as it drains and stores the shard bytes straight into
     slot (epoch & 1) of every rank's symmetric buffer -- the all-gather of
     mx/netbench.py:323-328 rides on the epilogue and overlaps the remaining
-    tiles' math; its last CTA releases the epoch into every peer's flag
-    array.  A second launch (k_push_dqsum) waits for the N flags and decodes
-    the N shards from local memory in rank order, with the optional residual
-    add fused into its store.  Bit-identical to ``CompressedAllReduce.linear``
+    tiles' math.  A second launch (k_push_dqsum) publishes this rank's epoch
+    into every rank's flag array (one system-scope fence, so none sits on the
+    GEMM's tail), waits for the N flags and decodes the N shards from local
+    memory in rank order, with the optional residual add fused into its
+    store.  Bit-identical to ``CompressedAllReduce.linear``
     (NCCL one-shot) on the same operands.  No NCCL kernel, no gather copy.
     Requirements: fp4_e2m1 E8M0 with B in {16, 32}; bf16 x [M, K] and
     W [N, K] contiguous, N % 256 == 0, K % 64 == 0, n = M*N % 1024 == 0;
@@ -592,11 +593,12 @@ class FusedLinearAllReduce:
         base = self.state.data_ptr()
         _native.check(be.lib.mx_gemm_allgather_push(
             P(x.data_ptr()), P(weight.data_ptr()), M, N, K, ctypes.byref(be.cs),
-            P(self.buf_ptrs.data_ptr()), P(self.flag_ptrs.data_ptr()), self.rank, self.world,
+            P(self.buf_ptrs.data_ptr()), self.rank, self.world,
             P(base + 4), P(self.flag.data_ptr()), be._st()), "mx_gemm_allgather_push")
         _native.check(be.lib.mx_push_dequant_sum(
-            P(self.buf.data_ptr()), self.n, ctypes.byref(be.cs), self.world,
-            P(self.flags_local.data_ptr()), P(base + 4), P(base), P(o.data_ptr()), be._dt(o),
+            P(self.buf.data_ptr()), self.n, ctypes.byref(be.cs), self.rank, self.world,
+            P(self.flag_ptrs.data_ptr()), P(self.flags_local.data_ptr()), P(base + 4), P(base),
+            P(o.data_ptr()), be._dt(o),
             P(residual.data_ptr()) if residual is not None else None, be._st()),
             "mx_push_dequant_sum")
         return o.view(*x.shape[:-1], N)

@@ -144,10 +144,9 @@ struct GArgs {
   Fmt f;
   // all-gather push (2-CTA form, PUSH = true): the epilogue writes this
   // rank's shard into slot (epoch & 1) of EVERY rank's symmetric buffer over
-  // NVLink, tile by tile as the accumulators drain; the last CTA to finish
-  // publishes the epoch to every peer's flag array (release, system scope)
+  // NVLink, tile by tile as the accumulators drain; the last CTA records the
+  // epoch (the decode launch publishes it, k_push.cu)
   uint8_t* const* push_peers;       // device [npush]: peer buffer bases
-  unsigned int* const* push_flags;  // device [npush]: peer flag arrays (u32 x npush)
   int npush, push_rank;
   int64_t push_slot_stride;         // bytes per slot (npush shards)
   int64_t push_off;                 // this rank's shard inside a slot
@@ -155,6 +154,7 @@ struct GArgs {
   unsigned int* push_state;         // local: [0] epoch, [1] CTA arrival counter
 };
 constexpr int kMaxPush = 8;
+
 
 // Work distribution.  With a workspace: stream-K -- the T tiles x KB
 // k-blocks are cut into gridDim.x contiguous ranges of (nearly) equal
@@ -237,20 +237,21 @@ __device__ __forceinline__ void epi_chunk(const GArgs& A, const Fmt& f, const ui
     LaneCodes<BITS> cw = quant_lane<__nv_bfloat16, B, ENC, BITS>(raw, f, stored, bad);
     if (bad) report_nonfinite_raw<__nv_bfloat16>(raw, kVPL, flat, A.nonfinite);
     if constexpr (PUSH) {  // one tensor, E8M0: the same bytes to every rank
-      constexpr int LPB = Geo<B>::LPB;
+      static_assert(BITS == 4, "push: FP4 codes");
+      const int64_t eo = A.push_elem_off + flat / 2, so = A.push_scale_off + flat / B;
+#pragma unroll 1
       for (int j = 0; j < A.npush; ++j) {
         uint8_t* base = pdst[j];
-        store_lane_codes<BITS>(base + A.push_elem_off + flat / 8 * BITS, cw, kVPL);
-        uint8_t* sp = base + A.push_scale_off + flat / B;
-        if constexpr (NSB == 4) {
-          *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
-                                             ((uint32_t)stored[2] << 16) |
-                                             ((uint32_t)stored[3] << 24);
-        } else if constexpr (NSB == 2) {
-          *reinterpret_cast<uint16_t*>(sp) = (uint16_t)(stored[0] | (stored[1] << 8));
+        asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(base + eo), "r"(cw.w[0]),
+                     "r"(cw.w[1]), "r"(cw.w[2]), "r"(cw.w[3])
+                     : "memory");
+        if constexpr (NSB == 2) {
+          asm volatile("st.global.u16 [%0], %1;" ::"l"(base + so),
+                       "h"((uint16_t)(stored[0] | (stored[1] << 8)))
+                       : "memory");
         } else {
-          (void)LPB;
-          *sp = (uint8_t)stored[0];
+          asm volatile("st.global.u8 [%0], %1;" ::"l"(base + so), "h"((uint16_t)stored[0])
+                       : "memory");
         }
       }
       return;
@@ -525,10 +526,6 @@ __device__ __forceinline__ void mma2_commit_both(uint64_t* bar) {
       : "memory");
 }
 
-__device__ __forceinline__ void st_release_sys_u32(unsigned int* p, unsigned int v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 template <int BN, int EPI, int MODE, int B, int ENC, int BITS, int KB = 8, bool PUSH = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm_threads<EPI>(), 1)
     k_gemm_mx2(const __grid_constant__ CUtensorMap map_x,
@@ -586,7 +583,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm_threads<EPI>(),
   __shared__ uint8_t* s_dst[PUSH ? kMaxPush : 1];
   __shared__ unsigned int s_epoch;
   if constexpr (PUSH) {
-    if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile unsigned int*>(A.push_state) + 1u;
+    if (threadIdx.x == 0)
+      s_epoch = *reinterpret_cast<volatile unsigned int*>(A.push_state) + 1u;
     __syncthreads();
     if ((int)threadIdx.x < A.npush)
       s_dst[threadIdx.x] = A.push_peers[threadIdx.x] +
@@ -717,16 +715,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm_threads<EPI>(),
                  : "memory");
   }
   if constexpr (PUSH) {
-    // every epilogue store of this CTA is ordered before thread 0 by the
-    // cluster barrier; the system fence + arrival counter make them visible
-    // before the last CTA's release of the epoch to every peer (the
-    // threadfence-reduction pattern at system scope)
+    // the last CTA (GPU-scope arrival counter) records this call's epoch;
+    // the system-scope publication to the peers is the first thing the
+    // decode launch (k_push_dqsum) does, so no system fence sits on the
+    // GEMM's tail -- the GEMM's stores precede that launch in stream order,
+    // and its release is cumulative over them
     if (threadIdx.x == 0) {
-      __threadfence_system();
-      const unsigned int prev = atomicAdd(A.push_state + 1, 1u);
+      unsigned int prev;
+      asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
+                   : "=r"(prev) : "l"(A.push_state + 1) : "memory");
       if (prev == gridDim.x - 1) {
-        __threadfence_system();
-        for (int j = 0; j < A.npush; ++j) st_release_sys_u32(A.push_flags[j] + A.push_rank, s_epoch);
         A.push_state[1] = 0u;
         *reinterpret_cast<volatile unsigned int*>(A.push_state) = s_epoch;
       }
@@ -935,10 +933,9 @@ cudaError_t launch_gemm_mx(const void* x, const void* w, int64_t M, int64_t N, i
 // form, one tensor, E8M0, fp4_e2m1 B in {16, 32}): returns
 // cudaErrorNotSupported outside it.
 cudaError_t launch_gemm_mx_push(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
-                                const Fmt* fmt, int enc_id, uint8_t* const* peers,
-                                unsigned int* const* peer_flags, int npush, int rank,
-                                int64_t slot_stride, int64_t shard_stride, int64_t scale_off,
-                                int64_t elem_off, unsigned int* state,
+                                const Fmt* fmt, int enc_id, uint8_t* const* peers, int npush,
+                                int rank, int64_t slot_stride, int64_t shard_stride,
+                                int64_t scale_off, int64_t elem_off, unsigned int* state,
                                 unsigned long long* nonfinite, cudaStream_t st) {
   using namespace gm;
   static const int two = env_int("MXB200_GEMM_2CTA", 1);
@@ -955,7 +952,7 @@ cudaError_t launch_gemm_mx_push(const void* x, const void* w, int64_t M, int64_t
   a.cv = M * N; a.chunk_stride = 0;
   a.nonfinite = nonfinite;
   a.f = *fmt;
-  a.push_peers = peers; a.push_flags = peer_flags; a.npush = npush; a.push_rank = rank;
+  a.push_peers = peers; a.npush = npush; a.push_rank = rank;
   a.push_slot_stride = slot_stride; a.push_off = (int64_t)rank * shard_stride;
   a.push_scale_off = scale_off; a.push_elem_off = elem_off; a.push_state = state;
   if (fmt->block == 32) return go_2cta<256, 8, 1, 32, ENC_E2M1, 4, 8, true>(a, x, w, st);

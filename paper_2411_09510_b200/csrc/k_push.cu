@@ -1,8 +1,10 @@
 // The consumer half of the GEMM + all-gather push (k_gemm.cu, PUSH = true):
 // every rank's GEMM epilogue has written its MX shard into slot (epoch & 1)
-// of THIS rank's symmetric buffer over NVLink and released the epoch into
-// this rank's flag array.  One kernel waits for the N flags (acquire, system
-// scope; a wait past the timeout sets a status word instead of hanging),
+// of THIS rank's symmetric buffer over NVLink.  This launch first publishes
+// its own rank's epoch into every rank's flag array (CTA 0: one system fence,
+// cumulative over the GEMM's stores that precede it in stream order), then
+// waits for the N flags (acquire, system scope; a wait past the timeout sets
+// a status word instead of hanging),
 // then decodes the N local shards in rank order, fp32 from +0.0
 // (mx/netbench.py:332-334), into bf16 / f32, with the optional residual
 // add fused into the store -- K2's arithmetic, so the result is
@@ -28,6 +30,15 @@ __global__ void __launch_bounds__(kLeanThreads2, 8) k_push_dqsum(const PArgs P) 
   if (threadIdx.x == 0) s_e = *reinterpret_cast<const volatile unsigned int*>(P.state);
   __syncthreads();
   const unsigned int e = s_e;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // publish this rank's call-e shard (written by the GEMM launch before
+    // this one on the stream) to every rank: one system-scope fence, then
+    // the epoch into every flag array
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    for (int j = 0; j < P.nranks; ++j)
+      asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(P.peer_flags[j] + P.rank), "r"(e)
+                   : "memory");
+  }
   if ((int)threadIdx.x < P.nranks) {
     const unsigned int* fl = P.flags + threadIdx.x;
     unsigned long long t0;

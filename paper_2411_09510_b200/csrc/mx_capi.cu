@@ -252,10 +252,9 @@ cudaError_t launch_gemm_mx(const void* x, const void* w, int64_t M, int64_t N, i
                            cudaStream_t st);
 int64_t gemm_workspace_bytes(int64_t M, int64_t N);
 cudaError_t launch_gemm_mx_push(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
-                                const Fmt* fmt, int enc_id, uint8_t* const* peers,
-                                unsigned int* const* peer_flags, int npush, int rank,
-                                int64_t slot_stride, int64_t shard_stride, int64_t scale_off,
-                                int64_t elem_off, unsigned int* state,
+                                const Fmt* fmt, int enc_id, uint8_t* const* peers, int npush,
+                                int rank, int64_t slot_stride, int64_t shard_stride,
+                                int64_t scale_off, int64_t elem_off, unsigned int* state,
                                 unsigned long long* nonfinite, cudaStream_t st);
 
 }  // namespace mxb
@@ -798,12 +797,11 @@ int mx_push_layout(int64_t n, const mx_scheme_t* s, int32_t nranks, int64_t* slo
 }
 
 int mx_gemm_allgather_push(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
-                           const mx_scheme_t* s, uint8_t* const* peer_bufs,
-                           uint32_t* const* peer_flags, int32_t rank, int32_t nranks,
-                           uint32_t* state, uint64_t* nonfinite, void* stream) {
+                           const mx_scheme_t* s, uint8_t* const* peer_bufs, int32_t rank,
+                           int32_t nranks, uint32_t* state, uint64_t* nonfinite, void* stream) {
   int rc = check_scheme(s);
   if (rc) return rc;
-  if (!x || !w || !peer_bufs || !peer_flags || !state)
+  if (!x || !w || !peer_bufs || !state)
     return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
   if (M < 1 || N < 1 || K < 1 || rank < 0 || rank >= nranks)
     return fail(MX_ERR_INVALID_ARGUMENT, "bad sizes");
@@ -811,8 +809,7 @@ int mx_gemm_allgather_push(const void* x, const void* w, int64_t M, int64_t N, i
   mx_push_layout(M * N, s, nranks, &slot, &sb, &foff, &total);
   mx_shard_layout(M * N, s, &so, &eo, &sbytes);
   Fmt f = make_fmt(s);
-  cudaError_t e = launch_gemm_mx_push(x, w, M, N, K, &f, enc_of(s), peer_bufs,
-                                      reinterpret_cast<unsigned int* const*>(peer_flags), nranks,
+  cudaError_t e = launch_gemm_mx_push(x, w, M, N, K, &f, enc_of(s), peer_bufs, nranks,
                                       rank, slot, sb, so, eo,
                                       reinterpret_cast<unsigned int*>(state),
                                       reinterpret_cast<unsigned long long*>(nonfinite),
@@ -825,12 +822,13 @@ int mx_gemm_allgather_push(const void* x, const void* w, int64_t M, int64_t N, i
   return cuda_check("k_gemm_mx2 push");
 }
 
-int mx_push_dequant_sum(const uint8_t* buf, int64_t n, const mx_scheme_t* s, int32_t nranks,
-                        const uint32_t* flags, const uint32_t* state, uint32_t* status,
-                        void* out, int32_t out_dtype, const void* residual, void* stream) {
+int mx_push_dequant_sum(const uint8_t* buf, int64_t n, const mx_scheme_t* s, int32_t rank,
+                        int32_t nranks, uint32_t* const* peer_flags, const uint32_t* flags,
+                        const uint32_t* state, uint32_t* status, void* out, int32_t out_dtype,
+                        const void* residual, void* stream) {
   int rc = check_scheme(s);
   if (rc) return rc;
-  if (!buf || !flags || !state || !status || !out)
+  if (!buf || !peer_flags || !flags || !state || !status || !out || rank < 0 || rank >= nranks)
     return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
   if (n <= 0 || n % 1024 != 0 || nranks < 1 || nranks > 8)
     return fail(MX_ERR_UNSUPPORTED, "push decode: n %% 1024 == 0, 1..8 ranks");
@@ -843,7 +841,8 @@ int mx_push_dequant_sum(const uint8_t* buf, int64_t n, const mx_scheme_t* s, int
   mx_shard_layout(n, s, &so, &eo, &sbytes);
   PArgs a;
   a.buf = buf; a.slot_stride = slot; a.shard_stride = sb; a.scale_off = so; a.elem_off = eo;
-  a.nranks = nranks; a.n = n;
+  a.nranks = nranks; a.n = n; a.rank = rank;
+  a.peer_flags = reinterpret_cast<unsigned int* const*>(peer_flags);
   a.flags = reinterpret_cast<const unsigned int*>(flags);
   a.state = reinterpret_cast<const unsigned int*>(state);
   a.status = reinterpret_cast<unsigned int*>(status);

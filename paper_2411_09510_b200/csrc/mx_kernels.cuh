@@ -1421,8 +1421,9 @@ struct SArgs {
 struct PArgs {
   const uint8_t* buf;            // this rank's symmetric buffer base
   int64_t slot_stride, shard_stride, scale_off, elem_off;
-  int nranks;
+  int nranks, rank;
   int64_t n;                     // multiple of 1024
+  unsigned int* const* peer_flags;  // device [nranks]: every rank's flag array (CTA 0 publishes)
   const unsigned int* flags;     // this rank's flag array: peer j releases [j] = epoch
   const unsigned int* state;     // local [0]: this call's epoch (set by this rank's GEMM)
   unsigned int* status;          // local u32: 1 if a peer wait timed out

@@ -7,8 +7,8 @@ k_gemm.cu PUSH) and its flag-waiting decode (k_push.cu).
   and without the fused residual, bf16 and f32 outputs;
 * N = 2..8 ranks as N concurrent launches on one device (the K5 harness's
   approach): each rank's GEMM pushes its shard into every rank's buffer
-  (plain device pointers standing in for peer mappings) and releases its
-  epoch into every rank's flag array; every rank's decode equals the
+  (plain device pointers standing in for peer mappings); its decode launch
+  publishes its epoch into every rank's flag array; every rank's decode equals the
   oracle's one-shot all-reduce of the ranks' bf16 partials
   (mx/netbench.py:323-334), identical on every rank."""
 
@@ -131,12 +131,13 @@ def test_push_multirank_one_device(nranks):
             x, w = ops[r]
             _native.check(lib.mx_gemm_allgather_push(
                 P(x.data_ptr()), P(w.data_ptr()), M, N, K, ctypes.byref(cs), P(bptr.data_ptr()),
-                P(fptr.data_ptr()), r, nranks, P(state[r].data_ptr() + 4), P(nf[r].data_ptr()),
+                r, nranks, P(state[r].data_ptr() + 4), P(nf[r].data_ptr()),
                 P(streams[r].cuda_stream)), "mx_gemm_allgather_push")
         for r in range(nranks):
             _native.check(lib.mx_push_dequant_sum(
-                P(bufs[r].data_ptr()), n, ctypes.byref(cs), nranks, P(bufs[r].data_ptr() + foff),
-                P(state[r].data_ptr() + 4), P(state[r].data_ptr()), P(outs[r].data_ptr()),
+                P(bufs[r].data_ptr()), n, ctypes.byref(cs), r, nranks, P(fptr.data_ptr()),
+                P(bufs[r].data_ptr() + foff), P(state[r].data_ptr() + 4), P(state[r].data_ptr()),
+                P(outs[r].data_ptr()),
                 _native.MX_BF16, None, P(streams[r].cuda_stream)), "mx_push_dequant_sum")
         torch.cuda.synchronize()
         for r in range(nranks):

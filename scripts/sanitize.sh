@@ -32,4 +32,9 @@ T_R2="tests/test_gpu_residual.py tests/test_gpu_mxc1.py"
 run memcheck_r2 memcheck $T_R2 tests/test_gpu_parity.py -k "e5m0 or e4m0 or residual or serialize"
 run racecheck_r2 racecheck $T_R2 tests/test_gpu_parity.py -k "e5m0 or e4m0"
 run synccheck_r2 synccheck tests/test_gpu_parity.py -k "e5m0 or e4m0"
+# the GEMM + all-gather push (peer stores from the epilogue, flag publish /
+# acquire in the decode launch)
+run memcheck_push memcheck tests/test_gpu_push.py
+run racecheck_push racecheck tests/test_gpu_push.py
+run synccheck_push synccheck tests/test_gpu_push.py
 cat $out/summary.txt

@@ -662,6 +662,67 @@ def ttft_block(torch, dist, args, world, dev):
     return out
 
 
+def linear_collective_block(torch, dist, args, world, dev):
+    """The row-parallel producer and its all-reduce together, per rank, at
+    the Llama-3.1-8B o_proj shape of TP=N (x [2048, 4096/N] . W [4096,
+    4096/N]^T, residual fused where the path allows):
+      bf16_nccl   cuBLAS GEMM -> NCCL bf16 all_reduce -> residual add
+      mx_nccl     tcgen05 GEMM + quantiser -> NCCL all-gather -> K2 (+res)
+      mx_push     GEMM + quantiser + all-gather push in ONE kernel -> decode
+    CUDA-graph replays over operand sets rotated beyond L2, device time, max
+    over ranks; mx_push checked bit-identical to mx_nccl."""
+    import torch.nn.functional as F
+
+    from paper_2411_09510_b200.collective import CompressedAllReduce, FusedLinearAllReduce
+
+    M, N = 2048, 4096
+    K = 4096 // world
+    n = M * N
+    per = 2 * (M * K + N * K)
+    R = max(2, -(-3 * L2_BYTES // per))
+    g = torch.Generator(device=dev).manual_seed(1234 + dist.get_rank())
+    xs = [torch.randn(M, K, device=dev, generator=g).to(torch.bfloat16) for _ in range(R)]
+    ws = [(torch.randn(N, K, device=dev, generator=g) / K ** 0.5).to(torch.bfloat16)
+          for _ in range(R)]
+    h = torch.randn(M, N, device=dev, generator=g).to(torch.bfloat16)
+    car = CompressedAllReduce(args.scheme, n, algo="oneshot", out_dtype=torch.bfloat16,
+                              device=dev)
+    fl = FusedLinearAllReduce(args.scheme, n, out_dtype=torch.bfloat16, device=dev)
+    out = {"shape": f"x [{M}, {K}] . W [{N}, {K}]^T per rank (8B o_proj, TP={world})",
+           "scheme": args.scheme}
+
+    def bf16(i):
+        y = F.linear(xs[i], ws[i])
+        dist.all_reduce(y)
+        return h + y
+
+    variants = [("bf16_nccl", bf16), ("mx_nccl", lambda i: car.linear(xs[i], ws[i], residual=h)),
+                ("mx_push", lambda i: fl.linear(xs[i], ws[i], residual=h))]
+    a = car.linear(xs[0], ws[0], residual=h).clone()
+    b = fl.linear(xs[0], ws[0], residual=h).clone()
+    torch.cuda.synchronize()
+    out["mx_push_bit_exact_vs_mx_nccl"] = bool(torch.equal(a.view(torch.int16),
+                                                           b.view(torch.int16)))
+    reps = max(4, min(40, args.steps // 10))
+    for label, fn in variants:
+        gph = capture(torch, lambda fn=fn: [fn(i) for i in range(R)])
+        for _ in range(3):
+            gph.replay()
+        torch.cuda.synchronize()
+        dist.barrier()
+        ms = time_graph_replays(torch, [gph], reps) / (reps * R)
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out[label + "_us"] = round(float(t.item()) * 1e3, 2)
+        del gph
+    for label in ("mx_nccl", "mx_push"):
+        out[label + "_speedup_vs_bf16"] = round(out["bf16_nccl_us"] / out[label + "_us"], 3)
+    fl.check_status()
+    del xs, ws, car, fl
+    torch.cuda.empty_cache()
+    return out
+
+
 def ttft_tp1_block(torch, args):
     """TP=1 prefill TTFT on this GPU (no process group, no exchange): the
     MX path's whole codec cost on the forward -- per row-parallel layer the
@@ -1152,10 +1213,22 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
 
     ttft = None
     gemm = None
-    if dist_mode and not args.no_ttft:
+    lincoll = None
+    if dist_mode:
         del sets
         torch.cuda.empty_cache()
-        ttft = ttft_block(torch, dist, args, world, dev)
+        err = None
+        try:
+            lincoll = linear_collective_block(torch, dist, args, world, dev)
+        except Exception as exc:  # noqa: BLE001
+            err = f"{type(exc).__name__}: {exc}"[:200]
+        t_ok = torch.tensor([1 if err is None else 0], device=dev, dtype=torch.int32)
+        dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
+        if not bool(t_ok.item()):
+            lincoll = {"error": err or "failed on another rank"}
+        torch.cuda.empty_cache()
+        if not args.no_ttft:
+            ttft = ttft_block(torch, dist, args, world, dev)
     elif not dist_mode:
         del sets
         torch.cuda.empty_cache()
@@ -1183,7 +1256,7 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
             "bf16_nccl_allreduce": bf16_ar, "symmetric_memory_fused": symm,
             "collective": coll, "simulated_tp_fused_step": sim_more, "shape_70b": shape70,
-            "producer_gemm": gemm, "ttft": ttft}
+            "producer_gemm": gemm, "linear_collective": lincoll, "ttft": ttft}
     print(json.dumps(line), flush=True)
 
 

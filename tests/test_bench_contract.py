@@ -72,6 +72,9 @@ def test_gpu_arm_world1_nccl_line():
              "--no-70b"])
     assert d["n_gpus"] == 1 and d["value"] > 0
     assert d["collective"] is not None
+    lc = d["linear_collective"]
+    assert lc["mx_push_bit_exact_vs_mx_nccl"] is True, lc
+    assert lc["bf16_nccl_us"] > 0 and lc["mx_nccl_us"] > 0 and lc["mx_push_us"] > 0
     t = d["ttft"]["llama-3.1-8b"]
     assert t["layers"] == 2
     for k in ("bf16_nccl", "mx_oneshot", "mx_oneshot_unfused", "mx_twoshot", "mx_symm", "mx_symm2",

@@ -667,8 +667,11 @@ def linear_collective_block(torch, dist, args, world, dev):
     the Llama-3.1-8B o_proj shape of TP=N (x [2048, 4096/N] . W [4096,
     4096/N]^T, residual fused where the path allows):
       bf16_nccl   cuBLAS GEMM -> NCCL bf16 all_reduce -> residual add
-      mx_nccl     tcgen05 GEMM + quantiser -> NCCL all-gather -> K2 (+res)
-      mx_push     GEMM + quantiser + all-gather push in ONE kernel -> decode
+      mx_nccl     tcgen05 GEMM + quantiser -> NCCL all-gather -> K2 (+res);
+                  two-shot from TP=4 (all_to_all -> K3 -> all-gather -> K2)
+      mx_push     GEMM + quantiser + all-gather push in ONE kernel -> decode;
+                  two-shot from TP=4 (the GEMM scatters the reduce-scatter
+                  leg, a requantise launch pushes the all-gather leg)
     CUDA-graph replays over operand sets rotated beyond L2, device time, max
     over ranks; mx_push checked bit-identical to mx_nccl."""
     import torch.nn.functional as F
@@ -685,11 +688,11 @@ def linear_collective_block(torch, dist, args, world, dev):
     ws = [(torch.randn(N, K, device=dev, generator=g) / K ** 0.5).to(torch.bfloat16)
           for _ in range(R)]
     h = torch.randn(M, N, device=dev, generator=g).to(torch.bfloat16)
-    car = CompressedAllReduce(args.scheme, n, algo="oneshot", out_dtype=torch.bfloat16,
-                              device=dev)
-    fl = FusedLinearAllReduce(args.scheme, n, out_dtype=torch.bfloat16, device=dev)
+    algo = "oneshot" if world <= 2 else "twoshot"
+    car = CompressedAllReduce(args.scheme, n, algo=algo, out_dtype=torch.bfloat16, device=dev)
+    fl = FusedLinearAllReduce(args.scheme, n, out_dtype=torch.bfloat16, device=dev, algo=algo)
     out = {"shape": f"x [{M}, {K}] . W [{N}, {K}]^T per rank (8B o_proj, TP={world})",
-           "scheme": args.scheme}
+           "scheme": args.scheme, "algo": algo}
 
     def bf16(i):
         y = F.linear(xs[i], ws[i])

@@ -291,6 +291,31 @@ int mx_push_dequant_sum(const uint8_t* buf, int64_t n, const mx_scheme_t* scheme
                         const uint32_t* state, uint32_t* status, void* out, int32_t out_dtype,
                         const void* residual, void* stream);
 
+/* Two-shot form (the TP >= 4 algorithm; n % (1024*nranks) == 0): the GEMM's
+ * epilogue scatters chunk j of its shard to rank j (the reduce-scatter leg,
+ * one store per value group); mx_push2_requant publishes, waits for every
+ * rank's chunk j, sums the N shards of this rank's chunk in rank order,
+ * re-quantises (K3's arithmetic) and pushes the reduced chunk shard into
+ * every rank (the all-gather leg); mx_push2_decode publishes, waits and
+ * decodes every owner's reduced chunk, residual fused.  Bit-identical to
+ * the NCCL two-shot.  Buffer: mx_push2_layout bytes (two slots of 2 x
+ * nranks chunk shards; flags: nranks RS then nranks AG u32, zeroed once);
+ * peer_flags: device array of every rank's flag array. */
+int mx_push2_layout(int64_t n, const mx_scheme_t* scheme, int32_t nranks, int64_t* chunk_values,
+                    int64_t* slot_stride, int64_t* shard_stride, int64_t* flags_offset,
+                    int64_t* buffer_bytes);
+int mx_gemm_reducescatter_push(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
+                               const mx_scheme_t* scheme, uint8_t* const* peer_bufs,
+                               int32_t rank, int32_t nranks, uint32_t* state, uint64_t* nonfinite,
+                               void* stream);
+int mx_push2_requant(const uint8_t* buf, int64_t n, const mx_scheme_t* scheme, int32_t rank,
+                     int32_t nranks, uint8_t* const* peer_bufs, uint32_t* const* peer_flags,
+                     const uint32_t* state, uint32_t* status, uint64_t* nonfinite, void* stream);
+int mx_push2_decode(const uint8_t* buf, int64_t n, const mx_scheme_t* scheme, int32_t rank,
+                    int32_t nranks, uint32_t* const* peer_flags, const uint32_t* state,
+                    uint32_t* status, void* out, int32_t out_dtype, const void* residual,
+                    void* stream);
+
 /* serialize (mx/codec.py:340-348) on the device: out = header || scale
  * stream || element stream, one launch, any byte alignment.  `header` is a
  * HOST pointer to the pack_header bytes (mx/codec.py:300-308), at most 544

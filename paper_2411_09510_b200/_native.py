@@ -76,6 +76,13 @@ SIGNATURES = {
     "mx_memset_async": (c_i32, [c_vp, c_i32, c_i64, c_vp]),
     "mx_serialize": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "mx_push_layout": (c_i32, [c_i64, _SP, c_i32, c_i64p, c_i64p, c_i64p, c_i64p]),
+    "mx_push2_layout": (c_i32, [c_i64, _SP, c_i32, c_i64p, c_i64p, c_i64p, c_i64p, c_i64p]),
+    "mx_gemm_reducescatter_push": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i64, _SP, c_vp, c_i32,
+                                           c_i32, c_vp, c_vp, c_vp]),
+    "mx_push2_requant": (c_i32, [c_vp, c_i64, _SP, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                 c_vp]),
+    "mx_push2_decode": (c_i32, [c_vp, c_i64, _SP, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32,
+                                c_vp, c_vp]),
     "mx_gemm_allgather_push": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i64, _SP, c_vp, c_i32, c_i32,
                                        c_vp, c_vp, c_vp]),
     "mx_push_dequant_sum": (c_i32, [c_vp, c_i64, _SP, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
@@ -184,6 +191,16 @@ def push_layout(n: int, cs: MxScheme, nranks: int) -> tuple[int, int, int, int]:
     v = [c_i64() for _ in range(4)]
     check(lib.mx_push_layout(n, ctypes.byref(cs), nranks, *[ctypes.byref(x) for x in v]),
           "mx_push_layout")
+    return tuple(x.value for x in v)
+
+
+def push2_layout(n: int, cs: MxScheme, nranks: int) -> tuple[int, int, int, int, int]:
+    """(chunk_values, slot_stride, shard_stride, flags_offset, buffer_bytes)
+    of the two-shot GEMM push (mx_push2_layout)."""
+    lib = load()
+    v = [c_i64() for _ in range(5)]
+    check(lib.mx_push2_layout(n, ctypes.byref(cs), nranks, *[ctypes.byref(x) for x in v]),
+          "mx_push2_layout")
     return tuple(x.value for x in v)
 
 

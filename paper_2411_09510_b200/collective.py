@@ -521,6 +521,12 @@ class FusedLinearAllReduce:
     memory in rank order, with the optional residual add fused into its
     store.  Bit-identical to ``CompressedAllReduce.linear``
     (NCCL one-shot) on the same operands.  No NCCL kernel, no gather copy.
+    ``algo="twoshot"`` (TP >= 4): the epilogue scatters chunk j of the shard
+    to rank j only (the reduce-scatter leg rides on the GEMM); a requantise
+    launch sums this rank's chunk over the N senders in rank order,
+    re-quantises it and pushes it into every rank (the all-gather leg); the
+    decode launch decodes every owner's chunk -- bit-identical to the NCCL
+    two-shot (n % (1024 * world) == 0).
     Requirements: fp4_e2m1 E8M0 with B in {16, 32}; bf16 x [M, K] and
     W [N, K] contiguous, N % 256 == 0, K % 64 == 0, n = M*N % 1024 == 0;
     at most 8 ranks.  Slots alternate by epoch parity, which is safe because a
@@ -528,7 +534,8 @@ class FusedLinearAllReduce:
     i.e. after every peer finished reading slot (e & 1) in call e-2.
     """
 
-    def __init__(self, scheme, n: int, group=None, out_dtype=None, device=None):
+    def __init__(self, scheme, n: int, group=None, out_dtype=None, device=None,
+                 algo: str = "oneshot"):
         import torch
         import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm_mem
@@ -545,8 +552,15 @@ class FusedLinearAllReduce:
             "cuda", torch.cuda.current_device())
         self.out_dtype = out_dtype or torch.bfloat16
         self.backend = NativeBackend(scheme)
-        self.slot, self.shard_stride, flags_off, total = _native.push_layout(
-            self.n, self.backend.cs, self.world)
+        if algo not in ("oneshot", "twoshot"):
+            raise ValueError("algo must be 'oneshot' or 'twoshot'")
+        self.algo = algo
+        if algo == "oneshot":
+            self.slot, self.shard_stride, flags_off, total = _native.push_layout(
+                self.n, self.backend.cs, self.world)
+        else:
+            _c, self.slot, self.shard_stride, flags_off, total = _native.push2_layout(
+                self.n, self.backend.cs, self.world)
         self.buf = symm_mem.empty(total, dtype=torch.uint8, device=self.device)
         self.hdl = symm_mem.rendezvous(self.buf, self.group)
         self.buf[flags_off:].zero_()  # flags start at zero before anyone can signal
@@ -569,6 +583,7 @@ class FusedLinearAllReduce:
         sch = self.scheme
         return (sch.element.name == "fp4_e2m1" and sch.scale.exponent_bits == 8
                 and sch.block_size in (16, 32) and x.dtype == torch.bfloat16
+                and (self.algo == "oneshot" or self.n % (1024 * self.world) == 0)
                 and w.dtype == torch.bfloat16 and w.dim() == 2 and x.shape[-1] == w.shape[1]
                 and w.shape[0] % 256 == 0 and x.shape[-1] % 64 == 0 and self.n % 1024 == 0
                 and x.is_contiguous() and w.is_contiguous()
@@ -591,6 +606,21 @@ class FusedLinearAllReduce:
         be = self.backend
         P = ctypes.c_void_p
         base = self.state.data_ptr()
+        res = P(residual.data_ptr()) if residual is not None else None
+        if self.algo == "twoshot":
+            _native.check(be.lib.mx_gemm_reducescatter_push(
+                P(x.data_ptr()), P(weight.data_ptr()), M, N, K, ctypes.byref(be.cs),
+                P(self.buf_ptrs.data_ptr()), self.rank, self.world, P(base + 4),
+                P(self.flag.data_ptr()), be._st()), "mx_gemm_reducescatter_push")
+            _native.check(be.lib.mx_push2_requant(
+                P(self.buf.data_ptr()), self.n, ctypes.byref(be.cs), self.rank, self.world,
+                P(self.buf_ptrs.data_ptr()), P(self.flag_ptrs.data_ptr()), P(base + 4), P(base),
+                P(self.flag.data_ptr()), be._st()), "mx_push2_requant")
+            _native.check(be.lib.mx_push2_decode(
+                P(self.buf.data_ptr()), self.n, ctypes.byref(be.cs), self.rank, self.world,
+                P(self.flag_ptrs.data_ptr()), P(base + 4), P(base), P(o.data_ptr()), be._dt(o),
+                res, be._st()), "mx_push2_decode")
+            return o.view(*x.shape[:-1], N)
         _native.check(be.lib.mx_gemm_allgather_push(
             P(x.data_ptr()), P(weight.data_ptr()), M, N, K, ctypes.byref(be.cs),
             P(self.buf_ptrs.data_ptr()), self.rank, self.world,

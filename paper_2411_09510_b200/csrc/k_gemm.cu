@@ -148,6 +148,8 @@ struct GArgs {
   // epoch (the decode launch publishes it, k_push.cu)
   uint8_t* const* push_peers;       // device [npush]: peer buffer bases
   int npush, push_rank;
+  int push_scatter;                 // 1: chunk j (cv values) goes to rank j only (two-shot
+                                    // reduce-scatter leg); 0: the whole shard to every rank
   int64_t push_slot_stride;         // bytes per slot (npush shards)
   int64_t push_off;                 // this rank's shard inside a slot
   int64_t push_scale_off, push_elem_off;  // shard layout
@@ -236,8 +238,26 @@ __device__ __forceinline__ void epi_chunk(const GArgs& A, const Fmt& f, const ui
     bool bad;
     LaneCodes<BITS> cw = quant_lane<__nv_bfloat16, B, ENC, BITS>(raw, f, stored, bad);
     if (bad) report_nonfinite_raw<__nv_bfloat16>(raw, kVPL, flat, A.nonfinite);
-    if constexpr (PUSH) {  // one tensor, E8M0: the same bytes to every rank
+    if constexpr (PUSH) {  // E8M0 FP4: the shard (or chunk j of it) to the ranks
       static_assert(BITS == 4, "push: FP4 codes");
+      if (A.push_scatter) {  // two-shot: a 32-value group never straddles a chunk
+        const int64_t j = flat / A.cv, local = flat - j * A.cv;
+        uint8_t* base = pdst[j];
+        asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(
+                         base + A.push_elem_off + local / 2),
+                     "r"(cw.w[0]), "r"(cw.w[1]), "r"(cw.w[2]), "r"(cw.w[3])
+                     : "memory");
+        if constexpr (NSB == 2) {
+          asm volatile("st.global.u16 [%0], %1;" ::"l"(base + A.push_scale_off + local / B),
+                       "h"((uint16_t)(stored[0] | (stored[1] << 8)))
+                       : "memory");
+        } else {
+          asm volatile("st.global.u8 [%0], %1;" ::"l"(base + A.push_scale_off + local / B),
+                       "h"((uint16_t)stored[0])
+                       : "memory");
+        }
+        return;
+      }
       const int64_t eo = A.push_elem_off + flat / 2, so = A.push_scale_off + flat / B;
 #pragma unroll 1
       for (int j = 0; j < A.npush; ++j) {
@@ -934,9 +954,10 @@ cudaError_t launch_gemm_mx(const void* x, const void* w, int64_t M, int64_t N, i
 // cudaErrorNotSupported outside it.
 cudaError_t launch_gemm_mx_push(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
                                 const Fmt* fmt, int enc_id, uint8_t* const* peers, int npush,
-                                int rank, int64_t slot_stride, int64_t shard_stride,
-                                int64_t scale_off, int64_t elem_off, unsigned int* state,
-                                unsigned long long* nonfinite, cudaStream_t st) {
+                                int rank, int64_t slot_stride, int64_t push_off,
+                                int64_t scale_off, int64_t elem_off, int64_t scatter_chunk,
+                                unsigned int* state, unsigned long long* nonfinite,
+                                cudaStream_t st) {
   using namespace gm;
   static const int two = env_int("MXB200_GEMM_2CTA", 1);
   if (!two || !fmt || M < 1 || N < 256 || N % 256 != 0 || K < BK || K % BK != 0)
@@ -949,11 +970,14 @@ cudaError_t launch_gemm_mx_push(const void* x, const void* w, int64_t M, int64_t
   GArgs a;
   memset(&a, 0, sizeof(a));
   a.M = M; a.N = N; a.K = K;
-  a.cv = M * N; a.chunk_stride = 0;
+  a.cv = scatter_chunk > 0 ? scatter_chunk : M * N; a.chunk_stride = 0;
+  if (scatter_chunk > 0 && (scatter_chunk % 32 != 0 || scatter_chunk * npush != M * N))
+    return cudaErrorNotSupported;
+  a.push_scatter = scatter_chunk > 0;
   a.nonfinite = nonfinite;
   a.f = *fmt;
   a.push_peers = peers; a.npush = npush; a.push_rank = rank;
-  a.push_slot_stride = slot_stride; a.push_off = (int64_t)rank * shard_stride;
+  a.push_slot_stride = slot_stride; a.push_off = push_off;
   a.push_scale_off = scale_off; a.push_elem_off = elem_off; a.push_state = state;
   if (fmt->block == 32) return go_2cta<256, 8, 1, 32, ENC_E2M1, 4, 8, true>(a, x, w, st);
   return go_2cta<256, 8, 1, 16, ENC_E2M1, 4, 8, true>(a, x, w, st);

@@ -79,6 +79,127 @@ __global__ void __launch_bounds__(kLeanThreads2, 8) k_push_dqsum(const PArgs P) 
                                         : nullptr);
 }
 
+// publish this rank's epoch into flag [idx] of every rank (CTA 0, thread 0:
+// one system fence, cumulative over the previous launches' stores), then
+// wait (threads < nranks) until flag [base + j] >= epoch for every j
+__device__ __forceinline__ void publish_and_wait(unsigned int* const* peer_flags, int idx,
+                                                 const unsigned int* flags, int base, int nr,
+                                                 unsigned int e, unsigned int* status,
+                                                 unsigned long long timeout_ns) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    for (int j = 0; j < nr; ++j)
+      asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(peer_flags[j] + idx), "r"(e)
+                   : "memory");
+  }
+  if ((int)threadIdx.x < nr) {
+    const unsigned int* fl = flags + base + threadIdx.x;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while ((int)(ld_acquire_sys_u32(fl) - e) < 0) {
+      __nanosleep(64);
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        atomicExch(status, 1u);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// reduce-scatter leg done everywhere -> this rank's chunk: N shards decoded
+// in rank order, fp32 sum from +0.0, re-quantised (K3's arithmetic) and
+// pushed into every rank's all-gather region
+template <int B>
+__global__ void __launch_bounds__(kLeanThreads2) k_push2_requant(const P2Args P) {
+  constexpr int BITS = 4;
+  constexpr int NSB = Geo<B>::NSB;
+  using RL = RankLoad<B, BITS, kVPL>;
+  pdl_prologue();
+  __shared__ unsigned int s_e;
+  if (threadIdx.x == 0) s_e = *reinterpret_cast<const volatile unsigned int*>(P.state);
+  __syncthreads();
+  const unsigned int e = s_e;
+  const int nr = P.nranks;
+  publish_and_wait(P.peer_flags, P.rank, P.flags, 0, nr, e, P.status, P.timeout_ns);
+  const int lane = threadIdx.x & 31;
+  const uint32_t q = blockIdx.x * kLeanWarps2 + (threadIdx.x >> 5);
+  if (q >= (uint32_t)(P.c / kUnit)) return;
+  const int64_t slot = (int64_t)(e & 1u) * P.slot_stride;
+  const uint8_t* rs = P.buf + slot;
+  const Fmt f = P.f;
+  float acc[kVPL];
+#pragma unroll
+  for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // +0.0 (mx/netbench.py:332)
+  for (int r = 0; r < nr; r += 2) {
+    RL x0, x1;
+    load_rank<B, BITS, kVPL, true>(x0, rs + (int64_t)r * P.shard_stride, P.scale_off, P.elem_off,
+                                   (int64_t)q * kUnit, lane, kVPL, 8);
+    if (r + 1 < nr)
+      load_rank<B, BITS, kVPL, true>(x1, rs + (int64_t)(r + 1) * P.shard_stride, P.scale_off,
+                                     P.elem_off, (int64_t)q * kUnit, lane, kVPL, 8);
+    decode_rank<B, ENC_E2M1, BITS, kVPL>(x0, f, acc, false, nullptr);
+    if (r + 1 < nr) decode_rank<B, ENC_E2M1, BITS, kVPL>(x1, f, acc, false, nullptr);
+  }
+  Raw<float> raw;
+#pragma unroll
+  for (int i = 0; i < kVPL; ++i) raw.w[i] = __float_as_uint(acc[i]);
+  int stored[NSB];
+  bool bad;
+  LaneCodes<BITS> cc = quant_lane<float, B, ENC_E2M1, BITS>(raw, f, stored, bad);
+  if (bad)
+    report_nonfinite_raw<float>(raw, kVPL, (int64_t)P.rank * P.c + (int64_t)q * kUnit + lane * kVPL,
+                                P.nonfinite);
+  const int64_t ag = slot + (int64_t)nr * P.shard_stride + (int64_t)P.rank * P.shard_stride;
+  for (int j = 0; j < nr; ++j) {
+    uint8_t* dst = P.peer_bufs[j] + ag;
+    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(
+                     dst + P.elem_off + (int64_t)q * (kUnit / 2) + lane * 16),
+                 "r"(cc.w[0]), "r"(cc.w[1]), "r"(cc.w[2]), "r"(cc.w[3])
+                 : "memory");
+    uint8_t* sp = dst + P.scale_off + (int64_t)q * (kUnit / B) + lane * NSB;
+    if constexpr (NSB == 2)
+      asm volatile("st.global.u16 [%0], %1;" ::"l"(sp), "h"((uint16_t)(stored[0] | (stored[1] << 8)))
+                   : "memory");
+    else
+      asm volatile("st.global.u8 [%0], %1;" ::"l"(sp), "h"((uint16_t)stored[0]) : "memory");
+  }
+}
+
+// all-gather leg done everywhere -> decode every owner's reduced chunk
+template <typename OutT, int B>
+__global__ void __launch_bounds__(kLeanThreads2, 8) k_push2_decode(const P2Args P) {
+  constexpr int BITS = 4;
+  using RL = RankLoad<B, BITS, kVPL>;
+  pdl_prologue();
+  __shared__ unsigned int s_e;
+  if (threadIdx.x == 0) s_e = *reinterpret_cast<const volatile unsigned int*>(P.state);
+  __syncthreads();
+  const unsigned int e = s_e;
+  const int nr = P.nranks;
+  publish_and_wait(P.peer_flags, nr + P.rank, P.flags, nr, nr, e, P.status, P.timeout_ns);
+  const int lane = threadIdx.x & 31;
+  const uint32_t u = blockIdx.x * kLeanWarps2 + (threadIdx.x >> 5);
+  if (u >= (uint32_t)(P.n / kUnit)) return;
+  const uint32_t upc = (uint32_t)(P.c / kUnit);
+  const uint32_t j = u / upc, q = u - j * upc;
+  const uint8_t* base = P.buf + (int64_t)(e & 1u) * P.slot_stride +
+                        (int64_t)(nr + (int)j) * P.shard_stride;
+  RL x;
+  load_rank<B, BITS, kVPL, true>(x, base, P.scale_off, P.elem_off, (int64_t)q * kUnit, lane, kVPL,
+                                 8);
+  float acc[kVPL];
+#pragma unroll
+  for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // K2's two-shot final decode: from +0.0
+  decode_rank<B, ENC_E2M1, BITS, kVPL>(x, P.f, acc, false, nullptr);
+  const size_t o = (size_t)u * kUnit + lane * kVPL;
+  store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(P.out) + o, kVPL, acc,
+                             P.residual ? reinterpret_cast<const OutT*>(P.residual) + o
+                                        : nullptr);
+}
+
 template <typename OutT>
 bool go(const PArgs& a, int block, cudaStream_t st) {
   const dim3 grid((unsigned)((a.n / kUnit + kLeanWarps2 - 1) / kLeanWarps2));
@@ -96,6 +217,27 @@ bool go(const PArgs& a, int block, cudaStream_t st) {
 
 bool launch_push_dqsum(const PArgs& a, int out_is_bf16, int block, cudaStream_t st) {
   return out_is_bf16 ? go<__nv_bfloat16>(a, block, st) : go<float>(a, block, st);
+}
+
+bool launch_push2_requant(const P2Args& a, int block, cudaStream_t st) {
+  const dim3 grid((unsigned)((a.c / kUnit + kLeanWarps2 - 1) / kLeanWarps2));
+  if (block == 32) launch_pdl(k_push2_requant<32>, grid, dim3(kLeanThreads2), 0, st, a);
+  else if (block == 16) launch_pdl(k_push2_requant<16>, grid, dim3(kLeanThreads2), 0, st, a);
+  else return false;
+  return true;
+}
+
+bool launch_push2_decode(const P2Args& a, int out_is_bf16, int block, cudaStream_t st) {
+  const dim3 grid((unsigned)((a.n / kUnit + kLeanWarps2 - 1) / kLeanWarps2));
+  if (block != 16 && block != 32) return false;
+  if (out_is_bf16) {
+    if (block == 32) launch_pdl(k_push2_decode<__nv_bfloat16, 32>, grid, dim3(kLeanThreads2), 0, st, a);
+    else launch_pdl(k_push2_decode<__nv_bfloat16, 16>, grid, dim3(kLeanThreads2), 0, st, a);
+  } else {
+    if (block == 32) launch_pdl(k_push2_decode<float, 32>, grid, dim3(kLeanThreads2), 0, st, a);
+    else launch_pdl(k_push2_decode<float, 16>, grid, dim3(kLeanThreads2), 0, st, a);
+  }
+  return true;
 }
 
 }  // namespace mxb

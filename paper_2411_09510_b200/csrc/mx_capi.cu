@@ -253,9 +253,10 @@ cudaError_t launch_gemm_mx(const void* x, const void* w, int64_t M, int64_t N, i
 int64_t gemm_workspace_bytes(int64_t M, int64_t N);
 cudaError_t launch_gemm_mx_push(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
                                 const Fmt* fmt, int enc_id, uint8_t* const* peers, int npush,
-                                int rank, int64_t slot_stride, int64_t shard_stride,
-                                int64_t scale_off, int64_t elem_off, unsigned int* state,
-                                unsigned long long* nonfinite, cudaStream_t st);
+                                int rank, int64_t slot_stride, int64_t push_off,
+                                int64_t scale_off, int64_t elem_off, int64_t scatter_chunk,
+                                unsigned int* state, unsigned long long* nonfinite,
+                                cudaStream_t st);
 
 }  // namespace mxb
 
@@ -810,7 +811,7 @@ int mx_gemm_allgather_push(const void* x, const void* w, int64_t M, int64_t N, i
   mx_shard_layout(M * N, s, &so, &eo, &sbytes);
   Fmt f = make_fmt(s);
   cudaError_t e = launch_gemm_mx_push(x, w, M, N, K, &f, enc_of(s), peer_bufs, nranks,
-                                      rank, slot, sb, so, eo,
+                                      rank, slot, (int64_t)rank * sb, so, eo, 0,
                                       reinterpret_cast<unsigned int*>(state),
                                       reinterpret_cast<unsigned long long*>(nonfinite),
                                       (cudaStream_t)stream);
@@ -851,6 +852,109 @@ int mx_push_dequant_sum(const uint8_t* buf, int64_t n, const mx_scheme_t* s, int
   if (!launch_push_dqsum(a, out_dtype == MX_BF16, (int)s->block_size, (cudaStream_t)stream))
     return fail(MX_ERR_UNSUPPORTED, "push decode: B in {16, 32}");
   return cuda_check("k_push_dqsum");
+}
+
+int mx_push2_layout(int64_t n, const mx_scheme_t* s, int32_t nranks, int64_t* chunk_values,
+                    int64_t* slot_stride, int64_t* shard_stride, int64_t* flags_offset,
+                    int64_t* buffer_bytes) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (n <= 0 || nranks < 1 || n % (1024 * (int64_t)nranks) != 0)
+    return fail(MX_ERR_UNSUPPORTED, "two-shot push: n %% (1024 * nranks) == 0");
+  const int64_t c = n / nranks;
+  int64_t so, eo, sb;
+  mx_shard_layout(c, s, &so, &eo, &sb);
+  const int64_t slot = 2 * (int64_t)nranks * sb;  // RS region, then AG region
+  const int64_t foff = (2 * slot + 255) / 256 * 256;
+  if (chunk_values) *chunk_values = c;
+  if (slot_stride) *slot_stride = slot;
+  if (shard_stride) *shard_stride = sb;
+  if (flags_offset) *flags_offset = foff;
+  if (buffer_bytes) *buffer_bytes = foff + ((int64_t)nranks * 8 + 255) / 256 * 256;
+  return MX_OK;
+}
+
+int mx_gemm_reducescatter_push(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
+                               const mx_scheme_t* s, uint8_t* const* peer_bufs, int32_t rank,
+                               int32_t nranks, uint32_t* state, uint64_t* nonfinite,
+                               void* stream) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (!x || !w || !peer_bufs || !state) return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (M < 1 || N < 1 || K < 1 || rank < 0 || rank >= nranks)
+    return fail(MX_ERR_INVALID_ARGUMENT, "bad sizes");
+  int64_t c, slot, sb, foff, total, so, eo, sbytes;
+  rc = mx_push2_layout(M * N, s, nranks, &c, &slot, &sb, &foff, &total);
+  if (rc) return rc;
+  mx_shard_layout(c, s, &so, &eo, &sbytes);
+  Fmt f = make_fmt(s);
+  cudaError_t e = launch_gemm_mx_push(x, w, M, N, K, &f, enc_of(s), peer_bufs, nranks, rank,
+                                      slot, (int64_t)rank * sb, so, eo, c,
+                                      reinterpret_cast<unsigned int*>(state),
+                                      reinterpret_cast<unsigned long long*>(nonfinite),
+                                      (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported)
+    return fail(MX_ERR_UNSUPPORTED,
+                "GEMM + reduce-scatter push: fp4_e2m1 E8M0 with B in {16, 32}, N %% 256 == 0, "
+                "K %% 64 == 0, M*N %% (1024 * nranks) == 0, at most 8 ranks");
+  if (e != cudaSuccess) return fail(MX_ERR_CUDA, "k_gemm_mx2 push: %s", cudaGetErrorString(e));
+  return cuda_check("k_gemm_mx2 reduce-scatter push");
+}
+
+static int push2_args(P2Args& a, const uint8_t* buf, int64_t n, const mx_scheme_t* s,
+                      int32_t rank, int32_t nranks, uint8_t* const* peer_bufs,
+                      uint32_t* const* peer_flags, const uint32_t* state, uint32_t* status) {
+  int rc = check_scheme(s);
+  if (rc) return rc;
+  if (!buf || !peer_flags || !state || !status || rank < 0 || rank >= nranks || nranks > 8)
+    return fail(MX_ERR_INVALID_ARGUMENT, "bad buffers or ranks");
+  Fmt f = make_fmt(s);
+  if (f.kbits != 8 || f.bits != 4 || enc_of(s) != ENC_E2M1)
+    return fail(MX_ERR_UNSUPPORTED, "two-shot push: fp4_e2m1 E8M0");
+  int64_t c, slot, sb, foff, total, so, eo, sbytes;
+  rc = mx_push2_layout(n, s, nranks, &c, &slot, &sb, &foff, &total);
+  if (rc) return rc;
+  mx_shard_layout(c, s, &so, &eo, &sbytes);
+  a.buf = buf; a.slot_stride = slot; a.shard_stride = sb; a.scale_off = so; a.elem_off = eo;
+  a.nranks = nranks; a.rank = rank; a.n = n; a.c = c;
+  a.peer_bufs = peer_bufs;
+  a.peer_flags = reinterpret_cast<unsigned int* const*>(peer_flags);
+  a.flags = reinterpret_cast<const unsigned int*>(buf + foff);
+  a.state = reinterpret_cast<const unsigned int*>(state);
+  a.status = reinterpret_cast<unsigned int*>(status);
+  a.timeout_ns = symm_timeout_ns();
+  a.nonfinite = nullptr; a.out = nullptr; a.residual = nullptr;
+  a.f = f;
+  return MX_OK;
+}
+
+int mx_push2_requant(const uint8_t* buf, int64_t n, const mx_scheme_t* s, int32_t rank,
+                     int32_t nranks, uint8_t* const* peer_bufs, uint32_t* const* peer_flags,
+                     const uint32_t* state, uint32_t* status, uint64_t* nonfinite, void* stream) {
+  P2Args a;
+  int rc = push2_args(a, buf, n, s, rank, nranks, peer_bufs, peer_flags, state, status);
+  if (rc) return rc;
+  if (!peer_bufs) return fail(MX_ERR_INVALID_ARGUMENT, "NULL peer buffers");
+  a.nonfinite = reinterpret_cast<unsigned long long*>(nonfinite);
+  if (!launch_push2_requant(a, (int)s->block_size, (cudaStream_t)stream))
+    return fail(MX_ERR_UNSUPPORTED, "two-shot push: B in {16, 32}");
+  return cuda_check("k_push2_requant");
+}
+
+int mx_push2_decode(const uint8_t* buf, int64_t n, const mx_scheme_t* s, int32_t rank,
+                    int32_t nranks, uint32_t* const* peer_flags, const uint32_t* state,
+                    uint32_t* status, void* out, int32_t out_dtype, const void* residual,
+                    void* stream) {
+  P2Args a;
+  int rc = push2_args(a, buf, n, s, rank, nranks, nullptr, peer_flags, state, status);
+  if (rc) return rc;
+  if (!out || (out_dtype != MX_BF16 && out_dtype != MX_F32) || !aligned(out, 32) ||
+      !aligned(residual, 32))
+    return fail(MX_ERR_UNSUPPORTED, "two-shot push decode: bf16/f32 out, 32-B aligned");
+  a.out = out; a.residual = residual;
+  if (!launch_push2_decode(a, out_dtype == MX_BF16, (int)s->block_size, (cudaStream_t)stream))
+    return fail(MX_ERR_UNSUPPORTED, "two-shot push: B in {16, 32}");
+  return cuda_check("k_push2_decode");
 }
 
 int mx_symm_layout(int64_t n, const mx_scheme_t* s, int32_t nranks, int64_t* slot_stride,

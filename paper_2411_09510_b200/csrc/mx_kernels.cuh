@@ -1433,6 +1433,29 @@ struct PArgs {
   Fmt f;
 };
 bool launch_push_dqsum(const PArgs& a, int out_is_bf16, int block, cudaStream_t st);
+// two-shot push (k_push.cu): the GEMM scatters chunk j of its shard to rank
+// j (reduce-scatter leg), k_push2_requant sums + requantises this rank's
+// chunk and pushes it to every rank (all-gather leg), k_push2_decode decodes
+struct P2Args {
+  const uint8_t* buf;            // this rank's symmetric buffer base
+  int64_t slot_stride;           // 2 x nranks chunk shards (RS region, then AG region)
+  int64_t shard_stride;          // one chunk shard (c values)
+  int64_t scale_off, elem_off;   // chunk shard layout
+  int nranks, rank;
+  int64_t n, c;                  // c = n / nranks, multiple of 1024
+  uint8_t* const* peer_bufs;     // device [nranks]: every rank's buffer base
+  unsigned int* const* peer_flags;  // device [nranks]: flag arrays (RS [nranks], AG [nranks])
+  const unsigned int* flags;     // this rank's flag array
+  const unsigned int* state;     // local [0]: this call's epoch (set by this rank's GEMM)
+  unsigned int* status;
+  unsigned long long timeout_ns;
+  unsigned long long* nonfinite;
+  void* out;
+  const void* residual;
+  Fmt f;
+};
+bool launch_push2_requant(const P2Args& a, int block, cudaStream_t st);
+bool launch_push2_decode(const P2Args& a, int out_is_bf16, int block, cudaStream_t st);
 
 // two-shot over symmetric memory (k_fused.cuh, k_symm2_flow)
 struct S2Args {

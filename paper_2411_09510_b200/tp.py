@@ -493,13 +493,17 @@ def make_module_classes():
             return car(y.contiguous(), residual=residual.contiguous())
 
         def _push(self, n, dtype, device):
+            import torch.distributed as dist
+
             from .collective import FusedLinearAllReduce
 
             key = (id(self.group), str(self.scheme), n, dtype)
             fl = _PUSH_CACHE.get(key)
             if fl is None:
+                ws = dist.get_world_size(self.group)
+                algo = "oneshot" if ws <= 2 or n % (1024 * ws) else "twoshot"
                 fl = FusedLinearAllReduce(self.scheme, n, group=self.group, out_dtype=dtype,
-                                          device=device)
+                                          device=device, algo=algo)
                 _PUSH_CACHE[key] = fl
             self._car[("push",) + key] = fl
             return fl
@@ -509,8 +513,9 @@ def make_module_classes():
             the Llama block's residual update -- with the add fused into the
             compressed collective's dequant-sum store (the bf16 NCCL path
             adds after the all-reduce; identical bits either way).
-            ``algo="push"``: the GEMM, the quantiser and the all-gather in
-            one kernel (FusedLinearAllReduce), K5 where it does not apply."""
+            ``algo="push"``: the GEMM, the quantiser and the all-gather
+            (one-shot to TP=2) or the reduce-scatter leg (two-shot beyond)
+            in one kernel (FusedLinearAllReduce), K5 where it does not apply."""
             if self.scheme is not None and self.algo == "push":
                 n = x.numel() // x.shape[-1] * self.weight.shape[0]
                 fl = self._push(n, x.dtype, x.device)

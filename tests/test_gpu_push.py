@@ -164,3 +164,72 @@ def test_row_parallel_push_equals_oneshot(pg):
     assert torch.equal(a, b)
     assert torch.equal(push(x).clone(), one(x).clone())
     tp._PUSH_CACHE.clear()
+
+
+@pytest.mark.parametrize("spec", [SPEC, "fp4_e2m1:16:e8m0"])
+def test_push_twoshot_world1_equals_nccl_twoshot(pg, spec):
+    from paper_2411_09510_b200.collective import CompressedAllReduce, FusedLinearAllReduce
+
+    M, N, K = 512, 1024, 256
+    fl = FusedLinearAllReduce(spec, M * N, algo="twoshot")
+    car = CompressedAllReduce(spec, M * N, algo="twoshot", out_dtype=torch.bfloat16)
+    for it in range(5):
+        x, w = operands(M, N, K, seed=300 + it)
+        got = fl.linear(x, w).clone()
+        want = car.linear(x, w).clone()
+        h = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+        got_r = fl.linear(x, w, residual=h).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(got.view(-1), want.view(-1)), it
+        assert torch.equal(got_r, h + want), it
+    fl.check_status()
+
+
+@pytest.mark.parametrize("nranks", [2, 4, 8])
+def test_push_twoshot_multirank_one_device(nranks):
+    """Two-shot push with N concurrent ranks on one device == the oracle's
+    two-shot (reduce-scatter, fp32 sum, requantise, all-gather)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2411_09510_b200 import _native
+    from paper_2411_09510_b200.formats import parse_scheme
+
+    lib = _native.load()
+    cs = parse_scheme(SPEC).to_c()
+    M, N, K = 256, 512, 256
+    n = M * N
+    c, slot, shard, foff, total = _native.push2_layout(n, cs, nranks)
+    bufs = [torch.zeros(total, dtype=torch.uint8, device="cuda") for _ in range(nranks)]
+    bptr = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    fptr = torch.tensor([b.data_ptr() + foff for b in bufs], dtype=torch.int64, device="cuda")
+    state = [torch.zeros(4, dtype=torch.int32, device="cuda") for _ in range(nranks)]
+    nf = [torch.full((1,), -1, dtype=torch.int64, device="cuda") for _ in range(nranks)]
+    outs = [torch.empty(n, dtype=torch.bfloat16, device="cuda") for _ in range(nranks)]
+    streams = [torch.cuda.Stream() for _ in range(nranks)]
+    P = ctypes.c_void_p
+    for call in range(3):
+        ops = [operands(M, N, K, seed=2000 * call + r) for r in range(nranks)]
+        parts = [_plain_partial(lib, x, w) for x, w in ops]
+        torch.cuda.synchronize()
+        host = [p.float().cpu().numpy().ravel().astype(np.float64) for p in parts]
+        want = torch.from_numpy(O.allreduce_twoshot(host, O.scheme(SPEC))).to(torch.bfloat16)
+        for r in range(nranks):
+            x, w = ops[r]
+            _native.check(lib.mx_gemm_reducescatter_push(
+                P(x.data_ptr()), P(w.data_ptr()), M, N, K, ctypes.byref(cs), P(bptr.data_ptr()),
+                r, nranks, P(state[r].data_ptr() + 4), P(nf[r].data_ptr()),
+                P(streams[r].cuda_stream)), "mx_gemm_reducescatter_push")
+        for r in range(nranks):
+            _native.check(lib.mx_push2_requant(
+                P(bufs[r].data_ptr()), n, ctypes.byref(cs), r, nranks, P(bptr.data_ptr()),
+                P(fptr.data_ptr()), P(state[r].data_ptr() + 4), P(state[r].data_ptr()),
+                P(nf[r].data_ptr()), P(streams[r].cuda_stream)), "mx_push2_requant")
+        for r in range(nranks):
+            _native.check(lib.mx_push2_decode(
+                P(bufs[r].data_ptr()), n, ctypes.byref(cs), r, nranks, P(fptr.data_ptr()),
+                P(state[r].data_ptr() + 4), P(state[r].data_ptr()), P(outs[r].data_ptr()),
+                _native.MX_BF16, None, P(streams[r].cuda_stream)), "mx_push2_decode")
+        torch.cuda.synchronize()
+        for r in range(nranks):
+            assert int(state[r][0].item()) == 0, "peer wait timed out"
+            assert torch.equal(outs[r].cpu(), want), (nranks, call, r)

@@ -280,7 +280,9 @@ int mx_pack_codes(const uint8_t* codes, int64_t count, int32_t width, uint8_t* p
  * rank (two slots of nranks shards, then nranks u32 flags, zeroed once);
  * state: 2 local u32 zeroed once ([0] epoch, [1] CTA counter); status: one
  * local u32 (1 = a peer wait timed out after MXB200_SYMM_TIMEOUT_MS).
- * fp4_e2m1 E8M0, B in {16, 32}, N % 256 == 0, at most 8 ranks. */
+ * The push set: fp4_e2m1 E8M0 with B in {16, 32}, and the paper's E5M0
+ * schemes -- fp4_e2m1 with B in {8, 16, 32}, fp5_e2m2 with B = 32; N % 256
+ * == 0, at most 8 ranks (MX_ERR_UNSUPPORTED outside it). */
 int mx_push_layout(int64_t n, const mx_scheme_t* scheme, int32_t nranks, int64_t* slot_stride,
                    int64_t* shard_stride, int64_t* flags_offset, int64_t* buffer_bytes);
 int mx_gemm_allgather_push(const void* x, const void* w, int64_t M, int64_t N, int64_t K,

@@ -238,41 +238,34 @@ __device__ __forceinline__ void epi_chunk(const GArgs& A, const Fmt& f, const ui
     bool bad;
     LaneCodes<BITS> cw = quant_lane<__nv_bfloat16, B, ENC, BITS>(raw, f, stored, bad);
     if (bad) report_nonfinite_raw<__nv_bfloat16>(raw, kVPL, flat, A.nonfinite);
-    if constexpr (PUSH) {  // E8M0 FP4: the shard (or chunk j of it) to the ranks
-      static_assert(BITS == 4, "push: FP4 codes");
-      if (A.push_scatter) {  // two-shot: a 32-value group never straddles a chunk
-        const int64_t j = flat / A.cv, local = flat - j * A.cv;
-        uint8_t* base = pdst[j];
-        asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(
-                         base + A.push_elem_off + local / 2),
-                     "r"(cw.w[0]), "r"(cw.w[1]), "r"(cw.w[2]), "r"(cw.w[3])
-                     : "memory");
-        if constexpr (NSB == 2) {
-          asm volatile("st.global.u16 [%0], %1;" ::"l"(base + A.push_scale_off + local / B),
-                       "h"((uint16_t)(stored[0] | (stored[1] << 8)))
-                       : "memory");
-        } else {
-          asm volatile("st.global.u8 [%0], %1;" ::"l"(base + A.push_scale_off + local / B),
-                       "h"((uint16_t)stored[0])
-                       : "memory");
+    if constexpr (PUSH) {  // the shard (or chunk j of it) to the ranks
+      // two-shot: a 32-value group (an 8-block scale group) never straddles
+      // a chunk; KB < 8: the scale codes go back to the caller, which packs
+      // and pushes whole groups
+      auto put = [&](uint8_t* base, int64_t v) {
+        store_lane_codes<BITS>(base + A.push_elem_off + v / 8 * BITS, cw, kVPL);
+        if constexpr (KB == 8) {
+          uint8_t* sp = base + A.push_scale_off + v / B;
+          if constexpr (NSB == 4)
+            *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
+                                               ((uint32_t)stored[2] << 16) |
+                                               ((uint32_t)stored[3] << 24);
+          else if constexpr (NSB == 2)
+            *reinterpret_cast<uint16_t*>(sp) = (uint16_t)(stored[0] | (stored[1] << 8));
+          else
+            *sp = (uint8_t)stored[0];
         }
-        return;
-      }
-      const int64_t eo = A.push_elem_off + flat / 2, so = A.push_scale_off + flat / B;
+      };
+      if (A.push_scatter) {
+        const int64_t j = flat / A.cv;
+        put(pdst[j], flat - j * A.cv);
+      } else {
 #pragma unroll 1
-      for (int j = 0; j < A.npush; ++j) {
-        uint8_t* base = pdst[j];
-        asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(base + eo), "r"(cw.w[0]),
-                     "r"(cw.w[1]), "r"(cw.w[2]), "r"(cw.w[3])
-                     : "memory");
-        if constexpr (NSB == 2) {
-          asm volatile("st.global.u16 [%0], %1;" ::"l"(base + so),
-                       "h"((uint16_t)(stored[0] | (stored[1] << 8)))
-                       : "memory");
-        } else {
-          asm volatile("st.global.u8 [%0], %1;" ::"l"(base + so), "h"((uint16_t)stored[0])
-                       : "memory");
-        }
+        for (int j = 0; j < A.npush; ++j) put(pdst[j], flat);
+      }
+      if constexpr (KB != 8) {
+#pragma unroll
+        for (int sb = 0; sb < NSB; ++sb) stored_out[sb] = stored[sb];
       }
       return;
     }
@@ -697,8 +690,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm_threads<EPI>(),
         tmem_ld32(taddr + 32 * c, v);
         tmem_ld_wait();
         const int64_t flat = row * N + (int64_t)nb * BN + 32 * c;
-        if constexpr (PUSH) {
+        if constexpr (PUSH && KB == 8) {
           if (live) epi_chunk<MODE, B, ENC, BITS, 8, true>(A, f, v, flat, nullptr, s_dst);
+        } else if constexpr (PUSH) {  // E5M0 push: whole groups, to every destination
+          constexpr int NSB = Geo<B>::NSB;
+          if (live) {
+            int st[NSB];
+            epi_chunk<MODE, B, ENC, BITS, KB, true>(A, f, v, flat, st, s_dst);
+#pragma unroll
+            for (int sb = 0; sb < NSB; ++sb) pk |= (uint64_t)st[sb] << ((nbk + sb) * KB);
+            nbk += NSB;
+            if (nbk == 8) {
+              const int64_t g0 = flat + 32 - 8 * B;  // the group's first value
+              const int j0 = A.push_scatter ? (int)(g0 / A.cv) : 0;
+              const int j1 = A.push_scatter ? j0 + 1 : A.npush;
+              const int64_t local = A.push_scatter ? g0 - j0 * A.cv : g0;
+#pragma unroll 1
+              for (int j = j0; j < j1; ++j) {
+                uint8_t* sp = s_dst[j] + A.push_scale_off + (local / B / 8) * KB;
+#pragma unroll
+                for (int i = 0; i < KB; ++i) sp[i] = (uint8_t)(pk >> (8 * i));
+              }
+              pk = 0;
+              nbk = 0;
+            }
+          }
         } else if constexpr (KB == 8) {
           if (live) epi_chunk<MODE, B, ENC, BITS>(A, f, v, flat);
         } else {
@@ -950,8 +966,8 @@ cudaError_t launch_gemm_mx(const void* x, const void* w, int64_t M, int64_t N, i
 }
 
 // The GEMM with the quantiser AND the all-gather in its epilogue (2-CTA
-// form, one tensor, E8M0, fp4_e2m1 B in {16, 32}): returns
-// cudaErrorNotSupported outside it.
+// form, one tensor; fp4_e2m1 E8M0 B in {16, 32}, fp4_e2m1 E5M0 B in
+// {8, 16, 32}, fp5_e2m2 E5M0 B = 32): returns cudaErrorNotSupported outside it.
 cudaError_t launch_gemm_mx_push(const void* x, const void* w, int64_t M, int64_t N, int64_t K,
                                 const Fmt* fmt, int enc_id, uint8_t* const* peers, int npush,
                                 int rank, int64_t slot_stride, int64_t push_off,
@@ -964,14 +980,19 @@ cudaError_t launch_gemm_mx_push(const void* x, const void* w, int64_t M, int64_t
     return cudaErrorNotSupported;
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15)
     return cudaErrorNotSupported;
-  if (fmt->kbits != 8 || enc_id != ENC_E2M1 || (fmt->block != 16 && fmt->block != 32) ||
-      npush < 1 || npush > kMaxPush || rank < 0 || rank >= npush)
+  if (npush < 1 || npush > kMaxPush || rank < 0 || rank >= npush) return cudaErrorNotSupported;
+  const int blk = fmt->block;
+  const bool fp4 = enc_id == ENC_E2M1 && fmt->bits == 4;
+  const bool fp5 = enc_id == ENC_E2M2 && fmt->bits == 5;
+  if (fmt->kbits == 8 ? !(fp4 && (blk == 16 || blk == 32))
+                      : !(fmt->kbits == 5 && ((fp4 && (blk == 8 || blk == 16 || blk == 32)) ||
+                                              (fp5 && blk == 32))))
     return cudaErrorNotSupported;
   GArgs a;
   memset(&a, 0, sizeof(a));
   a.M = M; a.N = N; a.K = K;
   a.cv = scatter_chunk > 0 ? scatter_chunk : M * N; a.chunk_stride = 0;
-  if (scatter_chunk > 0 && (scatter_chunk % 32 != 0 || scatter_chunk * npush != M * N))
+  if (scatter_chunk > 0 && (scatter_chunk % (8 * blk) != 0 || scatter_chunk * npush != M * N))
     return cudaErrorNotSupported;
   a.push_scatter = scatter_chunk > 0;
   a.nonfinite = nonfinite;
@@ -979,7 +1000,13 @@ cudaError_t launch_gemm_mx_push(const void* x, const void* w, int64_t M, int64_t
   a.push_peers = peers; a.npush = npush; a.push_rank = rank;
   a.push_slot_stride = slot_stride; a.push_off = push_off;
   a.push_scale_off = scale_off; a.push_elem_off = elem_off; a.push_state = state;
-  if (fmt->block == 32) return go_2cta<256, 8, 1, 32, ENC_E2M1, 4, 8, true>(a, x, w, st);
+  if (fmt->kbits == 5) {  // E5M0: B = 32 takes 4 epilogue warps (one thread, one group)
+    if (fp5) return go_2cta<256, 4, 1, 32, ENC_E2M2, 5, 5, true>(a, x, w, st);
+    if (blk == 32) return go_2cta<256, 4, 1, 32, ENC_E2M1, 4, 5, true>(a, x, w, st);
+    if (blk == 16) return go_2cta<256, 8, 1, 16, ENC_E2M1, 4, 5, true>(a, x, w, st);
+    return go_2cta<256, 8, 1, 8, ENC_E2M1, 4, 5, true>(a, x, w, st);
+  }
+  if (blk == 32) return go_2cta<256, 8, 1, 32, ENC_E2M1, 4, 8, true>(a, x, w, st);
   return go_2cta<256, 8, 1, 16, ENC_E2M1, 4, 8, true>(a, x, w, st);
 }
 

@@ -21,10 +21,12 @@ __device__ __forceinline__ unsigned int ld_acquire_sys_u32(const unsigned int* p
   return v;
 }
 
-template <typename OutT, int B>
+template <typename OutT, int B, int ENC, int BITS, int KB>
 __global__ void __launch_bounds__(kLeanThreads2, 8) k_push_dqsum(const PArgs P) {
-  constexpr int BITS = 4;
+  constexpr int DEC = dec_of(ENC, BITS);
   using RL = RankLoad<B, BITS, kVPL>;
+  __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
+  if constexpr (DEC != ENC_E2M1) fill_lut(s_lut, P.f);  // visible after the wait's barrier
   pdl_prologue();  // this rank's GEMM (same stream) is complete: state[0] = epoch
   __shared__ unsigned int s_e;
   if (threadIdx.x == 0) s_e = *reinterpret_cast<const volatile unsigned int*>(P.state);
@@ -66,12 +68,12 @@ __global__ void __launch_bounds__(kLeanThreads2, 8) k_push_dqsum(const PArgs P) 
   for (int r = 0; r < nr; r += 2) {
     RL x0, x1;
     load_rank<B, BITS, kVPL, true>(x0, base + (int64_t)r * P.shard_stride, P.scale_off,
-                                   P.elem_off, (int64_t)u * kUnit, lane, kVPL, 8);
+                                   P.elem_off, (int64_t)u * kUnit, lane, kVPL, KB);
     if (r + 1 < nr)
       load_rank<B, BITS, kVPL, true>(x1, base + (int64_t)(r + 1) * P.shard_stride, P.scale_off,
-                                     P.elem_off, (int64_t)u * kUnit, lane, kVPL, 8);
-    decode_rank<B, ENC_E2M1, BITS, kVPL>(x0, f, acc, false, nullptr);
-    if (r + 1 < nr) decode_rank<B, ENC_E2M1, BITS, kVPL>(x1, f, acc, false, nullptr);
+                                     P.elem_off, (int64_t)u * kUnit, lane, kVPL, KB);
+    decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
+    if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
   }
   const size_t o = (size_t)u * kUnit + lane * kVPL;
   store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(P.out) + o, kVPL, acc,
@@ -112,11 +114,13 @@ __device__ __forceinline__ void publish_and_wait(unsigned int* const* peer_flags
 // reduce-scatter leg done everywhere -> this rank's chunk: N shards decoded
 // in rank order, fp32 sum from +0.0, re-quantised (K3's arithmetic) and
 // pushed into every rank's all-gather region
-template <int B>
+template <int B, int ENC, int BITS, int KB>
 __global__ void __launch_bounds__(kLeanThreads2) k_push2_requant(const P2Args P) {
-  constexpr int BITS = 4;
+  constexpr int DEC = dec_of(ENC, BITS);
   constexpr int NSB = Geo<B>::NSB;
   using RL = RankLoad<B, BITS, kVPL>;
+  __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
+  if constexpr (DEC != ENC_E2M1) fill_lut(s_lut, P.f);  // visible after the wait's barrier
   pdl_prologue();
   __shared__ unsigned int s_e;
   if (threadIdx.x == 0) s_e = *reinterpret_cast<const volatile unsigned int*>(P.state);
@@ -136,43 +140,57 @@ __global__ void __launch_bounds__(kLeanThreads2) k_push2_requant(const P2Args P)
   for (int r = 0; r < nr; r += 2) {
     RL x0, x1;
     load_rank<B, BITS, kVPL, true>(x0, rs + (int64_t)r * P.shard_stride, P.scale_off, P.elem_off,
-                                   (int64_t)q * kUnit, lane, kVPL, 8);
+                                   (int64_t)q * kUnit, lane, kVPL, KB);
     if (r + 1 < nr)
       load_rank<B, BITS, kVPL, true>(x1, rs + (int64_t)(r + 1) * P.shard_stride, P.scale_off,
-                                     P.elem_off, (int64_t)q * kUnit, lane, kVPL, 8);
-    decode_rank<B, ENC_E2M1, BITS, kVPL>(x0, f, acc, false, nullptr);
-    if (r + 1 < nr) decode_rank<B, ENC_E2M1, BITS, kVPL>(x1, f, acc, false, nullptr);
+                                     P.elem_off, (int64_t)q * kUnit, lane, kVPL, KB);
+    decode_rank<B, DEC, BITS, kVPL>(x0, f, acc, false, s_lut);
+    if (r + 1 < nr) decode_rank<B, DEC, BITS, kVPL>(x1, f, acc, false, s_lut);
   }
   Raw<float> raw;
 #pragma unroll
   for (int i = 0; i < kVPL; ++i) raw.w[i] = __float_as_uint(acc[i]);
   int stored[NSB];
   bool bad;
-  LaneCodes<BITS> cc = quant_lane<float, B, ENC_E2M1, BITS>(raw, f, stored, bad);
+  LaneCodes<BITS> cc = quant_lane<float, B, ENC, BITS>(raw, f, stored, bad);
   if (bad)
     report_nonfinite_raw<float>(raw, kVPL, (int64_t)P.rank * P.c + (int64_t)q * kUnit + lane * kVPL,
                                 P.nonfinite);
   const int64_t ag = slot + (int64_t)nr * P.shard_stride + (int64_t)P.rank * P.shard_stride;
+  [[maybe_unused]] uint64_t pk = 0;
+  if constexpr (KB != 8) pk = pack_unit_scales_k<B>(stored, lane, KB);  // warp-collective
   for (int j = 0; j < nr; ++j) {
     uint8_t* dst = P.peer_bufs[j] + ag;
-    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(
-                     dst + P.elem_off + (int64_t)q * (kUnit / 2) + lane * 16),
-                 "r"(cc.w[0]), "r"(cc.w[1]), "r"(cc.w[2]), "r"(cc.w[3])
-                 : "memory");
-    uint8_t* sp = dst + P.scale_off + (int64_t)q * (kUnit / B) + lane * NSB;
-    if constexpr (NSB == 2)
-      asm volatile("st.global.u16 [%0], %1;" ::"l"(sp), "h"((uint16_t)(stored[0] | (stored[1] << 8)))
-                   : "memory");
-    else
-      asm volatile("st.global.u8 [%0], %1;" ::"l"(sp), "h"((uint16_t)stored[0]) : "memory");
+    store_lane_codes<BITS>(dst + P.elem_off + (int64_t)q * (kUnit / 8 * BITS) + lane * (4 * BITS),
+                           cc, kVPL);
+    if constexpr (KB != 8) {
+      constexpr int G = scale_group_lanes<B>();
+      if (lane % G == 0) {
+        uint8_t* sp = dst + P.scale_off + ((int64_t)q * (kUnit / B) / 8 + lane / G) * KB;
+#pragma unroll
+        for (int i = 0; i < KB; ++i) sp[i] = (uint8_t)(pk >> (8 * i));
+      }
+    } else {
+      uint8_t* sp = dst + P.scale_off + (int64_t)q * (kUnit / B) + lane * NSB;
+      if constexpr (NSB == 4)
+        *reinterpret_cast<uint32_t*>(sp) = (uint32_t)stored[0] | ((uint32_t)stored[1] << 8) |
+                                           ((uint32_t)stored[2] << 16) |
+                                           ((uint32_t)stored[3] << 24);
+      else if constexpr (NSB == 2)
+        *reinterpret_cast<uint16_t*>(sp) = (uint16_t)(stored[0] | (stored[1] << 8));
+      else
+        *sp = (uint8_t)stored[0];
+    }
   }
 }
 
 // all-gather leg done everywhere -> decode every owner's reduced chunk
-template <typename OutT, int B>
+template <typename OutT, int B, int ENC, int BITS, int KB>
 __global__ void __launch_bounds__(kLeanThreads2, 8) k_push2_decode(const P2Args P) {
-  constexpr int BITS = 4;
+  constexpr int DEC = dec_of(ENC, BITS);
   using RL = RankLoad<B, BITS, kVPL>;
+  __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
+  if constexpr (DEC != ENC_E2M1) fill_lut(s_lut, P.f);  // visible after the wait's barrier
   pdl_prologue();
   __shared__ unsigned int s_e;
   if (threadIdx.x == 0) s_e = *reinterpret_cast<const volatile unsigned int*>(P.state);
@@ -189,55 +207,76 @@ __global__ void __launch_bounds__(kLeanThreads2, 8) k_push2_decode(const P2Args 
                         (int64_t)(nr + (int)j) * P.shard_stride;
   RL x;
   load_rank<B, BITS, kVPL, true>(x, base, P.scale_off, P.elem_off, (int64_t)q * kUnit, lane, kVPL,
-                                 8);
+                                 KB);
   float acc[kVPL];
 #pragma unroll
   for (int i = 0; i < kVPL; ++i) acc[i] = 0.f;  // K2's two-shot final decode: from +0.0
-  decode_rank<B, ENC_E2M1, BITS, kVPL>(x, P.f, acc, false, nullptr);
+  decode_rank<B, DEC, BITS, kVPL>(x, P.f, acc, false, s_lut);
   const size_t o = (size_t)u * kUnit + lane * kVPL;
   store_lane_out<OutT, kVPL>(reinterpret_cast<OutT*>(P.out) + o, kVPL, acc,
                              P.residual ? reinterpret_cast<const OutT*>(P.residual) + o
                                         : nullptr);
 }
 
+// the push set: (block, element encoding, bits, scale bits)
+#define MXB_PUSH_SET(X)        \
+  X(32, ENC_E2M1, 4, 8)        \
+  X(16, ENC_E2M1, 4, 8)        \
+  X(32, ENC_E2M1, 4, 5)        \
+  X(16, ENC_E2M1, 4, 5)        \
+  X(8, ENC_E2M1, 4, 5)         \
+  X(32, ENC_E2M2, 5, 5)
+
 template <typename OutT>
-bool go(const PArgs& a, int block, cudaStream_t st) {
+bool go_dqsum(const PArgs& a, int block, int enc, cudaStream_t st) {
   const dim3 grid((unsigned)((a.n / kUnit + kLeanWarps2 - 1) / kLeanWarps2));
-  if (block == 32) {
-    launch_pdl(k_push_dqsum<OutT, 32>, grid, dim3(kLeanThreads2), 0, st, a);
-    return true;
+  const int kb = a.f.kbits, bits = a.f.bits;
+#define X(B_, E_, BT_, KB_)                                                              \
+  if (block == B_ && enc == E_ && bits == BT_ && kb == KB_) {                            \
+    launch_pdl(k_push_dqsum<OutT, B_, E_, BT_, KB_>, grid, dim3(kLeanThreads2), 0, st, a); \
+    return true;                                                                         \
   }
-  if (block == 16) {
-    launch_pdl(k_push_dqsum<OutT, 16>, grid, dim3(kLeanThreads2), 0, st, a);
-    return true;
+  MXB_PUSH_SET(X)
+#undef X
+  return false;
+}
+
+template <typename OutT>
+bool go_decode(const P2Args& a, int block, int enc, cudaStream_t st) {
+  const dim3 grid((unsigned)((a.n / kUnit + kLeanWarps2 - 1) / kLeanWarps2));
+  const int kb = a.f.kbits, bits = a.f.bits;
+#define X(B_, E_, BT_, KB_)                                                                \
+  if (block == B_ && enc == E_ && bits == BT_ && kb == KB_) {                              \
+    launch_pdl(k_push2_decode<OutT, B_, E_, BT_, KB_>, grid, dim3(kLeanThreads2), 0, st, a); \
+    return true;                                                                           \
   }
+  MXB_PUSH_SET(X)
+#undef X
   return false;
 }
 }  // namespace
 
-bool launch_push_dqsum(const PArgs& a, int out_is_bf16, int block, cudaStream_t st) {
-  return out_is_bf16 ? go<__nv_bfloat16>(a, block, st) : go<float>(a, block, st);
+bool launch_push_dqsum(const PArgs& a, int out_is_bf16, int block, int enc, cudaStream_t st) {
+  return out_is_bf16 ? go_dqsum<__nv_bfloat16>(a, block, enc, st)
+                     : go_dqsum<float>(a, block, enc, st);
 }
 
-bool launch_push2_requant(const P2Args& a, int block, cudaStream_t st) {
+bool launch_push2_requant(const P2Args& a, int block, int enc, cudaStream_t st) {
   const dim3 grid((unsigned)((a.c / kUnit + kLeanWarps2 - 1) / kLeanWarps2));
-  if (block == 32) launch_pdl(k_push2_requant<32>, grid, dim3(kLeanThreads2), 0, st, a);
-  else if (block == 16) launch_pdl(k_push2_requant<16>, grid, dim3(kLeanThreads2), 0, st, a);
-  else return false;
-  return true;
+  const int kb = a.f.kbits, bits = a.f.bits;
+#define X(B_, E_, BT_, KB_)                                                           \
+  if (block == B_ && enc == E_ && bits == BT_ && kb == KB_) {                         \
+    launch_pdl(k_push2_requant<B_, E_, BT_, KB_>, grid, dim3(kLeanThreads2), 0, st, a); \
+    return true;                                                                      \
+  }
+  MXB_PUSH_SET(X)
+#undef X
+  return false;
 }
 
-bool launch_push2_decode(const P2Args& a, int out_is_bf16, int block, cudaStream_t st) {
-  const dim3 grid((unsigned)((a.n / kUnit + kLeanWarps2 - 1) / kLeanWarps2));
-  if (block != 16 && block != 32) return false;
-  if (out_is_bf16) {
-    if (block == 32) launch_pdl(k_push2_decode<__nv_bfloat16, 32>, grid, dim3(kLeanThreads2), 0, st, a);
-    else launch_pdl(k_push2_decode<__nv_bfloat16, 16>, grid, dim3(kLeanThreads2), 0, st, a);
-  } else {
-    if (block == 32) launch_pdl(k_push2_decode<float, 32>, grid, dim3(kLeanThreads2), 0, st, a);
-    else launch_pdl(k_push2_decode<float, 16>, grid, dim3(kLeanThreads2), 0, st, a);
-  }
-  return true;
+bool launch_push2_decode(const P2Args& a, int out_is_bf16, int block, int enc, cudaStream_t st) {
+  return out_is_bf16 ? go_decode<__nv_bfloat16>(a, block, enc, st)
+                     : go_decode<float>(a, block, enc, st);
 }
 
 }  // namespace mxb

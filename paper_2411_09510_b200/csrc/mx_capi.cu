@@ -781,6 +781,10 @@ int mx_gemm_quantize_chunks(const void* x, const void* w, int64_t M, int64_t N, 
                    partial, nonfinite, stream);
 }
 
+#define PUSH_SET                                                                     \
+  "fp4_e2m1 E8M0 with B in {16, 32}, fp4_e2m1 E5M0 with B in {8, 16, 32} or fp5_e2m2 " \
+  "E5M0 with B = 32"
+
 int mx_push_layout(int64_t n, const mx_scheme_t* s, int32_t nranks, int64_t* slot_stride,
                    int64_t* shard_stride, int64_t* flags_offset, int64_t* buffer_bytes) {
   int rc = check_scheme(s);
@@ -817,8 +821,8 @@ int mx_gemm_allgather_push(const void* x, const void* w, int64_t M, int64_t N, i
                                       (cudaStream_t)stream);
   if (e == cudaErrorNotSupported)
     return fail(MX_ERR_UNSUPPORTED,
-                "GEMM + all-gather push: fp4_e2m1 E8M0 with B in {16, 32}, N %% 256 == 0, "
-                "K %% 64 == 0, at most 8 ranks, 16-byte aligned operands");
+                "GEMM + all-gather push: " PUSH_SET ", N %% 256 == 0, K %% 64 == 0, at most "
+                "8 ranks, 16-byte aligned operands");
   if (e != cudaSuccess) return fail(MX_ERR_CUDA, "k_gemm_mx2 push: %s", cudaGetErrorString(e));
   return cuda_check("k_gemm_mx2 push");
 }
@@ -834,9 +838,9 @@ int mx_push_dequant_sum(const uint8_t* buf, int64_t n, const mx_scheme_t* s, int
   if (n <= 0 || n % 1024 != 0 || nranks < 1 || nranks > 8)
     return fail(MX_ERR_UNSUPPORTED, "push decode: n %% 1024 == 0, 1..8 ranks");
   Fmt f = make_fmt(s);
-  if ((out_dtype != MX_BF16 && out_dtype != MX_F32) || f.kbits != 8 || f.bits != 4 ||
-      enc_of(s) != ENC_E2M1 || !aligned(out, 32) || !aligned(residual, 32))
-    return fail(MX_ERR_UNSUPPORTED, "push decode: fp4_e2m1 E8M0, bf16/f32 out, 32-B aligned");
+  if ((out_dtype != MX_BF16 && out_dtype != MX_F32) || !aligned(out, 32) ||
+      !aligned(residual, 32))
+    return fail(MX_ERR_UNSUPPORTED, "push decode: bf16/f32 out, 32-B aligned");
   int64_t slot, sb, foff, total, so, eo, sbytes;
   mx_push_layout(n, s, nranks, &slot, &sb, &foff, &total);
   mx_shard_layout(n, s, &so, &eo, &sbytes);
@@ -849,8 +853,9 @@ int mx_push_dequant_sum(const uint8_t* buf, int64_t n, const mx_scheme_t* s, int
   a.status = reinterpret_cast<unsigned int*>(status);
   a.timeout_ns = symm_timeout_ns();
   a.out = out; a.residual = residual; a.f = f;
-  if (!launch_push_dqsum(a, out_dtype == MX_BF16, (int)s->block_size, (cudaStream_t)stream))
-    return fail(MX_ERR_UNSUPPORTED, "push decode: B in {16, 32}");
+  if (!launch_push_dqsum(a, out_dtype == MX_BF16, (int)s->block_size, enc_of(s),
+                         (cudaStream_t)stream))
+    return fail(MX_ERR_UNSUPPORTED, "push decode: " PUSH_SET);
   return cuda_check("k_push_dqsum");
 }
 
@@ -895,8 +900,8 @@ int mx_gemm_reducescatter_push(const void* x, const void* w, int64_t M, int64_t 
                                       (cudaStream_t)stream);
   if (e == cudaErrorNotSupported)
     return fail(MX_ERR_UNSUPPORTED,
-                "GEMM + reduce-scatter push: fp4_e2m1 E8M0 with B in {16, 32}, N %% 256 == 0, "
-                "K %% 64 == 0, M*N %% (1024 * nranks) == 0, at most 8 ranks");
+                "GEMM + reduce-scatter push: " PUSH_SET ", N %% 256 == 0, K %% 64 == 0, "
+                "M*N %% (1024 * nranks) == 0, at most 8 ranks");
   if (e != cudaSuccess) return fail(MX_ERR_CUDA, "k_gemm_mx2 push: %s", cudaGetErrorString(e));
   return cuda_check("k_gemm_mx2 reduce-scatter push");
 }
@@ -909,8 +914,6 @@ static int push2_args(P2Args& a, const uint8_t* buf, int64_t n, const mx_scheme_
   if (!buf || !peer_flags || !state || !status || rank < 0 || rank >= nranks || nranks > 8)
     return fail(MX_ERR_INVALID_ARGUMENT, "bad buffers or ranks");
   Fmt f = make_fmt(s);
-  if (f.kbits != 8 || f.bits != 4 || enc_of(s) != ENC_E2M1)
-    return fail(MX_ERR_UNSUPPORTED, "two-shot push: fp4_e2m1 E8M0");
   int64_t c, slot, sb, foff, total, so, eo, sbytes;
   rc = mx_push2_layout(n, s, nranks, &c, &slot, &sb, &foff, &total);
   if (rc) return rc;
@@ -936,8 +939,8 @@ int mx_push2_requant(const uint8_t* buf, int64_t n, const mx_scheme_t* s, int32_
   if (rc) return rc;
   if (!peer_bufs) return fail(MX_ERR_INVALID_ARGUMENT, "NULL peer buffers");
   a.nonfinite = reinterpret_cast<unsigned long long*>(nonfinite);
-  if (!launch_push2_requant(a, (int)s->block_size, (cudaStream_t)stream))
-    return fail(MX_ERR_UNSUPPORTED, "two-shot push: B in {16, 32}");
+  if (!launch_push2_requant(a, (int)s->block_size, enc_of(s), (cudaStream_t)stream))
+    return fail(MX_ERR_UNSUPPORTED, "two-shot push: " PUSH_SET);
   return cuda_check("k_push2_requant");
 }
 
@@ -952,8 +955,9 @@ int mx_push2_decode(const uint8_t* buf, int64_t n, const mx_scheme_t* s, int32_t
       !aligned(residual, 32))
     return fail(MX_ERR_UNSUPPORTED, "two-shot push decode: bf16/f32 out, 32-B aligned");
   a.out = out; a.residual = residual;
-  if (!launch_push2_decode(a, out_dtype == MX_BF16, (int)s->block_size, (cudaStream_t)stream))
-    return fail(MX_ERR_UNSUPPORTED, "two-shot push: B in {16, 32}");
+  if (!launch_push2_decode(a, out_dtype == MX_BF16, (int)s->block_size, enc_of(s),
+                           (cudaStream_t)stream))
+    return fail(MX_ERR_UNSUPPORTED, "two-shot push: " PUSH_SET);
   return cuda_check("k_push2_decode");
 }
 

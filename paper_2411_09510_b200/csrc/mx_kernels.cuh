@@ -676,12 +676,17 @@ __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
   return ((uint64_t)hi << 32) | lo;
 }
 
+// warp-collective: lanes whose lane % scale_group_lanes<B>() == 0 return the
+// k-bit codes of the 8-block group (lane / G) of the unit, packed
 template <int B>
-__device__ __forceinline__ void store_unit_scales_k(uint8_t* __restrict__ sc, int64_t blk0,
-                                                    const int* stored, int lane, int k) {
+__host__ __device__ constexpr int scale_group_lanes() {
+  return 8 * Geo<B>::LPB / Geo<B>::NSB;
+}
+template <int B>
+__device__ __forceinline__ uint64_t pack_unit_scales_k(const int* stored, int lane, int k) {
   constexpr int NSB = Geo<B>::NSB;
   constexpr int LPB = Geo<B>::LPB;
-  constexpr int G = 8 * LPB / NSB;  // lanes per group of 8 blocks
+  constexpr int G = scale_group_lanes<B>();  // lanes per group of 8 blocks
   uint64_t v = 0;
   if (lane % LPB == 0) {
     const int b0 = ((lane / LPB) * NSB) % 8;  // first owned block inside its group
@@ -690,6 +695,14 @@ __device__ __forceinline__ void store_unit_scales_k(uint8_t* __restrict__ sc, in
   }
 #pragma unroll
   for (int m = 1; m < G; m <<= 1) v |= shfl_xor_u64(v, m);
+  return v;
+}
+
+template <int B>
+__device__ __forceinline__ void store_unit_scales_k(uint8_t* __restrict__ sc, int64_t blk0,
+                                                    const int* stored, int lane, int k) {
+  constexpr int G = scale_group_lanes<B>();
+  const uint64_t v = pack_unit_scales_k<B>(stored, lane, k);
   if (lane % G == 0) {
     uint8_t* p = sc + (blk0 / 8 + lane / G) * k;
     for (int i = 0; i < k; ++i) p[i] = (uint8_t)(v >> (8 * i));
@@ -1432,7 +1445,9 @@ struct PArgs {
   const void* residual;          // nullable, out's dtype (see DArgs)
   Fmt f;
 };
-bool launch_push_dqsum(const PArgs& a, int out_is_bf16, int block, cudaStream_t st);
+// enc: ENC_* of the element format; the push set is fp4_e2m1 E8M0 (B 16 / 32)
+// and E5M0 (B 8 / 16 / 32), fp5_e2m2 E5M0 (B 32) -- false outside it
+bool launch_push_dqsum(const PArgs& a, int out_is_bf16, int block, int enc, cudaStream_t st);
 // two-shot push (k_push.cu): the GEMM scatters chunk j of its shard to rank
 // j (reduce-scatter leg), k_push2_requant sums + requantises this rank's
 // chunk and pushes it to every rank (all-gather leg), k_push2_decode decodes
@@ -1454,8 +1469,8 @@ struct P2Args {
   const void* residual;
   Fmt f;
 };
-bool launch_push2_requant(const P2Args& a, int block, cudaStream_t st);
-bool launch_push2_decode(const P2Args& a, int out_is_bf16, int block, cudaStream_t st);
+bool launch_push2_requant(const P2Args& a, int block, int enc, cudaStream_t st);
+bool launch_push2_decode(const P2Args& a, int out_is_bf16, int block, int enc, cudaStream_t st);
 
 // two-shot over symmetric memory (k_fused.cuh, k_symm2_flow)
 struct S2Args {

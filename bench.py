@@ -633,7 +633,8 @@ def ttft_block(torch, dist, args, world, dev):
                "method": "one model, one CUDA graph per variant, replays interleaved "
                          "round-robin; median ms, max over ranks"}
         err, got = None, {}
-        vs = variants + [("mx_paper_scheme", paper[name], "auto", "auto")]
+        vs = variants + [("mx_paper_scheme", paper[name], "auto", "auto"),
+                         ("mx_paper_scheme_push", paper[name], "push", None)]
         try:
             got = tp.measure_ttft_ab(cfg, 1, seq, vs, tp=world, layers=args.ttft_layers,
                                      reps=9, warmup=2)

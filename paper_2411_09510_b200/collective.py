@@ -507,6 +507,18 @@ class SymmetricAllReduce:
 # ---------------------------------------------------------------------------
 
 
+def push_scheme_ok(sch) -> bool:
+    """The GEMM push's scheme set (k_gemm.cu launch_gemm_mx_push, k_push.cu
+    MXB_PUSH_SET): fp4_e2m1 E8M0 B 16/32 and the paper's E5M0 schemes --
+    fp4_e2m1 B 8/16/32, fp5_e2m2 B 32."""
+    e, k, b = sch.element.name, sch.scale.exponent_bits, sch.block_size
+    if k == 8:
+        return e == "fp4_e2m1" and b in (16, 32)
+    if k == 5:
+        return (e == "fp4_e2m1" and b in (8, 16, 32)) or (e == "fp5_e2m2" and b == 32)
+    return False
+
+
 class FusedLinearAllReduce:
     """all_reduce(x @ W^T) with the GEMM, the MX quantiser AND the all-gather
     in ONE kernel per rank, over torch symmetric memory (NVLink / NVSwitch).
@@ -527,7 +539,9 @@ class FusedLinearAllReduce:
     re-quantises it and pushes it into every rank (the all-gather leg); the
     decode launch decodes every owner's chunk -- bit-identical to the NCCL
     two-shot (n % (1024 * world) == 0).
-    Requirements: fp4_e2m1 E8M0 with B in {16, 32}; bf16 x [M, K] and
+    Requirements: a scheme of the push set (``push_scheme_ok``: fp4_e2m1
+    E8M0 with B in {16, 32}, the paper's fp4_e2m1 E5M0 with B in {8, 16, 32}
+    and fp5_e2m2 E5M0 with B = 32); bf16 x [M, K] and
     W [N, K] contiguous, N % 256 == 0, K % 64 == 0, n = M*N % 1024 == 0;
     at most 8 ranks.  Slots alternate by epoch parity, which is safe because a
     rank starts call e only after its call e-1 saw every peer's e-1 flag,
@@ -581,8 +595,7 @@ class FusedLinearAllReduce:
         import torch
 
         sch = self.scheme
-        return (sch.element.name == "fp4_e2m1" and sch.scale.exponent_bits == 8
-                and sch.block_size in (16, 32) and x.dtype == torch.bfloat16
+        return (push_scheme_ok(sch) and x.dtype == torch.bfloat16
                 and (self.algo == "oneshot" or self.n % (1024 * self.world) == 0)
                 and w.dtype == torch.bfloat16 and w.dim() == 2 and x.shape[-1] == w.shape[1]
                 and w.shape[0] % 256 == 0 and x.shape[-1] % 64 == 0 and self.n % 1024 == 0

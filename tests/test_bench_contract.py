@@ -78,5 +78,5 @@ def test_gpu_arm_world1_nccl_line():
     t = d["ttft"]["llama-3.1-8b"]
     assert t["layers"] == 2
     for k in ("bf16_nccl", "mx_oneshot", "mx_oneshot_unfused", "mx_twoshot", "mx_symm", "mx_symm2",
-              "mx_push", "mx_paper_scheme"):
+              "mx_push", "mx_paper_scheme", "mx_paper_scheme_push"):
         assert "ms" in t[k], (k, t[k])

@@ -25,6 +25,11 @@ pytestmark = pytest.mark.gpu
 from oracle import mx_oracle as O  # noqa: E402
 
 SPEC = "fp4_e2m1:32:e8m0"
+# the push set: fp4 E8M0 B 16/32 and the paper's E5M0 schemes (8B:
+# fp4_e2m1:8:e5m0, 70B: fp5_e2m2:32:e5m0)
+PUSH_SPECS = [SPEC, "fp4_e2m1:16:e8m0", "fp4_e2m1:8:e5m0", "fp4_e2m1:16:e5m0",
+              "fp4_e2m1:32:e5m0", "fp5_e2m2:32:e5m0"]
+PAPER_SPECS = ["fp4_e2m1:8:e5m0", "fp5_e2m2:32:e5m0"]
 
 
 def operands(M, N, K, seed):
@@ -56,7 +61,7 @@ def pg():
 
 
 @pytest.mark.parametrize("out_dtype", [torch.bfloat16, torch.float32])
-@pytest.mark.parametrize("spec", [SPEC, "fp4_e2m1:16:e8m0"])
+@pytest.mark.parametrize("spec", PUSH_SPECS)
 def test_push_world1_equals_nccl_oneshot(pg, out_dtype, spec):
     from paper_2411_09510_b200.collective import CompressedAllReduce, FusedLinearAllReduce
 
@@ -86,6 +91,10 @@ def test_push_unsupported_raises(pg):
     assert not fl.supported(x, w)
     with pytest.raises(ShapeMismatch):
         fl.linear(x, w)
+    x, w = operands(256, 512, 128, seed=1)
+    assert FusedLinearAllReduce(SPEC, 256 * 512).supported(x, w)
+    for spec in ("fp4_e2m1:64:e8m0", "fp5_e2m2:16:e5m0", "fp4_e2m1:32:e4m0"):
+        assert not FusedLinearAllReduce(spec, 256 * 512).supported(x, w), spec
 
 
 def _plain_partial(lib, x, w):
@@ -101,15 +110,16 @@ def _plain_partial(lib, x, w):
     return part
 
 
-@pytest.mark.parametrize("nranks", [2, 3, 4, 8])
-def test_push_multirank_one_device(nranks):
+@pytest.mark.parametrize("nranks,spec", [(2, SPEC), (3, SPEC), (4, SPEC), (8, SPEC)] +
+                         [(r, sp) for sp in PAPER_SPECS for r in (2, 3, 8)])
+def test_push_multirank_one_device(nranks, spec):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     from paper_2411_09510_b200 import _native
     from paper_2411_09510_b200.formats import parse_scheme
 
     lib = _native.load()
-    cs = parse_scheme(SPEC).to_c()
+    cs = parse_scheme(spec).to_c()
     M, N, K = 256, 512, 256  # 2 tiles: every rank's GEMM and decode stay co-resident
     n = M * N
     slot, shard, foff, total = _native.push_layout(n, cs, nranks)
@@ -126,7 +136,7 @@ def test_push_multirank_one_device(nranks):
         parts = [_plain_partial(lib, x, w) for x, w in ops]
         torch.cuda.synchronize()
         host = [p.float().cpu().numpy().ravel().astype(np.float64) for p in parts]
-        want = torch.from_numpy(O.allreduce_oneshot(host, O.scheme(SPEC))).to(torch.bfloat16)
+        want = torch.from_numpy(O.allreduce_oneshot(host, O.scheme(spec))).to(torch.bfloat16)
         for r in range(nranks):  # every GEMM first, then every decode
             x, w = ops[r]
             _native.check(lib.mx_gemm_allgather_push(
@@ -146,7 +156,8 @@ def test_push_multirank_one_device(nranks):
             assert torch.equal(outs[r].cpu(), want), (nranks, call, r)
 
 
-def test_row_parallel_push_equals_oneshot(pg):
+@pytest.mark.parametrize("spec", [SPEC, "fp5_e2m2:32:e5m0"])
+def test_row_parallel_push_equals_oneshot(pg, spec):
     """RowParallelLinear(algo="push") == the NCCL one-shot hook, residual
     fused, bit for bit (world size 1)."""
     from paper_2411_09510_b200 import tp
@@ -155,8 +166,9 @@ def test_row_parallel_push_equals_oneshot(pg):
     torch.manual_seed(3)
     x = torch.randn(2, 128, 512, device="cuda").to(torch.bfloat16)
     h = torch.randn(2, 128, 1024, device="cuda").to(torch.bfloat16)
-    push = RowParallelLinear(512, 1024, scheme=SPEC, algo="push", device="cuda")
-    one = RowParallelLinear(512, 1024, scheme=SPEC, algo="oneshot", device="cuda",
+    push = RowParallelLinear(512, 1024, scheme=spec, algo="push", device="cuda")
+    assert push._push(2 * 128 * 1024, torch.bfloat16, x.device).supported(x, push.weight)
+    one = RowParallelLinear(512, 1024, scheme=spec, algo="oneshot", device="cuda",
                             fused_gemm=True)
     one.weight.data.copy_(push.weight.data)
     a = push(x, residual=h).clone()
@@ -166,7 +178,7 @@ def test_row_parallel_push_equals_oneshot(pg):
     tp._PUSH_CACHE.clear()
 
 
-@pytest.mark.parametrize("spec", [SPEC, "fp4_e2m1:16:e8m0"])
+@pytest.mark.parametrize("spec", PUSH_SPECS)
 def test_push_twoshot_world1_equals_nccl_twoshot(pg, spec):
     from paper_2411_09510_b200.collective import CompressedAllReduce, FusedLinearAllReduce
 
@@ -185,8 +197,9 @@ def test_push_twoshot_world1_equals_nccl_twoshot(pg, spec):
     fl.check_status()
 
 
-@pytest.mark.parametrize("nranks", [2, 4, 8])
-def test_push_twoshot_multirank_one_device(nranks):
+@pytest.mark.parametrize("nranks,spec", [(2, SPEC), (4, SPEC), (8, SPEC)] +
+                         [(r, sp) for sp in PAPER_SPECS for r in (2, 4, 8)])
+def test_push_twoshot_multirank_one_device(nranks, spec):
     """Two-shot push with N concurrent ranks on one device == the oracle's
     two-shot (reduce-scatter, fp32 sum, requantise, all-gather)."""
     if not torch.cuda.is_available():
@@ -195,7 +208,7 @@ def test_push_twoshot_multirank_one_device(nranks):
     from paper_2411_09510_b200.formats import parse_scheme
 
     lib = _native.load()
-    cs = parse_scheme(SPEC).to_c()
+    cs = parse_scheme(spec).to_c()
     M, N, K = 256, 512, 256
     n = M * N
     c, slot, shard, foff, total = _native.push2_layout(n, cs, nranks)
@@ -212,7 +225,7 @@ def test_push_twoshot_multirank_one_device(nranks):
         parts = [_plain_partial(lib, x, w) for x, w in ops]
         torch.cuda.synchronize()
         host = [p.float().cpu().numpy().ravel().astype(np.float64) for p in parts]
-        want = torch.from_numpy(O.allreduce_twoshot(host, O.scheme(SPEC))).to(torch.bfloat16)
+        want = torch.from_numpy(O.allreduce_twoshot(host, O.scheme(spec))).to(torch.bfloat16)
         for r in range(nranks):
             x, w = ops[r]
             _native.check(lib.mx_gemm_reducescatter_push(

@@ -5,7 +5,7 @@ to HBM instead of NVLink -- an upper bound on the epilogue's extra store
 work) plus its end-of-kernel publish.  CUDA-graph replays, operand sets
 rotated beyond L2; us per GEMM.
 
-    python scripts/push_bench.py
+    python scripts/push_bench.py [scheme ...]   (default fp4_e2m1:32:e8m0)
 """
 import ctypes
 import json
@@ -25,7 +25,11 @@ L2 = 126 * 1024 * 1024
 
 def main():
     lib = _native.load()
-    spec = "fp4_e2m1:32:e8m0"
+    for spec in sys.argv[1:] or ["fp4_e2m1:32:e8m0"]:
+        run(lib, spec)
+
+
+def run(lib, spec):
     cs = parse_scheme(spec).to_c()
     P = ctypes.c_void_p
     st = lambda: P(torch.cuda.current_stream().cuda_stream)  # noqa: E731
@@ -37,7 +41,7 @@ def main():
         ws = [(torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16) for _ in range(R)]
         so, eo, S = _native.shard_layout(M * N, cs)
         shard = torch.empty(S, dtype=torch.uint8, device="cuda")
-        res = {"shape": label, "M": M, "N": N, "K": K}
+        res = {"scheme": spec, "shape": label, "M": M, "N": N, "K": K}
 
         def local(i):
             _native.check(lib.mx_gemm_quantize(P(xs[i].data_ptr()), P(ws[i].data_ptr()), M, N, K,

@@ -272,14 +272,15 @@ int mx_pack_codes(const uint8_t* codes, int64_t count, int32_t width, uint8_t* p
  * ONE kernel per rank: the tcgen05 GEMM's epilogue quantises each drained
  * accumulator tile and stores the shard bytes straight into slot
  * (epoch & 1) of EVERY rank's symmetric buffer (peer memory, NVLink), so the
- * transfer overlaps the remaining tiles' math; its last CTA records the
- * epoch.  mx_push_dequant_sum then publishes this rank's epoch into every
- * rank's flag array (one system-scope fence, cumulative over the GEMM's
- * stores), waits for the N flags and decodes the N local shards in rank
- * order (bit-identical to the NCCL one-shot).  Buffer: mx_push_layout bytes per
- * rank (two slots of nranks shards, then nranks u32 flags, zeroed once);
- * state: 2 local u32 zeroed once ([0] epoch, [1] CTA counter); status: one
- * local u32 (1 = a peer wait timed out after MXB200_SYMM_TIMEOUT_MS).
+ * transfer overlaps the remaining tiles' math; its last CTA (GPU-scope
+ * arrival counter) issues one system-scope fence and stores the epoch into
+ * flag [rank] of every rank's flag array.  mx_push_dequant_sum waits for the
+ * N local flags (`flags`, this rank's array) and decodes the N local shards
+ * in rank order (bit-identical to the NCCL one-shot).  Buffer: mx_push_layout
+ * bytes per rank (two slots of nranks shards, then nranks u32 flags, zeroed
+ * once); state: 2 local u32 zeroed once ([0] epoch, [1] CTA counter);
+ * status: one local u32 (1 = a peer wait timed out after
+ * MXB200_SYMM_TIMEOUT_MS).
  * The push set: fp4_e2m1 E8M0 with B in {16, 32}, and the paper's E5M0
  * schemes -- fp4_e2m1 with B in {8, 16, 32}, fp5_e2m2 with B = 32; N % 256
  * == 0, at most 8 ranks (MX_ERR_UNSUPPORTED outside it). */
@@ -289,20 +290,23 @@ int mx_gemm_allgather_push(const void* x, const void* w, int64_t M, int64_t N, i
                            const mx_scheme_t* scheme, uint8_t* const* peer_bufs, int32_t rank,
                            int32_t nranks, uint32_t* state, uint64_t* nonfinite, void* stream);
 int mx_push_dequant_sum(const uint8_t* buf, int64_t n, const mx_scheme_t* scheme, int32_t rank,
-                        int32_t nranks, uint32_t* const* peer_flags, const uint32_t* flags,
-                        const uint32_t* state, uint32_t* status, void* out, int32_t out_dtype,
-                        const void* residual, void* stream);
+                        int32_t nranks, const uint32_t* flags, const uint32_t* state,
+                        uint32_t* status, void* out, int32_t out_dtype, const void* residual,
+                        void* stream);
 
 /* Two-shot form (the TP >= 4 algorithm; n % (1024*nranks) == 0): the GEMM's
  * epilogue scatters chunk j of its shard to rank j (the reduce-scatter leg,
- * one store per value group); mx_push2_requant publishes, waits for every
- * rank's chunk j, sums the N shards of this rank's chunk in rank order,
- * re-quantises (K3's arithmetic) and pushes the reduced chunk shard into
- * every rank (the all-gather leg); mx_push2_decode publishes, waits and
- * decodes every owner's reduced chunk, residual fused.  Bit-identical to
- * the NCCL two-shot.  Buffer: mx_push2_layout bytes (two slots of 2 x
- * nranks chunk shards; flags: nranks RS then nranks AG u32, zeroed once);
- * peer_flags: device array of every rank's flag array. */
+ * one store per value group) and its last CTA publishes RS flag [rank]
+ * everywhere; mx_push2_requant waits for every rank's chunk, sums the N
+ * shards of this rank's chunk in rank order, re-quantises (K3's arithmetic),
+ * pushes the reduced chunk shard into every rank (the all-gather leg) and
+ * its last CTA publishes AG flag [nranks + rank] everywhere (one system
+ * fence); mx_push2_decode waits for the AG flags and decodes every owner's
+ * reduced chunk, residual fused.  Bit-identical to the NCCL two-shot.
+ * Buffer: mx_push2_layout bytes (two slots of 2 x nranks chunk shards;
+ * flags: nranks RS then nranks AG u32, zeroed once); peer_flags: device
+ * array of every rank's flag array; state: 3 local u32 zeroed once ([0]
+ * epoch, [1] GEMM CTA counter, [2] requantiser CTA counter). */
 int mx_push2_layout(int64_t n, const mx_scheme_t* scheme, int32_t nranks, int64_t* chunk_values,
                     int64_t* slot_stride, int64_t* shard_stride, int64_t* flags_offset,
                     int64_t* buffer_bytes);
@@ -312,11 +316,10 @@ int mx_gemm_reducescatter_push(const void* x, const void* w, int64_t M, int64_t 
                                void* stream);
 int mx_push2_requant(const uint8_t* buf, int64_t n, const mx_scheme_t* scheme, int32_t rank,
                      int32_t nranks, uint8_t* const* peer_bufs, uint32_t* const* peer_flags,
-                     const uint32_t* state, uint32_t* status, uint64_t* nonfinite, void* stream);
+                     uint32_t* state, uint32_t* status, uint64_t* nonfinite, void* stream);
 int mx_push2_decode(const uint8_t* buf, int64_t n, const mx_scheme_t* scheme, int32_t rank,
-                    int32_t nranks, uint32_t* const* peer_flags, const uint32_t* state,
-                    uint32_t* status, void* out, int32_t out_dtype, const void* residual,
-                    void* stream);
+                    int32_t nranks, const uint32_t* state, uint32_t* status, void* out,
+                    int32_t out_dtype, const void* residual, void* stream);
 
 /* serialize (mx/codec.py:340-348) on the device: out = header || scale
  * stream || element stream, one launch, any byte alignment.  `header` is a

@@ -81,11 +81,11 @@ SIGNATURES = {
                                            c_i32, c_vp, c_vp, c_vp]),
     "mx_push2_requant": (c_i32, [c_vp, c_i64, _SP, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
                                  c_vp]),
-    "mx_push2_decode": (c_i32, [c_vp, c_i64, _SP, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32,
-                                c_vp, c_vp]),
+    "mx_push2_decode": (c_i32, [c_vp, c_i64, _SP, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp,
+                                c_vp]),
     "mx_gemm_allgather_push": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i64, _SP, c_vp, c_i32, c_i32,
                                        c_vp, c_vp, c_vp]),
-    "mx_push_dequant_sum": (c_i32, [c_vp, c_i64, _SP, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
+    "mx_push_dequant_sum": (c_i32, [c_vp, c_i64, _SP, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,
                                     c_i32, c_vp, c_vp]),
     "mx_copy_bytes": (c_i32, [c_vp, c_i64, c_vp, c_vp]),
     "mx_nonfinite_reset": (c_i32, [c_vp, c_vp]),

@@ -527,18 +527,19 @@ class FusedLinearAllReduce:
     accumulator tile as it drains and stores the shard bytes straight into
     slot (epoch & 1) of every rank's symmetric buffer -- the all-gather of
     mx/netbench.py:323-328 rides on the epilogue and overlaps the remaining
-    tiles' math.  A second launch (k_push_dqsum) publishes this rank's epoch
-    into every rank's flag array (one system-scope fence, so none sits on the
-    GEMM's tail), waits for the N flags and decodes the N shards from local
-    memory in rank order, with the optional residual add fused into its
-    store.  Bit-identical to ``CompressedAllReduce.linear``
+    tiles' math; its last CTA (GPU-scope arrival counter) issues one
+    system-scope fence and publishes the epoch into every rank's flag array.
+    A second launch (k_push_dqsum) waits for the N flags and decodes the N
+    shards from local memory in rank order, with the optional residual add
+    fused into its store.  Bit-identical to ``CompressedAllReduce.linear``
     (NCCL one-shot) on the same operands.  No NCCL kernel, no gather copy.
     ``algo="twoshot"`` (TP >= 4): the epilogue scatters chunk j of the shard
     to rank j only (the reduce-scatter leg rides on the GEMM); a requantise
-    launch sums this rank's chunk over the N senders in rank order,
-    re-quantises it and pushes it into every rank (the all-gather leg); the
-    decode launch decodes every owner's chunk -- bit-identical to the NCCL
-    two-shot (n % (1024 * world) == 0).
+    launch waits for the N chunks, sums this rank's chunk over the senders in
+    rank order, re-quantises it and pushes it into every rank (the
+    all-gather leg, published by its last CTA); the decode launch waits and
+    decodes every owner's chunk -- bit-identical to the NCCL two-shot
+    (n % (1024 * world) == 0).
     Requirements: a scheme of the push set (``push_scheme_ok``: fp4_e2m1
     E8M0 with B in {16, 32}, the paper's fp4_e2m1 E5M0 with B in {8, 16, 32}
     and fp5_e2m2 E5M0 with B = 32); bf16 x [M, K] and
@@ -631,8 +632,8 @@ class FusedLinearAllReduce:
                 P(self.flag.data_ptr()), be._st()), "mx_push2_requant")
             _native.check(be.lib.mx_push2_decode(
                 P(self.buf.data_ptr()), self.n, ctypes.byref(be.cs), self.rank, self.world,
-                P(self.flag_ptrs.data_ptr()), P(base + 4), P(base), P(o.data_ptr()), be._dt(o),
-                res, be._st()), "mx_push2_decode")
+                P(base + 4), P(base), P(o.data_ptr()), be._dt(o), res, be._st()),
+                "mx_push2_decode")
             return o.view(*x.shape[:-1], N)
         _native.check(be.lib.mx_gemm_allgather_push(
             P(x.data_ptr()), P(weight.data_ptr()), M, N, K, ctypes.byref(be.cs),
@@ -640,8 +641,7 @@ class FusedLinearAllReduce:
             P(base + 4), P(self.flag.data_ptr()), be._st()), "mx_gemm_allgather_push")
         _native.check(be.lib.mx_push_dequant_sum(
             P(self.buf.data_ptr()), self.n, ctypes.byref(be.cs), self.rank, self.world,
-            P(self.flag_ptrs.data_ptr()), P(self.flags_local.data_ptr()), P(base + 4), P(base),
-            P(o.data_ptr()), be._dt(o),
+            P(self.flags_local.data_ptr()), P(base + 4), P(base), P(o.data_ptr()), be._dt(o),
             P(residual.data_ptr()) if residual is not None else None, be._st()),
             "mx_push_dequant_sum")
         return o.view(*x.shape[:-1], N)

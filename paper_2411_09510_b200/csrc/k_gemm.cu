@@ -144,8 +144,9 @@ struct GArgs {
   Fmt f;
   // all-gather push (2-CTA form, PUSH = true): the epilogue writes this
   // rank's shard into slot (epoch & 1) of EVERY rank's symmetric buffer over
-  // NVLink, tile by tile as the accumulators drain; the last CTA records the
-  // epoch (the decode launch publishes it, k_push.cu)
+  // NVLink, tile by tile as the accumulators drain; the last CTA (GPU-scope
+  // arrival counter) publishes the epoch into every rank's flag array with
+  // one system-scope fence, and records it locally
   uint8_t* const* push_peers;       // device [npush]: peer buffer bases
   int npush, push_rank;
   int push_scatter;                 // 1: chunk j (cv values) goes to rank j only (two-shot
@@ -154,6 +155,7 @@ struct GArgs {
   int64_t push_off;                 // this rank's shard inside a slot
   int64_t push_scale_off, push_elem_off;  // shard layout
   unsigned int* push_state;         // local: [0] epoch, [1] CTA arrival counter
+  int64_t push_flags_off;           // flag array inside every peer buffer (u32 [npush])
 };
 constexpr int kMaxPush = 8;
 
@@ -751,17 +753,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm_threads<EPI>(),
                  : "memory");
   }
   if constexpr (PUSH) {
-    // the last CTA (GPU-scope arrival counter) records this call's epoch;
-    // the system-scope publication to the peers is the first thing the
-    // decode launch (k_push_dqsum) does, so no system fence sits on the
-    // GEMM's tail -- the GEMM's stores precede that launch in stream order,
-    // and its release is cumulative over them
+    // threadfence-reduction at two scopes: every CTA's epilogue stores are
+    // ordered before its GPU-scope acq_rel arrival (bar.sync above, then
+    // cumulativity); the last CTA to arrive has acquired them all, and ONE
+    // system-scope fence then makes them visible before its relaxed flag
+    // stores reach the peers -- no per-CTA system fence on the tail
     if (threadIdx.x == 0) {
       unsigned int prev;
       asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
                    : "=r"(prev) : "l"(A.push_state + 1) : "memory");
       if (prev == gridDim.x - 1) {
         A.push_state[1] = 0u;
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        for (int j = 0; j < A.npush; ++j)
+          asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(
+                           A.push_peers[j] + A.push_flags_off + 4 * (int64_t)A.push_rank),
+                       "r"(s_epoch)
+                       : "memory");
         *reinterpret_cast<volatile unsigned int*>(A.push_state) = s_epoch;
       }
     }
@@ -972,8 +980,8 @@ cudaError_t launch_gemm_mx_push(const void* x, const void* w, int64_t M, int64_t
                                 const Fmt* fmt, int enc_id, uint8_t* const* peers, int npush,
                                 int rank, int64_t slot_stride, int64_t push_off,
                                 int64_t scale_off, int64_t elem_off, int64_t scatter_chunk,
-                                unsigned int* state, unsigned long long* nonfinite,
-                                cudaStream_t st) {
+                                int64_t flags_off, unsigned int* state,
+                                unsigned long long* nonfinite, cudaStream_t st) {
   using namespace gm;
   static const int two = env_int("MXB200_GEMM_2CTA", 1);
   if (!two || !fmt || M < 1 || N < 256 || N % 256 != 0 || K < BK || K % BK != 0)
@@ -1000,6 +1008,7 @@ cudaError_t launch_gemm_mx_push(const void* x, const void* w, int64_t M, int64_t
   a.push_peers = peers; a.npush = npush; a.push_rank = rank;
   a.push_slot_stride = slot_stride; a.push_off = push_off;
   a.push_scale_off = scale_off; a.push_elem_off = elem_off; a.push_state = state;
+  a.push_flags_off = flags_off;
   if (fmt->kbits == 5) {  // E5M0: B = 32 takes 4 epilogue warps (one thread, one group)
     if (fp5) return go_2cta<256, 4, 1, 32, ENC_E2M2, 5, 5, true>(a, x, w, st);
     if (blk == 32) return go_2cta<256, 4, 1, 32, ENC_E2M1, 4, 5, true>(a, x, w, st);

@@ -1,10 +1,9 @@
 // The consumer half of the GEMM + all-gather push (k_gemm.cu, PUSH = true):
 // every rank's GEMM epilogue has written its MX shard into slot (epoch & 1)
-// of THIS rank's symmetric buffer over NVLink.  This launch first publishes
-// its own rank's epoch into every rank's flag array (CTA 0: one system fence,
-// cumulative over the GEMM's stores that precede it in stream order), then
-// waits for the N flags (acquire, system scope; a wait past the timeout sets
-// a status word instead of hanging),
+// of THIS rank's symmetric buffer over NVLink, and its last CTA has
+// published the epoch into flag [rank] of every rank (one system fence).
+// This launch waits for the N flags (acquire, system scope; a wait past the
+// timeout sets a status word instead of hanging),
 // then decodes the N local shards in rank order, fp32 from +0.0
 // (mx/netbench.py:332-334), into bf16 / f32, with the optional residual
 // add fused into the store -- K2's arithmetic, so the result is
@@ -21,6 +20,27 @@ __device__ __forceinline__ unsigned int ld_acquire_sys_u32(const unsigned int* p
   return v;
 }
 
+// wait (threads < nr) until flags[j] >= epoch for every j, then bar.sync:
+// the acquiring threads' view covers the whole CTA
+__device__ __forceinline__ void wait_flags(const unsigned int* flags, int nr, unsigned int e,
+                                           unsigned int* status, unsigned long long timeout_ns) {
+  if ((int)threadIdx.x < nr) {
+    const unsigned int* fl = flags + threadIdx.x;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while ((int)(ld_acquire_sys_u32(fl) - e) < 0) {
+      __nanosleep(64);
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        atomicExch(status, 1u);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
 template <typename OutT, int B, int ENC, int BITS, int KB>
 __global__ void __launch_bounds__(kLeanThreads2, 8) k_push_dqsum(const PArgs P) {
   constexpr int DEC = dec_of(ENC, BITS);
@@ -32,30 +52,7 @@ __global__ void __launch_bounds__(kLeanThreads2, 8) k_push_dqsum(const PArgs P) 
   if (threadIdx.x == 0) s_e = *reinterpret_cast<const volatile unsigned int*>(P.state);
   __syncthreads();
   const unsigned int e = s_e;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    // publish this rank's call-e shard (written by the GEMM launch before
-    // this one on the stream) to every rank: one system-scope fence, then
-    // the epoch into every flag array
-    asm volatile("fence.acq_rel.sys;" ::: "memory");
-    for (int j = 0; j < P.nranks; ++j)
-      asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(P.peer_flags[j] + P.rank), "r"(e)
-                   : "memory");
-  }
-  if ((int)threadIdx.x < P.nranks) {
-    const unsigned int* fl = P.flags + threadIdx.x;
-    unsigned long long t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    while ((int)(ld_acquire_sys_u32(fl) - e) < 0) {
-      __nanosleep(64);
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > P.timeout_ns) {
-        atomicExch(P.status, 1u);
-        break;
-      }
-    }
-  }
-  __syncthreads();
+  wait_flags(P.flags, P.nranks, e, P.status, P.timeout_ns);
   const int lane = threadIdx.x & 31;
   const uint32_t u = blockIdx.x * kLeanWarps2 + (threadIdx.x >> 5);
   if (u >= (uint32_t)(P.n / kUnit)) return;
@@ -81,56 +78,13 @@ __global__ void __launch_bounds__(kLeanThreads2, 8) k_push_dqsum(const PArgs P) 
                                         : nullptr);
 }
 
-// publish this rank's epoch into flag [idx] of every rank (CTA 0, thread 0:
-// one system fence, cumulative over the previous launches' stores), then
-// wait (threads < nranks) until flag [base + j] >= epoch for every j
-__device__ __forceinline__ void publish_and_wait(unsigned int* const* peer_flags, int idx,
-                                                 const unsigned int* flags, int base, int nr,
-                                                 unsigned int e, unsigned int* status,
-                                                 unsigned long long timeout_ns) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    asm volatile("fence.acq_rel.sys;" ::: "memory");
-    for (int j = 0; j < nr; ++j)
-      asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(peer_flags[j] + idx), "r"(e)
-                   : "memory");
-  }
-  if ((int)threadIdx.x < nr) {
-    const unsigned int* fl = flags + base + threadIdx.x;
-    unsigned long long t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    while ((int)(ld_acquire_sys_u32(fl) - e) < 0) {
-      __nanosleep(64);
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > timeout_ns) {
-        atomicExch(status, 1u);
-        break;
-      }
-    }
-  }
-  __syncthreads();
-}
-
-// reduce-scatter leg done everywhere -> this rank's chunk: N shards decoded
-// in rank order, fp32 sum from +0.0, re-quantised (K3's arithmetic) and
-// pushed into every rank's all-gather region
 template <int B, int ENC, int BITS, int KB>
-__global__ void __launch_bounds__(kLeanThreads2) k_push2_requant(const P2Args P) {
+__device__ __forceinline__ void requant_unit(const P2Args& P, unsigned int e, uint32_t q,
+                                             int lane, const float* s_lut) {
   constexpr int DEC = dec_of(ENC, BITS);
   constexpr int NSB = Geo<B>::NSB;
   using RL = RankLoad<B, BITS, kVPL>;
-  __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
-  if constexpr (DEC != ENC_E2M1) fill_lut(s_lut, P.f);  // visible after the wait's barrier
-  pdl_prologue();
-  __shared__ unsigned int s_e;
-  if (threadIdx.x == 0) s_e = *reinterpret_cast<const volatile unsigned int*>(P.state);
-  __syncthreads();
-  const unsigned int e = s_e;
   const int nr = P.nranks;
-  publish_and_wait(P.peer_flags, P.rank, P.flags, 0, nr, e, P.status, P.timeout_ns);
-  const int lane = threadIdx.x & 31;
-  const uint32_t q = blockIdx.x * kLeanWarps2 + (threadIdx.x >> 5);
-  if (q >= (uint32_t)(P.c / kUnit)) return;
   const int64_t slot = (int64_t)(e & 1u) * P.slot_stride;
   const uint8_t* rs = P.buf + slot;
   const Fmt f = P.f;
@@ -184,6 +138,42 @@ __global__ void __launch_bounds__(kLeanThreads2) k_push2_requant(const P2Args P)
   }
 }
 
+// reduce-scatter leg done everywhere -> this rank's chunk: N shards decoded
+// in rank order, fp32 sum from +0.0, re-quantised (K3's arithmetic) and
+// pushed into every rank's all-gather region
+template <int B, int ENC, int BITS, int KB>
+__global__ void __launch_bounds__(kLeanThreads2) k_push2_requant(const P2Args P) {
+  constexpr int DEC = dec_of(ENC, BITS);
+  __shared__ float s_lut[DEC == ENC_E2M1 ? 1 : 256];
+  if constexpr (DEC != ENC_E2M1) fill_lut(s_lut, P.f);  // visible after the wait's barrier
+  pdl_prologue();
+  __shared__ unsigned int s_e;
+  if (threadIdx.x == 0) s_e = *reinterpret_cast<const volatile unsigned int*>(P.state);
+  __syncthreads();
+  const unsigned int e = s_e;
+  const int nr = P.nranks;
+  wait_flags(P.flags, nr, e, P.status, P.timeout_ns);  // RS flags [0, nr): every GEMM's chunk
+  const int lane = threadIdx.x & 31;
+  const uint32_t q = blockIdx.x * kLeanWarps2 + (threadIdx.x >> 5);
+  if (q < (uint32_t)(P.c / kUnit)) requant_unit<B, ENC, BITS, KB>(P, e, q, lane, s_lut);
+  // the last CTA to finish publishes the all-gather leg: AG flag [nr + rank]
+  // of every rank, one system fence (the GEMM's pattern)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int prev;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
+                 : "=r"(prev) : "l"(P.state + 2) : "memory");
+    if (prev == gridDim.x - 1) {
+      P.state[2] = 0u;
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      for (int j = 0; j < nr; ++j)
+        asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(P.peer_flags[j] + nr + P.rank),
+                     "r"(e)
+                     : "memory");
+    }
+  }
+}
+
 // all-gather leg done everywhere -> decode every owner's reduced chunk
 template <typename OutT, int B, int ENC, int BITS, int KB>
 __global__ void __launch_bounds__(kLeanThreads2, 8) k_push2_decode(const P2Args P) {
@@ -197,7 +187,7 @@ __global__ void __launch_bounds__(kLeanThreads2, 8) k_push2_decode(const P2Args 
   __syncthreads();
   const unsigned int e = s_e;
   const int nr = P.nranks;
-  publish_and_wait(P.peer_flags, nr + P.rank, P.flags, nr, nr, e, P.status, P.timeout_ns);
+  wait_flags(P.flags + nr, nr, e, P.status, P.timeout_ns);  // AG flags [nr, 2 nr)
   const int lane = threadIdx.x & 31;
   const uint32_t u = blockIdx.x * kLeanWarps2 + (threadIdx.x >> 5);
   if (u >= (uint32_t)(P.n / kUnit)) return;

@@ -255,8 +255,8 @@ cudaError_t launch_gemm_mx_push(const void* x, const void* w, int64_t M, int64_t
                                 const Fmt* fmt, int enc_id, uint8_t* const* peers, int npush,
                                 int rank, int64_t slot_stride, int64_t push_off,
                                 int64_t scale_off, int64_t elem_off, int64_t scatter_chunk,
-                                unsigned int* state, unsigned long long* nonfinite,
-                                cudaStream_t st);
+                                int64_t flags_off, unsigned int* state,
+                                unsigned long long* nonfinite, cudaStream_t st);
 
 }  // namespace mxb
 
@@ -815,7 +815,7 @@ int mx_gemm_allgather_push(const void* x, const void* w, int64_t M, int64_t N, i
   mx_shard_layout(M * N, s, &so, &eo, &sbytes);
   Fmt f = make_fmt(s);
   cudaError_t e = launch_gemm_mx_push(x, w, M, N, K, &f, enc_of(s), peer_bufs, nranks,
-                                      rank, slot, (int64_t)rank * sb, so, eo, 0,
+                                      rank, slot, (int64_t)rank * sb, so, eo, 0, foff,
                                       reinterpret_cast<unsigned int*>(state),
                                       reinterpret_cast<unsigned long long*>(nonfinite),
                                       (cudaStream_t)stream);
@@ -828,12 +828,12 @@ int mx_gemm_allgather_push(const void* x, const void* w, int64_t M, int64_t N, i
 }
 
 int mx_push_dequant_sum(const uint8_t* buf, int64_t n, const mx_scheme_t* s, int32_t rank,
-                        int32_t nranks, uint32_t* const* peer_flags, const uint32_t* flags,
-                        const uint32_t* state, uint32_t* status, void* out, int32_t out_dtype,
-                        const void* residual, void* stream) {
+                        int32_t nranks, const uint32_t* flags, const uint32_t* state,
+                        uint32_t* status, void* out, int32_t out_dtype, const void* residual,
+                        void* stream) {
   int rc = check_scheme(s);
   if (rc) return rc;
-  if (!buf || !peer_flags || !flags || !state || !status || !out || rank < 0 || rank >= nranks)
+  if (!buf || !flags || !state || !status || !out || rank < 0 || rank >= nranks)
     return fail(MX_ERR_INVALID_ARGUMENT, "NULL buffer");
   if (n <= 0 || n % 1024 != 0 || nranks < 1 || nranks > 8)
     return fail(MX_ERR_UNSUPPORTED, "push decode: n %% 1024 == 0, 1..8 ranks");
@@ -847,7 +847,6 @@ int mx_push_dequant_sum(const uint8_t* buf, int64_t n, const mx_scheme_t* s, int
   PArgs a;
   a.buf = buf; a.slot_stride = slot; a.shard_stride = sb; a.scale_off = so; a.elem_off = eo;
   a.nranks = nranks; a.n = n; a.rank = rank;
-  a.peer_flags = reinterpret_cast<unsigned int* const*>(peer_flags);
   a.flags = reinterpret_cast<const unsigned int*>(flags);
   a.state = reinterpret_cast<const unsigned int*>(state);
   a.status = reinterpret_cast<unsigned int*>(status);
@@ -894,7 +893,7 @@ int mx_gemm_reducescatter_push(const void* x, const void* w, int64_t M, int64_t 
   mx_shard_layout(c, s, &so, &eo, &sbytes);
   Fmt f = make_fmt(s);
   cudaError_t e = launch_gemm_mx_push(x, w, M, N, K, &f, enc_of(s), peer_bufs, nranks, rank,
-                                      slot, (int64_t)rank * sb, so, eo, c,
+                                      slot, (int64_t)rank * sb, so, eo, c, foff,
                                       reinterpret_cast<unsigned int*>(state),
                                       reinterpret_cast<unsigned long long*>(nonfinite),
                                       (cudaStream_t)stream);
@@ -908,10 +907,10 @@ int mx_gemm_reducescatter_push(const void* x, const void* w, int64_t M, int64_t 
 
 static int push2_args(P2Args& a, const uint8_t* buf, int64_t n, const mx_scheme_t* s,
                       int32_t rank, int32_t nranks, uint8_t* const* peer_bufs,
-                      uint32_t* const* peer_flags, const uint32_t* state, uint32_t* status) {
+                      uint32_t* const* peer_flags, uint32_t* state, uint32_t* status) {
   int rc = check_scheme(s);
   if (rc) return rc;
-  if (!buf || !peer_flags || !state || !status || rank < 0 || rank >= nranks || nranks > 8)
+  if (!buf || !state || !status || rank < 0 || rank >= nranks || nranks > 8)
     return fail(MX_ERR_INVALID_ARGUMENT, "bad buffers or ranks");
   Fmt f = make_fmt(s);
   int64_t c, slot, sb, foff, total, so, eo, sbytes;
@@ -923,7 +922,7 @@ static int push2_args(P2Args& a, const uint8_t* buf, int64_t n, const mx_scheme_
   a.peer_bufs = peer_bufs;
   a.peer_flags = reinterpret_cast<unsigned int* const*>(peer_flags);
   a.flags = reinterpret_cast<const unsigned int*>(buf + foff);
-  a.state = reinterpret_cast<const unsigned int*>(state);
+  a.state = state;
   a.status = reinterpret_cast<unsigned int*>(status);
   a.timeout_ns = symm_timeout_ns();
   a.nonfinite = nullptr; a.out = nullptr; a.residual = nullptr;
@@ -933,11 +932,11 @@ static int push2_args(P2Args& a, const uint8_t* buf, int64_t n, const mx_scheme_
 
 int mx_push2_requant(const uint8_t* buf, int64_t n, const mx_scheme_t* s, int32_t rank,
                      int32_t nranks, uint8_t* const* peer_bufs, uint32_t* const* peer_flags,
-                     const uint32_t* state, uint32_t* status, uint64_t* nonfinite, void* stream) {
+                     uint32_t* state, uint32_t* status, uint64_t* nonfinite, void* stream) {
   P2Args a;
   int rc = push2_args(a, buf, n, s, rank, nranks, peer_bufs, peer_flags, state, status);
   if (rc) return rc;
-  if (!peer_bufs) return fail(MX_ERR_INVALID_ARGUMENT, "NULL peer buffers");
+  if (!peer_bufs || !peer_flags) return fail(MX_ERR_INVALID_ARGUMENT, "NULL peer buffers");
   a.nonfinite = reinterpret_cast<unsigned long long*>(nonfinite);
   if (!launch_push2_requant(a, (int)s->block_size, enc_of(s), (cudaStream_t)stream))
     return fail(MX_ERR_UNSUPPORTED, "two-shot push: " PUSH_SET);
@@ -945,11 +944,11 @@ int mx_push2_requant(const uint8_t* buf, int64_t n, const mx_scheme_t* s, int32_
 }
 
 int mx_push2_decode(const uint8_t* buf, int64_t n, const mx_scheme_t* s, int32_t rank,
-                    int32_t nranks, uint32_t* const* peer_flags, const uint32_t* state,
-                    uint32_t* status, void* out, int32_t out_dtype, const void* residual,
-                    void* stream) {
+                    int32_t nranks, const uint32_t* state, uint32_t* status, void* out,
+                    int32_t out_dtype, const void* residual, void* stream) {
   P2Args a;
-  int rc = push2_args(a, buf, n, s, rank, nranks, nullptr, peer_flags, state, status);
+  int rc = push2_args(a, buf, n, s, rank, nranks, nullptr, nullptr,
+                      const_cast<uint32_t*>(state), status);
   if (rc) return rc;
   if (!out || (out_dtype != MX_BF16 && out_dtype != MX_F32) || !aligned(out, 32) ||
       !aligned(residual, 32))

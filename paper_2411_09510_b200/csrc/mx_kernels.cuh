@@ -1436,8 +1436,7 @@ struct PArgs {
   int64_t slot_stride, shard_stride, scale_off, elem_off;
   int nranks, rank;
   int64_t n;                     // multiple of 1024
-  unsigned int* const* peer_flags;  // device [nranks]: every rank's flag array (CTA 0 publishes)
-  const unsigned int* flags;     // this rank's flag array: peer j releases [j] = epoch
+  const unsigned int* flags;     // this rank's flag array: peer j's GEMM releases [j] = epoch
   const unsigned int* state;     // local [0]: this call's epoch (set by this rank's GEMM)
   unsigned int* status;          // local u32: 1 if a peer wait timed out
   unsigned long long timeout_ns;
@@ -1461,7 +1460,8 @@ struct P2Args {
   uint8_t* const* peer_bufs;     // device [nranks]: every rank's buffer base
   unsigned int* const* peer_flags;  // device [nranks]: flag arrays (RS [nranks], AG [nranks])
   const unsigned int* flags;     // this rank's flag array
-  const unsigned int* state;     // local [0]: this call's epoch (set by this rank's GEMM)
+  unsigned int* state;           // local [0]: this call's epoch (set by this rank's GEMM),
+                                 // [2]: the requantiser's CTA arrival counter
   unsigned int* status;
   unsigned long long timeout_ns;
   unsigned long long* nonfinite;

@@ -73,7 +73,7 @@ def run(lib, spec):
                 def pair(i):  # push GEMM + publish / wait / decode (world 1)
                     push(i)
                     _native.check(lib.mx_push_dequant_sum(
-                        P(bufs[0].data_ptr()), M * N, ctypes.byref(cs), 0, 1, P(fptr.data_ptr()),
+                        P(bufs[0].data_ptr()), M * N, ctypes.byref(cs), 0, 1,
                         P(bufs[0].data_ptr() + foff), P(state.data_ptr() + 4), P(state.data_ptr()),
                         P(out.data_ptr()), _native.MX_BF16, None, st()), "decode")
                 res["push1_plus_decode_us"] = round(time_graph(pair, R), 2)

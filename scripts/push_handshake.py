@@ -1,6 +1,6 @@
 """Where the push decode's extra time goes at world size 1 (one B200):
 K2 over one shard, against mx_push_dequant_sum on the same shard with its
-flag already set (fence + publish + an immediately satisfied wait + decode),
+flag already set (an immediately satisfied wait + decode),
 and against the full push GEMM + decode pair.  CUDA-graph replays.
 
     python scripts/push_handshake.py
@@ -43,7 +43,7 @@ def main():
 
             def decode(i):
                 _native.check(lib.mx_push_dequant_sum(
-                    P(buf.data_ptr()), n, ctypes.byref(cs), 0, 1, P(fptr.data_ptr()),
+                    P(buf.data_ptr()), n, ctypes.byref(cs), 0, 1,
                     P(buf.data_ptr() + foff), P(state.data_ptr() + 4), P(state.data_ptr()),
                     P(out.data_ptr()), _native.MX_BF16, None, st()), "decode")
 

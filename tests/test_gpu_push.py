@@ -145,7 +145,7 @@ def test_push_multirank_one_device(nranks, spec):
                 P(streams[r].cuda_stream)), "mx_gemm_allgather_push")
         for r in range(nranks):
             _native.check(lib.mx_push_dequant_sum(
-                P(bufs[r].data_ptr()), n, ctypes.byref(cs), r, nranks, P(fptr.data_ptr()),
+                P(bufs[r].data_ptr()), n, ctypes.byref(cs), r, nranks,
                 P(bufs[r].data_ptr() + foff), P(state[r].data_ptr() + 4), P(state[r].data_ptr()),
                 P(outs[r].data_ptr()),
                 _native.MX_BF16, None, P(streams[r].cuda_stream)), "mx_push_dequant_sum")
@@ -239,7 +239,7 @@ def test_push_twoshot_multirank_one_device(nranks, spec):
                 P(nf[r].data_ptr()), P(streams[r].cuda_stream)), "mx_push2_requant")
         for r in range(nranks):
             _native.check(lib.mx_push2_decode(
-                P(bufs[r].data_ptr()), n, ctypes.byref(cs), r, nranks, P(fptr.data_ptr()),
+                P(bufs[r].data_ptr()), n, ctypes.byref(cs), r, nranks,
                 P(state[r].data_ptr() + 4), P(state[r].data_ptr()), P(outs[r].data_ptr()),
                 _native.MX_BF16, None, P(streams[r].cuda_stream)), "mx_push2_decode")
         torch.cuda.synchronize()

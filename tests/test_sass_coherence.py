@@ -75,3 +75,28 @@ def test_shard_reads_are_l1_bypassing():
             assert any(".128" in op and "CONSTANT" not in op for op in lds), lds
             return
     pytest.fail("k_fused_flow<*, 32, E2M1, 4> not found")
+
+
+PUSH_KERNELS = ("k_push_dqsum", "k_push2_requant", "k_push2_decode")
+
+
+def test_push_kernels_no_noncoherent_reads():
+    """The push consumers (k_push.cu) read only bytes written during the
+    call -- peer shards pushed over NVLink by the GEMM epilogues, the
+    requantised chunks -- and the residual, which may alias the output: no
+    load in them may take the non-coherent path, whatever its width."""
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe) or not os.path.exists(LIB):
+        pytest.skip("cuobjdump or libmxb200.so missing")
+    syms = subprocess.run([exe, "-symbols", LIB], capture_output=True, text=True,
+                          check=True).stdout
+    names = sorted({ln.split()[-1] for ln in syms.splitlines()
+                    if "STO_ENTRY" in ln and any(k in ln for k in PUSH_KERNELS)})
+    assert len(names) >= 18, names
+    sass = subprocess.run([exe, "-sass", "-fun", ",".join(names), LIB], capture_output=True,
+                          text=True, check=True).stdout
+    funcs = re.split(r"\n\s*Function : ", sass)[1:]
+    assert len(funcs) == len(names)
+    bad = [(f.split("\n", 1)[0].strip()[:80], op) for f in funcs
+           for op in re.findall(r"\b(LDG\.[A-Z0-9_.]*)", f) if "CONSTANT" in op]
+    assert not bad, bad[:10]

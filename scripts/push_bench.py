@@ -70,7 +70,7 @@ def run(lib, spec):
                     P(bptr.data_ptr()), 0, npush, P(state.data_ptr() + 4), None, st()), "push")
             res[f"push{npush}_us"] = round(time_graph(push, R), 2)
             if npush == 1:
-                def pair(i):  # push GEMM + publish / wait / decode (world 1)
+                def pair(i):  # push GEMM (+ publish) -> wait / decode (world 1)
                     push(i)
                     _native.check(lib.mx_push_dequant_sum(
                         P(bufs[0].data_ptr()), M * N, ctypes.byref(cs), 0, 1,

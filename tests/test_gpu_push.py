@@ -7,8 +7,8 @@ k_gemm.cu PUSH) and its flag-waiting decode (k_push.cu).
   and without the fused residual, bf16 and f32 outputs;
 * N = 2..8 ranks as N concurrent launches on one device (the K5 harness's
   approach): each rank's GEMM pushes its shard into every rank's buffer
-  (plain device pointers standing in for peer mappings); its decode launch
-  publishes its epoch into every rank's flag array; every rank's decode equals the
+  (plain device pointers standing in for peer mappings) and its last CTA
+  publishes the epoch into every rank's flag array; every rank's decode equals the
   oracle's one-shot all-reduce of the ranks' bf16 partials
   (mx/netbench.py:323-334), identical on every rank."""
 

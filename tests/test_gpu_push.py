@@ -178,18 +178,19 @@ def test_row_parallel_push_equals_oneshot(pg, spec):
     tp._PUSH_CACHE.clear()
 
 
+@pytest.mark.parametrize("out_dtype", [torch.bfloat16, torch.float32])
 @pytest.mark.parametrize("spec", PUSH_SPECS)
-def test_push_twoshot_world1_equals_nccl_twoshot(pg, spec):
+def test_push_twoshot_world1_equals_nccl_twoshot(pg, spec, out_dtype):
     from paper_2411_09510_b200.collective import CompressedAllReduce, FusedLinearAllReduce
 
     M, N, K = 512, 1024, 256
-    fl = FusedLinearAllReduce(spec, M * N, algo="twoshot")
-    car = CompressedAllReduce(spec, M * N, algo="twoshot", out_dtype=torch.bfloat16)
+    fl = FusedLinearAllReduce(spec, M * N, algo="twoshot", out_dtype=out_dtype)
+    car = CompressedAllReduce(spec, M * N, algo="twoshot", out_dtype=out_dtype)
     for it in range(5):
         x, w = operands(M, N, K, seed=300 + it)
         got = fl.linear(x, w).clone()
         want = car.linear(x, w).clone()
-        h = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+        h = torch.randn(M, N, device="cuda").to(out_dtype)
         got_r = fl.linear(x, w, residual=h).clone()
         torch.cuda.synchronize()
         assert torch.equal(got.view(-1), want.view(-1)), it

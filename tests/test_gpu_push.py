@@ -247,3 +247,27 @@ def test_push_twoshot_multirank_one_device(nranks, spec):
         for r in range(nranks):
             assert int(state[r][0].item()) == 0, "peer wait timed out"
             assert torch.equal(outs[r].cpu(), want), (nranks, call, r)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_push_random_shapes_world1(pg, seed):
+    """Ragged M (partial 256-row tiles), K from one 64-wide k-block up, N a
+    few 256-wide tiles, random push-set scheme, both algorithms: the push
+    equals the NCCL path of the same fused GEMM bit for bit."""
+    from paper_2411_09510_b200.collective import CompressedAllReduce, FusedLinearAllReduce
+
+    rng = np.random.default_rng(seed)
+    M = int(rng.choice([4, 36, 300, 1000, 1028]))
+    N = 256 * int(rng.integers(1, 5))
+    K = 64 * int(rng.integers(1, 9))
+    spec = PUSH_SPECS[int(rng.integers(len(PUSH_SPECS)))]
+    for algo in ("oneshot", "twoshot"):
+        fl = FusedLinearAllReduce(spec, M * N, algo=algo)
+        car = CompressedAllReduce(spec, M * N, algo=algo, out_dtype=torch.bfloat16)
+        x, w = operands(M, N, K, seed=900 + seed)
+        assert fl.supported(x, w), (M, N, K, spec)
+        got = fl.linear(x, w).clone()
+        want = car.linear(x, w).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(got.view(-1), want.view(-1)), (M, N, K, spec, algo)
+        fl.check_status()

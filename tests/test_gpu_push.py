@@ -198,9 +198,12 @@ def test_push_twoshot_world1_equals_nccl_twoshot(pg, spec, out_dtype):
     fl.check_status()
 
 
-@pytest.mark.parametrize("nranks,spec", [(2, SPEC), (4, SPEC), (8, SPEC)] +
-                         [(r, sp) for sp in PAPER_SPECS for r in (2, 4, 8)])
-def test_push_twoshot_multirank_one_device(nranks, spec):
+@pytest.mark.parametrize("nranks,spec,shape", [(2, SPEC, None), (4, SPEC, None), (8, SPEC, None)] +
+                         [(r, sp, None) for sp in PAPER_SPECS for r in (2, 4, 8)] +
+                         # chunk boundaries in the middle of a row and of a tile
+                         [(3, sp, (260, 768)) for sp in (SPEC, "fp5_e2m2:32:e5m0")] +
+                         [(5, "fp4_e2m1:8:e5m0", (260, 768))])
+def test_push_twoshot_multirank_one_device(nranks, spec, shape):
     """Two-shot push with N concurrent ranks on one device == the oracle's
     two-shot (reduce-scatter, fp32 sum, requantise, all-gather)."""
     if not torch.cuda.is_available():
@@ -210,7 +213,8 @@ def test_push_twoshot_multirank_one_device(nranks, spec):
 
     lib = _native.load()
     cs = parse_scheme(spec).to_c()
-    M, N, K = 256, 512, 256
+    M, N = shape or (256, 512)
+    K = 256
     n = M * N
     c, slot, shard, foff, total = _native.push2_layout(n, cs, nranks)
     bufs = [torch.zeros(total, dtype=torch.uint8, device="cuda") for _ in range(nranks)]

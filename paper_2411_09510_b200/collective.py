@@ -586,7 +586,8 @@ class FusedLinearAllReduce:
                                       dtype=torch.int64, device=self.device)
         torch.cuda.synchronize()
         dist.barrier(self.group)
-        # [0] status (as SymmetricAllReduce), [1] epoch, [2] CTA counter
+        # [0] status (as SymmetricAllReduce), [1] epoch, [2] GEMM CTA counter,
+        # [3] two-shot requantiser CTA counter
         self.state = torch.zeros(4, dtype=torch.int32, device=self.device)
         self.flag = torch.empty(1, dtype=torch.int64, device=self.device)
         self.backend.reset_flag(self.flag)

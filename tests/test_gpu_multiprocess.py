@@ -203,7 +203,7 @@ def test_processes_peer_collectives(WORLD):
     for p in ps:
         p.start()
     try:
-        got = dict(qs["out"].get(timeout=900) for _ in ps)
+        got = dict(qs["out"].get(timeout=300) for _ in ps)
     finally:
         for p in ps:
             p.join(timeout=120)

@@ -71,6 +71,11 @@ def parse():
                          "single-GPU simulation")
     ap.add_argument("--no-ttft", action="store_true", help="skip the TTFT block (N=1: TP=1 codec overhead; N>1: TP=N)")
     ap.add_argument("--no-70b", action="store_true", help="skip the 70B-shape kernel block")
+    ap.add_argument("--deadline-s", type=float,
+                    default=float(os.environ.get("MXB200_BENCH_DEADLINE_S", "600")),
+                    help="wall-clock budget: once the headline numbers exist, a watchdog "
+                         "prints the line built so far (+ 'truncated') and exits 0 if the "
+                         "informational blocks run past it")
     ap.add_argument("--ttft-layers", type=int, default=None,
                     help="truncate the TTFT stacks (default: full 32 / 80 layers)")
     return ap.parse_args()
@@ -839,6 +844,52 @@ def _parse(spec):
     return parse_scheme(spec, extensions=True)
 
 
+class Deadline:
+    """Bounds the bench's wall clock.  The line dict is filled in as blocks
+    finish; if the deadline passes before the last block, rank 0 prints the
+    line built so far with ``"truncated"`` naming the block that was running,
+    and every rank exits 0 -- a stuck informational block (a peer that never
+    arrives, a slow TTFT stack) can never cost the headline number."""
+
+    def __init__(self, t0, budget_s, rank):
+        self.t0, self.budget, self.rank = t0, budget_s, rank
+        self.line, self.block = None, "core"
+        self.lock = threading.Lock()
+        self.done = False
+        th = threading.Thread(target=self._run, daemon=True)
+        th.start()
+
+    def at(self, block):
+        self.block = block
+
+    def put(self, **kw):
+        if self.line is not None:
+            self.line.update(kw)
+
+    def emit(self):
+        with self.lock:
+            if self.done:
+                return
+            self.done = True
+            if self.rank == 0 and self.line is not None:
+                print(json.dumps(self.line), flush=True)
+
+    def _run(self):
+        while True:
+            time.sleep(1.0)
+            if self.done:
+                return
+            if time.time() - self.t0 > self.budget:
+                if self.line is None:
+                    continue  # the headline is not measured yet: no line to give
+                self.put(truncated=f"deadline {self.budget:.0f} s passed in block "
+                                   f"'{self.block}'; later blocks not run")
+                self.emit()
+                sys.stdout.flush()
+                sys.stderr.flush()
+                os._exit(0)
+
+
 def run_ours(args, shape, rank, world, local_rank, dist_mode):
     import torch
     import torch.distributed as dist
@@ -849,6 +900,10 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
     from paper_2411_09510_b200.formats import parse_scheme
     from paper_2411_09510_b200.synth import rank_partials
 
+    dl = Deadline(time.time(), args.deadline_s, rank)
+    # a peer wait of the NVLink kernels that exceeds this reports a status
+    # error (the block records it) instead of spinning for the library's 30 s
+    os.environ.setdefault("MXB200_SYMM_TIMEOUT_MS", "5000")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     _native.load()
@@ -885,6 +940,7 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
         for i in range(3):
             step_fn(i % R)()
         torch.cuda.synchronize()
+        dl.done = True
         return
 
     graphs = [capture(torch, step_fn(i)) for i in range(R)]
@@ -1030,8 +1086,35 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
                 "share_of_step": round(nranks * kq["us"] / (ms_step * 1e3), 3),
                 "other_kernels": {k: v for k, v in kernels.items() if k != "k_quant"}}
 
+    # ---- the headline is measured: the line exists from here on, so the
+    # deadline watchdog can always print it (informational blocks follow)
+    wire = ((nranks - 1) * S if args.algo == "oneshot" else
+            2 * (nranks - 1) * _native.shard_layout(
+                twoshot_chunk_values(n, nranks, sch.block_size), sch.to_c())[2])
+    cpu = None
+    if rank == 0 and not (args.no_cpu_baseline or dist_mode):
+        dl.at("cpu_baseline")
+        cpu = cpu_baseline(args.scheme, shape, nranks)
+    dl.line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+               "us_per_allreduce": round(ms_step * 1e3, 3),
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+               "dtype": "bf16",
+               "data": "synthetic (gaussian_with_outliers N(0,1) with 1% x100 outliers, "
+                       "mx/synth.py), bf16 partial sums",
+               "config": config_dict(args, shape, world, dist_mode, R),
+               "step_parity": parity,
+               "wire_bytes_per_rank": wire,
+               "roofline": roof, "cpu_baseline": cpu, "e2e": None,
+               "reference_api_e2e": None,
+               "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
+               "bf16_nccl_allreduce": None, "symmetric_memory_fused": None,
+               "collective": None, "simulated_tp_fused_step": None, "shape_70b": None,
+               "producer_gemm": None, "linear_collective": None, "ttft": None}
+
     # ---- simulated TP=4 and TP=8 on this GPU (N=1): the fused one-kernel
     # step with 4 / 8 rank partials (inputs rotated > 3x L2), informational
+    dl.at("simulated_tp_fused_step")
     sim_more = None
     if sim and args.algo == "oneshot" and args.sim_ranks == 2:
         sim_more = {}
@@ -1056,7 +1139,9 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
         except Exception as exc:  # noqa: BLE001  (informational only)
             sim_more = {"error": f"{type(exc).__name__}: {exc}"[:200]}
 
+    dl.put(simulated_tp_fused_step=sim_more)
     # ---- the 70B prefill partial shape (N=1): K4, K1, K2 + parity
+    dl.at("shape_70b")
     shape70 = None
     if sim and not args.no_70b and args.algo == "oneshot" and tuple(shape) != (4096, 8192):
         try:
@@ -1067,6 +1152,8 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
     # ---- end to end through the public API with pinned host buffers:
     # HostPipeline (chunked H2D -> compressed all-reduce -> D2H on three
     # streams), the host-array-in / host-array-out shape of the reference API
+    dl.put(shape_70b=shape70)
+    dl.at("e2e")
     e2e = None
     if not args.no_e2e:
         from paper_2411_09510_b200.collective import HostPipeline
@@ -1117,6 +1204,8 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
                "api": "HostPipeline.__call__ (pinned host partials -> pinned host result)"}
         del pipe
 
+    dl.put(e2e=e2e)
+    dl.at("reference_api_e2e")
     ref_api = None
     if sim and not args.no_e2e:
         try:
@@ -1125,6 +1214,8 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
             ref_api = {"error": f"{type(exc).__name__}: {exc}"[:200]}
 
     # ---- uncompressed bf16 NCCL all-reduce on the same tensor (TP=N path)
+    dl.put(reference_api_e2e=ref_api)
+    dl.at("bf16_nccl_allreduce")
     bf16_ar = None
     if dist_mode:
         xs = [s_[0][0].clone() for s_ in sets]
@@ -1146,6 +1237,8 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
     # ---- the NVLink-pull fused kernel over symmetric memory (TP=N path).
     # Every stage that can fail agrees across ranks first (all_reduce MIN of
     # an ok flag), so one rank's failure never leaves the others waiting.
+    dl.put(bf16_nccl_allreduce=bf16_ar)
+    dl.at("symmetric_memory_fused")
     symm = None
     if dist_mode and os.environ.get("MXB200_BENCH_SYMM", "1") == "1":
         from paper_2411_09510_b200.collective import SymmetricAllReduce
@@ -1203,10 +1296,8 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
 
     # the collective against NVLink (TP=N): effective (uncompressed-
     # equivalent, nccl-tests "algbw") and wire GB/s per rank vs 900 GB/s
+    dl.put(symmetric_memory_fused=symm)
     coll = None
-    wire = ((nranks - 1) * S if args.algo == "oneshot" else
-            2 * (nranks - 1) * _native.shard_layout(
-                twoshot_chunk_values(n, nranks, sch.block_size), sch.to_c())[2])
     if dist_mode:
         t = ms_step * 1e-3
         coll = {"effective_algbw_gbs": round(2 * n / t / 1e9, 1),
@@ -1215,6 +1306,7 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
                 "nvlink_gbs_per_direction": 900.0,
                 "wire_frac_of_nvlink": round(wire / t / 1e9 / 900.0, 4)}
 
+    dl.put(collective=coll)
     ttft = None
     gemm = None
     lincoll = None
@@ -1222,6 +1314,7 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
         del sets
         torch.cuda.empty_cache()
         err = None
+        dl.at("linear_collective")
         try:
             lincoll = linear_collective_block(torch, dist, args, world, dev)
         except Exception as exc:  # noqa: BLE001
@@ -1231,37 +1324,28 @@ def run_ours(args, shape, rank, world, local_rank, dist_mode):
         if not bool(t_ok.item()):
             lincoll = {"error": err or "failed on another rank"}
         torch.cuda.empty_cache()
+        dl.put(linear_collective=lincoll)
+        dl.at("ttft")
         if not args.no_ttft:
             ttft = ttft_block(torch, dist, args, world, dev)
     elif not dist_mode:
         del sets
         torch.cuda.empty_cache()
+        dl.at("producer_gemm")
         try:
             gemm = gemm_block(torch, args, _bf16_peak())
         except Exception as exc:  # noqa: BLE001
             gemm = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+        dl.put(producer_gemm=gemm)
+        dl.at("ttft")
         if not args.no_ttft:
             ttft = {"tp1": ttft_tp1_block(torch, args)}
 
     if rank != 0:
+        dl.done = True
         return
-    cpu = None if (args.no_cpu_baseline or dist_mode) else cpu_baseline(args.scheme, shape, nranks)
-    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
-            "us_per_allreduce": round(ms_step * 1e3, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (gaussian_with_outliers N(0,1) with 1% x100 outliers, "
-                    "mx/synth.py), bf16 partial sums",
-            "config": config_dict(args, shape, world, dist_mode, R),
-            "step_parity": parity,
-            "wire_bytes_per_rank": wire,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-            "reference_api_e2e": ref_api,
-            "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
-            "bf16_nccl_allreduce": bf16_ar, "symmetric_memory_fused": symm,
-            "collective": coll, "simulated_tp_fused_step": sim_more, "shape_70b": shape70,
-            "producer_gemm": gemm, "linear_collective": lincoll, "ttft": ttft}
-    print(json.dumps(line), flush=True)
+    dl.put(producer_gemm=gemm, linear_collective=lincoll, ttft=ttft)
+    dl.emit()
 
 
 def main():

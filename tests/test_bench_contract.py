@@ -80,3 +80,25 @@ def test_gpu_arm_world1_nccl_line():
     for k in ("bf16_nccl", "mx_oneshot", "mx_oneshot_unfused", "mx_twoshot", "mx_symm", "mx_symm2",
               "mx_push", "mx_paper_scheme", "mx_paper_scheme_push"):
         assert "ms" in t[k], (k, t[k])
+
+
+def test_deadline_prints_partial_line_and_exits_zero():
+    """The watchdog: once the headline line exists, an overrunning block
+    ends the run with that line (plus ``truncated``) and exit status 0; a
+    run that finishes in time prints the line exactly once."""
+    code = ("import sys, time; sys.path.insert(0, %r); import bench; "
+            "d = bench.Deadline(time.time(), %s, 0); d.at('ttft'); "
+            "d.line = {'metric': 'm', 'value': 1.0}; %s")
+    p = subprocess.run([sys.executable, "-c", code % (ROOT, 1.0, "time.sleep(30)")],
+                       capture_output=True, text=True, timeout=60)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["value"] == 1.0 and "'ttft'" in d["truncated"]
+    p = subprocess.run([sys.executable, "-c",
+                        code % (ROOT, 30.0, "d.put(ttft=None); d.emit(); d.emit()")],
+                       capture_output=True, text=True, timeout=60)
+    assert p.returncode == 0
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1 and "truncated" not in json.loads(lines[0])

@@ -72,7 +72,7 @@ def parse():
     ap.add_argument("--no-ttft", action="store_true", help="skip the TTFT block (N=1: TP=1 codec overhead; N>1: TP=N)")
     ap.add_argument("--no-70b", action="store_true", help="skip the 70B-shape kernel block")
     ap.add_argument("--deadline-s", type=float,
-                    default=float(os.environ.get("MXB200_BENCH_DEADLINE_S", "600")),
+                    default=float(os.environ.get("MXB200_BENCH_DEADLINE_S", "420")),
                     help="wall-clock budget: once the headline numbers exist, a watchdog "
                          "prints the line built so far (+ 'truncated') and exits 0 if the "
                          "informational blocks run past it")

@@ -60,6 +60,10 @@ def run_ranks(_native, spec, parts, calls, out_dtype=torch.float32, algo="onesho
     results = []
     for c in range(calls):
         xs = sets[c % len(sets)]
+        # the rank streams are non-blocking: order each call after the
+        # current stream's work (the previous call's result clones below)
+        for st in streams:
+            st.wait_stream(torch.cuda.current_stream())
         for r in range(N):
             st = streams[r]
             odt = _native.MX_F32 if out_dtype == torch.float32 else _native.MX_BF16
@@ -79,6 +83,7 @@ def run_ranks(_native, spec, parts, calls, out_dtype=torch.float32, algo="onesho
         torch.cuda.synchronize()
         assert all(int(s[0].item()) == 0 for s in state), "peer wait timed out"
         results.append([o.clone() for o in outs])
+    torch.cuda.synchronize()
     return results
 
 

@@ -341,6 +341,8 @@ def calibrate_codec_throughput(scheme, sample_sizes=(1 << 22,), repeats: int = 5
 
     def measure(size):
         data = torch.from_numpy(rng.standard_normal(size).astype(np.float16)).to(dev)
+        # the worker threads use their own non-blocking streams
+        torch.cuda.current_stream(dev).synchronize()
 
         def thread_rates():
             torch.cuda.set_device(dev)

@@ -143,8 +143,11 @@ inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
 // ---------------------------------------------------------------------------
 // 256-bit global accesses (sm_100)
 // ---------------------------------------------------------------------------
+#ifndef MXB_LDG_HINT
+#define MXB_LDG_HINT ""
+#endif
 __device__ __forceinline__ void ldg256(const void* p, uint32_t* r) {
-  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+  asm volatile("ld.global.nc.L1::no_allocate" MXB_LDG_HINT ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
                  "=r"(r[6]), "=r"(r[7])
                : "l"(p));
